@@ -1,0 +1,216 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY (arXiv 2512.13319).
+
+A plain, slow, sequential CPU fp64 reference (``oracle.c``: discrete Kalman
+filter + RTS smoother, backward-information two-filter smoother, iterated
+linearisation) and its ctypes binding.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline / ``--impl
+reference`` leg may import this package.  It shares no code with the CUDA
+product path in ``paper_2512_13319_b200/`` and never imports it.
+
+Every function cites the PAPER.md passage it follows ("P:n" = line n).
+Pins: see tests/test_oracle_pins.py and DESIGN.md section "Oracle pins".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIBS = {False: os.path.join(_HERE, "liboracle.so"), True: os.path.join(_HERE, "liboracle_ld.so")}
+
+
+def build(force: bool = False) -> None:
+    """Compile oracle.c (plain C, -O2, no fast-math) into the two shared objects."""
+    for ld, path in _LIBS.items():
+        if not force and os.path.exists(path) and os.path.getmtime(path) >= os.path.getmtime(_SRC):
+            continue
+        cmd = ["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-o", path, _SRC, "-lm"]
+        if ld:
+            cmd.insert(1, "-DORA_LONG_DOUBLE")
+        subprocess.check_call(cmd)
+
+
+class OraModel(ctypes.Structure):
+    _fields_ = [
+        ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nw", ctypes.c_int),
+        ("T", ctypes.c_long), ("t0", ctypes.c_double), ("tf", ctypes.c_double),
+    ] + [(n, ctypes.c_void_p) for n in ("F", "c", "L", "W", "H", "r", "R")] + [
+        (n, ctypes.c_long) for n in ("sF", "sc", "sL", "sW", "sH", "sr", "sR")
+    ] + [("m0", ctypes.c_void_p), ("P0", ctypes.c_void_p)]
+
+
+_loaded: dict = {}
+
+
+def _lib(long_double: bool = False):
+    if long_double not in _loaded:
+        build()
+        lib = ctypes.CDLL(_LIBS[long_double])
+        P = ctypes.c_void_p
+        lib.ora_kf_rts.argtypes = [ctypes.POINTER(OraModel), P, P, P, P]
+        lib.ora_two_filter.argtypes = [ctypes.POINTER(OraModel), P, P]
+        lib.ora_batch.argtypes = [ctypes.POINTER(OraModel), ctypes.c_long, P, P, ctypes.c_int]
+        lib.ora_ieks.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long,
+                                 ctypes.c_double, ctypes.c_double, P, P, P, P, P, P, ctypes.c_int, P, P, P]
+        for n in ("ora_ct_f", "ora_ct_dfdx", "ora_ct_h", "ora_ct_dhdx"):
+            getattr(lib, n).argtypes = [P, P]
+        lib.ora_vdp_f.argtypes = [ctypes.c_double, P, P]
+        lib.ora_vdp_dfdx.argtypes = [ctypes.c_double, P, P]
+        lib.ora_num_threads.restype = ctypes.c_int
+        _loaded[long_double] = lib
+    return _loaded[long_double]
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+class LinearModel:
+    """Linear-affine model of P:134-140 sampled on the grid.
+
+    Each of F, c, L, W, H, r, R is either one matrix (constant in time) or an
+    array with a leading node axis of length T+1 (time-varying)."""
+
+    def __init__(self, F, L, W, H, R, m0, P0, c=None, r=None):
+        self.F, self.L, self.W, self.H, self.R = map(_f64, (F, L, W, H, R))
+        self.c = None if c is None else _f64(c)
+        self.r = None if r is None else _f64(r)
+        self.m0, self.P0 = _f64(m0), _f64(P0)
+
+    @property
+    def nx(self) -> int:
+        return self.m0.shape[-1]
+
+    @property
+    def ny(self) -> int:
+        return self.H.shape[-2]
+
+    @property
+    def nw(self) -> int:
+        return self.L.shape[-1]
+
+    def _struct(self, T: int, t0: float, tf: float) -> OraModel:
+        def stride(a, base_ndim):
+            if a is None:
+                return 0
+            if a.ndim == base_ndim:
+                return 0
+            assert a.shape[0] == T + 1, "time-varying arrays need T+1 node entries"
+            return int(np.prod(a.shape[1:]))
+
+        s = OraModel()
+        s.nx, s.ny, s.nw, s.T, s.t0, s.tf = self.nx, self.ny, self.nw, T, t0, tf
+        for name, nd in (("F", 2), ("c", 1), ("L", 2), ("W", 2), ("H", 2), ("r", 1), ("R", 2)):
+            a = getattr(self, name)
+            setattr(s, name, _ptr(a))
+            setattr(s, "s" + name, stride(a, nd))
+        s.m0, s.P0 = _ptr(self.m0), _ptr(self.P0)
+        return s
+
+
+def kf_rts(model: LinearModel, y, T: int, t0: float, tf: float, long_double: bool = False,
+           want_filter: bool = False):
+    """Discrete KF + RTS MAP (P:200-226 discretised).
+
+    Returns x_map [T+1, nx] (and filter means [T+1, nx], covariances
+    [T+1, nx, nx] when want_filter)."""
+    y = _f64(y).reshape(T + 1, model.ny)
+    N, nx = T + 1, model.nx
+    x = np.empty((N, nx))
+    fm = np.empty((N, nx)) if want_filter else None
+    fP = np.empty((N, nx, nx)) if want_filter else None
+    s = model._struct(T, t0, tf)
+    rc = _lib(long_double).ora_kf_rts(ctypes.byref(s), _ptr(y), _ptr(x), _ptr(fm), _ptr(fP))
+    if rc:
+        raise FloatingPointError(f"oracle kf_rts failed rc={rc}")
+    return (x, fm, fP) if want_filter else x
+
+
+def two_filter(model: LinearModel, y, T: int, t0: float, tf: float, long_double: bool = False):
+    """Two-filter MAP via the textbook backward information filter."""
+    y = _f64(y).reshape(T + 1, model.ny)
+    x = np.empty((T + 1, model.nx))
+    s = model._struct(T, t0, tf)
+    rc = _lib(long_double).ora_two_filter(ctypes.byref(s), _ptr(y), _ptr(x))
+    if rc:
+        raise FloatingPointError(f"oracle two_filter failed rc={rc}")
+    return x
+
+
+def batch(model: LinearModel, y, T: int, t0: float, tf: float, mode: int = 0):
+    """Batched linear MAP over independent trajectories (OpenMP); y [B, T+1, ny]."""
+    y = _f64(y)
+    B = y.shape[0]
+    x = np.empty((B, T + 1, model.nx))
+    s = model._struct(T, t0, tf)
+    rc = _lib().ora_batch(ctypes.byref(s), B, _ptr(y), _ptr(x), mode)
+    if rc:
+        raise FloatingPointError(f"oracle batch failed rc={rc}")
+    return x
+
+
+def ieks(kind: int, params, L, W, R, m0, P0, y, T: int, t0: float, tf: float, passes: int,
+         x_init=None):
+    """Iterated linearisation MAP (5 passes in P:625). kind 1 = CT, 2 = VdP.
+
+    Returns (x_map [T+1, nx], per-pass max |dx|)."""
+    L, W, R, m0, P0 = map(_f64, (L, W, R, m0, P0))
+    nx, nw, ny = L.shape[0], L.shape[1], R.shape[0]
+    y = _f64(y).reshape(T + 1, ny)
+    params = _f64(params if params is not None else [0.0])
+    xi = None if x_init is None else _f64(x_init)
+    x = np.empty((T + 1, nx))
+    delta = np.empty(max(passes, 1))
+    rc = _lib().ora_ieks(kind, _ptr(params), nx, ny, nw, T, t0, tf, _ptr(L), _ptr(W), _ptr(R),
+                         _ptr(m0), _ptr(P0), _ptr(y), passes, _ptr(xi), _ptr(x), _ptr(delta))
+    if rc:
+        raise FloatingPointError(f"oracle ieks failed rc={rc}")
+    return x, delta[:passes]
+
+
+def ct_f(x):
+    x, out = _f64(x), np.empty(5)
+    _lib().ora_ct_f(_ptr(x), _ptr(out))
+    return out
+
+
+def ct_dfdx(x):
+    x, out = _f64(x), np.empty((5, 5))
+    _lib().ora_ct_dfdx(_ptr(x), _ptr(out))
+    return out
+
+
+def ct_h(x):
+    x, out = _f64(x), np.empty(2)
+    _lib().ora_ct_h(_ptr(x), _ptr(out))
+    return out
+
+
+def ct_dhdx(x):
+    x, out = _f64(x), np.empty((2, 5))
+    _lib().ora_ct_dhdx(_ptr(x), _ptr(out))
+    return out
+
+
+def vdp_f(mu, x):
+    x, out = _f64(x), np.empty(2)
+    _lib().ora_vdp_f(mu, _ptr(x), _ptr(out))
+    return out
+
+
+def vdp_dfdx(mu, x):
+    x, out = _f64(x), np.empty((2, 2))
+    _lib().ora_vdp_dfdx(mu, _ptr(x), _ptr(out))
+    return out
+
+
+def num_threads() -> int:
+    return int(_lib().ora_num_threads())

@@ -1,0 +1,506 @@
+/*
+ * oracle/oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, sequential CPU reference for arXiv 2512.13319 ("Temporal
+ * parallelisation of continuous-time MAP trajectory estimation").  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load, call or link this file.  It shares no code, header,
+ * table or helper with the CUDA product path in paper_2512_13319_b200/.
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX; readings of the
+ * paper are listed in DESIGN.md ("R-" ids) and SURVEY.md section 8(c) ("G" ids).
+ *
+ * What it computes:
+ *   The linear-affine SDE of P:134-140 discretised on the grid t_i = t0 + i*dt,
+ *   i = 0..T, dt = (tf - t0)/T, one node per grid point:
+ *     x_{i-1} = (I - dt F_i) x_i - dt c_i + w_i,   w_i ~ N(0, dt Q_i), Q = L W L^T
+ *     y_i     = H_i x_i + r_i + nu_i,             nu_i ~ N(0, R_i / dt)
+ *     x_0     ~ N(m0, P0)
+ *   i.e. the forward transition x_i = Phi_i (x_{i-1} + dt c_i) + Phi_i w_i with
+ *   Phi_i = (I - dt F_i)^{-1}.  Its MAP trajectory (= posterior mean, the minimiser
+ *   of the discretised Onsager--Machlup / LQT objective P:63-97 for linear models)
+ *   is computed by the textbook sequential Kalman filter + RTS smoother, the
+ *   discrete counterpart of the Kalman--Bucy filter and continuous RTS smoother
+ *   of P:200-226.  The two-filter variant uses the textbook
+ *   backward information filter.  The nonlinear variant is the
+ *   iterated extended Kalman smoother (Gauss--Newton): re-linearise f, h about the
+ *   previous trajectory and re-run the linear smoother.
+ *
+ * All arithmetic in REAL (double by default; -DORA_LONG_DOUBLE builds the
+ * long-double self-check used by pin P10).  Inputs/outputs are double.
+ */
+#include <stdlib.h>
+#include <string.h>
+#include <tgmath.h>
+
+#ifdef ORA_LONG_DOUBLE
+typedef long double REAL;
+#else
+typedef double REAL;
+#endif
+
+#define MAXN 8
+
+typedef struct {
+  int nx, ny, nw;
+  long T;            /* grid steps; nodes 0..T */
+  double t0, tf;
+  const double *F, *c, *L, *W, *H, *r, *R; /* per-node arrays, row-major */
+  long sF, sc, sL, sW, sH, sr, sR;          /* element stride between nodes (0 = constant) */
+  const double *m0, *P0;
+} ora_model;
+
+/* ---------------- small dense helpers (row-major, n <= MAXN) ---------------- */
+
+static void mat_mul(int n, int k, int m, const REAL* A, const REAL* B, REAL* C) {
+  /* C(n x m) = A(n x k) B(k x m) */
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < m; ++j) {
+      REAL s = 0;
+      for (int l = 0; l < k; ++l) s += A[i * k + l] * B[l * m + j];
+      C[i * m + j] = s;
+    }
+}
+
+static void mat_mul_bt(int n, int k, int m, const REAL* A, const REAL* B, REAL* C) {
+  /* C(n x m) = A(n x k) B(m x k)^T */
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < m; ++j) {
+      REAL s = 0;
+      for (int l = 0; l < k; ++l) s += A[i * k + l] * B[j * k + l];
+      C[i * m + j] = s;
+    }
+}
+
+static void mat_vec(int n, int k, const REAL* A, const REAL* x, REAL* y) {
+  for (int i = 0; i < n; ++i) {
+    REAL s = 0;
+    for (int l = 0; l < k; ++l) s += A[i * k + l] * x[l];
+    y[i] = s;
+  }
+}
+
+static void symmetrize(int n, REAL* P) {
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      REAL a = (P[i * n + j] + P[j * n + i]) / 2;
+      P[i * n + j] = a;
+      P[j * n + i] = a;
+    }
+}
+
+/* Solve A X = B (A n x n, B n x m) by Gaussian elimination with partial
+ * pivoting; A and B are overwritten (X returned in B).  Returns 0 on success. */
+static int lu_solve(int n, int m, REAL* A, REAL* B) {
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    for (int i = k + 1; i < n; ++i)
+      if (fabs(A[i * n + k]) > fabs(A[p * n + k])) p = i;
+    if (A[p * n + k] == 0) return 1;
+    if (p != k) {
+      for (int j = 0; j < n; ++j) { REAL t = A[k * n + j]; A[k * n + j] = A[p * n + j]; A[p * n + j] = t; }
+      for (int j = 0; j < m; ++j) { REAL t = B[k * m + j]; B[k * m + j] = B[p * m + j]; B[p * m + j] = t; }
+    }
+    for (int i = k + 1; i < n; ++i) {
+      REAL f = A[i * n + k] / A[k * n + k];
+      for (int j = k; j < n; ++j) A[i * n + j] -= f * A[k * n + j];
+      for (int j = 0; j < m; ++j) B[i * m + j] -= f * B[k * m + j];
+    }
+  }
+  for (int k = n - 1; k >= 0; --k)
+    for (int j = 0; j < m; ++j) {
+      REAL s = B[k * m + j];
+      for (int l = k + 1; l < n; ++l) s -= A[k * n + l] * B[l * m + j];
+      B[k * m + j] = s / A[k * n + k];
+    }
+  return 0;
+}
+
+/* Solve S X = B for symmetric positive definite S via Cholesky; S, B overwritten.
+ * Returns 0 on success, 1 if S is not positive definite. */
+static int chol_solve(int n, int m, REAL* S, REAL* B) {
+  for (int j = 0; j < n; ++j) {
+    REAL d = S[j * n + j];
+    for (int k = 0; k < j; ++k) d -= S[j * n + k] * S[j * n + k];
+    if (!(d > 0)) return 1;
+    d = sqrt(d);
+    S[j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      REAL s = S[i * n + j];
+      for (int k = 0; k < j; ++k) s -= S[i * n + k] * S[j * n + k];
+      S[i * n + j] = s / d;
+    }
+  }
+  for (int c = 0; c < m; ++c) {
+    for (int i = 0; i < n; ++i) { /* L z = b */
+      REAL s = B[i * m + c];
+      for (int k = 0; k < i; ++k) s -= S[i * n + k] * B[k * m + c];
+      B[i * m + c] = s / S[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) { /* L^T x = z */
+      REAL s = B[i * m + c];
+      for (int k = i + 1; k < n; ++k) s -= S[k * n + i] * B[k * m + c];
+      B[i * m + c] = s / S[i * n + i];
+    }
+  }
+  return 0;
+}
+
+static void load(int cnt, const double* src, REAL* dst) {
+  for (int i = 0; i < cnt; ++i) dst[i] = (REAL)src[i];
+}
+
+/* Model quantities at node i (P:134-140 sampled at t_i). */
+typedef struct {
+  REAL F[MAXN * MAXN], c[MAXN], Q[MAXN * MAXN], H[MAXN * MAXN], r[MAXN], R[MAXN * MAXN];
+} node_model;
+
+static void model_at(const ora_model* m, long i, node_model* nm) {
+  int nx = m->nx, ny = m->ny, nw = m->nw;
+  REAL L[MAXN * MAXN], W[MAXN * MAXN], LW[MAXN * MAXN];
+  load(nx * nx, m->F + i * m->sF, nm->F);
+  if (m->c) load(nx, m->c + i * m->sc, nm->c); else memset(nm->c, 0, sizeof nm->c);
+  load(nx * nw, m->L + i * m->sL, L);
+  load(nw * nw, m->W + i * m->sW, W);
+  mat_mul(nx, nw, nw, L, W, LW);
+  mat_mul_bt(nx, nw, nx, LW, L, nm->Q); /* Q = L W L^T */
+  symmetrize(nx, nm->Q);
+  load(ny * nx, m->H + i * m->sH, nm->H);
+  if (m->r) load(ny, m->r + i * m->sr, nm->r); else memset(nm->r, 0, sizeof nm->r);
+  load(ny * ny, m->R + i * m->sR, nm->R);
+}
+
+/* Prediction to node i (i >= 1) from the filter moments (m, P) at node i-1:
+ *   Phi = (I - dt F_i)^{-1};  mp = Phi (m + dt c_i);  Pp = Phi (P + dt Q_i) Phi^T. */
+static int predict(int nx, REAL dt, const node_model* nm, const REAL* m, const REAL* P,
+                   REAL* Phi, REAL* mp, REAL* Pp) {
+  REAL A[MAXN * MAXN], t[MAXN], PQ[MAXN * MAXN], T1[MAXN * MAXN];
+  for (int a = 0; a < nx; ++a)
+    for (int b = 0; b < nx; ++b) {
+      A[a * nx + b] = (a == b ? 1 : 0) - dt * nm->F[a * nx + b];
+      Phi[a * nx + b] = (a == b ? 1 : 0);
+    }
+  if (lu_solve(nx, nx, A, Phi)) return 1;
+  for (int a = 0; a < nx; ++a) t[a] = m[a] + dt * nm->c[a];
+  mat_vec(nx, nx, Phi, t, mp);
+  for (int a = 0; a < nx * nx; ++a) PQ[a] = P[a] + dt * nm->Q[a];
+  mat_mul(nx, nx, nx, Phi, PQ, T1);
+  mat_mul_bt(nx, nx, nx, T1, Phi, Pp);
+  symmetrize(nx, Pp);
+  return 0;
+}
+
+/* Kalman update at node i with measurement y (noise covariance R_i/dt). */
+static int update(int nx, int ny, REAL dt, const node_model* nm, const double* y,
+                  const REAL* mp, const REAL* Pp, REAL* m, REAL* P) {
+  REAL HP[MAXN * MAXN], Sy[MAXN * MAXN], Kt[MAXN * MAXN], e[MAXN], Hm[MAXN];
+  mat_mul(ny, nx, nx, nm->H, Pp, HP);             /* H Pp */
+  mat_mul_bt(ny, nx, ny, HP, nm->H, Sy);          /* H Pp H^T */
+  for (int a = 0; a < ny * ny; ++a) Sy[a] += nm->R[a] / dt;
+  memcpy(Kt, HP, sizeof(REAL) * ny * nx);
+  if (chol_solve(ny, nx, Sy, Kt)) return 1;       /* Kt = Sy^{-1} H Pp = K^T */
+  mat_vec(ny, nx, nm->H, mp, Hm);
+  for (int a = 0; a < ny; ++a) e[a] = (REAL)y[a] - Hm[a] - nm->r[a];
+  for (int a = 0; a < nx; ++a) {
+    REAL s = mp[a];
+    for (int b = 0; b < ny; ++b) s += Kt[b * nx + a] * e[b];
+    m[a] = s;
+  }
+  /* P = Pp - K H Pp */
+  for (int a = 0; a < nx; ++a)
+    for (int b = 0; b < nx; ++b) {
+      REAL s = Pp[a * nx + b];
+      for (int l = 0; l < ny; ++l) s -= Kt[l * nx + a] * HP[l * nx + b];
+      P[a * nx + b] = s;
+    }
+  symmetrize(nx, P);
+  return 0;
+}
+
+/* Forward Kalman filter over nodes 0..T; stores m_i, P_i (full). */
+static int kf_forward(const ora_model* md, const double* y, REAL* ms, REAL* Ps) {
+  int nx = md->nx, ny = md->ny;
+  REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)md->T;
+  REAL mp[MAXN], Pp[MAXN * MAXN], Phi[MAXN * MAXN];
+  node_model nm;
+  for (long i = 0; i <= md->T; ++i) {
+    model_at(md, i, &nm);
+    if (i == 0) {
+      load(nx, md->m0, mp);
+      load(nx * nx, md->P0, Pp);
+    } else if (predict(nx, dt, &nm, ms + (i - 1) * nx, Ps + (i - 1) * nx * nx, Phi, mp, Pp)) {
+      return 1;
+    }
+    if (update(nx, ny, dt, &nm, y + i * ny, mp, Pp, ms + i * nx, Ps + i * nx * nx)) return 1;
+  }
+  return 0;
+}
+
+/* RTS smoother: x_T = m_T; x_i = m_i + G_i (x_{i+1} - mp_{i+1}),
+ * G_i = P_i Phi_{i+1}^T Pp_{i+1}^{-1}  (discrete counterpart of P:219-223). */
+static int rts_backward(const ora_model* md, const REAL* ms, const REAL* Ps, REAL* xs) {
+  int nx = md->nx;
+  REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)md->T;
+  REAL mp[MAXN], Pp[MAXN * MAXN], Phi[MAXN * MAXN], Gt[MAXN * MAXN], d[MAXN];
+  node_model nm;
+  long T = md->T;
+  memcpy(xs + T * nx, ms + T * nx, sizeof(REAL) * nx);
+  for (long i = T - 1; i >= 0; --i) {
+    model_at(md, i + 1, &nm);
+    if (predict(nx, dt, &nm, ms + i * nx, Ps + i * nx * nx, Phi, mp, Pp)) return 1;
+    mat_mul_bt(nx, nx, nx, Phi, Ps + i * nx * nx, Gt); /* Phi P_i (P_i symmetric) = (P_i Phi^T)^T */
+    if (chol_solve(nx, nx, Pp, Gt)) return 1;          /* Gt = Pp^{-1} Phi P_i = G^T */
+    for (int a = 0; a < nx; ++a) d[a] = xs[(i + 1) * nx + a] - mp[a];
+    for (int a = 0; a < nx; ++a) {
+      REAL s = ms[i * nx + a];
+      for (int b = 0; b < nx; ++b) s += Gt[b * nx + a] * d[b];
+      xs[i * nx + a] = s;
+    }
+  }
+  return 0;
+}
+
+static void store(long cnt, const REAL* src, double* dst) {
+  for (long i = 0; i < cnt; ++i) dst[i] = (double)src[i];
+}
+
+/* Linear MAP (RTS form).  y: [T+1][ny]; x_map: [T+1][nx]; filt_m: [T+1][nx] or
+ * NULL; filt_P: [T+1][nx][nx] or NULL.  Returns 0, or 1 on a numeric failure. */
+int ora_kf_rts(const ora_model* md, const double* y, double* x_map, double* filt_m, double* filt_P) {
+  long N = md->T + 1;
+  int nx = md->nx;
+  if (nx > MAXN || md->ny > MAXN || md->nw > MAXN || md->T < 1) return 2;
+  REAL* ms = malloc(sizeof(REAL) * N * nx);
+  REAL* Ps = malloc(sizeof(REAL) * N * nx * nx);
+  REAL* xs = malloc(sizeof(REAL) * N * nx);
+  int rc = (!ms || !Ps || !xs) ? 3 : kf_forward(md, y, ms, Ps);
+  if (!rc) rc = rts_backward(md, ms, Ps, xs);
+  if (!rc) {
+    store(N * nx, xs, x_map);
+    if (filt_m) store(N * nx, ms, filt_m);
+    if (filt_P) store(N * nx * nx, Ps, filt_P);
+  }
+  free(ms); free(Ps); free(xs);
+  return rc;
+}
+
+/* Two-filter MAP: forward filter (S_i = P_i^{-1}, v_i = S_i m_i)
+ * combined with the backward information filter (Lb_i, xb_i) = information on
+ * x_i from y_{i+1..T}:  x_i = (S_i + Lb_i)^{-1} (v_i + xb_i).
+ * Backward recursion (textbook information form): start Lb_T = 0, xb_T = 0;
+ * add measurement i:  Lu = Lb_i + dt H^T R^{-1} H,  xu = xb_i + dt H^T R^{-1} (y_i - r_i);
+ * predict through x_i = M x_{i-1} + d + e, M = Phi_i, d = Phi_i dt c_i,
+ * e ~ N(0, Sig), Sig = Phi_i dt Q_i Phi_i^T:
+ *   Lt = (I + Lu Sig)^{-1} Lu,  xt = (I + Lu Sig)^{-1} xu,
+ *   Lb_{i-1} = M^T Lt M,  xb_{i-1} = M^T (xt - Lt d). */
+int ora_two_filter(const ora_model* md, const double* y, double* x_map) {
+  long N = md->T + 1, T = md->T;
+  int nx = md->nx, ny = md->ny;
+  if (nx > MAXN || ny > MAXN || md->nw > MAXN || T < 1) return 2;
+  REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)T;
+  REAL* ms = malloc(sizeof(REAL) * N * nx);
+  REAL* Ps = malloc(sizeof(REAL) * N * nx * nx);
+  int rc = (!ms || !Ps) ? 3 : kf_forward(md, y, ms, Ps);
+  REAL Lb[MAXN * MAXN] = {0}, xb[MAXN] = {0};
+  node_model nm;
+  for (long i = T; i >= 0 && !rc; --i) {
+    /* combine */
+    REAL S[MAXN * MAXN], Sm[MAXN * MAXN], v[MAXN];
+    for (int a = 0; a < nx * nx; ++a) { S[a] = (a % (nx + 1) == 0) ? 1 : 0; Sm[a] = Ps[i * nx * nx + a]; }
+    if (chol_solve(nx, nx, Sm, S)) { rc = 1; break; } /* S = P_i^{-1} */
+    symmetrize(nx, S);
+    mat_vec(nx, nx, S, ms + i * nx, v);
+    REAL Ssum[MAXN * MAXN], rhs[MAXN];
+    for (int a = 0; a < nx * nx; ++a) Ssum[a] = S[a] + Lb[a];
+    for (int a = 0; a < nx; ++a) rhs[a] = v[a] + xb[a];
+    if (chol_solve(nx, 1, Ssum, rhs)) { rc = 1; break; }
+    store(nx, rhs, x_map + i * nx);
+    if (i == 0) break;
+    /* measurement i */
+    model_at(md, i, &nm);
+    REAL Rinv[MAXN * MAXN], Rm[MAXN * MAXN], HtRi[MAXN * MAXN], e[MAXN];
+    for (int a = 0; a < ny * ny; ++a) { Rinv[a] = (a % (ny + 1) == 0) ? 1 : 0; Rm[a] = nm.R[a]; }
+    if (chol_solve(ny, ny, Rm, Rinv)) { rc = 1; break; }
+    for (int a = 0; a < nx; ++a)
+      for (int b = 0; b < ny; ++b) {
+        REAL s = 0;
+        for (int l = 0; l < ny; ++l) s += nm.H[l * nx + a] * Rinv[l * ny + b];
+        HtRi[a * ny + b] = dt * s; /* dt H^T R^{-1} */
+      }
+    REAL Lu[MAXN * MAXN], xu[MAXN];
+    mat_mul(nx, ny, nx, HtRi, nm.H, Lu);
+    for (int a = 0; a < nx * nx; ++a) Lu[a] += Lb[a];
+    for (int a = 0; a < ny; ++a) e[a] = (REAL)y[i * ny + a] - nm.r[a];
+    mat_vec(nx, ny, HtRi, e, xu);
+    for (int a = 0; a < nx; ++a) xu[a] += xb[a];
+    /* predict through the transition into node i */
+    REAL A[MAXN * MAXN], M[MAXN * MAXN], d[MAXN], t[MAXN], Sig[MAXN * MAXN], T1[MAXN * MAXN];
+    for (int a = 0; a < nx; ++a)
+      for (int b = 0; b < nx; ++b) {
+        A[a * nx + b] = (a == b ? 1 : 0) - dt * nm.F[a * nx + b];
+        M[a * nx + b] = (a == b ? 1 : 0);
+      }
+    if (lu_solve(nx, nx, A, M)) { rc = 1; break; }
+    for (int a = 0; a < nx; ++a) t[a] = dt * nm.c[a];
+    mat_vec(nx, nx, M, t, d);
+    for (int a = 0; a < nx * nx; ++a) T1[a] = dt * nm.Q[a];
+    REAL T2[MAXN * MAXN];
+    mat_mul(nx, nx, nx, M, T1, T2);
+    mat_mul_bt(nx, nx, nx, T2, M, Sig);
+    REAL IL[MAXN * MAXN], RHS[MAXN * (MAXN + 1)];
+    mat_mul(nx, nx, nx, Lu, Sig, IL);
+    for (int a = 0; a < nx; ++a) IL[a * nx + a] += 1;
+    for (int a = 0; a < nx; ++a) {
+      for (int b = 0; b < nx; ++b) RHS[a * (nx + 1) + b] = Lu[a * nx + b];
+      RHS[a * (nx + 1) + nx] = xu[a];
+    }
+    if (lu_solve(nx, nx + 1, IL, RHS)) { rc = 1; break; }
+    REAL Lt[MAXN * MAXN], xt[MAXN], Ltd[MAXN], u[MAXN];
+    for (int a = 0; a < nx; ++a) {
+      for (int b = 0; b < nx; ++b) Lt[a * nx + b] = RHS[a * (nx + 1) + b];
+      xt[a] = RHS[a * (nx + 1) + nx];
+    }
+    symmetrize(nx, Lt);
+    mat_vec(nx, nx, Lt, d, Ltd);
+    for (int a = 0; a < nx; ++a) u[a] = xt[a] - Ltd[a];
+    REAL LtM[MAXN * MAXN];
+    mat_mul(nx, nx, nx, Lt, M, LtM);
+    for (int a = 0; a < nx; ++a) {
+      for (int b = 0; b < nx; ++b) {
+        REAL s = 0;
+        for (int l = 0; l < nx; ++l) s += M[l * nx + a] * LtM[l * nx + b];
+        Lb[a * nx + b] = s;
+      }
+      REAL s = 0;
+      for (int l = 0; l < nx; ++l) s += M[l * nx + a] * u[l];
+      xb[a] = s;
+    }
+    symmetrize(nx, Lb);
+  }
+  free(ms); free(Ps);
+  return rc;
+}
+
+/* ---------------- nonlinear models (P:588-623 and DESIGN.md R-VDP) ---------------- */
+
+/* Coordinated turn: x = (xi, zeta, xi_dot, zeta_dot, omega),
+ * f = (xi_dot, zeta_dot, -omega zeta_dot, omega xi_dot, 0),
+ * h = (sqrt(xi^2 + zeta^2), atan2(zeta, xi))  (G13: arctan(zeta/xi) read as atan2). */
+void ora_ct_f(const double* x, double* f) {
+  f[0] = x[2]; f[1] = x[3]; f[2] = -x[4] * x[3]; f[3] = x[4] * x[2]; f[4] = 0;
+}
+void ora_ct_dfdx(const double* x, double* J) {
+  for (int a = 0; a < 25; ++a) J[a] = 0;
+  J[0 * 5 + 2] = 1;
+  J[1 * 5 + 3] = 1;
+  J[2 * 5 + 3] = -x[4]; J[2 * 5 + 4] = -x[3];
+  J[3 * 5 + 2] = x[4];  J[3 * 5 + 4] = x[2];
+}
+void ora_ct_h(const double* x, double* h) {
+  h[0] = sqrt(x[0] * x[0] + x[1] * x[1]);
+  h[1] = atan2(x[1], x[0]);
+}
+void ora_ct_dhdx(const double* x, double* J) {
+  double r2 = x[0] * x[0] + x[1] * x[1], r = sqrt(r2);
+  for (int a = 0; a < 10; ++a) J[a] = 0;
+  J[0] = x[0] / r;   J[1] = x[1] / r;
+  J[5] = -x[1] / r2; J[6] = x[0] / r2;
+}
+/* Van der Pol (not in the paper; DESIGN.md R-VDP): x = (x1, x2),
+ * f = (x2, mu (1 - x1^2) x2 - x1), h = x1. */
+void ora_vdp_f(double mu, const double* x, double* f) {
+  f[0] = x[1]; f[1] = mu * (1 - x[0] * x[0]) * x[1] - x[0];
+}
+void ora_vdp_dfdx(double mu, const double* x, double* J) {
+  J[0] = 0; J[1] = 1;
+  J[2] = -2 * mu * x[0] * x[1] - 1; J[3] = mu * (1 - x[0] * x[0]);
+}
+
+static double wrap_pi(double a) { /* to (-pi, pi] */
+  const double PI = 3.14159265358979323846, TWO_PI = 6.28318530717958647692;
+  while (a > PI) a -= TWO_PI;
+  while (a <= -PI) a += TWO_PI;
+  return a;
+}
+
+/* Iterated linearisation (IEKS).  kind 1 = coordinated turn,
+ * kind 2 = Van der Pol (params[0] = mu).  Pass p linearises about xbar:
+ *   F_i = df(xbar_i), c_i = f(xbar_i) - F_i xbar_i, H_i = dh(xbar_i),
+ *   r_i = h(xbar_i) - H_i xbar_i,
+ * and replaces y_i by y_eff_i = r_i + H_i xbar_i + wrap(y_i - h(xbar_i)) (bearing
+ * residual wrapped, G13), then solves the linear MAP with ora_kf_rts.
+ * xbar^(0) = x_init, or m0 at every node when x_init is NULL (G18).
+ * delta[p] = max_i |x^(p) - x^(p-1)|_inf.  Returns 0 on success. */
+int ora_ieks(int kind, const double* params, int nx, int ny, int nw, long T, double t0, double tf,
+             const double* L, const double* W, const double* R, const double* m0, const double* P0,
+             const double* y, int passes, const double* x_init, double* x_map, double* delta) {
+  long N = T + 1;
+  if ((kind == 1 && (nx != 5 || ny != 2)) || (kind == 2 && (nx != 2 || ny != 1)) || kind < 1 || kind > 2)
+    return 2;
+  double *F = malloc(sizeof(double) * N * nx * nx), *c = malloc(sizeof(double) * N * nx);
+  double *H = malloc(sizeof(double) * N * ny * nx), *r = malloc(sizeof(double) * N * ny);
+  double *ye = malloc(sizeof(double) * N * ny), *xb = malloc(sizeof(double) * N * nx);
+  int rc = (!F || !c || !H || !r || !ye || !xb) ? 3 : 0;
+  for (long i = 0; i < N && !rc; ++i)
+    for (int a = 0; a < nx; ++a) xb[i * nx + a] = x_init ? x_init[i * nx + a] : m0[a];
+  for (int p = 0; p < passes && !rc; ++p) {
+    for (long i = 0; i < N; ++i) {
+      const double* xi = xb + i * nx;
+      double f[MAXN], h[MAXN];
+      double* Fi = F + i * nx * nx; double* Hi = H + i * ny * nx;
+      if (kind == 1) { ora_ct_f(xi, f); ora_ct_dfdx(xi, Fi); ora_ct_h(xi, h); ora_ct_dhdx(xi, Hi); }
+      else { ora_vdp_f(params[0], xi, f); ora_vdp_dfdx(params[0], xi, Fi); h[0] = xi[0]; Hi[0] = 1; Hi[1] = 0; }
+      for (int a = 0; a < nx; ++a) {
+        double s = f[a];
+        for (int b = 0; b < nx; ++b) s -= Fi[a * nx + b] * xi[b];
+        c[i * nx + a] = s;
+      }
+      for (int a = 0; a < ny; ++a) {
+        double hx = 0;
+        for (int b = 0; b < nx; ++b) hx += Hi[a * nx + b] * xi[b];
+        r[i * ny + a] = h[a] - hx;
+        double res = y[i * ny + a] - h[a];
+        if (kind == 1 && a == 1) res = wrap_pi(res);
+        ye[i * ny + a] = r[i * ny + a] + hx + res;
+      }
+    }
+    ora_model md = {nx, ny, nw, T, t0, tf, F, c, L, W, H, r, R,
+                    nx * nx, nx, 0, 0, ny * nx, ny, 0, m0, P0};
+    rc = ora_kf_rts(&md, ye, x_map, NULL, NULL);
+    if (rc) break;
+    double dmax = 0;
+    for (long i = 0; i < N * nx; ++i) {
+      double d = fabs(x_map[i] - xb[i]);
+      if (d > dmax) dmax = d;
+      xb[i] = x_map[i];
+    }
+    if (delta) delta[p] = dmax;
+  }
+  free(F); free(c); free(H); free(r); free(ye); free(xb);
+  return rc;
+}
+
+/* Batched linear MAP: `batch` independent trajectories sharing the model;
+ * y: [batch][T+1][ny], x_map: [batch][T+1][nx].  mode 0 = RTS, 1 = two-filter.
+ * OpenMP over trajectories (each recursion is sequential).  Returns the
+ * first non-zero per-trajectory status. */
+int ora_batch(const ora_model* md, long batch, const double* y, double* x_map, int mode) {
+  long N = md->T + 1;
+  int rc = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : rc)
+  for (long b = 0; b < batch; ++b) {
+    int r = mode ? ora_two_filter(md, y + b * N * md->ny, x_map + b * N * md->nx)
+                 : ora_kf_rts(md, y + b * N * md->ny, x_map + b * N * md->nx, NULL, NULL);
+    if (r > rc) rc = r;
+  }
+  return rc;
+}
+
+int ora_num_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
