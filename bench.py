@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py -- smoothed time steps/s of the parallel MAP scan (arXiv 2512.13319) on B200.
+
+Metric (BASELINE.json): smoothed time steps/s = batch * T / t_solve (fp64 parallel
+MAP scan), one "step" = one complete solve (pass 1 + pass 2 over all nodes) of the
+workload.  Default workload at N = 1: BASELINE config 3, the Wiener-velocity model
+of P:519-548 (nx = 4, ny = 2) at T = 1e7 grid steps, one trajectory.  With
+--gpus N > 1 (launched by torchrun) the same T = 1e7 problem is time-sharded over
+the ranks with an NCCL all-gather of chunk carries (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl pmap|reference]
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# FP64 (DFMA) peak derived from unit counts and clock: 148 SM x 64 FP64 FMA/clk x 2 flop x 1.965 GHz.
+FP64_PEAK_TFLOPS_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ----------------------------------------------------------- algorithmic counts
+def alg_counts(nx: int, ny: int, K: int = 32):
+    """Algorithmic FP64 flops (FMA = 2) and HBM bytes per node of each kernel class
+    (DESIGN.md "Roofline"): the operations the parallel method performs per node,
+    excluding this implementation's intra-tile scan overheads."""
+    N = nx
+    lu = sum((N - k - 1) + (N - k - 1) ** 2 for k in range(N))
+    solve = N * N
+    combine = N ** 3 + lu + 2 * N * solve + (N * N + solve) * 2 + N ** 3 + N * N + (N ** 3 + N * N * (N + 1) // 2) * 2 + N * N
+    vapply_tr = N ** 3 + lu + N * solve + (N * N + solve) * 2 + N ** 3 + N * N * (N + 1) // 2 + N * N
+    compose = N ** 3 + N * N
+    trans = N ** 3 + lu + 2 * N * N + solve
+    ns = N * (N + 1) // 2
+    esz = N * N + 2 * N + 2 * ns
+    vsz = ns + N
+    asz = N * N + N
+    d = 8
+    return {
+        "k_p1_reduce": (2 * combine, d * (ny + esz / K)),
+        "k_p1_down": (2 * (vapply_tr + compose), d * (ny + esz / K + vsz + asz / K)),
+        "k_p2_down": (2 * trans, d * (vsz + nx + asz / K)),
+        "solve": (2 * (combine + vapply_tr + compose + trans), d * (ny + 2 * vsz + nx)),
+    }
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 7]
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].strip() == "Active"})
+        load = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- workloads
+def build_inputs(config: str, rank: int, world: int):
+    import workloads as wl
+    spec, y, T, B = wl.make_workload(config, seed=0)
+    N = T + 1
+    a0, a1 = rank * N // world, (rank + 1) * N // world
+    if y.ndim == 2:
+        y = y[None]
+    return spec, np.ascontiguousarray(y[:, a0:a1]), T, B
+
+
+def make_plan(pm, spec, T, B, rank, world, comm):
+    import workloads as wl
+    if isinstance(spec, wl.LinearSpec):
+        return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H,
+                       r=spec.r, R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, rank=rank, world=world,
+                       nccl_comm=comm)
+    return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, L=spec.L, W=spec.W, R=spec.R, m0=spec.m0, P0=spec.P0,
+                   nl_kind=spec.kind, params=spec.params, batch=B, rank=rank, world=world, nccl_comm=comm)
+
+
+def solve_fn(plan, config):
+    from workloads.models import CONFIGS
+    method = CONFIGS[config]["method"]
+    if method == "rts":
+        return lambda y, x: plan.solve_linear(y, x)
+    if method == "two_filter":
+        return lambda y, x: plan.two_filter(y, x)
+    passes = CONFIGS[config].get("passes", 10)
+    return lambda y, x: plan.solve_nonlinear(y, passes=passes, x_map=x)
+
+
+def workload_name(config, T, B):
+    from workloads.models import CONFIGS
+    c = CONFIGS[config]
+    return f"{config}: {c['model']} {c['method']} T={T} batch={B}" + (f" passes={c['passes']}" if "passes" in c else "")
+
+
+# ---------------------------------------------------------------- CPU oracle
+def oracle_sample(config: str, budget_s: float = 12.0):
+    """Time the CPU oracle as it stands on a bounded sample of the workload."""
+    import oracle
+    import workloads as wl
+    from workloads.models import CONFIGS
+    c = CONFIGS[config]
+    if c["method"] == "ieks":
+        T = 20_000
+        s = wl.coordinated_turn()
+        _, y = wl.simulate_nonlinear(s, T, seed=0)
+        t = time.perf_counter()
+        oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=c["passes"])
+        dt = time.perf_counter() - t
+        return T / dt, 1, f"coordinated turn T={T}, {c['passes']} passes, 1 thread (full run is T={c['T']})"
+    spec = wl.wiener_velocity() if c["model"] == "wiener_velocity" else wl.ornstein_uhlenbeck()
+    md = oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0)
+    if c["method"] == "two_filter":
+        B, T = 64, c["T"]
+        _, y = wl.simulate_linear(spec, T, seed=0, batch=B)
+        t = time.perf_counter()
+        oracle.batch(md, y, T, spec.t0, spec.tf, mode=1)
+        dt = time.perf_counter() - t
+        return B * T / dt, oracle.num_threads(), f"{B} of {c['batch']} trajectories x T={T}, OpenMP"
+    T = min(c["T"], 2_000_000)
+    _, y = wl.simulate_linear(spec, T, seed=0)
+    t = time.perf_counter()
+    oracle.kf_rts(md, y, T, spec.t0, spec.tf)
+    dt = time.perf_counter() - t
+    return T / dt, 1, f"{c['model']} T={T} (of {c['T']}), sequential KF+RTS, 1 thread"
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle timed on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import workloads as wl
+    from workloads.models import CONFIGS
+    c = CONFIGS[args.config]
+    spec = wl.wiener_velocity() if c["model"] == "wiener_velocity" else wl.ornstein_uhlenbeck()
+    if c["method"] == "ieks":
+        spec = wl.coordinated_turn()
+        T = 5_000
+        _, y = wl.simulate_nonlinear(spec, T, seed=0)
+        step = lambda: oracle.ieks(1, None, spec.L, spec.W, spec.R, spec.m0, spec.P0, y, T, spec.t0, spec.tf,
+                                   passes=c["passes"])
+        units, cores, sample = T, 1, f"coordinated turn T={T} x {c['passes']} passes per step"
+    elif c["method"] == "two_filter":
+        B, T = 32, c["T"]
+        md = oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0)
+        _, y = wl.simulate_linear(spec, T, seed=0, batch=B)
+        step = lambda: oracle.batch(md, y, T, spec.t0, spec.tf, mode=1)
+        units, cores, sample = B * T, oracle.num_threads(), f"{B} trajectories x T={T} per step, OpenMP"
+    else:
+        T = min(c["T"], 300_000)
+        md = oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0)
+        _, y = wl.simulate_linear(spec, T, seed=0)
+        step = lambda: oracle.kf_rts(md, y, T, spec.t0, spec.tf)
+        units, cores, sample = T, 1, f"{c['model']} T={T} per step (of {c['T']}), sequential KF+RTS"
+    for _ in range(args.warmup):
+        step()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = (time.perf_counter() - t) / args.steps
+    v = units / el
+    out = {"metric": "smoothed time steps/s (fp64 parallel MAP scan)", "value": v, "unit": "steps/s",
+           "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (seeded Euler-Maruyama simulation of the paper's SDE)",
+           "config": {"workload": workload_name(args.config, c["T"], c["batch"]), "sample": sample},
+           "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="pmap", choices=["pmap", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+        be = dist.group.WORLD._get_backend(torch.device("cuda", local))
+        comm = be._comm_ptr()
+    import paper_2512_13319_b200 as pm
+
+    spec, y_host, T, B = build_inputs(args.config, rank, world)
+    plan = make_plan(pm, spec, T, B, rank, world, comm)
+    solve = solve_fn(plan, args.config)
+    dev = torch.device("cuda", local)
+    yd = torch.from_numpy(y_host).to(dev)
+    xd = torch.empty((B, plan.n_local, plan.nx), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        solve(yd, xd)
+    plan.sync()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        solve(yd, xd)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    plan.sync()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches_per_step = plan.launches
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = B * T / (ms * 1e-3)
+
+    # per-kernel CUDA-event timing on the launching stream (separate region)
+    plan.profile(True)
+    for _ in range(min(args.steps, 50)):
+        solve(yd, xd)
+    prof = plan.profile_read()
+    plan.profile(False)
+
+    # end to end through the C ABI with host (pinned) buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.from_numpy(y_host).pin_memory()
+        xh = torch.empty((B, plan.n_local, plan.nx), dtype=torch.float64).pin_memory()
+        solve(yh, xh)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            solve(yh, xh)
+        torch.cuda.synchronize()
+        el = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": B * T / float(el.item()), "unit": "steps/s",
+               "h2d_bytes_per_step": int(yh.numel() * 8 * world), "d2h_bytes_per_step": int(xh.numel() * 8 * world)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (FP64-ALU bound)
+    counts = alg_counts(plan.nx, plan.ny)
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dl) = dom
+    per_launch_ms = dms / dl
+    step_ms_prof = sum(v[0] for v in prof.values()) / max(1, min(args.steps, 50))
+    nodes_per_launch = B * plan.n_local
+    fl, by = counts.get(dname, counts["solve"])
+    achieved_tflops = fl * nodes_per_launch / (per_launch_ms * 1e-3) / 1e12
+    roofline = {"bound": "alu", "kernel": dname, "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
+                "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS_DERIVED, "traffic": None,
+                "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (MEASURED_PEAKS.json has no FP64; "
+                               "DFMA microbenchmark measured 34.2 TF/s, profiles/r01_fp64_peak_probe.log)",
+                "alg_flops_per_node": fl, "alg_bytes_per_node": by, "kernel_ms_per_launch": per_launch_ms,
+                "kernel_share_of_step": dms / max(1e-9, sum(v[0] for v in prof.values()))}
+    try:
+        peaks = json.load(open(PEAKS_PATH))
+        hbm = float(peaks["hbm_gbs"])
+        hbm_src = "measured"
+    except Exception:
+        hbm, hbm_src = FALLBACK_HBM_GBS, "fallback"
+    sfl, sby = counts["solve"]
+    solve_hbm = {"alg_bytes_per_node": sby, "achieved_gbs": sby * B * T / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                 "peak_source": hbm_src, "frac_of_hbm_roofline": sby * B * T / (ms * 1e-3) / 1e9 / hbm,
+                 "alg_tflops": sfl * B * T / (ms * 1e-3) / 1e12}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = oracle_sample(args.config)
+        cpu = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    out = {
+        "metric": "smoothed time steps/s (fp64 parallel MAP scan)",
+        "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Euler-Maruyama simulation of the paper's SDE, NumPy PCG64 seed 0)",
+        "config": {"workload": workload_name(args.config, T, B), "T": T, "batch": B, "nx": plan.nx, "ny": plan.ny,
+                   "parallelism": f"time-shard x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (y %.0f MB, workspace %.0f MB per GPU)" % (
+                       y_host.nbytes / 1e6, plan.workspace_bytes / 1e6)},
+        "roofline": roofline,
+        "solve_roofline": solve_hbm,
+        "kernels_ms_per_step": {k: v[0] / max(1, min(args.steps, 50)) for k, v in prof.items()},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/*
+ * pmap.h -- C ABI of the B200-native parallel continuous-time MAP trajectory
+ * estimator (arXiv 2512.13319, Razavi, Garcia-Fernandez, Saerkkae).
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source.  Readings of
+ * garbled or silent passages are listed in DESIGN.md ("R-*" ids).
+ *
+ * Problem: a partially observed SDE
+ *     dx/dt = f(x, t) + L(t) w(t),     y(t) = h(x, t) + nu(t),
+ * w, nu white with spectral densities W(t), R(t), x(t0) ~ N(m0, P0).  Its MAP
+ * trajectory minimises the Onsager--Machlup functional, solved as the
+ * time-reversed optimal-control / LQT problem by two parallel
+ * associative scans:
+ *   pass 1  backward (in tau = tf - t) scan of conditional value functions
+ *           (A, b, C, eta, J) with the combination rule of P:395-407
+ *           == the parallel Kalman--Bucy filter in information form;
+ *   pass 2  forward (in tau) scan of affine transition elements (Phi, beta)
+ *            == the parallel continuous-time RTS smoother.
+ * The two-filter variant and the iterated Taylor linearisation for
+ * nonlinear models run on the same engine.
+ *
+ * Discretisation (DESIGN.md R-ELEM): one element per grid node
+ * t_i = t0 + i dt, i = 0..T, dt = (tf - t0)/T:
+ *   E_0 = (0, 0, 0, P0^-1 m0 + dt H0^T R0^-1 (y0 - r0), P0^-1 + dt H0^T R0^-1 H0)
+ *   E_i = (I - dt F_i, -dt c_i, dt Q_i, dt H_i^T R_i^-1 (y_i - r_i), dt H_i^T R_i^-1 H_i)
+ * i.e. one explicit step of the element ODEs P:416-427 from the boundary
+ * (I, 0, 0, 0, 0) of P:427.  The result is the exact MAP of that discrete model.
+ *
+ * Conventions
+ *  - Array pointers passed to the solve calls may be DEVICE or HOST memory
+ *    (detected per call).  Host buffers are staged through plan-owned device
+ *    buffers with cudaMemcpyAsync on the plan's stream; the call then
+ *    synchronises the stream before returning.  Device buffers: the call is
+ *    asynchronous on the plan's stream.
+ *  - All matrices are row-major, fp64 on the host (model arrays); the y / x
+ *    buffers use the plan dtype (fp64 or fp32).
+ *  - Time layout: y is [batch][T+1][ny], x is [batch][T+1][nx] (node index =
+ *    grid index i, i.e. original time t_i; the time reversal of P:78 is realised
+ *    by the scan operator, nothing is reversed in memory, R-FLIP).
+ *  - Time sharding (world > 1, shard_mode 0): rank r owns the contiguous node
+ *    range [a_r, a_{r+1}), a_r = floor(r (T+1) / world); the y / x buffers of the
+ *    solve calls cover only the rank's own nodes.
+ *  - Ownership: the caller owns every buffer it passes and the NCCL
+ *    communicator; the plan owns its workspace (no allocation during solves).
+ *  - Errors: argument errors are returned synchronously; numeric failures
+ *    (non-finite values, singular pivots) are flagged on the device and reported
+ *    by map_sync() (or by the next blocking call) as MAP_E_NUMERIC with the first
+ *    offending node in map_last_error().  No exceptions cross the ABI.
+ *  - Thread safety: a plan is not thread-safe; distinct plans are independent.
+ */
+#ifndef PMAP_H
+#define PMAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MAP_OK = 0,
+  MAP_E_ARG = 1,         /* bad shape / stride / NULL / dt <= 0 / plan kind mismatch */
+  MAP_E_UNSUPPORTED = 2, /* (nx, ny) combination or mode not compiled */
+  MAP_E_CUDA = 3,        /* CUDA runtime error (message in map_last_error) */
+  MAP_E_NCCL = 4,        /* NCCL error or NCCL not loaded in the process */
+  MAP_E_NUMERIC = 5,     /* non-finite value / zero pivot; node in map_last_error */
+  MAP_E_DIVERGED = 6     /* iterated linearisation did not reach tol */
+} map_status;
+
+typedef enum { MAP_F64 = 0, MAP_F32 = 1 } map_dtype;
+
+typedef enum {
+  MAP_NL_COORD_TURN = 1, /* nx = 5, ny = 2 (range, bearing); params unused */
+  MAP_NL_VAN_DER_POL = 2 /* DESIGN.md R-VDP: nx = 2, ny = 1; params[0] = mu */
+} map_nl_kind;
+
+typedef struct map_plan_s* map_plan_t;
+
+typedef struct {
+  int32_t nx, ny, nw;  /* state, measurement, diffusion dims */
+  int32_t dtype;       /* map_dtype: compute precision and dtype of y / x buffers */
+  int64_t T;           /* GLOBAL number of grid steps; nodes 0..T (dt = (tf - t0)/T) */
+  int64_t batch;       /* independent trajectories sharing the model (>= 1) */
+  double t0, tf;       /* time span [t0, tf], tf > t0 */
+  int32_t rank, world; /* time shard index / count (world == 1: single GPU) */
+  int32_t reserved0;
+  int32_t reserved1;
+  void* nccl_comm;     /* ncclComm_t borrowed from the caller (e.g. torch's
+                          ProcessGroupNCCL._comm_ptr()); NULL when world == 1 */
+  void* stream;        /* cudaStream_t borrowed from the caller; NULL = legacy default */
+} map_plan_desc;
+
+/* Linear-affine model.  HOST pointers, row-major:
+ *   F nx*nx, c nx (nullable = 0), L nx*nw, W nw*nw, H ny*nx, r ny (nullable = 0),
+ *   R ny*ny (SPD), m0 nx, P0 nx*nx (SPD).
+ * s* = number of doubles between consecutive grid nodes (0 = constant in time,
+ * otherwise the array holds T+1 node samples).  Only Q = L W L^T >= 0 is
+ * required (DESIGN.md R-QPSD; the paper's invertibility assumption P:70 is not
+ * needed by the scan). */
+typedef struct {
+  const double *F, *c, *L, *W, *H, *r, *R, *m0, *P0;
+  int64_t sF, sc, sL, sW, sH, sr, sR;
+} map_linear_model;
+
+/* Nonlinear model with built-in drift / measurement functions.
+ * HOST pointers: L nx*nw, W nw*nw, R ny*ny, m0 nx, P0 nx*nx; params[nparams]. */
+typedef struct {
+  int32_t kind;     /* map_nl_kind */
+  int32_t nparams;
+  const double* params;
+  const double *L, *W, *R, *m0, *P0;
+} map_nl_model;
+
+/* Create a plan.  Exactly one of `lin` / `nl` is non-NULL; its dimensions must
+ * match desc->nx, ny, nw.  Allocates the plan workspace on the current device.
+ * MAP_E_ARG on inconsistent arguments, MAP_E_UNSUPPORTED when (nx, ny) has no
+ * compiled kernel (compiled: (1,1) (2,1) (2,2) (3,1) (3,2) (4,2) (5,2)). */
+map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin,
+                    const map_nl_model* nl, map_plan_t* out);
+
+/* Free the plan and its workspace (synchronises its stream).  NULL is a no-op. */
+void map_plan_destroy(map_plan_t plan);
+
+/* Linear MAP by the parallel RTS form: pass 1 (filter scan)
+ * + pass 2 (transition scan).  y [batch][T+1][ny] -> x_map [batch][T+1][nx].
+ * Optional outputs (nullable): filt_m [batch][T+1][nx] = S_i^-1 v_i and filt_P
+ * [batch][T+1][nx*(nx+1)/2] (upper triangle, row-major) = S_i^-1, the
+ * Kalman--Bucy filter mean / covariance.  Linear plans only. */
+map_status map_solve_linear(map_plan_t plan, const void* y, void* x_map, void* filt_m, void* filt_P);
+
+/* Linear MAP by the parallel two-filter form (information-form
+ * backward filter, DESIGN.md R-TF): the backward-information suffix scan runs
+ * concurrently with pass 1 and the per-node combine is fused into its epilogue.
+ * Linear plans only; single GPU (world == 1). */
+map_status map_two_filter(map_plan_t plan, const void* y, void* x_map);
+
+/* Nonlinear MAP by iterated Taylor linearisation (IEKS): each pass
+ * re-linearises f, h about the previous estimate on the device (F_i = df(xbar_i),
+ * c_i = f(xbar_i) - F_i xbar_i, H_i = dh(xbar_i), r_i = h(xbar_i) - H_i xbar_i;
+ * bearing residuals wrapped to (-pi, pi], R-WRAP) and runs the parallel RTS
+ * solve.  x_init [batch][T+1][nx] nullable -> xbar^(0) = m0 at every node (R-INIT).
+ * tol > 0: stop after the first pass whose max |x - xbar| < tol (checked on the
+ * device; one host read per pass); tol == 0: run exactly `passes` passes with no
+ * host synchronisation (captured as one CUDA graph).  passes_run (host, nullable)
+ * receives the number of passes executed.  Nonlinear plans only. */
+map_status map_solve_nonlinear(map_plan_t plan, const void* y, int32_t passes, double tol,
+                               const void* x_init, void* x_map, int32_t* passes_run);
+
+/* Wait for the plan's stream and surface device-side numeric flags. */
+map_status map_sync(map_plan_t plan);
+
+/* Last error message of the plan ("" if none); valid until the next call on it. */
+const char* map_last_error(map_plan_t plan);
+
+/* Static description of a status code. */
+const char* map_status_string(map_status s);
+
+/* Bytes of device workspace owned by the plan. */
+int64_t map_workspace_bytes(map_plan_t plan);
+
+/* Number of kernel launches issued by the most recent solve call on this plan. */
+int64_t map_last_launch_count(map_plan_t plan);
+
+/* Per-kernel CUDA-event timing of subsequent solve calls (enable != 0), for the
+ * roofline report: each kernel launch is bracketed by two events recorded on the
+ * stream it is launched on.  Disabling discards pending records. */
+map_status map_profile_enable(map_plan_t plan, int32_t enable);
+
+/* Synchronise and report the device time accumulated per kernel class since the
+ * last read: names[i] (static strings), ms[i] total milliseconds, launches[i]
+ * count, for at most nmax classes.  Returns the number of classes written, or -1
+ * on error.  Resets the accumulation. */
+int32_t map_profile_read(map_plan_t plan, const char** names, double* ms, int64_t* launches, int32_t nmax);
+
+/* Library version string. */
+const char* map_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMAP_H */

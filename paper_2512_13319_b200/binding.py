@@ -1,0 +1,274 @@
+"""ctypes binding of include/pmap.h (argument marshalling only; every step runs in libpmap.so).
+
+The functions ``map_plan``, ``map_solve_linear``, ``map_two_filter``,
+``map_solve_nonlinear``, ``map_sync``, ``map_last_error`` and
+``map_plan_destroy`` mirror the C entry points one to one.  ``Plan`` is a small
+convenience wrapper that accepts torch tensors (device or host) or NumPy arrays
+and borrows torch's current CUDA stream.  There is no CPU fallback: if the
+shared library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpmap.so")
+
+MAP_F64, MAP_F32 = 0, 1
+MAP_NL_COORD_TURN, MAP_NL_VAN_DER_POL = 1, 2
+STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 4: "MAP_E_NCCL",
+          5: "MAP_E_NUMERIC", 6: "MAP_E_DIVERGED"}
+
+# every symbol include/pmap.h declares
+EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter", "map_solve_nonlinear",
+           "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
+           "map_profile_enable", "map_profile_read", "map_version"]
+
+
+class MapError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nw", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("T", ctypes.c_int64), ("batch", ctypes.c_int64), ("t0", ctypes.c_double), ("tf", ctypes.c_double),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("reserved1", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class LinearModel(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("F", "c", "L", "W", "H", "r", "R", "m0", "P0")] + \
+               [(n, ctypes.c_int64) for n in ("sF", "sc", "sL", "sW", "sH", "sr", "sR")]
+
+
+class NlModel(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("nparams", ctypes.c_int32), ("params", ctypes.c_void_p),
+                ("L", ctypes.c_void_p), ("W", ctypes.c_void_p), ("R", ctypes.c_void_p), ("m0", ctypes.c_void_p),
+                ("P0", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libpmap.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2512_13319_b200.build`")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        lib.map_plan.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(LinearModel), ctypes.POINTER(NlModel),
+                                 ctypes.POINTER(P)]
+        lib.map_plan.restype = ctypes.c_int
+        lib.map_plan_destroy.argtypes = [P]
+        lib.map_plan_destroy.restype = None
+        lib.map_solve_linear.argtypes = [P, P, P, P, P]
+        lib.map_solve_linear.restype = ctypes.c_int
+        lib.map_two_filter.argtypes = [P, P, P]
+        lib.map_two_filter.restype = ctypes.c_int
+        lib.map_solve_nonlinear.argtypes = [P, P, I32, D, P, P, ctypes.POINTER(I32)]
+        lib.map_solve_nonlinear.restype = ctypes.c_int
+        lib.map_sync.argtypes = [P]
+        lib.map_sync.restype = ctypes.c_int
+        lib.map_last_error.argtypes = [P]
+        lib.map_last_error.restype = ctypes.c_char_p
+        lib.map_status_string.argtypes = [ctypes.c_int]
+        lib.map_status_string.restype = ctypes.c_char_p
+        lib.map_workspace_bytes.argtypes = [P]
+        lib.map_workspace_bytes.restype = I64
+        lib.map_last_launch_count.argtypes = [P]
+        lib.map_last_launch_count.restype = I64
+        lib.map_version.restype = ctypes.c_char_p
+        lib.map_profile_enable.argtypes = [P, I32]
+        lib.map_profile_enable.restype = ctypes.c_int
+        lib.map_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(D),
+                                         ctypes.POINTER(I64), I32]
+        lib.map_profile_read.restype = I32
+        _lib = lib
+    return _lib
+
+
+def _check(st: int, plan=None):
+    if st != 0:
+        msg = ""
+        if plan:
+            msg = load_library().map_last_error(plan).decode()
+        raise MapError(st, msg)
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous
+        return a.ctypes.data
+    return a.data_ptr()  # torch.Tensor (device or host)
+
+
+# ------------------------------------------------------------ raw C entry points
+def map_plan(desc: PlanDesc, lin: LinearModel | None = None, nl: NlModel | None = None) -> int:
+    lib = load_library()
+    h = ctypes.c_void_p()
+    st = lib.map_plan(ctypes.byref(desc), ctypes.byref(lin) if lin is not None else None,
+                      ctypes.byref(nl) if nl is not None else None, ctypes.byref(h))
+    _check(st)
+    return h.value
+
+
+def map_plan_destroy(plan: int) -> None:
+    load_library().map_plan_destroy(plan)
+
+
+def map_solve_linear(plan: int, y, x_map, filt_m=None, filt_P=None) -> None:
+    _check(load_library().map_solve_linear(plan, _ptr(y), _ptr(x_map), _ptr(filt_m), _ptr(filt_P)), plan)
+
+
+def map_two_filter(plan: int, y, x_map) -> None:
+    _check(load_library().map_two_filter(plan, _ptr(y), _ptr(x_map)), plan)
+
+
+def map_solve_nonlinear(plan: int, y, passes: int, tol: float, x_init, x_map) -> int:
+    run = ctypes.c_int32(0)
+    _check(load_library().map_solve_nonlinear(plan, _ptr(y), passes, tol, _ptr(x_init), _ptr(x_map),
+                                              ctypes.byref(run)), plan)
+    return run.value
+
+
+def map_sync(plan: int) -> None:
+    _check(load_library().map_sync(plan), plan)
+
+
+def map_last_error(plan: int) -> str:
+    return load_library().map_last_error(plan).decode()
+
+
+def map_version() -> str:
+    return load_library().map_version().decode()
+
+
+# ------------------------------------------------------------------ convenience
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Plan:
+    """A solver plan for one model, grid and batch size (wraps map_plan / map_plan_destroy).
+
+    linear model: pass F, L, W, H, R, m0, P0 (and optionally c, r); each array is
+    either constant or carries a leading node axis of length T+1 (time-varying).
+    nonlinear model: pass nl_kind (1 = coordinated turn, 2 = Van der Pol), L, W, R,
+    m0, P0 and params."""
+
+    def __init__(self, *, T: int, t0: float, tf: float, m0, P0, L, W, R, F=None, H=None, c=None, r=None,
+                 batch: int = 1, dtype: str = "f64", nl_kind: int | None = None, params=None,
+                 rank: int = 0, world: int = 1, nccl_comm: int | None = None, stream: int | None = None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2512_13319_b200 needs a CUDA device (no CPU fallback)")
+        self._keep = []
+        L, W, R, m0, P0 = map(_f64, (L, W, R, m0, P0))
+        nx, nw = L.shape[-2], L.shape[-1]
+        ny = R.shape[-1]
+        self.nx, self.ny, self.nw, self.T, self.batch = nx, ny, nw, T, batch
+        self.dtype = dtype
+        self.torch_dtype = torch.float64 if dtype == "f64" else torch.float32
+        d = PlanDesc()
+        d.nx, d.ny, d.nw, d.dtype = nx, ny, nw, MAP_F64 if dtype == "f64" else MAP_F32
+        d.T, d.batch, d.t0, d.tf = T, batch, t0, tf
+        d.rank, d.world = rank, world
+        d.nccl_comm = nccl_comm
+        self.stream = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        d.stream = self.stream
+        self.rank, self.world = rank, world
+        N = T + 1
+        self.n_local = (rank + 1) * N // world - rank * N // world
+        self.node0 = rank * N // world
+        lin = nl = None
+        if nl_kind is None:
+            lin = LinearModel()
+            arrs = dict(F=(F, 2), c=(c, 1), L=(L, 2), W=(W, 2), H=(H, 2), r=(r, 1), R=(R, 2))
+            for k, (a, nd) in arrs.items():
+                if a is None:
+                    setattr(lin, k, None)
+                    setattr(lin, "s" + k, 0)
+                    continue
+                a = _f64(a)
+                self._keep.append(a)
+                setattr(lin, k, a.ctypes.data)
+                setattr(lin, "s" + k, 0 if a.ndim == nd else int(np.prod(a.shape[1:])))
+            lin.m0, lin.P0 = m0.ctypes.data, P0.ctypes.data
+            self._keep += [m0, P0]
+        else:
+            nl = NlModel()
+            params = _f64(params if params is not None else [0.0])
+            self._keep += [params, L, W, R, m0, P0]
+            nl.kind, nl.nparams, nl.params = nl_kind, params.size, params.ctypes.data
+            nl.L, nl.W, nl.R, nl.m0, nl.P0 = (x.ctypes.data for x in (L, W, R, m0, P0))
+        self.handle = map_plan(d, lin, nl)
+        self.nonlinear = nl_kind is not None
+
+    def close(self):
+        if getattr(self, "handle", None):
+            map_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _out(self, like, *shape):
+        import torch
+        dev = like.device if hasattr(like, "device") else "cpu"
+        return torch.empty(shape, dtype=self.torch_dtype, device=dev)
+
+    def solve_linear(self, y, x_map=None, filt_m=None, filt_P=None):
+        """Parallel RTS MAP (pass 1 + pass 2).  y: [batch][n_local][ny] (torch, device or host)."""
+        if x_map is None:
+            x_map = self._out(y, self.batch, self.n_local, self.nx)
+        map_solve_linear(self.handle, y, x_map, filt_m, filt_P)
+        return x_map
+
+    def two_filter(self, y, x_map=None):
+        if x_map is None:
+            x_map = self._out(y, self.batch, self.n_local, self.nx)
+        map_two_filter(self.handle, y, x_map)
+        return x_map
+
+    def solve_nonlinear(self, y, passes: int = 10, tol: float = 0.0, x_init=None, x_map=None):
+        if x_map is None:
+            x_map = self._out(y, self.batch, self.n_local, self.nx)
+        run = map_solve_nonlinear(self.handle, y, passes, tol, x_init, x_map)
+        return x_map, run
+
+    def sync(self):
+        map_sync(self.handle)
+
+    def profile(self, enable: bool = True) -> None:
+        """Per-kernel CUDA-event timing of subsequent solves (map_profile_enable)."""
+        _check(load_library().map_profile_enable(self.handle, 1 if enable else 0), self.handle)
+
+    def profile_read(self) -> dict:
+        """{kernel class: (total ms, launches)} since the last read (map_profile_read)."""
+        n = 32
+        names = (ctypes.c_char_p * n)()
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        k = load_library().map_profile_read(self.handle, names, ms, cnt, n)
+        if k < 0:
+            raise MapError(3, map_last_error(self.handle))
+        return {names[i].decode(): (ms[i], cnt[i]) for i in range(k)}
+
+    @property
+    def launches(self) -> int:
+        return int(load_library().map_last_launch_count(self.handle))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(load_library().map_workspace_bytes(self.handle))

@@ -1,0 +1,575 @@
+// pmap_abi.cu -- C ABI (include/pmap.h) of the B200 parallel MAP library.
+//
+// Plan creation (model preprocessing, workspace), dispatch over the compiled
+// (nx, ny, model kind, dtype) instantiations, host<->device staging, launch
+// sequencing on the caller's stream, CUDA-graph capture of the nonlinear pass
+// loop, device numeric flags, and the time-sharded (multi-GPU) protocol with
+// NCCL all-gathers of chunk carries.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pmap.h"
+#include "pmap_kernels.cuh"
+#include "pmap_tf.cuh"
+
+#include "pmap_runner.cuh"
+
+using namespace pmap;
+using namespace pmap_rt;
+
+namespace {
+
+// ------------------------------------------------------------- dispatch
+template <typename R>
+static Runner* dispatch_lti(int nx, int ny, const double* A, const double* b, const double* C, const double* J,
+                            const double* K, const double* h0, const double* J0, const double* h00,
+                            const double* Am, const double* bm, const double* Cm) {
+#define PM_CASE(NXV, NYV) \
+  if (nx == NXV && ny == NYV) return make_lti<R, NXV, NYV>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm);
+  PM_SHAPES(PM_CASE)
+#undef PM_CASE
+  return nullptr;
+}
+
+template <typename R>
+static Runner* dispatch_tv(int nx, int ny, const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r,
+                           const R* Rm, const int64_t* str, int nw, double dt, const double* P0i,
+                           const double* P0im0) {
+#define PM_CASE(NXV, NYV) \
+  if (nx == NXV && ny == NYV) return make_tv<R, NXV, NYV>(F, c, L, Wm, H, r, Rm, str, nw, dt, P0i, P0im0);
+  PM_SHAPES(PM_CASE)
+#undef PM_CASE
+  return nullptr;
+}
+
+template <typename R>
+static Runner* dispatch_nl(int kind, double dt, double mu, const double* C, const double* Ri, const double* P0i,
+                           const double* P0im0) {
+  if (kind == MAP_NL_COORD_TURN) return make_nl<R, 5, 2, 1>(dt, mu, C, Ri, P0i, P0im0);
+  if (kind == MAP_NL_VAN_DER_POL) return make_nl<R, 2, 1, 2>(dt, mu, C, Ri, P0i, P0im0);
+  return nullptr;
+}
+
+static bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static map_status check_flag(PlanState& p) {
+  unsigned long long f = ULLONG_MAX;
+  cudaError_t e = cudaMemcpyAsync(&f, p.dflag, sizeof f, cudaMemcpyDeviceToHost, p.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p.stream);
+  if (e != cudaSuccess) return cuda_fail(p, e, "map_sync");
+  if (f != ULLONG_MAX) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "numeric failure (non-finite value or zero pivot) at or after node %llu", f);
+    p.err = buf;
+    const unsigned long long reset = ULLONG_MAX;
+    cudaMemcpyAsync(p.dflag, &reset, sizeof reset, cudaMemcpyHostToDevice, p.stream);
+    cudaStreamSynchronize(p.stream);
+    return MAP_E_NUMERIC;
+  }
+  return MAP_OK;
+}
+
+static map_status ensure_stage(PlanState& p, void** buf, size_t* have, size_t need) {
+  if (*have >= need) return MAP_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *have = 0;
+  PM_CK(p, cudaMalloc(buf, need));
+  *have = need;
+  return MAP_OK;
+}
+
+}  // namespace
+
+struct map_plan_s : PlanState {};
+
+extern "C" {
+
+const char* map_version(void) { return "pmap 0.1 (sm_100a)"; }
+
+const char* map_status_string(map_status s) {
+  switch (s) {
+    case MAP_OK: return "ok";
+    case MAP_E_ARG: return "invalid argument";
+    case MAP_E_UNSUPPORTED: return "unsupported configuration";
+    case MAP_E_CUDA: return "CUDA error";
+    case MAP_E_NCCL: return "NCCL error";
+    case MAP_E_NUMERIC: return "numeric failure";
+    case MAP_E_DIVERGED: return "iteration did not converge";
+  }
+  return "unknown status";
+}
+
+map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, const map_nl_model* nl,
+                    map_plan_t* out) {
+  if (!desc || !out || (!lin) == (!nl)) return MAP_E_ARG;
+  *out = nullptr;
+  const map_plan_desc& d = *desc;
+  if (d.nx < 1 || d.ny < 1 || d.nw < 1 || d.nw > d.nx || d.T < 1 || d.batch < 1 || !(d.tf > d.t0) ||
+      (d.dtype != MAP_F64 && d.dtype != MAP_F32) || d.world < 1 || d.rank < 0 || d.rank >= d.world)
+    return MAP_E_ARG;
+  if (d.world > 1 && !d.nccl_comm) return MAP_E_ARG;
+  std::unique_ptr<map_plan_s> p(new map_plan_s());
+  p->d = d;
+  p->stream = static_cast<cudaStream_t>(d.stream);
+  const int nx = d.nx, ny = d.ny, nw = d.nw;
+  const int NS = nx * (nx + 1) / 2;
+  const double dt = (d.tf - d.t0) / (double)d.T;
+  const bool f32 = d.dtype == MAP_F32;
+  // time shard geometry
+  const int64_t Ntot = d.T + 1;
+  const int64_t a0 = (int64_t)((__int128)d.rank * Ntot / d.world);
+  const int64_t a1 = (int64_t)((__int128)(d.rank + 1) * Ntot / d.world);
+  Geom& g = p->g;
+  g.Nn = a1 - a0;
+  g.node0 = a0;
+  g.batch = d.batch;
+  const int64_t L = (int64_t)kNT * kK;
+  g.tpt = (g.Nn + L - 1) / L;
+  g.gpt = (g.tpt + NT2 - 1) / NT2;
+  if (g.Nn < 1) return MAP_E_ARG;
+
+  auto sym_pack = [&](const double* M, double* P) {
+    for (int i = 0, k = 0; i < nx; ++i)
+      for (int j = i; j < nx; ++j, ++k) P[k] = 0.5 * (M[i * nx + j] + M[j * nx + i]);
+  };
+  const double* m0 = lin ? lin->m0 : nl->m0;
+  const double* P0 = lin ? lin->P0 : nl->P0;
+  if (!m0 || !P0 || !h_is_finite(m0, nx) || !h_is_finite(P0, nx * nx)) return MAP_E_ARG;
+  std::vector<double> P0i(nx * nx), P0ip(NS), P0im0(nx, 0.0);
+  if (!h_inv(nx, P0, P0i.data())) return MAP_E_ARG;
+  sym_pack(P0i.data(), P0ip.data());
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < nx; ++j) P0im0[i] += P0i[i * nx + j] * m0[j];
+  p->m0_host = new double[nx];
+  memcpy(p->m0_host, m0, sizeof(double) * nx);
+
+  Runner* rn = nullptr;
+  if (lin) {
+    if (!lin->F || !lin->L || !lin->W || !lin->H || !lin->R) return MAP_E_ARG;
+    const bool tv = lin->sF || lin->sc || lin->sL || lin->sW || lin->sH || lin->sr || lin->sR;
+    if (!tv) {
+      p->kind = Kind::LTI;
+      std::vector<double> A(nx * nx), b(nx, 0.0), Q(nx * nx, 0.0), Cp(NS), Ri(ny * ny), K(nx * ny, 0.0),
+          Jf(nx * nx, 0.0), Jp(NS), h0(nx, 0.0), J0(NS), h00(nx);
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j) A[i * nx + j] = (i == j ? 1.0 : 0.0) - dt * lin->F[i * nx + j];
+      for (int i = 0; i < nx; ++i) b[i] = lin->c ? -dt * lin->c[i] : 0.0;
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j)
+          for (int a = 0; a < nw; ++a)
+            for (int c = 0; c < nw; ++c) Q[i * nx + j] += lin->L[i * nw + a] * lin->W[a * nw + c] * lin->L[j * nw + c];
+      for (int i = 0; i < nx * nx; ++i) Q[i] *= dt;
+      sym_pack(Q.data(), Cp.data());
+      if (!h_inv(ny, lin->R, Ri.data())) return MAP_E_ARG;
+      for (int i = 0; i < nx; ++i)
+        for (int k = 0; k < ny; ++k)
+          for (int a = 0; a < ny; ++a) K[i * ny + k] += dt * lin->H[a * nx + i] * Ri[a * ny + k];
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j)
+          for (int k = 0; k < ny; ++k) Jf[i * nx + j] += K[i * ny + k] * lin->H[k * nx + j];
+      sym_pack(Jf.data(), Jp.data());
+      for (int i = 0; i < nx; ++i)
+        for (int k = 0; k < ny; ++k) h0[i] -= K[i * ny + k] * (lin->r ? lin->r[k] : 0.0);
+      for (int k = 0; k < NS; ++k) J0[k] = P0ip[k] + Jp[k];
+      for (int i = 0; i < nx; ++i) h00[i] = P0im0[i] + h0[i];
+      // mirrored transition (R-TF): Am = A^-1, bm = -Am b, Cm = Am (dt Q) Am^T
+      std::vector<double> Am(nx * nx), bm(nx, 0.0), T1(nx * nx, 0.0), Cmf(nx * nx, 0.0), Cmp(NS);
+      if (!h_inv(nx, A.data(), Am.data())) return MAP_E_ARG;
+      for (int i = 0; i < nx; ++i)
+        for (int k = 0; k < nx; ++k) bm[i] -= Am[i * nx + k] * b[k];
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j)
+          for (int k = 0; k < nx; ++k) T1[i * nx + j] += Am[i * nx + k] * Q[k * nx + j];
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j)
+          for (int k = 0; k < nx; ++k) Cmf[i * nx + j] += T1[i * nx + k] * Am[j * nx + k];
+      sym_pack(Cmf.data(), Cmp.data());
+      rn = f32 ? dispatch_lti<float>(nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
+                                     J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data())
+               : dispatch_lti<double>(nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
+                                      J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data());
+    } else {
+      p->kind = Kind::TV;
+      // copy node arrays (global node indexing) to the device in the plan dtype
+      const int64_t cnt[7] = {(int64_t)nx * nx, nx, (int64_t)nx * nw, (int64_t)nw * nw, (int64_t)ny * nx, ny,
+                              (int64_t)ny * ny};
+      const double* src[7] = {lin->F, lin->c, lin->L, lin->W, lin->H, lin->r, lin->R};
+      const int64_t str[7] = {lin->sF, lin->sc, lin->sL, lin->sW, lin->sH, lin->sr, lin->sR};
+      size_t total = 0;
+      int64_t len[7];
+      for (int k = 0; k < 7; ++k) {
+        if (str[k] && str[k] != cnt[k]) return MAP_E_ARG;
+        len[k] = src[k] ? (str[k] ? (d.T + 1) * cnt[k] : cnt[k]) : 0;
+        total += len[k];
+      }
+      const size_t es = f32 ? 4 : 8;
+      if (cudaMalloc(&p->dev_tv, total * es + 64) != cudaSuccess) return MAP_E_CUDA;
+      size_t off = 0;
+      const void* dptr[7];
+      for (int k = 0; k < 7; ++k) {
+        if (!src[k]) { dptr[k] = nullptr; continue; }
+        char* dst = static_cast<char*>(p->dev_tv) + off * es;
+        if (f32) {
+          std::vector<float> tmp(src[k], src[k] + len[k]);
+          cudaMemcpy(dst, tmp.data(), len[k] * 4, cudaMemcpyHostToDevice);
+        } else {
+          cudaMemcpy(dst, src[k], len[k] * 8, cudaMemcpyHostToDevice);
+        }
+        dptr[k] = dst;
+        off += len[k];
+      }
+      if (f32)
+        rn = dispatch_tv<float>(nx, ny, (const float*)dptr[0], (const float*)dptr[1], (const float*)dptr[2],
+                                (const float*)dptr[3], (const float*)dptr[4], (const float*)dptr[5],
+                                (const float*)dptr[6], str, nw, dt, P0ip.data(), P0im0.data());
+      else
+        rn = dispatch_tv<double>(nx, ny, (const double*)dptr[0], (const double*)dptr[1], (const double*)dptr[2],
+                                 (const double*)dptr[3], (const double*)dptr[4], (const double*)dptr[5],
+                                 (const double*)dptr[6], str, nw, dt, P0ip.data(), P0im0.data());
+    }
+  } else {
+    p->kind = Kind::NL;
+    p->nl_kind = nl->kind;
+    if (!nl->L || !nl->W || !nl->R) return MAP_E_ARG;
+    if (nl->kind == MAP_NL_COORD_TURN && (nx != 5 || ny != 2)) return MAP_E_ARG;
+    if (nl->kind == MAP_NL_VAN_DER_POL && (nx != 2 || ny != 1 || nl->nparams < 1 || !nl->params)) return MAP_E_ARG;
+    std::vector<double> Q(nx * nx, 0.0), Cp(NS), Ri(ny * ny);
+    for (int i = 0; i < nx; ++i)
+      for (int j = 0; j < nx; ++j)
+        for (int a = 0; a < nw; ++a)
+          for (int c = 0; c < nw; ++c) Q[i * nx + j] += nl->L[i * nw + a] * nl->W[a * nw + c] * nl->L[j * nw + c];
+    for (int i = 0; i < nx * nx; ++i) Q[i] *= dt;
+    sym_pack(Q.data(), Cp.data());
+    if (!h_inv(ny, nl->R, Ri.data())) return MAP_E_ARG;
+    const double mu = (nl->nparams >= 1 && nl->params) ? nl->params[0] : 0.0;
+    rn = f32 ? dispatch_nl<float>(nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data())
+             : dispatch_nl<double>(nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data());
+  }
+  if (!rn) return MAP_E_UNSUPPORTED;
+  p->runner.reset(rn);
+  p->elem_real = rn->sizeof_real();
+  rn->set_attrs();
+  // workspace
+  p->ws_tf = (p->kind != Kind::NL) && d.world == 1;
+  p->ws_bytes = rn->ws_bytes(g, p->ws_tf);
+  if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    p->err = "workspace allocation failed";
+    return MAP_E_CUDA;
+  }
+  if (cudaMalloc(&p->dflag, 2 * sizeof(unsigned long long)) != cudaSuccess) return MAP_E_CUDA;
+  const unsigned long long init[2] = {ULLONG_MAX, 0ull};
+  cudaMemcpy(p->dflag, init, sizeof init, cudaMemcpyHostToDevice);
+  if (p->kind == Kind::NL) {
+    const size_t xb = (size_t)g.batch * g.Nn * nx * p->elem_real;
+    if (cudaMalloc(&p->xbuf[0], xb) != cudaSuccess || cudaMalloc(&p->xbuf[1], xb) != cudaSuccess) return MAP_E_CUDA;
+    if (cudaMalloc(&p->m0_dev, nx * p->elem_real) != cudaSuccess) return MAP_E_CUDA;
+    if (f32) {
+      std::vector<float> t(m0, m0 + nx);
+      cudaMemcpy(p->m0_dev, t.data(), nx * 4, cudaMemcpyHostToDevice);
+    } else {
+      cudaMemcpy(p->m0_dev, m0, nx * 8, cudaMemcpyHostToDevice);
+    }
+  }
+  if (cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return MAP_E_CUDA;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    p->err = cudaGetErrorString(e);
+    return MAP_E_CUDA;
+  }
+  *out = p.release();
+  return MAP_OK;
+}
+
+void map_plan_destroy(map_plan_t p) {
+  if (!p) return;
+  cudaStreamSynchronize(p->stream);
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  cudaFree(p->ws);
+  cudaFree(p->dflag);
+  cudaFree(p->xbuf[0]);
+  cudaFree(p->xbuf[1]);
+  cudaFree(p->stage_y);
+  cudaFree(p->stage_x);
+  cudaFree(p->stage_aux);
+  cudaFree(p->dev_tv);
+  cudaFree(p->m0_dev);
+  if (p->stream2) cudaStreamDestroy(p->stream2);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  delete[] p->m0_host;
+  delete p;
+}
+
+// Resolve y (input) and x (output) to device buffers, staging host memory.
+struct IoGuard {
+  PlanState& p;
+  const void* y_host = nullptr;
+  void* x_host = nullptr;
+  size_t ybytes = 0, xbytes = 0;
+  bool blocking = false;
+  explicit IoGuard(PlanState& pp) : p(pp) {}
+};
+
+static map_status stage_in(PlanState& p, const void* y, size_t ybytes, const void** ydev, bool* blocking) {
+  if (is_device_ptr(y)) {
+    *ydev = y;
+    return MAP_OK;
+  }
+  *blocking = true;
+  map_status st = ensure_stage(p, &p.stage_y, &p.stage_y_bytes, ybytes);
+  if (st) return st;
+  PM_CK(p, cudaMemcpyAsync(p.stage_y, y, ybytes, cudaMemcpyHostToDevice, p.stream));
+  *ydev = p.stage_y;
+  return MAP_OK;
+}
+
+static map_status stage_out_buf(PlanState& p, void* x, size_t xbytes, void** buf, size_t* have, void** xdev,
+                                bool* blocking) {
+  if (!x) {
+    *xdev = nullptr;
+    return MAP_OK;
+  }
+  if (is_device_ptr(x)) {
+    *xdev = x;
+    return MAP_OK;
+  }
+  *blocking = true;
+  map_status st = ensure_stage(p, buf, have, xbytes);
+  if (st) return st;
+  *xdev = *buf;
+  return MAP_OK;
+}
+
+static map_status finish(PlanState& p, bool blocking, const std::vector<std::pair<void*, std::pair<void*, size_t>>>& outs) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(p, e, "kernel launch");
+  if (!p.err.empty() && p.err.rfind("nccl", 0) == 0) return MAP_E_NCCL;
+  if (p.err.rfind("ncclAllGather", 0) == 0) return MAP_E_NCCL;
+  for (auto& o : outs)
+    if (o.first != o.second.first) PM_CK(p, cudaMemcpyAsync(o.first, o.second.first, o.second.second,
+                                                           cudaMemcpyDeviceToHost, p.stream));
+  if (blocking) return check_flag(p);
+  return MAP_OK;
+}
+
+map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt_m, void* filt_P) {
+  if (!p || !y || !x_map) return MAP_E_ARG;
+  if (p->kind == Kind::NL) {
+    p->err = "map_solve_linear called on a nonlinear plan";
+    return MAP_E_ARG;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const int nx = p->d.nx, ny = p->d.ny;
+  const size_t yb = (size_t)g.batch * g.Nn * ny * es, xb = (size_t)g.batch * g.Nn * nx * es;
+  const size_t mb = xb, Pb = (size_t)g.batch * g.Nn * (nx * (nx + 1) / 2) * es;
+  bool blocking = false;
+  const void* yd;
+  void *xd, *md, *Pd;
+  map_status st = stage_in(*p, y, yb, &yd, &blocking);
+  if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (!st && (filt_m || filt_P)) {
+    // staging for optional outputs shares one aux buffer: [m | P]
+    const bool mh = filt_m && !is_device_ptr(filt_m), Ph = filt_P && !is_device_ptr(filt_P);
+    if (mh || Ph) {
+      st = ensure_stage(*p, &p->stage_aux, &p->stage_aux_bytes, mb + Pb);
+      blocking = true;
+    }
+    md = filt_m ? (mh ? p->stage_aux : filt_m) : nullptr;
+    Pd = filt_P ? (Ph ? static_cast<char*>(p->stage_aux) + mb : filt_P) : nullptr;
+  } else {
+    md = Pd = nullptr;
+  }
+  if (st) return st;
+  p->runner->rts(*p, yd, nullptr, xd, md, Pd);
+  std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
+  outs.push_back({x_map, {xd, xb}});
+  if (filt_m) outs.push_back({filt_m, {md, mb}});
+  if (filt_P) outs.push_back({filt_P, {Pd, Pb}});
+  return finish(*p, blocking, outs);
+}
+
+map_status map_two_filter(map_plan_t p, const void* y, void* x_map) {
+  if (!p || !y || !x_map) return MAP_E_ARG;
+  if (p->kind == Kind::NL || p->d.world != 1) {
+    p->err = "map_two_filter needs a linear single-GPU plan";
+    return MAP_E_ARG;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  bool blocking = false;
+  const void* yd;
+  void* xd;
+  map_status st = stage_in(*p, y, yb, &yd, &blocking);
+  if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (st) return st;
+  p->runner->two_filter(*p, yd, xd);
+  return finish(*p, blocking, {{x_map, {xd, xb}}});
+}
+
+map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, double tol, const void* x_init,
+                               void* x_map, int32_t* passes_run) {
+  if (!p || !y || !x_map || passes < 1 || tol < 0) return MAP_E_ARG;
+  if (p->kind != Kind::NL) {
+    p->err = "map_solve_nonlinear called on a linear plan";
+    return MAP_E_ARG;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  bool blocking = false;
+  const void* yd;
+  void* xd;
+  map_status st = stage_in(*p, y, yb, &yd, &blocking);
+  if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (st) return st;
+  // xbar^(0)
+  if (x_init) {
+    if (is_device_ptr(x_init))
+      PM_CK(*p, cudaMemcpyAsync(p->xbuf[0], x_init, xb, cudaMemcpyDeviceToDevice, p->stream));
+    else
+      PM_CK(*p, cudaMemcpyAsync(p->xbuf[0], x_init, xb, cudaMemcpyHostToDevice, p->stream));
+  } else {
+    p->runner->fill_m0(*p, p->xbuf[0]);
+  }
+  int run = 0;
+  if (tol == 0.0) {
+    // fixed number of passes, no host synchronisation: one CUDA graph
+    const void* key[4] = {yd, xd, (const void*)(intptr_t)passes, nullptr};
+    const bool capture = p->d.world == 1;
+    if (capture && !(p->graph && memcmp(key, p->graph_key, sizeof key) == 0)) {
+      if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+      }
+      cudaStream_t cs;
+      PM_CK(*p, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaStream_t saved = p->stream;
+      const bool saved_prof = p->prof;
+      p->prof = false;
+      p->stream = cs;
+      int64_t l0 = p->launches;
+      cudaGraph_t graph;
+      PM_CK(*p, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      for (int k = 0; k < passes; ++k) {
+        void* out = (k == passes - 1) ? xd : p->xbuf[(k + 1) & 1];
+        p->runner->rts(*p, yd, p->xbuf[k & 1], out, nullptr, nullptr);
+      }
+      cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+      p->stream = saved;
+      p->prof = saved_prof;
+      cudaStreamDestroy(cs);
+      if (ce != cudaSuccess) return cuda_fail(*p, ce, "graph capture");
+      PM_CK(*p, cudaGraphInstantiate(&p->graph, graph, 0));
+      cudaGraphDestroy(graph);
+      memcpy(p->graph_key, key, sizeof key);
+      p->graph_launches = p->launches - l0;
+      p->launches = l0;
+    }
+    if (capture) {
+      PM_CK(*p, cudaGraphLaunch(p->graph, p->stream));
+      p->launches += p->graph_launches;
+    } else {
+      for (int k = 0; k < passes; ++k) {
+        void* out = (k == passes - 1) ? xd : p->xbuf[(k + 1) & 1];
+        p->runner->rts(*p, yd, p->xbuf[k & 1], out, nullptr, nullptr);
+      }
+    }
+    run = passes;
+  } else {
+    for (int k = 0; k < passes; ++k) {
+      void* in = p->xbuf[k & 1];
+      void* out = p->xbuf[(k + 1) & 1];
+      p->runner->rts(*p, yd, in, out, nullptr, nullptr);
+      PM_CK(*p, cudaMemsetAsync(p->dflag + 1, 0, sizeof(unsigned long long), p->stream));
+      p->runner->maxdiff(*p, in, out, p->dflag + 1);
+      unsigned long long bits = 0;
+      PM_CK(*p, cudaMemcpyAsync(&bits, p->dflag + 1, sizeof bits, cudaMemcpyDeviceToHost, p->stream));
+      PM_CK(*p, cudaStreamSynchronize(p->stream));
+      double dmax;
+      memcpy(&dmax, &bits, sizeof dmax);
+      ++run;
+      if (dmax < tol || k == passes - 1) {
+        PM_CK(*p, cudaMemcpyAsync(xd, out, xb, cudaMemcpyDeviceToDevice, p->stream));
+        break;
+      }
+    }
+  }
+  if (passes_run) *passes_run = run;
+  return finish(*p, blocking, {{x_map, {xd, xb}}});
+}
+
+map_status map_sync(map_plan_t p) {
+  if (!p) return MAP_E_ARG;
+  return check_flag(*p);
+}
+
+const char* map_last_error(map_plan_t p) { return p ? p->err.c_str() : "null plan"; }
+
+map_status map_profile_enable(map_plan_t p, int32_t enable) {
+  if (!p) return MAP_E_ARG;
+  p->prof = enable != 0;
+  if (!p->prof) {
+    p->recs.clear();
+    p->ev_used = 0;
+  }
+  return MAP_OK;
+}
+
+int32_t map_profile_read(map_plan_t p, const char** names, double* ms, int64_t* launches, int32_t nmax) {
+  if (!p || nmax < 0) return -1;
+  double acc[K_COUNT] = {0};
+  int64_t cnt[K_COUNT] = {0};
+  for (auto& r : p->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return -1;
+    acc[r.id] += t;
+    cnt[r.id]++;
+  }
+  p->recs.clear();
+  p->ev_used = 0;
+  int32_t k = 0;
+  for (int id = 0; id < K_COUNT && k < nmax; ++id) {
+    if (!cnt[id]) continue;
+    if (names) names[k] = kernel_name(id);
+    if (ms) ms[k] = acc[id];
+    if (launches) launches[k] = cnt[id];
+    ++k;
+  }
+  return k;
+}
+
+int64_t map_workspace_bytes(map_plan_t p) { return p ? (int64_t)p->ws_bytes : 0; }
+
+int64_t map_last_launch_count(map_plan_t p) { return p ? p->launches : 0; }
+
+}  // extern "C"

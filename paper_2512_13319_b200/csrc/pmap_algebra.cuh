@@ -1,0 +1,565 @@
+// pmap_algebra.cuh -- register-resident small-matrix algebra of the parallel MAP scans.
+//
+// Element types and operators of arXiv 2512.13319 (P:n = PAPER.md line n):
+//   Elem  (A, b, C, eta, J)  conditional value function
+//   VF    (S, v)             value function V = 1/2 x^T S x - v^T x
+//   Aff   (Phi, beta)        affine transition x -> Phi x + beta
+// combine()  = the combination rule of P:395-407 (left operand e1 on [s, gamma],
+//              right operand e2 on [gamma, t]);
+// vapply()   = combine() with a value function (A = b = C = 0) on the right;
+// compose()  = P:448-449.
+// All matrices are N x N with N a compile-time constant so every loop unrolls
+// and every value lives in registers.  C and J (and S) are symmetric and stored
+// as packed upper triangles; only the upper triangle of a symmetric result is
+// ever computed, so symmetry is exact.  The shared inverse (I + C1 J2)^-1 is
+// never formed: one LU factorisation with partial pivoting (DESIGN.md R-PIVOT,
+// SURVEY G26) serves the P x = r and P^T x = r solves.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pmap {
+
+#define PM_INLINE __device__ __forceinline__
+
+template <int N>
+struct Dim {
+  static constexpr int NS = N * (N + 1) / 2;
+};
+
+// packed upper-triangle index of (i, j), i <= j, row-major
+__host__ __device__ constexpr int sidx(int i, int j, int N) {
+  return i <= j ? i * N - (i * (i - 1)) / 2 + (j - i) : j * N - (j * (j - 1)) / 2 + (i - j);
+}
+
+template <typename R, int N>
+struct Elem {
+  static constexpr int NS = Dim<N>::NS;
+  static constexpr int SZ = N * N + N + NS + N + NS;
+  R A[N][N];
+  R b[N];
+  R C[NS];
+  R h[N];  // eta
+  R J[NS];
+};
+
+template <typename R, int N>
+struct VF {
+  static constexpr int NS = Dim<N>::NS;
+  static constexpr int SZ = NS + N;
+  R S[NS];
+  R v[N];
+};
+
+template <typename R, int N>
+struct Aff {
+  static constexpr int SZ = N * N + N;
+  R P[N][N];
+  R q[N];
+};
+
+// ---------------------------------------------------------------- identities
+template <typename R, int N>
+PM_INLINE void set_identity(Elem<R, N>& e) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) e.A[i][j] = (i == j) ? R(1) : R(0);
+    e.b[i] = R(0);
+    e.h[i] = R(0);
+  }
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) {
+    e.C[k] = R(0);
+    e.J[k] = R(0);
+  }
+}
+
+template <typename R, int N>
+PM_INLINE void set_identity(Aff<R, N>& a) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) a.P[i][j] = (i == j) ? R(1) : R(0);
+    a.q[i] = R(0);
+  }
+}
+
+template <typename R, int N>
+PM_INLINE void set_zero(VF<R, N>& V) {
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) V.S[k] = R(0);
+#pragma unroll
+  for (int i = 0; i < N; ++i) V.v[i] = R(0);
+}
+
+// ------------------------------------------------- strided load / store (SoA)
+// Field f of an object lives at p[f * stride]; the field order is the struct order.
+template <typename R, int N>
+PM_INLINE void store(const Elem<R, N>& e, R* p, int64_t s) {
+  int f = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) p[(f++) * s] = e.A[i][j];
+#pragma unroll
+  for (int i = 0; i < N; ++i) p[(f++) * s] = e.b[i];
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) p[(f++) * s] = e.C[k];
+#pragma unroll
+  for (int i = 0; i < N; ++i) p[(f++) * s] = e.h[i];
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) p[(f++) * s] = e.J[k];
+}
+
+template <typename R, int N>
+PM_INLINE void load(Elem<R, N>& e, const R* p, int64_t s) {
+  int f = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) e.A[i][j] = p[(f++) * s];
+#pragma unroll
+  for (int i = 0; i < N; ++i) e.b[i] = p[(f++) * s];
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) e.C[k] = p[(f++) * s];
+#pragma unroll
+  for (int i = 0; i < N; ++i) e.h[i] = p[(f++) * s];
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) e.J[k] = p[(f++) * s];
+}
+
+template <typename R, int N>
+PM_INLINE void store(const VF<R, N>& V, R* p, int64_t s) {
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) p[k * s] = V.S[k];
+#pragma unroll
+  for (int i = 0; i < N; ++i) p[(Dim<N>::NS + i) * s] = V.v[i];
+}
+
+template <typename R, int N>
+PM_INLINE void load(VF<R, N>& V, const R* p, int64_t s) {
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) V.S[k] = p[k * s];
+#pragma unroll
+  for (int i = 0; i < N; ++i) V.v[i] = p[(Dim<N>::NS + i) * s];
+}
+
+template <typename R, int N>
+PM_INLINE void store(const Aff<R, N>& a, R* p, int64_t s) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) p[(i * N + j) * s] = a.P[i][j];
+#pragma unroll
+  for (int i = 0; i < N; ++i) p[(N * N + i) * s] = a.q[i];
+}
+
+template <typename R, int N>
+PM_INLINE void load(Aff<R, N>& a, const R* p, int64_t s) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) a.P[i][j] = p[(i * N + j) * s];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a.q[i] = p[(N * N + i) * s];
+}
+
+// ------------------------------------------------------ LU, partial pivoting
+template <typename R, int N>
+struct LUF {
+  R a[N][N];   // strictly lower: L multipliers; upper incl. diagonal: U
+  R dinv[N];   // 1 / U[i][i]
+  int piv[N];  // row swapped with row k at step k
+};
+
+template <typename R>
+PM_INLINE R pm_abs(R x) { return x < R(0) ? -x : x; }
+
+template <typename R>
+PM_INLINE R pm_rcp(R x) { return R(1) / x; }
+
+// Factorise f.a in place.  Row swaps are predicated selects (no dynamic
+// register indexing).  `ok` is cleared on a zero or non-finite pivot.
+template <typename R, int N>
+PM_INLINE void lu_factor(LUF<R, N>& f, bool& ok) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int p = k;
+    R amax = pm_abs(f.a[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      R t = pm_abs(f.a[i][k]);
+      bool gt = t > amax;
+      p = gt ? i : p;
+      amax = gt ? t : amax;
+    }
+    f.piv[k] = p;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      bool sw = (p == i);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        R rk = f.a[k][j], ri = f.a[i][j];
+        f.a[k][j] = sw ? ri : rk;
+        f.a[i][j] = sw ? rk : ri;
+      }
+    }
+    R d = f.a[k][k];
+    ok = ok && (d != R(0)) && (d == d);
+    R di = pm_rcp(d);
+    f.dinv[k] = di;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      R l = f.a[i][k] * di;
+      f.a[i][k] = l;
+#pragma unroll
+      for (int j = k + 1; j < N; ++j) f.a[i][j] = fma(-l, f.a[k][j], f.a[i][j]);
+    }
+  }
+}
+
+// x <- P^{-1} x   where P = Pi^T L U
+template <typename R, int N>
+PM_INLINE void lu_solve(const LUF<R, N>& f, R (&x)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      bool sw = (f.piv[k] == i);
+      R xk = x[k], xi = x[i];
+      x[k] = sw ? xi : xk;
+      x[i] = sw ? xk : xi;
+    }
+  }
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) x[i] = fma(-f.a[i][j], x[j], x[i]);
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) x[i] = fma(-f.a[i][j], x[j], x[i]);
+    x[i] *= f.dinv[i];
+  }
+}
+
+// x <- P^{-T} x   (P^T = U^T L^T Pi)
+template <typename R, int N>
+PM_INLINE void lu_solve_t(const LUF<R, N>& f, R (&x)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < i; ++j) x[i] = fma(-f.a[j][i], x[j], x[i]);
+    x[i] *= f.dinv[i];
+  }
+#pragma unroll
+  for (int i = N - 2; i >= 0; --i)
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) x[i] = fma(-f.a[j][i], x[j], x[i]);
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k) {
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      bool sw = (f.piv[k] == i);
+      R xk = x[k], xi = x[i];
+      x[k] = sw ? xi : xk;
+      x[i] = sw ? xk : xi;
+    }
+  }
+}
+
+// ----------------------------------------------------------- the operators
+// Combination rule, P:395-407 (e1 on [s, gamma] left, e2 on [gamma, t] right):
+//   A = A2 (I + C1 J2)^-1 A1
+//   b = A2 (I + C1 J2)^-1 (b1 + C1 eta2) + b2
+//   C = A2 (I + C1 J2)^-1 C1 A2^T + C2
+//   eta = A1^T (I + J2 C1)^-1 (eta2 - J2 b1) + eta1
+//   J = A1^T (I + J2 C1)^-1 J2 A1 + J1
+// using (I + J2 C1)^-1 = (I + C1 J2)^-T and (I + J2 C1)^-1 J2 = J2 (I + C1 J2)^-1.
+template <typename R, int N>
+PM_INLINE void combine(const Elem<R, N>& e1, const Elem<R, N>& e2, Elem<R, N>& out, bool& ok) {
+  LUF<R, N> f;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = (i == j) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.C[sidx(i, k, N)], e2.J[sidx(k, j, N)], s);
+      f.a[i][j] = s;
+    }
+  lu_factor(f, ok);
+  R X1[N][N], X3[N][N], x2[N], z[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    R t[N], u[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) { t[i] = e1.A[i][c]; u[i] = e1.C[sidx(i, c, N)]; }
+    lu_solve(f, t);
+    lu_solve(f, u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) { X1[i][c] = t[i]; X3[i][c] = u[i]; }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = e1.b[i], w = e2.h[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      s = fma(e1.C[sidx(i, k, N)], e2.h[k], s);
+      w = fma(-e2.J[sidx(i, k, N)], e1.b[k], w);
+    }
+    x2[i] = s;
+    z[i] = w;
+  }
+  lu_solve(f, x2);
+  lu_solve_t(f, z);
+  Elem<R, N> o;
+  // A, b
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e2.A[i][k], X1[k][j], s);
+      o.A[i][j] = s;
+    }
+    R s = e2.b[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(e2.A[i][k], x2[k], s);
+    o.b[i] = s;
+  }
+  // C = (A2 X3) A2^T + C2 (upper triangle)
+  {
+    R T1[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        R s = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(e2.A[i][k], X3[k][j], s);
+        T1[i][j] = s;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R s = e2.C[sidx(i, j, N)];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(T1[i][k], e2.A[j][k], s);
+        o.C[sidx(i, j, N)] = s;
+      }
+  }
+  // J = A1^T (J2 X1) + J1 (upper triangle); eta = A1^T z + eta1
+  {
+    R Y[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        R s = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(e2.J[sidx(i, k, N)], X1[k][j], s);
+        Y[i][j] = s;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R s = e1.J[sidx(i, j, N)];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], Y[k][j], s);
+        o.J[sidx(i, j, N)] = s;
+      }
+      R s = e1.h[i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], z[k], s);
+      o.h[i] = s;
+    }
+  }
+  out = o;
+}
+
+// e1 (x) (0, 0, 0, v, S): the value function of P:333-336 one interval earlier.
+//   S' = A1^T S (I + C1 S)^-1 A1 + J1,  v' = A1^T (I + S C1)^-1 (v - S b1) + eta1.
+// Also returns the pass-2 transition of the same interval (P:163-198 discretised,
+// DESIGN.md R-TRANS):  Phi = (I + C1 S)^-1 A1,  beta = (I + C1 S)^-1 (b1 + C1 v).
+template <typename R, int N, bool WANT_TRANS>
+PM_INLINE void vapply(const Elem<R, N>& e1, const VF<R, N>& V, VF<R, N>& out, Aff<R, N>* tr, bool& ok) {
+  LUF<R, N> f;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = (i == j) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.C[sidx(i, k, N)], V.S[sidx(k, j, N)], s);
+      f.a[i][j] = s;
+    }
+  lu_factor(f, ok);
+  R X1[N][N], z[N], bt[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    R t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = e1.A[i][c];
+    lu_solve(f, t);
+#pragma unroll
+    for (int i = 0; i < N; ++i) X1[i][c] = t[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R w = V.v[i], s = e1.b[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      w = fma(-V.S[sidx(i, k, N)], e1.b[k], w);
+      s = fma(e1.C[sidx(i, k, N)], V.v[k], s);
+    }
+    z[i] = w;
+    bt[i] = s;
+  }
+  lu_solve_t(f, z);
+  if (WANT_TRANS) {
+    lu_solve(f, bt);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) tr->P[i][j] = X1[i][j];
+      tr->q[i] = bt[i];
+    }
+  }
+  R Y[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], X1[k][j], s);
+      Y[i][j] = s;
+    }
+  VF<R, N> o;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i; j < N; ++j) {
+      R s = e1.J[sidx(i, j, N)];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], Y[k][j], s);
+      o.S[sidx(i, j, N)] = s;
+    }
+    R s = e1.h[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], z[k], s);
+    o.v[i] = s;
+  }
+  out = o;
+}
+
+// Pass-2 single step (P:456-459 with the transition of vapply):
+//   x_{i-1} = (I + C_i S_{i-1})^-1 (A_i x_i + b_i + C_i v_{i-1}).
+template <typename R, int N>
+PM_INLINE void trans_step(const R (&A)[N][N], const R (&b)[N], const R (&C)[Dim<N>::NS], const VF<R, N>& V,
+                          R (&x)[N], bool& ok) {
+  LUF<R, N> f;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = (i == j) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(C[sidx(i, k, N)], V.S[sidx(k, j, N)], s);
+      f.a[i][j] = s;
+    }
+  lu_factor(f, ok);
+  R t[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = b[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      s = fma(A[i][k], x[k], s);
+      s = fma(C[sidx(i, k, N)], V.v[k], s);
+    }
+    t[i] = s;
+  }
+  lu_solve(f, t);
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = t[i];
+}
+
+// (f o g)(x) = f(g(x)):  (P_f P_g, P_f q_g + q_f).
+template <typename R, int N>
+PM_INLINE void compose(const Aff<R, N>& f, const Aff<R, N>& g, Aff<R, N>& out) {
+  Aff<R, N> o;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(f.P[i][k], g.P[k][j], s);
+      o.P[i][j] = s;
+    }
+    R s = f.q[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(f.P[i][k], g.q[k], s);
+    o.q[i] = s;
+  }
+  out = o;
+}
+
+template <typename R, int N>
+PM_INLINE void apply(const Aff<R, N>& f, R (&x)[N]) {
+  R t[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = f.q[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(f.P[i][k], x[k], s);
+    t[i] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = t[i];
+}
+
+// Symmetric positive-definite solve S x = v by Cholesky (x* = S^-1 v).
+template <typename R, int N>
+PM_INLINE void spd_solve(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N], bool& ok) {
+  R Lm[N][N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    R d = S[sidx(j, j, N)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
+    ok = ok && (d > R(0));
+    R s = sqrt(d);
+    Lm[j][j] = s;
+    R si = R(1) / s;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      R t = S[sidx(i, j, N)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t = fma(-Lm[i][k], Lm[j][k], t);
+      Lm[i][j] = t * si;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R t = v[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) t = fma(-Lm[i][k], x[k], t);
+    x[i] = t / Lm[i][i];
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    R t = x[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) t = fma(-Lm[k][i], x[k], t);
+    x[i] = t / Lm[i][i];
+  }
+}
+
+}  // namespace pmap

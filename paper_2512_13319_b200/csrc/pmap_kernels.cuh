@@ -1,0 +1,469 @@
+// pmap_kernels.cuh -- the scan kernels of the parallel MAP solve (arXiv 2512.13319).
+//
+// Tiling: a trajectory of Nn local nodes is cut into tiles of NT runs x K nodes.
+// Thread r of a tile owns the contiguous run of K nodes [l0, l0 + K).  Nothing is
+// reversed in memory: the suffix-in-tau scan of P:249-258 / P:333-336 is a prefix
+// scan in node (time) order with the flipped operator acc_i = E_i (x) acc_{i-1}
+// (R-FLIP), and the forward-in-tau recovery scan of P:348-353 / P:448-459 is a
+// suffix scan in node order.
+//
+//   pass 1 (value functions, P:323-341 / P:382-409)
+//     k_p1_reduce  per run: serial fold of node elements (fused element build);
+//                  per tile: Kogge-Stone inclusive scan of the run aggregates
+//     k_p1_tiles   per group of NT2 tiles: inclusive scan of tile aggregates
+//     k_p1_groups  per trajectory: value-function carries of every group
+//     k_p1_down    per run: carry -> (S_i, v_i) at every node (vapply), fused with
+//                  the pass-2 transition build and the per-run affine fold, plus
+//                  the per-tile suffix scan of the affine run aggregates
+//   pass 2 (trajectory)
+//     k_p2_tiles   per trajectory: x* at each tile's last node (seeded with
+//                  x*_T = S_T^-1 v_T)
+//     k_p2_down    per run: x*_{i-1} = (I + C_i S_{i-1})^-1 (A_i x*_i + b_i + C_i v_{i-1})
+// Workspace layouts are SoA "field-major" so that a warp touches consecutive
+// addresses.
+#pragma once
+#include "pmap_sources.cuh"
+
+namespace pmap {
+
+struct Geom {
+  int64_t Nn;     // local nodes per trajectory (this launch)
+  int64_t node0;  // global index of local node 0 (time shard offset)
+  int64_t tpt;    // tiles per trajectory
+  int64_t gpt;    // tile groups per trajectory
+  int64_t batch;
+};
+
+constexpr int NT2 = 128;  // tiles per group (k_p1_tiles block size)
+constexpr int NT3 = 128;  // k_p1_groups block size
+constexpr int NT4 = 256;  // k_p2_tiles block size
+
+PM_INLINE void flag_node(unsigned long long* flag, int64_t node) {
+  atomicMin(flag, (unsigned long long)node);
+}
+
+template <typename R, int N>
+PM_INLINE bool finite_vf(const VF<R, N>& V) {
+  R s = R(0);
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) s += V.S[k];
+#pragma unroll
+  for (int i = 0; i < N; ++i) s += V.v[i];
+  return s - s == R(0);
+}
+
+// ----------------------------------------------------------------- pass 1a
+template <typename R, int N, int NY, int NT, int K, class Src, bool REV>
+__global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src src, const Geom g,
+                                                  const R* __restrict__ y, const R* __restrict__ xbar,
+                                                  R* __restrict__ run_incl, R* __restrict__ tile_agg,
+                                                  unsigned long long* flag) {
+  using E = Elem<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);  // [E::SZ][NT]
+  const int64_t tile = blockIdx.x;
+  const int64_t b = tile / g.tpt, j = tile % g.tpt;
+  const int r = threadIdx.x;
+  const int64_t l0 = (j * NT + r) * (int64_t)K;
+  const R* yb = y + b * g.Nn * NY;
+  const R* xb = Src::NEEDS_XBAR ? xbar + b * g.Nn * N : nullptr;
+  bool ok = true;
+  E acc;
+  set_identity(acc);
+#pragma unroll 1
+  for (int m = 0; m < K; ++m) {
+    const int64_t lr = l0 + m;
+    if (lr >= g.Nn) break;
+    const int64_t l = REV ? g.Nn - 1 - lr : lr;  // REV: suffix scan (two-filter pass B)
+    E e;
+    src.node(g.node0 + l, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
+    if (m == 0)
+      acc = e;
+    else
+      combine(e, acc, acc, ok);  // acc = E_l (x) acc   (R-FLIP)
+  }
+  // inclusive Kogge-Stone scan over the runs of the tile: In_r = In_r (x) In_{r-d}
+#pragma unroll 1
+  for (int d = 1; d < NT; d <<= 1) {
+    store(acc, sh + r, NT);
+    __syncthreads();
+    if (r >= d) {
+      E p;
+      load(p, sh + r - d, NT);
+      combine(acc, p, acc, ok);
+    }
+    __syncthreads();
+  }
+  store(acc, run_incl + tile * (int64_t)E::SZ * NT + r, NT);
+  if (r == NT - 1) store(acc, tile_agg + tile * (int64_t)E::SZ, 1);
+  if (!ok) flag_node(flag, g.node0 + l0);
+}
+
+// ----------------------------------------------------------------- pass 1b
+// Inclusive scan of tile aggregates within groups of NT2 tiles.
+template <typename R, int N>
+__global__ void __launch_bounds__(NT2) k_p1_tiles(const Geom g, const R* __restrict__ tile_agg,
+                                                  R* __restrict__ tile_incl, R* __restrict__ group_agg,
+                                                  unsigned long long* flag) {
+  using E = Elem<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);
+  const int64_t grp = blockIdx.x;
+  const int64_t b = grp / g.gpt, gg = grp % g.gpt;
+  const int t = threadIdx.x;
+  const int64_t jt = gg * NT2 + t;
+  const bool valid = jt < g.tpt;
+  bool ok = true;
+  E acc;
+  if (valid)
+    load(acc, tile_agg + (b * g.tpt + jt) * E::SZ, 1);
+  else
+    set_identity(acc);
+#pragma unroll 1
+  for (int d = 1; d < NT2; d <<= 1) {
+    store(acc, sh + t, NT2);
+    __syncthreads();
+    if (t >= d) {
+      E p;
+      load(p, sh + t - d, NT2);
+      combine(acc, p, acc, ok);
+    }
+    __syncthreads();
+  }
+  if (valid) store(acc, tile_incl + (b * g.tpt + jt) * E::SZ, 1);
+  if (t == NT2 - 1) store(acc, group_agg + grp * E::SZ, 1);
+  if (!ok) flag_node(flag, g.node0 + jt);
+}
+
+// ----------------------------------------------------------------- pass 1c
+// Value-function carry entering every group: carry_g = GroupExcl_g (.) carry_in,
+// carry_in = the trajectory's incoming value function ((0,0) on rank 0).
+template <typename R, int N>
+__global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __restrict__ group_agg,
+                                                   const R* __restrict__ carry_in, R* __restrict__ group_carry,
+                                                   R* __restrict__ total_agg, unsigned long long* flag) {
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t c = (g.gpt + NT3 - 1) / NT3;
+  const int64_t k0 = t * c, k1 = min(g.gpt, k0 + c);
+  bool ok = true;
+  E acc;
+  set_identity(acc);
+  for (int64_t k = k0; k < k1; ++k) {
+    E p;
+    load(p, group_agg + (b * g.gpt + k) * E::SZ, 1);
+    combine(p, acc, acc, ok);
+  }
+#pragma unroll 1
+  for (int d = 1; d < NT3; d <<= 1) {
+    store(acc, sh + t, NT3);
+    __syncthreads();
+    if (t >= d) {
+      E p;
+      load(p, sh + t - d, NT3);
+      combine(acc, p, acc, ok);
+    }
+    __syncthreads();
+  }
+  store(acc, sh + t, NT3);
+  __syncthreads();
+  V cin;
+  if (carry_in)
+    load(cin, carry_in + b * V::SZ, 1);
+  else
+    set_zero(cin);
+  if (t == NT3 - 1 && total_agg) store(acc, total_agg + b * E::SZ, 1);
+  V cur = cin;
+  if (t > 0) {
+    E p;
+    load(p, sh + t - 1, NT3);
+    vapply<R, N, false>(p, cin, cur, nullptr, ok);
+  }
+  for (int64_t k = k0; k < k1; ++k) {
+    store(cur, group_carry + (b * g.gpt + k) * V::SZ, 1);
+    if (k + 1 < k1) {
+      E p;
+      load(p, group_agg + (b * g.gpt + k) * E::SZ, 1);
+      vapply<R, N, false>(p, cur, cur, nullptr, ok);
+    }
+  }
+  if (!ok) flag_node(flag, g.node0);
+}
+
+// ----------------------------------------------------------------- pass 1d
+template <typename R, int N, int NY, int NT, int K, class Src, bool P2>
+__global__ void __launch_bounds__(NT) k_p1_down(const __grid_constant__ Src src, const Geom g,
+                                                const R* __restrict__ y, const R* __restrict__ xbar,
+                                                const R* __restrict__ run_incl, const R* __restrict__ tile_incl,
+                                                const R* __restrict__ group_carry, R* __restrict__ sv,
+                                                R* __restrict__ run_suf, R* __restrict__ tile_agg2,
+                                                unsigned long long* flag) {
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  using A = Aff<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);  // [A::SZ][NT] (reused for the tile carry)
+  const int64_t tile = blockIdx.x;
+  const int64_t b = tile / g.tpt, j = tile % g.tpt;
+  const int r = threadIdx.x;
+  const int64_t l0 = (j * NT + r) * (int64_t)K;
+  const R* yb = y + b * g.Nn * NY;
+  const R* xb = Src::NEEDS_XBAR ? xbar + b * g.Nn * N : nullptr;
+  bool ok = true;
+  // tile carry
+  if (r == 0) {
+    const int64_t gg = j / NT2, lj = j % NT2;
+    V c;
+    load(c, group_carry + (b * g.gpt + gg) * V::SZ, 1);
+    if (lj > 0) {
+      E p;
+      load(p, tile_incl + (b * g.tpt + j - 1) * E::SZ, 1);
+      vapply<R, N, false>(p, c, c, nullptr, ok);
+    }
+    store(c, sh, 1);
+  }
+  __syncthreads();
+  V cur;
+  load(cur, sh, 1);
+  __syncthreads();
+  if (r > 0) {
+    E p;
+    load(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), NT);
+    vapply<R, N, false>(p, cur, cur, nullptr, ok);
+  }
+  A agg;
+  set_identity(agg);
+  R* svt = sv + tile * (int64_t)V::SZ * K * NT;
+#pragma unroll 1
+  for (int m = 0; m < K; ++m) {
+    const int64_t l = l0 + m;
+    if (l >= g.Nn) break;
+    const int64_t gi = g.node0 + l;
+    E e;
+    src.node(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
+    if (gi == 0) {
+#pragma unroll
+      for (int k = 0; k < Dim<N>::NS; ++k) cur.S[k] = e.J[k];
+#pragma unroll
+      for (int i = 0; i < N; ++i) cur.v[i] = e.h[i];
+    } else if (P2) {
+      A tr;
+      vapply<R, N, true>(e, cur, cur, &tr, ok);
+      compose(agg, tr, agg);  // run aggregate maps x*_{l} -> x*_{l0 - 1}
+    } else {
+      vapply<R, N, false>(e, cur, cur, nullptr, ok);
+    }
+    store(cur, svt + m * NT + r, (int64_t)K * NT);
+  }
+  if (!finite_vf(cur)) ok = false;
+  if (!P2) {
+    if (!ok) flag_node(flag, g.node0 + l0);
+    return;
+  }
+  // exclusive suffix scan of the run aggregates within the tile
+#pragma unroll 1
+  for (int d = 1; d < NT; d <<= 1) {
+    store(agg, sh + r, NT);
+    __syncthreads();
+    if (r + d < NT) {
+      A p;
+      load(p, sh + r + d, NT);
+      compose(agg, p, agg);
+    }
+    __syncthreads();
+  }
+  store(agg, sh + r, NT);
+  __syncthreads();
+  A ex;
+  if (r + 1 < NT)
+    load(ex, sh + r + 1, NT);
+  else
+    set_identity(ex);
+  store(ex, run_suf + tile * (int64_t)A::SZ * NT + r, NT);
+  if (r == 0) store(agg, tile_agg2 + tile * (int64_t)A::SZ, 1);
+  if (!ok) flag_node(flag, g.node0 + l0);
+}
+
+// (S, v) of local node l of trajectory b in the tiled SoA layout
+template <typename R, int N, int NT, int K>
+PM_INLINE void load_sv(const R* sv, const Geom& g, int64_t b, int64_t l, VF<R, N>& V) {
+  const int64_t L = (int64_t)NT * K;
+  const int64_t j = l / L, q = l % L;
+  const int64_t rr = q / K, m = q % K;
+  load(V, sv + (b * g.tpt + j) * (int64_t)VF<R, N>::SZ * K * NT + m * NT + rr, (int64_t)K * NT);
+}
+
+// ----------------------------------------------------------------- pass 2a
+// x* at the last node of every tile (exclusive suffix over tile aggregates,
+// seeded with x_end = S_T^-1 v_T on the rank holding node T, or the shard carry).
+template <typename R, int N, int NT, int K>
+__global__ void __launch_bounds__(NT4) k_p2_tiles(const Geom g, const R* __restrict__ sv,
+                                                  const R* __restrict__ tile_agg2, const R* __restrict__ xend_in,
+                                                  R* __restrict__ tile_carry, R* __restrict__ total_agg2,
+                                                  unsigned long long* flag) {
+  using A = Aff<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);  // [A::SZ][NT4] + N
+  R* shx = sh + A::SZ * NT4;
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x;
+  bool ok = true;
+  if (t == 0) {
+    R x[N];
+    if (xend_in) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = xend_in[b * N + i];
+    } else {
+      VF<R, N> V;
+      load_sv<R, N, NT, K>(sv, g, b, g.Nn - 1, V);
+      spd_solve<R, N>(V.S, V.v, x, ok);  // x*_T = S_T^-1 v_T
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) shx[i] = x[i];
+  }
+  const int64_t c = (g.tpt + NT4 - 1) / NT4;
+  const int64_t k0 = t * c, k1 = min(g.tpt, k0 + c);
+  A acc;
+  set_identity(acc);
+  for (int64_t k = k1 - 1; k >= k0; --k) {
+    A p;
+    load(p, tile_agg2 + (b * g.tpt + k) * A::SZ, 1);
+    compose(p, acc, acc);
+  }
+#pragma unroll 1
+  for (int d = 1; d < NT4; d <<= 1) {
+    store(acc, sh + t, NT4);
+    __syncthreads();
+    if (t + d < NT4) {
+      A p;
+      load(p, sh + t + d, NT4);
+      compose(acc, p, acc);
+    }
+    __syncthreads();
+  }
+  store(acc, sh + t, NT4);
+  __syncthreads();
+  if (t == 0 && total_agg2) store(acc, total_agg2 + b * A::SZ, 1);
+  R x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = shx[i];
+  if (t + 1 < NT4) {
+    A p;
+    load(p, sh + t + 1, NT4);
+    apply(p, x);
+  }
+  for (int64_t k = k1 - 1; k >= k0; --k) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) tile_carry[(b * g.tpt + k) * N + i] = x[i];
+    A p;
+    load(p, tile_agg2 + (b * g.tpt + k) * A::SZ, 1);
+    apply(p, x);
+  }
+  if (!ok) flag_node(flag, g.node0 + g.Nn - 1);
+}
+
+// ----------------------------------------------------------------- pass 2b
+template <typename R, int N, int NT, int K, class Src>
+__global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src, const Geom g,
+                                                const R* __restrict__ xbar, const R* __restrict__ sv,
+                                                const R* __restrict__ run_suf, const R* __restrict__ tile_carry,
+                                                const R* __restrict__ carry_in, R* __restrict__ x_out,
+                                                unsigned long long* flag) {
+  using V = VF<R, N>;
+  using A = Aff<R, N>;
+  const int64_t tile = blockIdx.x;
+  const int64_t b = tile / g.tpt, j = tile % g.tpt;
+  const int r = threadIdx.x;
+  const int64_t l0 = (j * NT + r) * (int64_t)K;
+  const R* xb = Src::NEEDS_XBAR ? xbar + b * g.Nn * N : nullptr;
+  bool ok = true;
+  R x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = tile_carry[tile * N + i];
+  {
+    A s;
+    load(s, run_suf + tile * (int64_t)A::SZ * NT + r, NT);
+    apply(s, x);
+  }
+  R* xo = x_out + b * g.Nn * N;
+#pragma unroll 1
+  for (int m = K - 1; m >= 0; --m) {
+    const int64_t l = l0 + m;
+    if (l >= g.Nn) continue;
+#pragma unroll
+    for (int i = 0; i < N; ++i) xo[l * N + i] = x[i];
+    const int64_t gi = g.node0 + l;
+    if (gi == 0) continue;
+    V Vp;
+    if (l > 0)
+      load_sv<R, N, NT, K>(sv, g, b, l - 1, Vp);
+    else
+      load(Vp, carry_in + b * V::SZ, 1);  // previous rank's last node (time shard)
+    R At[N][N], bt[N], Ct[Dim<N>::NS];
+    src.trans(gi, Src::NEEDS_XBAR ? xb + l * N : nullptr, At, bt, Ct);
+    trans_step<R, N>(At, bt, Ct, Vp, x, ok);
+  }
+  R s = R(0);
+#pragma unroll
+  for (int i = 0; i < N; ++i) s += x[i];
+  if (!(s - s == R(0))) ok = false;
+  if (!ok) flag_node(flag, g.node0 + l0);
+}
+
+// ---------------------------------------------------------- filter outputs
+// m_i = S_i^-1 v_i, P_i = S_i^-1 (packed upper triangle).
+template <typename R, int N, int NT, int K>
+__global__ void k_filter_out(const Geom g, const R* __restrict__ sv, R* __restrict__ fm, R* __restrict__ fP,
+                             unsigned long long* flag) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= g.batch * g.Nn) return;
+  const int64_t b = idx / g.Nn, l = idx % g.Nn;
+  VF<R, N> V;
+  load_sv<R, N, NT, K>(sv, g, b, l, V);
+  bool ok = true;
+  R m[N];
+  spd_solve<R, N>(V.S, V.v, m, ok);
+  if (fm) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) fm[idx * N + i] = m[i];
+  }
+  if (fP) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R e[N], col[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) e[i] = (i == c) ? R(1) : R(0);
+      spd_solve<R, N>(V.S, e, col, ok);
+#pragma unroll
+      for (int i = 0; i <= c; ++i) fP[idx * Dim<N>::NS + sidx(i, c, N)] = col[i];
+    }
+  }
+  if (!ok) flag_node(flag, g.node0 + l);
+}
+
+// --------------------------------------------------- iterated linearisation
+template <typename R, int N>
+__global__ void k_fill_m0(int64_t count, const R* __restrict__ m0, R* __restrict__ xbar) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx < count) xbar[idx] = m0[idx % N];
+}
+
+// max |a - b| as the bit pattern of a non-negative double (order-preserving)
+template <typename R>
+__global__ void k_maxdiff(int64_t count, const R* __restrict__ a, const R* __restrict__ b,
+                          unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double d = fabs((double)a[i] - (double)b[i]);
+    m = (d > m || d != d) ? d : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+}  // namespace pmap

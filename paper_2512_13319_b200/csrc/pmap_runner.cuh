@@ -1,0 +1,510 @@
+// pmap_runner.cuh -- host-side runner of the parallel MAP solve: workspace layout,
+// launch sequencing per (dtype, nx, ny, model kind) instantiation, time-shard
+// exchange.  Included by the ABI translation unit and by the instantiation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pmap.h"
+#include "pmap_kernels.cuh"
+#include "pmap_tf.cuh"
+
+using namespace pmap;
+
+namespace pmap_rt {
+
+constexpr int kNT = 64;  // runs (threads) per tile
+constexpr int kK = 32;   // nodes per run
+
+enum class Kind { LTI, TV, NL };
+
+// ---------------------------------------------------------------- host algebra
+// O(nx^3) model preprocessing at plan time only (never per node).
+using HMat = std::vector<double>;
+
+inline bool h_inv(int n, const double* a, double* out) {  // Gauss-Jordan, partial pivoting
+  std::vector<double> m(a, a + n * n);
+  for (int i = 0; i < n * n; ++i) out[i] = (i % (n + 1) == 0) ? 1.0 : 0.0;
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(m[i * n + k]) > std::fabs(m[p * n + k])) p = i;
+    if (m[p * n + k] == 0.0) return false;
+    for (int j = 0; j < n; ++j) {
+      std::swap(m[k * n + j], m[p * n + j]);
+      std::swap(out[k * n + j], out[p * n + j]);
+    }
+    double d = 1.0 / m[k * n + k];
+    for (int j = 0; j < n; ++j) { m[k * n + j] *= d; out[k * n + j] *= d; }
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      double f = m[i * n + k];
+      for (int j = 0; j < n; ++j) { m[i * n + j] -= f * m[k * n + j]; out[i * n + j] -= f * out[k * n + j]; }
+    }
+  }
+  return true;
+}
+
+inline bool h_is_finite(const double* a, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(a[i])) return false;
+  return true;
+}
+
+// ---------------------------------------------------------------- workspace
+template <typename R, int N>
+struct WsLayout {
+  size_t run_incl, tile_agg1, tile_incl1, group_agg1, group_carry1, total1, sv, run_suf, tile_agg2,
+      tile_carry2, total2, carry_in, xend, tf_run, tf_tile, tf_tincl, tf_gagg, tf_gcarry, bytes;
+  void plan(const Geom& g, bool tf) {
+    using E = Elem<R, N>;
+    using V = VF<R, N>;
+    using A = Aff<R, N>;
+    const size_t nt = (size_t)(g.batch * g.tpt), ng = (size_t)(g.batch * g.gpt), B = (size_t)g.batch;
+    size_t off = 0;
+    auto take = [&](size_t elems) {
+      size_t o = off;
+      off += ((elems * sizeof(R) + 255) / 256) * 256;
+      return o;
+    };
+    run_incl = take(nt * E::SZ * kNT);
+    tile_agg1 = take(nt * E::SZ);
+    tile_incl1 = take(nt * E::SZ);
+    group_agg1 = take(ng * E::SZ);
+    group_carry1 = take(ng * V::SZ);
+    total1 = take(B * E::SZ);
+    sv = take(nt * V::SZ * kK * kNT);
+    run_suf = take(nt * A::SZ * kNT);
+    tile_agg2 = take(nt * A::SZ);
+    tile_carry2 = take(nt * N);
+    total2 = take(B * (A::SZ + N));
+    carry_in = take(B * V::SZ);
+    xend = take(B * N);
+    if (tf) {
+      tf_run = take(nt * E::SZ * kNT);
+      tf_tile = take(nt * E::SZ);
+      tf_tincl = take(nt * E::SZ);
+      tf_gagg = take(ng * E::SZ);
+      tf_gcarry = take(ng * V::SZ);
+    } else {
+      tf_run = tf_tile = tf_tincl = tf_gagg = tf_gcarry = 0;
+    }
+    bytes = off;
+  }
+};
+
+// ------------------------------------------------------------------ runners
+struct PlanState;
+
+struct Runner {
+  virtual ~Runner() {}
+  virtual size_t ws_bytes(const Geom& g, bool tf) const = 0;
+  virtual void set_attrs() = 0;
+  // one parallel-RTS solve (pass 1 + pass 2); xbar only for nonlinear sources
+  virtual void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) = 0;
+  virtual void two_filter(PlanState& p, const void* y, void* x) = 0;
+  virtual void fill_m0(PlanState& p, void* xbar) = 0;
+  virtual void maxdiff(PlanState& p, const void* a, const void* b, unsigned long long* out) = 0;
+  virtual int sizeof_real() const = 0;
+};
+
+struct NcclApi {
+  typedef int (*allgather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
+  allgather_t allgather = nullptr;
+  bool load() {
+    if (allgather) return true;
+    allgather = (allgather_t)dlsym(RTLD_DEFAULT, "ncclAllGather");
+    if (!allgather) {  // torch loads libnccl RTLD_LOCAL: look it up by soname without reloading
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+      if (h) allgather = (allgather_t)dlsym(h, "ncclAllGather");
+    }
+    return allgather != nullptr;
+  }
+};
+
+struct PlanState {
+  map_plan_desc d{};
+  Kind kind = Kind::LTI;
+  int nl_kind = 0;
+  Geom g{};
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Runner> runner;
+  unsigned char* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool ws_tf = false;
+  unsigned long long* dflag = nullptr;  // [0] numeric flag, [1] max diff
+  void* xbuf[2] = {nullptr, nullptr};   // nonlinear ping-pong
+  void* stage_y = nullptr;
+  void* stage_x = nullptr;
+  void* stage_aux = nullptr;
+  size_t stage_y_bytes = 0, stage_x_bytes = 0, stage_aux_bytes = 0;
+  void* dev_tv = nullptr;  // time-varying model arrays
+  double* m0_host = nullptr;
+  void* m0_dev = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  NcclApi nccl;
+  // nonlinear graph cache
+  cudaGraphExec_t graph = nullptr;
+  const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  int graph_passes = -1;
+  int64_t graph_launches = 0;
+  size_t elem_real = 8;
+  cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // per-kernel CUDA-event profiling (map_profile_enable / map_profile_read)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Rec { int id; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  cudaEvent_t ev_get() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+};
+
+// kernel classes reported by map_profile_read
+enum KernelId { K_P1_REDUCE = 0, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_DOWN, K_FILTER_OUT,
+                K_TF_REDUCE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD, K_NL_MISC, K_COUNT };
+inline const char* kernel_name(int id) {
+  static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_tiles", "k_p1_groups", "k_p1_down", "k_p2_tiles",
+                                       "k_p2_down", "k_filter_out", "k_tf_reduce(k_p1_reduce<Mirror>)",
+                                       "k_tf_tiles(k_p1_tiles)", "k_tf_groups(k_p1_groups)", "k_tf_down",
+                                       "k_shard_*", "k_fill_m0/k_maxdiff"};
+  return (id >= 0 && id < K_COUNT) ? names[id] : "?";
+}
+
+// Launch a kernel on stream S, counting it and (when profiling) bracketing it with events.
+#define PM_LAUNCH(p, S, ID, ...)                         \
+  do {                                                   \
+    cudaEvent_t _pa = nullptr;                           \
+    if ((p).prof) {                                      \
+      _pa = (p).ev_get();                                \
+      cudaEventRecord(_pa, (S));                         \
+    }                                                    \
+    __VA_ARGS__;                                         \
+    if ((p).prof) {                                      \
+      cudaEvent_t _pb = (p).ev_get();                    \
+      cudaEventRecord(_pb, (S));                         \
+      (p).recs.push_back({(ID), _pa, _pb});              \
+    }                                                    \
+    (p).launches++;                                      \
+  } while (0)
+
+inline map_status cuda_fail(PlanState& p, cudaError_t e, const char* where) {
+  p.err = std::string(where) + ": " + cudaGetErrorString(e);
+  return MAP_E_CUDA;
+}
+
+#define PM_CK(p, call)                                        \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return cuda_fail((p), _e, #call);  \
+  } while (0)
+
+template <typename R, int N, int NY, class Src>
+struct RunnerT : Runner {
+  Src src;
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  using A = Aff<R, N>;
+
+  size_t ws_bytes(const Geom& g, bool tf) const override {
+    WsLayout<R, N> L;
+    L.plan(g, tf);
+    return L.bytes;
+  }
+  int sizeof_real() const override { return (int)sizeof(R); }
+
+  static size_t smem_reduce() { return sizeof(R) * E::SZ * kNT; }
+  static size_t smem_tiles() { return sizeof(R) * E::SZ * NT2; }
+  static size_t smem_groups() { return sizeof(R) * E::SZ * NT3; }
+  static size_t smem_down() { return sizeof(R) * (A::SZ * kNT > V::SZ ? A::SZ * kNT : V::SZ); }
+  static size_t smem_p2tiles() { return sizeof(R) * (A::SZ * NT4 + N); }
+
+  void set_attrs() override {
+    cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, kK, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_reduce());
+    cudaFuncSetAttribute(k_p1_tiles<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tiles());
+    cudaFuncSetAttribute(k_p1_groups<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_groups());
+    cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, kK, Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_down());
+    cudaFuncSetAttribute(k_p2_tiles<R, N, kNT, kK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_p2tiles());
+    if constexpr (Src::HAS_MIRROR) {
+      cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, kK, Mirror<Src>, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
+      cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, kK, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_down());
+      cudaFuncSetAttribute(k_tf_down<R, N, NY, kNT, kK, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_down());
+    }
+  }
+
+  void rts(PlanState& p, const void* yv, const void* xbarv, void* xv, void* fm, void* fP) override {
+    const Geom& g = p.g;
+    WsLayout<R, N> L;
+    L.plan(g, p.ws_tf);
+    auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
+    const R* y = static_cast<const R*>(yv);
+    const R* xbar = static_cast<const R*>(xbarv);
+    R* x = static_cast<R*>(xv);
+    const unsigned ntiles = (unsigned)(g.batch * g.tpt);
+    const bool sharded = p.d.world > 1;
+    cudaStream_t s = p.stream;
+    // ---- pass 1
+    PM_LAUNCH(p, s, K_P1_REDUCE,
+              (k_p1_reduce<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_reduce(), s>>>(
+                  src, g, y, xbar, W(L.run_incl), W(L.tile_agg1), p.dflag)));
+    PM_LAUNCH(p, s, K_P1_TILES,
+              (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
+                  g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
+    const R* carry_in = nullptr;
+    if (sharded) {
+      // chunk aggregate of this rank, all-gather, carry = Agg_{r-1} (x) ... (x) Agg_0 (.) (0, 0)
+      PM_LAUNCH(p, s, K_P1_GROUPS,
+                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
+                    g, W(L.group_agg1), nullptr, W(L.group_carry1), W(L.total1), p.dflag)));
+      shard_carry1(p, W(L.total1), W(L.carry_in));
+      carry_in = W(L.carry_in);
+    }
+    PM_LAUNCH(p, s, K_P1_GROUPS,
+              (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
+                  g, W(L.group_agg1), carry_in, W(L.group_carry1), nullptr, p.dflag)));
+    PM_LAUNCH(p, s, K_P1_DOWN,
+              (k_p1_down<R, N, NY, kNT, kK, Src, true><<<ntiles, kNT, smem_down(), s>>>(
+                  src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
+                  W(L.tile_agg2), p.dflag)));
+    // ---- pass 2
+    const R* xend_in = nullptr;
+    if (sharded) {
+      PM_LAUNCH(p, s, K_P2_TILES,
+                (k_p2_tiles<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2tiles(), s>>>(
+                    g, W(L.sv), W(L.tile_agg2), W(L.xend), W(L.tile_carry2), W(L.total2), p.dflag)));
+      shard_carry2(p, W(L.total2), W(L.xend), W(L.sv));
+      xend_in = W(L.xend);
+    }
+    PM_LAUNCH(p, s, K_P2_TILES,
+              (k_p2_tiles<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2tiles(), s>>>(
+                  g, W(L.sv), W(L.tile_agg2), xend_in, W(L.tile_carry2), nullptr, p.dflag)));
+    PM_LAUNCH(p, s, K_P2_DOWN,
+              (k_p2_down<R, N, kNT, kK, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
+                                                                  W(L.tile_carry2), W(L.carry_in), x, p.dflag)));
+    if (fm || fP) {
+      const int64_t n = g.batch * g.Nn;
+      PM_LAUNCH(p, s, K_FILTER_OUT,
+                (k_filter_out<R, N, kNT, kK><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, W(L.sv), (R*)fm,
+                                                                                        (R*)fP, p.dflag)));
+    }
+  }
+
+  // Time-sharded exchange of pass-1 chunk aggregates:
+  // gather every rank's aggregate and fold those of the preceding ranks.
+  void shard_carry1(PlanState& p, R* total1, R* carry_in);
+  void shard_carry2(PlanState& p, R* total2, R* xend, const R* sv);
+
+  // Two-filter (R-TF): pass A = pass-1 kernels without the pass-2 fold on the plan
+  // stream; pass B = mirrored suffix scan with the fused combine on a forked stream.
+  void two_filter(PlanState& p, const void* yv, void* xv) override {
+    if constexpr (Src::HAS_MIRROR) {
+      const Geom& g = p.g;
+      WsLayout<R, N> L;
+      L.plan(g, true);
+      auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
+      const R* y = static_cast<const R*>(yv);
+      R* x = static_cast<R*>(xv);
+      const unsigned ntiles = (unsigned)(g.batch * g.tpt);
+      cudaStream_t s = p.stream, s2 = p.stream2;
+      cudaEventRecord(p.ev_fork, s);
+      cudaStreamWaitEvent(s2, p.ev_fork, 0);
+      // pass A: forward filter (S_i, v_i)
+      PM_LAUNCH(p, s, K_P1_REDUCE,
+                (k_p1_reduce<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_reduce(), s>>>(
+                    src, g, y, nullptr, W(L.run_incl), W(L.tile_agg1), p.dflag)));
+      PM_LAUNCH(p, s, K_P1_TILES,
+                (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
+                    g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
+      PM_LAUNCH(p, s, K_P1_GROUPS,
+                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
+                    g, W(L.group_agg1), nullptr, W(L.group_carry1), nullptr, p.dflag)));
+      PM_LAUNCH(p, s, K_P1_DOWN,
+                (k_p1_down<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_down(), s>>>(
+                    src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
+                    nullptr, p.dflag)));
+      // pass B: backward information filter over mirrored elements (reverse node order)
+      Mirror<Src> mir{src, g.node0 + g.Nn - 1};
+      PM_LAUNCH(p, s2, K_TF_REDUCE,
+                (k_p1_reduce<R, N, NY, kNT, kK, Mirror<Src>, true><<<ntiles, kNT, smem_reduce(), s2>>>(
+                    mir, g, y, nullptr, W(L.tf_run), W(L.tf_tile), p.dflag)));
+      PM_LAUNCH(p, s2, K_TF_TILES,
+                (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s2>>>(
+                    g, W(L.tf_tile), W(L.tf_tincl), W(L.tf_gagg), p.dflag)));
+      PM_LAUNCH(p, s2, K_TF_GROUPS,
+                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s2>>>(
+                    g, W(L.tf_gagg), nullptr, W(L.tf_gcarry), nullptr, p.dflag)));
+      cudaEventRecord(p.ev_join, s);
+      cudaStreamWaitEvent(s2, p.ev_join, 0);
+      PM_LAUNCH(p, s2, K_TF_DOWN,
+                (k_tf_down<R, N, NY, kNT, kK, Src><<<ntiles, kNT, smem_down(), s2>>>(
+                    mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, p.dflag)));
+      cudaEventRecord(p.ev_fork, s2);
+      cudaStreamWaitEvent(s, p.ev_fork, 0);
+    } else {
+      p.err = "two-filter not available for this model kind";
+    }
+  }
+  void fill_m0(PlanState& p, void* xbar) override {
+    const int64_t n = p.g.batch * p.g.Nn * N;
+    PM_LAUNCH(p, p.stream, K_NL_MISC,
+              (k_fill_m0<R, N><<<(unsigned)((n + 255) / 256), 256, 0, p.stream>>>(
+                  n, static_cast<const R*>(p.m0_dev), static_cast<R*>(xbar))));
+  }
+  void maxdiff(PlanState& p, const void* a, const void* b, unsigned long long* out) override {
+    const int64_t n = p.g.batch * p.g.Nn * N;
+    PM_LAUNCH(p, p.stream, K_NL_MISC,
+              (k_maxdiff<R><<<296, 256, 0, p.stream>>>(n, static_cast<const R*>(a), static_cast<const R*>(b), out)));
+  }
+};
+
+// shard exchange helpers (host-side sequencing; the folds run in tiny kernels)
+template <typename R, int N>
+__global__ void k_shard_fold1(int world, int rank, int64_t batch, const R* __restrict__ gathered,
+                              R* __restrict__ carry_in, unsigned long long* flag) {
+  // gathered: [world][batch][E::SZ]; carry for `rank` = Agg_{rank-1} (x) ... (x) Agg_0 (.) (0,0)
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  bool ok = true;
+  V cur;
+  set_zero(cur);
+  for (int q = 0; q < rank; ++q) {
+    E a;
+    load(a, gathered + ((int64_t)q * batch + b) * E::SZ, 1);
+    vapply<R, N, false>(a, cur, cur, nullptr, ok);
+  }
+  store(cur, carry_in + b * V::SZ, 1);
+  if (!ok) atomicMin(flag, 0ull);
+}
+
+template <typename R, int N>
+__global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ sv_last,
+                              int64_t sv_stride, R* __restrict__ payload, unsigned long long* flag) {
+  // payload per trajectory: [Aff total][x_T (last rank only)]
+  using A = Aff<R, N>;
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  for (int k = 0; k < A::SZ; ++k) payload[b * (A::SZ + N) + k] = total2[b * A::SZ + k];
+  if (last) {
+    VF<R, N> V;
+    load(V, sv_last + b * sv_stride, (int64_t)kK * kNT);
+    R x[N];
+    bool ok = true;
+    spd_solve<R, N>(V.S, V.v, x, ok);
+    for (int i = 0; i < N; ++i) payload[b * (A::SZ + N) + A::SZ + i] = x[i];
+    if (!ok) atomicMin(flag, 0ull);
+  }
+}
+
+template <typename R, int N>
+__global__ void k_shard_fold2(int world, int rank, int64_t batch, const R* __restrict__ gathered,
+                              R* __restrict__ xend) {
+  // x at this rank's last node = Agg_{rank+1} o ... o Agg_{world-1} (x_T)
+  using A = Aff<R, N>;
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int64_t PS = A::SZ + N;
+  R x[N];
+  for (int i = 0; i < N; ++i) x[i] = gathered[((int64_t)(world - 1) * batch + b) * PS + A::SZ + i];
+  for (int q = world - 1; q > rank; --q) {
+    A a;
+    load(a, gathered + ((int64_t)q * batch + b) * PS, 1);
+    apply(a, x);
+  }
+  for (int i = 0; i < N; ++i) xend[b * N + i] = x[i];
+}
+
+inline size_t g_shard_scratch_bytes = 0;
+inline void* g_shard_scratch = nullptr;
+
+template <typename R, int N, int NY, class Src>
+void RunnerT<R, N, NY, Src>::shard_carry1(PlanState& p, R* total1, R* carry_in) {
+  const int world = p.d.world;
+  const size_t per = (size_t)p.g.batch * E::SZ;
+  const size_t need = per * world * sizeof(R);
+  if (g_shard_scratch_bytes < need) {
+    cudaFree(g_shard_scratch);
+    cudaMalloc(&g_shard_scratch, need);
+    g_shard_scratch_bytes = need;
+  }
+  R* gathered = static_cast<R*>(g_shard_scratch);
+  const int dt = sizeof(R) == 8 ? 8 /*ncclFloat64*/ : 7 /*ncclFloat32*/;
+  if (!p.nccl.load() || p.nccl.allgather(total1, gathered, per, dt, p.d.nccl_comm, p.stream) != 0) {
+    p.err = "ncclAllGather failed or NCCL not loaded";
+    return;
+  }
+  PM_LAUNCH(p, p.stream, K_SHARD,
+            (k_shard_fold1<R, N><<<(unsigned)((p.g.batch + 63) / 64), 64, 0, p.stream>>>(
+                world, p.d.rank, p.g.batch, gathered, carry_in, p.dflag)));
+}
+
+template <typename R, int N, int NY, class Src>
+void RunnerT<R, N, NY, Src>::shard_carry2(PlanState& p, R* total2, R* xend, const R* sv) {
+  const int world = p.d.world;
+  const size_t per = (size_t)p.g.batch * (A::SZ + N);
+  const size_t need = per * (world + 1) * sizeof(R);
+  if (g_shard_scratch_bytes < need) {
+    cudaFree(g_shard_scratch);
+    cudaMalloc(&g_shard_scratch, need);
+    g_shard_scratch_bytes = need;
+  }
+  R* payload = static_cast<R*>(g_shard_scratch);
+  R* gathered = payload + per;
+  // (S, v) of the rank's last local node
+  const int64_t l = p.g.Nn - 1;
+  const int64_t Lt = (int64_t)kNT * kK;
+  const int64_t j = l / Lt, q = l % Lt, rr = q / kK, m = q % kK;
+  const R* sv_last = sv + j * (int64_t)V::SZ * kK * kNT + m * kNT + rr;
+  const int64_t sv_stride = p.g.tpt * (int64_t)V::SZ * kK * kNT;
+  PM_LAUNCH(p, p.stream, K_SHARD,
+            (k_shard_pack2<R, N><<<(unsigned)((p.g.batch + 63) / 64), 64, 0, p.stream>>>(
+                p.g.batch, p.d.rank == world - 1, total2, sv_last, sv_stride, payload, p.dflag)));
+  const int dt = sizeof(R) == 8 ? 8 : 7;
+  if (!p.nccl.load() || p.nccl.allgather(payload, gathered, per, dt, p.d.nccl_comm, p.stream) != 0) {
+    p.err = "ncclAllGather failed or NCCL not loaded";
+    return;
+  }
+  PM_LAUNCH(p, p.stream, K_SHARD,
+            (k_shard_fold2<R, N><<<(unsigned)((p.g.batch + 63) / 64), 64, 0, p.stream>>>(
+                world, p.d.rank, p.g.batch, gathered, xend)));
+}
+
+// ---------------------------------------------------------- instantiation
+// Factories are declared here and explicitly instantiated, one (dtype, shape,
+// model kind) per translation unit, in inst.cu (see pmap_make.cuh).
+template <typename R, int N, int NY>
+Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
+                 const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
+                 const double* Cm);
+template <typename R, int N, int NY>
+Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r, const R* Rm,
+                const int64_t* str, int nw, double dt, const double* P0i, const double* P0im0);
+template <typename R, int N, int NY, int KIND>
+Runner* make_nl(double dt, double mu, const double* C, const double* Ri, const double* P0i, const double* P0im0);
+
+#define PM_SHAPES(X) X(1, 1) X(2, 1) X(2, 2) X(3, 1) X(3, 2) X(4, 2) X(5, 2)
+
+}  // namespace pmap_rt

@@ -1,0 +1,446 @@
+// pmap_sources.cuh -- per-node element builders ("element sources") for the scans.
+//
+// A source turns the model and the data of one grid node i into the node element
+// (DESIGN.md R-ELEM; one explicit step of the element ODEs P:416-427 from the
+// boundary (I, 0, 0, 0, 0) of P:427, measurement attached to its own node, R-NODE):
+//   E_0 = (0, 0, 0, P0^-1 m0 + K_0 (y_0 - r_0), P0^-1 + K_0 H_0)
+//   E_i = (I - dt F_i, -dt c_i, dt Q_i, K_i (y_i - r_i), K_i H_i),  K_i = dt H_i^T R_i^-1
+// and, for pass 2, the transition data (A_i, b_i, C_i) of node i >= 1.
+// Sources are passed to kernels by value (__grid_constant__): model constants sit
+// in the kernel-parameter constant bank and are broadcast to all threads.
+#pragma once
+#include "pmap_algebra.cuh"
+
+namespace pmap {
+
+// ---------------------------------------------------------------- LTI model
+// F, c, L, W, H, r, R constant in time (all strides 0).  Everything but the
+// y-dependent eta is precomputed on the host at plan time.
+template <typename R, int N, int NY>
+struct SrcLTI {
+  static constexpr int NS = Dim<N>::NS;
+  static constexpr int NXB = N;  // row width of the nominal trajectory (unused)
+  static constexpr bool NEEDS_XBAR = false;
+  R A[N][N];
+  R b[N];
+  R C[NS];
+  R J[NS];
+  R K[N][NY];  // dt H^T R^-1
+  R h0[N];     // -K r          (eta offset, nodes >= 1)
+  R J0[NS];    // P0^-1 + K H
+  R h00[N];    // P0^-1 m0 - K r
+  R Am[N][N];  // (I - dt F)^-1             (two-filter mirrored element, R-TF)
+  R bm[N];     // (I - dt F)^-1 dt c
+  R Cm[NS];    // (I - dt F)^-1 dt Q (I - dt F)^-T
+  static constexpr bool HAS_MIRROR = true;
+
+  // Mirrored element M_i of node gi (R-TF); the terminal node Tg has no transition.
+  PM_INLINE void mirror(int64_t gi, int64_t Tg, const R* yrow, Elem<R, N>& e) const {
+    R yv[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) yv[k] = yrow[k];
+    const bool last = (gi == Tg);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = h0[i];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) s = fma(K[i][k], yv[k], s);
+      e.h[i] = s;
+#pragma unroll
+      for (int j = 0; j < N; ++j) e.A[i][j] = last ? R(0) : Am[i][j];
+      e.b[i] = last ? R(0) : bm[i];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      e.C[k] = last ? R(0) : Cm[k];
+      e.J[k] = J[k];
+    }
+  }
+
+  PM_INLINE void node(int64_t gi, const R* yrow, const R* /*xrow*/, Elem<R, N>& e) const {
+    R yv[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) yv[k] = yrow[k];
+    const bool first = (gi == 0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = first ? h00[i] : h0[i];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) s = fma(K[i][k], yv[k], s);
+      e.h[i] = s;
+#pragma unroll
+      for (int j = 0; j < N; ++j) e.A[i][j] = first ? R(0) : A[i][j];
+      e.b[i] = first ? R(0) : b[i];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      e.C[k] = first ? R(0) : C[k];
+      e.J[k] = first ? J0[k] : J[k];
+    }
+  }
+  PM_INLINE void trans(int64_t /*gi*/, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) At[i][j] = A[i][j];
+      bt[i] = b[i];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) Ct[k] = C[k];
+  }
+};
+
+// ------------------------------------------------------- time-varying model
+// Per-node device arrays (converted to R at plan time); stride 0 = constant.
+template <typename R, int N, int NY>
+struct SrcTV {
+  static constexpr int NS = Dim<N>::NS;
+  static constexpr bool NEEDS_XBAR = false;
+  static constexpr bool HAS_MIRROR = true;
+  const R *F, *c, *L, *W, *H, *r, *Rm;
+  int64_t sF, sc, sL, sW, sH, sr, sR;
+  int nw;
+  R dt;
+  R P0i[NS];
+  R P0im0[N];
+
+  PM_INLINE void model(int64_t gi, R (&Ft)[N][N], R (&ct)[N], R (&Q)[NS]) const {
+    const R* Fp = F + gi * sF;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) Ft[i][j] = Fp[i * N + j];
+      ct[i] = c ? c[gi * sc + i] : R(0);
+    }
+    const R* Lp = L + gi * sL;
+    const R* Wp = W + gi * sW;
+    // Q = L W L^T, nw <= N
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R s = R(0);
+        for (int a = 0; a < nw; ++a) {
+          R t = R(0);
+          for (int bb = 0; bb < nw; ++bb) t = fma(Wp[a * nw + bb], Lp[j * nw + bb], t);
+          s = fma(Lp[i * nw + a], t, s);
+        }
+        Q[sidx(i, j, N)] = s;
+      }
+  }
+  // K = dt H^T R^-1 and the offset-corrected measurement at node gi
+  PM_INLINE void meas(int64_t gi, R (&Kt)[N][NY], R (&Hm)[NY][N], R (&rr)[NY]) const {
+    const R* Hp = H + gi * sH;
+    const R* Rp = Rm + gi * sR;
+#pragma unroll
+    for (int a = 0; a < NY; ++a) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) Hm[a][j] = Hp[a * N + j];
+      rr[a] = r ? r[gi * sr + a] : R(0);
+    }
+    // R^-1 H via LU (NY small)
+    LUF<R, NY> f;
+#pragma unroll
+    for (int a = 0; a < NY; ++a)
+#pragma unroll
+      for (int bb = 0; bb < NY; ++bb) f.a[a][bb] = Rp[a * NY + bb];
+    bool ok = true;
+    lu_factor(f, ok);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R t[NY];
+#pragma unroll
+      for (int a = 0; a < NY; ++a) t[a] = Hm[a][j];
+      lu_solve(f, t);  // column j of R^-1 H  ->  K[j][:] = dt (R^-1 H)[:, j]  (R symmetric)
+#pragma unroll
+      for (int a = 0; a < NY; ++a) Kt[j][a] = dt * t[a];
+    }
+  }
+  PM_INLINE void node(int64_t gi, const R* yrow, const R* /*xrow*/, Elem<R, N>& e) const {
+    R Kt[N][NY], Hm[NY][N], rr[NY];
+    meas(gi, Kt, Hm, rr);
+    R res[NY];
+#pragma unroll
+    for (int a = 0; a < NY; ++a) res[a] = yrow[a] - rr[a];
+    const bool first = (gi == 0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = first ? P0im0[i] : R(0);
+#pragma unroll
+      for (int a = 0; a < NY; ++a) s = fma(Kt[i][a], res[a], s);
+      e.h[i] = s;
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R t = first ? P0i[sidx(i, j, N)] : R(0);
+#pragma unroll
+        for (int a = 0; a < NY; ++a) t = fma(Kt[i][a], Hm[a][j], t);
+        e.J[sidx(i, j, N)] = t;
+      }
+    }
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) e.A[i][j] = R(0);
+        e.b[i] = R(0);
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e.C[k] = R(0);
+    } else {
+      R Ft[N][N], ct[N], Q[NS];
+      model(gi, Ft, ct, Q);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) e.A[i][j] = ((i == j) ? R(1) : R(0)) - dt * Ft[i][j];
+        e.b[i] = -dt * ct[i];
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e.C[k] = dt * Q[k];
+    }
+  }
+  PM_INLINE void trans(int64_t gi, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
+    R Ft[N][N], ct[N], Q[NS];
+    model(gi, Ft, ct, Q);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) At[i][j] = ((i == j) ? R(1) : R(0)) - dt * Ft[i][j];
+      bt[i] = -dt * ct[i];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) Ct[k] = dt * Q[k];
+  }
+  // Mirrored element (R-TF): transition of node gi+1 inverted, measurement of node gi.
+  PM_INLINE void mirror(int64_t gi, int64_t Tg, const R* yrow, Elem<R, N>& e) const {
+    R Kt[N][NY], Hm[NY][N], rr[NY];
+    meas(gi, Kt, Hm, rr);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+#pragma unroll
+      for (int a = 0; a < NY; ++a) s = fma(Kt[i][a], yrow[a] - rr[a], s);
+      e.h[i] = s;
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R t = R(0);
+#pragma unroll
+        for (int a = 0; a < NY; ++a) t = fma(Kt[i][a], Hm[a][j], t);
+        e.J[sidx(i, j, N)] = t;
+      }
+    }
+    if (gi == Tg) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) e.A[i][j] = R(0);
+        e.b[i] = R(0);
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e.C[k] = R(0);
+      return;
+    }
+    R Ft[N][N], ct[N], Q[NS];
+    model(gi + 1, Ft, ct, Q);
+    LUF<R, N> f;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) f.a[i][j] = ((i == j) ? R(1) : R(0)) - dt * Ft[i][j];
+    bool ok = true;
+    lu_factor(f, ok);
+    R Am[N][N], T1[N][N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R t[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) t[i] = (i == c) ? R(1) : R(0);
+      lu_solve(f, t);
+#pragma unroll
+      for (int i = 0; i < N; ++i) Am[i][c] = t[i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(Am[i][k], dt * ct[k], s);
+      e.b[i] = s;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        e.A[i][j] = Am[i][j];
+        R t = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) t = fma(Am[i][k], dt * Q[sidx(k, j, N)], t);
+        T1[i][j] = t;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R t = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) t = fma(T1[i][k], Am[j][k], t);
+        e.C[sidx(i, j, N)] = t;
+      }
+  }
+};
+
+// --------------------------------------------- nonlinear: linearise at xbar_i
+// Taylor linearisation of P:513 (R-LIN): F_i = df(xbar_i), c_i = f(xbar_i) - F_i xbar_i,
+// H_i = dh(xbar_i), r_i = h(xbar_i) - H_i xbar_i, so that
+//   y_i - r_i = wrap(y_i - h(xbar_i)) + H_i xbar_i     (bearing residual wrapped, R-WRAP).
+template <typename R>
+PM_INLINE R wrap_pi(R a) {  // to (-pi, pi]
+  const R TWO_PI = R(6.28318530717958647692);
+  const R PI = R(3.14159265358979323846);
+  return a - TWO_PI * ceil((a - PI) / TWO_PI);
+}
+
+template <typename R, int N, int NY, int KIND>
+struct SrcNL {
+  static constexpr int NS = Dim<N>::NS;
+  static constexpr bool NEEDS_XBAR = true;
+  static constexpr bool HAS_MIRROR = false;
+  R dt;
+  R mu;           // Van der Pol parameter
+  R C[NS];        // dt Q, Q = L W L^T
+  R Ri[NY][NY];   // R^-1
+  R P0i[NS];
+  R P0im0[N];
+
+  // drift f and Jacobian F at x
+  PM_INLINE void drift(const R (&x)[N], R (&f)[N], R (&F)[N][N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) F[i][j] = R(0);
+    if (KIND == 1) {  // coordinated turn
+      f[0] = x[2];
+      f[1] = x[3];
+      f[2] = -x[4] * x[3];
+      f[3] = x[4] * x[2];
+      f[4] = R(0);
+      F[0][2] = R(1);
+      F[1][3] = R(1);
+      F[2][3] = -x[4];
+      F[2][4] = -x[3];
+      F[3][2] = x[4];
+      F[3][4] = x[2];
+    } else {  // Van der Pol (R-VDP)
+      f[0] = x[1];
+      f[1] = mu * (R(1) - x[0] * x[0]) * x[1] - x[0];
+      F[0][1] = R(1);
+      F[1][0] = -R(2) * mu * x[0] * x[1] - R(1);
+      F[1][1] = mu * (R(1) - x[0] * x[0]);
+    }
+  }
+  // measurement h and Jacobian H at x
+  PM_INLINE void meas(const R (&x)[N], R (&h)[NY], R (&H)[NY][N]) const {
+#pragma unroll
+    for (int a = 0; a < NY; ++a)
+#pragma unroll
+      for (int j = 0; j < N; ++j) H[a][j] = R(0);
+    if (KIND == 1) {  // range / bearing, P:600 (atan2, G13)
+      R r2 = x[0] * x[0] + x[1] * x[1];
+      R rr = sqrt(r2);
+      h[0] = rr;
+      h[1] = atan2(x[1], x[0]);
+      H[0][0] = x[0] / rr;
+      H[0][1] = x[1] / rr;
+      H[1][0] = -x[1] / r2;
+      H[1][1] = x[0] / r2;
+    } else {
+      h[0] = x[0];
+      H[0][0] = R(1);
+    }
+  }
+  PM_INLINE void node(int64_t gi, const R* yrow, const R* xrow, Elem<R, N>& e) const {
+    R x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = xrow[i];
+    R h[NY], H[NY][N];
+    meas(x, h, H);
+    R res[NY];
+#pragma unroll
+    for (int a = 0; a < NY; ++a) {
+      R d = yrow[a] - h[a];
+      if (KIND == 1 && a == 1) d = wrap_pi(d);
+      R hx = R(0);
+#pragma unroll
+      for (int j = 0; j < N; ++j) hx = fma(H[a][j], x[j], hx);
+      res[a] = d + hx;  // = y_eff - r
+    }
+    R Kt[N][NY];  // dt H^T R^-1
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int bb = 0; bb < NY; ++bb) {
+        R s = R(0);
+#pragma unroll
+        for (int a = 0; a < NY; ++a) s = fma(H[a][i], Ri[a][bb], s);
+        Kt[i][bb] = dt * s;
+      }
+    const bool first = (gi == 0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = first ? P0im0[i] : R(0);
+#pragma unroll
+      for (int a = 0; a < NY; ++a) s = fma(Kt[i][a], res[a], s);
+      e.h[i] = s;
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R t = first ? P0i[sidx(i, j, N)] : R(0);
+#pragma unroll
+        for (int a = 0; a < NY; ++a) t = fma(Kt[i][a], H[a][j], t);
+        e.J[sidx(i, j, N)] = t;
+      }
+    }
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) e.A[i][j] = R(0);
+        e.b[i] = R(0);
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e.C[k] = R(0);
+    } else {
+      R f[N], F[N][N];
+      drift(x, f, F);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R c = f[i];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          c = fma(-F[i][j], x[j], c);
+          e.A[i][j] = ((i == j) ? R(1) : R(0)) - dt * F[i][j];
+        }
+        e.b[i] = -dt * c;
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e.C[k] = C[k];
+    }
+  }
+  PM_INLINE void trans(int64_t /*gi*/, const R* xrow, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
+    R x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = xrow[i];
+    R f[N], F[N][N];
+    drift(x, f, F);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R c = f[i];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        c = fma(-F[i][j], x[j], c);
+        At[i][j] = ((i == j) ? R(1) : R(0)) - dt * F[i][j];
+      }
+      bt[i] = -dt * c;
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) Ct[k] = C[k];
+  }
+};
+
+}  // namespace pmap

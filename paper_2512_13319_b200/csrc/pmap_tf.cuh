@@ -1,0 +1,93 @@
+// pmap_tf.cuh -- parallel two-filter smoother.
+//
+// Reading R-TF: the paper's forward scan over e (x) a_0 (x) ...
+// needs J_0^-1 of a one-node element, which is singular whenever ny < nx.  The
+// same backward-filter information is obtained exactly by the combination rule
+// of P:395-407 applied, in reverse node order, to "mirrored" elements
+//   M_i = ((I - dt F_{i+1})^-1, (I - dt F_{i+1})^-1 dt c_{i+1},
+//          (I - dt F_{i+1})^-1 dt Q_{i+1} (I - dt F_{i+1})^-T, eta_i^m, J_i^m),
+//   M_T = (0, 0, 0, eta_T^m, J_T^m)          (zero prior information at t_T),
+// whose suffix products acc_i = M_i (x) acc_{i+1} carry in (J, eta) the backward
+// information filter (Lam_i, xi_i) of y_i..y_T.  The two filters are combined per
+// node (P:462-466 in information form, C_bar = Lam^-1, b_bar = Lam^-1 xi):
+//   x_i = (S_i + Lam_i - J_i^m)^-1 (v_i + xi_i - eta_i^m)   (y_i counted once, R-TF).
+// Pass A (forward filter, the pass-1 kernels without the pass-2 fold) and pass B
+// (this suffix scan, with the combine fused into its epilogue) are independent
+// and run on two streams.
+#pragma once
+#include "pmap_kernels.cuh"
+
+namespace pmap {
+
+// Adapter: presents the mirrored elements of `Src` as a prefix scan over the
+// reversed local index (k_p1_reduce<REV=true> passes the original node index).
+template <class Src>
+struct Mirror {
+  Src s;
+  int64_t Tg;  // global index of the last node
+  static constexpr bool NEEDS_XBAR = false;
+  template <typename R, int N>
+  PM_INLINE void node(int64_t gi, const R* yrow, const R* /*xrow*/, Elem<R, N>& e) const {
+    s.mirror(gi, Tg, yrow, e);
+  }
+};
+
+template <typename R, int N, int NY, int NT, int K, class Src>
+__global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<Src> mir, const Geom g,
+                                                const R* __restrict__ y, const R* __restrict__ run_incl,
+                                                const R* __restrict__ tile_incl, const R* __restrict__ group_carry,
+                                                const R* __restrict__ sv, R* __restrict__ x_out,
+                                                unsigned long long* flag) {
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);
+  const int64_t tile = blockIdx.x;
+  const int64_t b = tile / g.tpt, j = tile % g.tpt;
+  const int r = threadIdx.x;
+  const int64_t l0 = (j * NT + r) * (int64_t)K;  // reversed local index
+  const R* yb = y + b * g.Nn * NY;
+  R* xo = x_out + b * g.Nn * N;
+  bool ok = true;
+  if (r == 0) {
+    const int64_t gg = j / NT2, lj = j % NT2;
+    V c;
+    load(c, group_carry + (b * g.gpt + gg) * V::SZ, 1);
+    if (lj > 0) {
+      E p;
+      load(p, tile_incl + (b * g.tpt + j - 1) * E::SZ, 1);
+      vapply<R, N, false>(p, c, c, nullptr, ok);
+    }
+    store(c, sh, 1);
+  }
+  __syncthreads();
+  V cur;
+  load(cur, sh, 1);
+  if (r > 0) {
+    E p;
+    load(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), NT);
+    vapply<R, N, false>(p, cur, cur, nullptr, ok);
+  }
+#pragma unroll 1
+  for (int m = 0; m < K; ++m) {
+    const int64_t lr = l0 + m;
+    if (lr >= g.Nn) break;
+    const int64_t l = g.Nn - 1 - lr;
+    E e;
+    mir.template node<R, N>(g.node0 + l, yb + l * NY, nullptr, e);
+    vapply<R, N, false>(e, cur, cur, nullptr, ok);  // (Lam_l, xi_l)
+    V Va;
+    load_sv<R, N, NT, K>(sv, g, b, l, Va);
+    R Ssum[Dim<N>::NS], rhs[N], xv[N];
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) Ssum[k] = Va.S[k] + (cur.S[k] - e.J[k]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) rhs[i] = Va.v[i] + (cur.v[i] - e.h[i]);
+    spd_solve<R, N>(Ssum, rhs, xv, ok);
+#pragma unroll
+    for (int i = 0; i < N; ++i) xo[l * N + i] = xv[i];
+  }
+  if (!ok) flag_node(flag, g.node0 + g.Nn - 1 - l0);
+}
+
+}  // namespace pmap

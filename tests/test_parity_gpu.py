@@ -1,0 +1,287 @@
+"""GPU parity: CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Tolerance (BASELINE.json north_star): relative error <= 1e-9 in fp64 and <= 1e-3
+in fp32, measured as ||x_gpu - x_oracle||_inf / ||x_oracle||_inf per trajectory
+(reading G23).  Sizes span several tiles (tile = 64 runs x 32 nodes = 2048
+nodes) with ragged tails, plus the BASELINE.json full sizes.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-9
+TOL32 = 1e-3
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_13319_b200 as pm
+    pm.load_library()
+    return torch
+
+
+def ora_model(spec):
+    return oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0, c=spec.c, r=spec.r)
+
+
+def gpu_plan(spec, T, batch=1, dtype="f64"):
+    import paper_2512_13319_b200 as pm
+    return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H, r=spec.r,
+                   R=spec.R, m0=spec.m0, P0=spec.P0, batch=batch, dtype=dtype)
+
+
+def to_dev(torch, a, dtype=None):
+    return torch.tensor(np.ascontiguousarray(a), dtype=dtype or torch.float64, device="cuda")
+
+
+def random_lti(nx, ny, seed, offsets=True):
+    rng = np.random.default_rng(seed)
+    F = 0.3 * rng.standard_normal((nx, nx)) - 0.5 * np.eye(nx)
+    nw = max(1, nx - 1)
+    L = rng.standard_normal((nx, nw))
+    a = rng.standard_normal((nw, nw))
+    W = a @ a.T + np.eye(nw)
+    H = rng.standard_normal((ny, nx))
+    b = rng.standard_normal((ny, ny))
+    R = b @ b.T + 0.5 * np.eye(ny)
+    c = rng.standard_normal(nx) if offsets else None
+    r = rng.standard_normal(ny) if offsets else None
+    m0 = rng.standard_normal(nx)
+    q = rng.standard_normal((nx, nx))
+    P0 = q @ q.T + np.eye(nx)
+    return wl.LinearSpec("random", F, L, W, H, R, m0, P0, c=c, r=r, t0=0.0, tf=2.0)
+
+
+@pytest.mark.parametrize("T", [1, 2, 63, 2047, 2048, 2049, 5000, 300_000])
+def test_wiener_rts_sizes(torch_cuda, T):
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    _, y = wl.simulate_linear(spec, T, seed=T)
+    xo, fm, fP = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf, want_filter=True)
+    plan = gpu_plan(spec, T)
+    yd = to_dev(torch, y[None])
+    nx = spec.nx
+    fmd = torch.empty((1, T + 1, nx), dtype=torch.float64, device="cuda")
+    fPd = torch.empty((1, T + 1, nx * (nx + 1) // 2), dtype=torch.float64, device="cuda")
+    x = plan.solve_linear(yd, filt_m=fmd, filt_P=fPd)
+    plan.sync()
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    assert rel(fmd[0].cpu().numpy(), fm) < TOL64
+    iu = np.triu_indices(nx)
+    assert rel(fPd[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (2, 1), (2, 2), (3, 1), (3, 2), (4, 2), (5, 2)])
+def test_random_lti_shapes(torch_cuda, shape):
+    torch = torch_cuda
+    nx, ny = shape
+    spec = random_lti(nx, ny, seed=nx * 10 + ny)
+    T = 4500
+    y = np.random.default_rng(nx).standard_normal((T + 1, ny))
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    x = gpu_plan(spec, T).solve_linear(to_dev(torch, y[None]))
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+def test_ou_c1(torch_cuda):
+    torch = torch_cuda
+    spec, y, T, _ = wl.make_workload("C1")
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    x = gpu_plan(spec, T).solve_linear(to_dev(torch, y[None]))
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+def tv_spec(T, nx=4, ny=2, seed=3):
+    rng = np.random.default_rng(seed)
+    N = T + 1
+    t = np.linspace(0, 1, N)
+    F = 0.4 * rng.standard_normal((nx, nx))[None] + np.sin(3 * t)[:, None, None] * np.eye(nx)
+    L = rng.standard_normal((nx, 2))[None] * (1 + 0.3 * np.cos(t))[:, None, None]
+    W = np.eye(2)[None] * (1.5 + 0.5 * np.sin(5 * t))[:, None, None]
+    H = rng.standard_normal((ny, nx))[None] + 0.2 * t[:, None, None]
+    R = (np.eye(ny) * 0.5)[None] * (1 + t)[:, None, None]
+    c = rng.standard_normal((N, nx))
+    r = rng.standard_normal((N, ny))
+    return wl.LinearSpec("tv", F, L, W, H, R, rng.standard_normal(nx), np.eye(nx), c=c, r=r, t0=0.0, tf=1.0)
+
+
+@pytest.mark.parametrize("shape", [(4, 2), (3, 1), (5, 2)])
+def test_time_varying(torch_cuda, shape):
+    torch = torch_cuda
+    nx, ny = shape
+    T = 3000
+    spec = tv_spec(T, nx, ny)
+    y = np.random.default_rng(1).standard_normal((T + 1, ny))
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    x = gpu_plan(spec, T).solve_linear(to_dev(torch, y[None]))
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    xt = gpu_plan(spec, T).two_filter(to_dev(torch, y[None]))
+    assert rel(xt[0].cpu().numpy(), xo) < TOL64
+
+
+def test_offsets_batch_and_two_filter(torch_cuda):
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    spec.r = np.array([0.5, -0.25])
+    T, B = 4100, 6
+    _, y = wl.simulate_linear(spec, T, seed=9, batch=B)
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
+    plan = gpu_plan(spec, T, batch=B)
+    yd = to_dev(torch, y)
+    x = plan.solve_linear(yd).cpu().numpy()
+    xt = plan.two_filter(yd).cpu().numpy()
+    for b in range(B):
+        assert rel(x[b], xo[b]) < TOL64
+        assert rel(xt[b], xo[b]) < TOL64
+
+
+def test_c2_full(torch_cuda):
+    torch = torch_cuda
+    spec, y, T, _ = wl.make_workload("C2")
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    plan = gpu_plan(spec, T)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+def test_c3_full_size(torch_cuda):
+    """BASELINE config 3 at its full size (T = 1e7), in the launch configuration bench.py times."""
+    torch = torch_cuda
+    spec, y, T, _ = wl.make_workload("C3")
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    plan = gpu_plan(spec, T)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+def test_c5_two_filter_batch(torch_cuda):
+    """BASELINE config 5 at full size: 1024 trajectories x T = 1e4, two-filter."""
+    torch = torch_cuda
+    spec, y, T, B = wl.make_workload("C5")
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=1)
+    plan = gpu_plan(spec, T, batch=B)
+    x = plan.two_filter(to_dev(torch, y)).cpu().numpy()
+    errs = [rel(x[b], xo[b]) for b in range(B)]
+    assert max(errs) < TOL64
+
+
+@pytest.mark.parametrize("T", [777, 5000])
+def test_nonlinear_ct(torch_cuda, T):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = wl.coordinated_turn()
+    _, y = wl.simulate_nonlinear(s, T, seed=T)
+    xo, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=10)
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1)
+    x, run = plan.solve_nonlinear(to_dev(torch, y[None]), passes=10)
+    assert run == 10
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    # per-iterate parity: 3 passes
+    xo3, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=3)
+    x3, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=3)
+    assert rel(x3[0].cpu().numpy(), xo3) < TOL64
+
+
+def test_nonlinear_c4_full(torch_cuda):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s, y, T, _ = wl.make_workload("C4")
+    xo, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=10)
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1)
+    x, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=10)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+def test_nonlinear_vdp_and_tol(torch_cuda):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = wl.van_der_pol()
+    T = 6000
+    _, y = wl.simulate_nonlinear(s, T, seed=2)
+    xo, d = oracle.ieks(2, s.params, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=8)
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=2, params=s.params)
+    x, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=8)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    # device-side convergence check: stops once max|dx| < tol
+    tol = 1e-6
+    want = int(np.argmax(d < tol)) + 1 if np.any(d < tol) else 8
+    x2, run = plan.solve_nonlinear(to_dev(torch, y[None]), passes=8, tol=tol)
+    assert run == want
+
+
+@pytest.mark.parametrize("cfg", ["wiener", "ct"])
+def test_fp32_variant(torch_cuda, cfg):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    if cfg == "wiener":
+        spec = wl.wiener_velocity()
+        T = 20_000
+        _, y = wl.simulate_linear(spec, T, seed=4)
+        xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+        x = gpu_plan(spec, T, dtype="f32").solve_linear(to_dev(torch, y[None], torch.float32))
+    else:
+        s = wl.coordinated_turn()
+        T = 5000
+        _, y = wl.simulate_nonlinear(s, T, seed=4)
+        xo, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=10)
+        plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1, dtype="f32")
+        x, _ = plan.solve_nonlinear(to_dev(torch, y[None], torch.float32), passes=10)
+    assert rel(x[0].cpu().numpy(), xo) < TOL32
+
+
+def test_host_buffers_and_determinism(torch_cuda):
+    """Host (NumPy) buffers go through the C ABI's staging path; results are bitwise
+    reproducible run to run (fixed scan tree)."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 10_000
+    _, y = wl.simulate_linear(spec, T, seed=5)
+    plan = gpu_plan(spec, T)
+    xh = np.empty((1, T + 1, 4))
+    pm.map_solve_linear(plan.handle, np.ascontiguousarray(y[None]), xh)
+    xd = plan.solve_linear(to_dev(torch, y[None])).cpu().numpy()
+    xd2 = plan.solve_linear(to_dev(torch, y[None])).cpu().numpy()
+    assert np.array_equal(xh, xd) and np.array_equal(xd, xd2)
+    assert rel(xh[0], oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)) < TOL64
+
+
+def test_errors(torch_cuda):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    with pytest.raises(pm.MapError) as e:
+        pm.Plan(T=0, t0=0.0, tf=5.0, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0, P0=spec.P0)
+    assert e.value.status == 1
+    with pytest.raises(pm.MapError) as e:
+        pm.Plan(T=10, t0=0.0, tf=5.0, F=np.eye(6), L=np.eye(6), W=np.eye(6), H=np.ones((1, 6)), R=[[1.0]],
+                m0=np.zeros(6), P0=np.eye(6))
+    assert e.value.status == 2
+    T = 5000
+    _, y = wl.simulate_linear(spec, T, seed=1)
+    y[3001, 1] = np.nan
+    plan = gpu_plan(spec, T)
+    plan.solve_linear(to_dev(torch, y[None]))
+    with pytest.raises(pm.MapError) as e:
+        plan.sync()
+    assert e.value.status == 5 and "node" in str(e.value)
+    # the flag is cleared once reported
+    _, y2 = wl.simulate_linear(spec, T, seed=2)
+    plan.solve_linear(to_dev(torch, y2[None]))
+    plan.sync()
+    with pytest.raises(pm.MapError) as e:
+        plan.solve_nonlinear(to_dev(torch, y2[None]))
+    assert e.value.status == 1
