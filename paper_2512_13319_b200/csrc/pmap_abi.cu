@@ -266,6 +266,11 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   p->runner.reset(rn);
   p->elem_real = rn->sizeof_real();
   rn->set_attrs();
+  if (!rn->prepare(*p)) {
+    cudaGetLastError();
+    p->err = "plan preparation (LTI tables) failed";
+    return MAP_E_CUDA;
+  }
   // workspace
   p->ws_tf = (p->kind != Kind::NL) && d.world == 1;
   p->ws_bytes = rn->ws_bytes(g, p->ws_tf);
@@ -289,6 +294,12 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     }
   }
   if (cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&p->stream3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&p->stream4, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_edge0, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_edge1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_edge2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_edge3, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess)
     return MAP_E_CUDA;
@@ -315,6 +326,10 @@ void map_plan_destroy(map_plan_t p) {
   cudaFree(p->dev_tv);
   cudaFree(p->m0_dev);
   if (p->stream2) cudaStreamDestroy(p->stream2);
+  if (p->stream3) cudaStreamDestroy(p->stream3);
+  if (p->stream4) cudaStreamDestroy(p->stream4);
+  for (cudaEvent_t e : {p->ev_edge0, p->ev_edge1, p->ev_edge2, p->ev_edge3})
+    if (e) cudaEventDestroy(e);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   delete[] p->m0_host;

@@ -171,18 +171,52 @@ struct LUF {
   R a[N][N];   // strictly lower: L multipliers; upper incl. diagonal: U
   R dinv[N];   // 1 / U[i][i]
   int piv[N];  // row swapped with row k at step k
+  bool nopiv;  // no swap happened (fast path)
 };
 
-template <typename R>
-PM_INLINE R pm_abs(R x) { return x < R(0) ? -x : x; }
+PM_INLINE double pm_abs(double x) { return fabs(x); }
+PM_INLINE float pm_abs(float x) { return fabsf(x); }
 
 template <typename R>
 PM_INLINE R pm_rcp(R x) { return R(1) / x; }
 
 // Factorise f.a in place.  Row swaps are predicated selects (no dynamic
 // register indexing).  `ok` is cleared on a zero or non-finite pivot.
+// Fast path: if the matrix is column diagonally dominant, Gaussian elimination
+// keeps it so and partial pivoting (strict ">" test) never swaps -- the
+// unpivoted factorisation below is then bit-identical to the pivoted one and
+// skips every select.  The (I + C J) matrices of the per-node updates are
+// dominant for small dt; general aggregates fall back to the pivoted path.
 template <typename R, int N>
 PM_INLINE void lu_factor(LUF<R, N>& f, bool& ok) {
+  bool dom = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    R off = R(0);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (i != k) off += pm_abs(f.a[i][k]);
+    dom = dom && (pm_abs(f.a[k][k]) >= off);
+  }
+  f.nopiv = dom;
+  if (dom) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      f.piv[k] = k;
+      R d = f.a[k][k];
+      ok = ok && (d != R(0)) && (d == d);
+      R di = pm_rcp(d);
+      f.dinv[k] = di;
+#pragma unroll
+      for (int i = k + 1; i < N; ++i) {
+        R l = f.a[i][k] * di;
+        f.a[i][k] = l;
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) f.a[i][j] = fma(-l, f.a[k][j], f.a[i][j]);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     int p = k;
@@ -222,6 +256,7 @@ PM_INLINE void lu_factor(LUF<R, N>& f, bool& ok) {
 // x <- P^{-1} x   where P = Pi^T L U
 template <typename R, int N>
 PM_INLINE void lu_solve(const LUF<R, N>& f, R (&x)[N]) {
+  if (!f.nopiv) {
 #pragma unroll
   for (int k = 0; k < N; ++k) {
 #pragma unroll
@@ -231,6 +266,7 @@ PM_INLINE void lu_solve(const LUF<R, N>& f, R (&x)[N]) {
       x[k] = sw ? xi : xk;
       x[i] = sw ? xk : xi;
     }
+  }
   }
 #pragma unroll
   for (int i = 1; i < N; ++i)
@@ -257,6 +293,7 @@ PM_INLINE void lu_solve_t(const LUF<R, N>& f, R (&x)[N]) {
   for (int i = N - 2; i >= 0; --i)
 #pragma unroll
     for (int j = i + 1; j < N; ++j) x[i] = fma(-f.a[j][i], x[j], x[i]);
+  if (f.nopiv) return;
 #pragma unroll
   for (int k = N - 1; k >= 0; --k) {
 #pragma unroll

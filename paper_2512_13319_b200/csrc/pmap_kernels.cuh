@@ -16,7 +16,8 @@
 //                  the pass-2 transition build and the per-run affine fold, plus
 //                  the per-tile suffix scan of the affine run aggregates
 //   pass 2 (trajectory)
-//     k_p2_tiles   per trajectory: x* at each tile's last node (seeded with
+//     k_p2_tiles   per group of NT2 tiles: suffix composition of tile aggregates
+//     k_p2_groups  per trajectory: x* at each group's last node (seeded with
 //                  x*_T = S_T^-1 v_T)
 //     k_p2_down    per run: x*_{i-1} = (I + C_i S_{i-1})^-1 (A_i x*_i + b_i + C_i v_{i-1})
 // Workspace layouts are SoA "field-major" so that a warp touches consecutive
@@ -36,7 +37,7 @@ struct Geom {
 
 constexpr int NT2 = 128;  // tiles per group (k_p1_tiles block size)
 constexpr int NT3 = 128;  // k_p1_groups block size
-constexpr int NT4 = 256;  // k_p2_tiles block size
+constexpr int NT4 = 256;  // k_p2_groups block size
 
 PM_INLINE void flag_node(unsigned long long* flag, int64_t node) {
   atomicMin(flag, (unsigned long long)node);
@@ -53,16 +54,25 @@ PM_INLINE bool finite_vf(const VF<R, N>& V) {
 }
 
 // ----------------------------------------------------------------- pass 1a
+// nsel > 0: only the listed tiles {jsel0, jsel1} of each trajectory (the boundary
+// tiles left over by the LTI-specialised reduce), else every tile.
 template <typename R, int N, int NY, int NT, int K, class Src, bool REV>
 __global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src src, const Geom g,
                                                   const R* __restrict__ y, const R* __restrict__ xbar,
                                                   R* __restrict__ run_incl, R* __restrict__ tile_agg,
-                                                  unsigned long long* flag) {
+                                                  unsigned long long* flag, int nsel, int64_t jsel0, int64_t jsel1) {
   using E = Elem<R, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sh = reinterpret_cast<R*>(smem_raw);  // [E::SZ][NT]
-  const int64_t tile = blockIdx.x;
-  const int64_t b = tile / g.tpt, j = tile % g.tpt;
+  int64_t b, j;
+  if (nsel > 0) {
+    b = blockIdx.x / nsel;
+    j = (blockIdx.x % nsel == 0) ? jsel0 : jsel1;
+  } else {
+    b = blockIdx.x / g.tpt;
+    j = blockIdx.x % g.tpt;
+  }
+  const int64_t tile = b * g.tpt + j;
   const int r = threadIdx.x;
   const int64_t l0 = (j * NT + r) * (int64_t)K;
   const R* yb = y + b * g.Nn * NY;
@@ -244,17 +254,19 @@ __global__ void __launch_bounds__(NT) k_p1_down(const __grid_constant__ Src src,
     if (l >= g.Nn) break;
     const int64_t gi = g.node0 + l;
     E e;
-    src.node(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
     if (gi == 0) {
+      src.node(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
 #pragma unroll
       for (int k = 0; k < Dim<N>::NS; ++k) cur.S[k] = e.J[k];
 #pragma unroll
       for (int i = 0; i < N; ++i) cur.v[i] = e.h[i];
     } else if (P2) {
+      src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       A tr;
       vapply<R, N, true>(e, cur, cur, &tr, ok);
       compose(agg, tr, agg);  // run aggregate maps x*_{l} -> x*_{l0 - 1}
     } else {
+      src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       vapply<R, N, false>(e, cur, cur, nullptr, ok);
     }
     store(cur, svt + m * NT + r, (int64_t)K * NT);
@@ -298,13 +310,54 @@ PM_INLINE void load_sv(const R* sv, const Geom& g, int64_t b, int64_t l, VF<R, N
 }
 
 // ----------------------------------------------------------------- pass 2a
-// x* at the last node of every tile (exclusive suffix over tile aggregates,
+// Exclusive suffix composition of tile affine aggregates within groups of NT2 tiles.
+template <typename R, int N>
+__global__ void __launch_bounds__(NT2) k_p2_tiles(const Geom g, const R* __restrict__ tile_agg2,
+                                                  R* __restrict__ tile_sufx, R* __restrict__ group_agg2) {
+  using A = Aff<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);  // [A::SZ][NT2]
+  const int64_t grp = blockIdx.x;
+  const int64_t b = grp / g.gpt, gg = grp % g.gpt;
+  const int t = threadIdx.x;
+  const int64_t jt = gg * NT2 + t;
+  const bool valid = jt < g.tpt;
+  A acc;
+  if (valid)
+    load(acc, tile_agg2 + (b * g.tpt + jt) * A::SZ, 1);
+  else
+    set_identity(acc);
+#pragma unroll 1
+  for (int d = 1; d < NT2; d <<= 1) {
+    store(acc, sh + t, NT2);
+    __syncthreads();
+    if (t + d < NT2) {
+      A p;
+      load(p, sh + t + d, NT2);
+      compose(acc, p, acc);
+    }
+    __syncthreads();
+  }
+  store(acc, sh + t, NT2);
+  __syncthreads();
+  if (valid) {
+    A ex;
+    if (t + 1 < NT2)
+      load(ex, sh + t + 1, NT2);
+    else
+      set_identity(ex);
+    store(ex, tile_sufx + (b * g.tpt + jt) * A::SZ, 1);
+  }
+  if (t == 0) store(acc, group_agg2 + grp * A::SZ, 1);
+}
+
+// x* at the last node of every tile group (exclusive suffix over group aggregates,
 // seeded with x_end = S_T^-1 v_T on the rank holding node T, or the shard carry).
 template <typename R, int N, int NT, int K>
-__global__ void __launch_bounds__(NT4) k_p2_tiles(const Geom g, const R* __restrict__ sv,
-                                                  const R* __restrict__ tile_agg2, const R* __restrict__ xend_in,
-                                                  R* __restrict__ tile_carry, R* __restrict__ total_agg2,
-                                                  unsigned long long* flag) {
+__global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __restrict__ sv,
+                                                   const R* __restrict__ group_agg2, const R* __restrict__ xend_in,
+                                                   R* __restrict__ group_carry, R* __restrict__ total_agg2,
+                                                   unsigned long long* flag) {
   using A = Aff<R, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sh = reinterpret_cast<R*>(smem_raw);  // [A::SZ][NT4] + N
@@ -325,13 +378,13 @@ __global__ void __launch_bounds__(NT4) k_p2_tiles(const Geom g, const R* __restr
 #pragma unroll
     for (int i = 0; i < N; ++i) shx[i] = x[i];
   }
-  const int64_t c = (g.tpt + NT4 - 1) / NT4;
-  const int64_t k0 = t * c, k1 = min(g.tpt, k0 + c);
+  const int64_t c = (g.gpt + NT4 - 1) / NT4;
+  const int64_t k0 = t * c, k1 = min(g.gpt, k0 + c);
   A acc;
   set_identity(acc);
   for (int64_t k = k1 - 1; k >= k0; --k) {
     A p;
-    load(p, tile_agg2 + (b * g.tpt + k) * A::SZ, 1);
+    load(p, group_agg2 + (b * g.gpt + k) * A::SZ, 1);
     compose(p, acc, acc);
   }
 #pragma unroll 1
@@ -358,9 +411,9 @@ __global__ void __launch_bounds__(NT4) k_p2_tiles(const Geom g, const R* __restr
   }
   for (int64_t k = k1 - 1; k >= k0; --k) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) tile_carry[(b * g.tpt + k) * N + i] = x[i];
+    for (int i = 0; i < N; ++i) group_carry[(b * g.gpt + k) * N + i] = x[i];
     A p;
-    load(p, tile_agg2 + (b * g.tpt + k) * A::SZ, 1);
+    load(p, group_agg2 + (b * g.gpt + k) * A::SZ, 1);
     apply(p, x);
   }
   if (!ok) flag_node(flag, g.node0 + g.Nn - 1);
@@ -370,9 +423,9 @@ __global__ void __launch_bounds__(NT4) k_p2_tiles(const Geom g, const R* __restr
 template <typename R, int N, int NT, int K, class Src>
 __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src, const Geom g,
                                                 const R* __restrict__ xbar, const R* __restrict__ sv,
-                                                const R* __restrict__ run_suf, const R* __restrict__ tile_carry,
-                                                const R* __restrict__ carry_in, R* __restrict__ x_out,
-                                                unsigned long long* flag) {
+                                                const R* __restrict__ run_suf, const R* __restrict__ tile_sufx,
+                                                const R* __restrict__ group_carry, const R* __restrict__ carry_in,
+                                                R* __restrict__ x_out, unsigned long long* flag) {
   using V = VF<R, N>;
   using A = Aff<R, N>;
   const int64_t tile = blockIdx.x;
@@ -383,10 +436,12 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
   bool ok = true;
   R x[N];
 #pragma unroll
-  for (int i = 0; i < N; ++i) x[i] = tile_carry[tile * N + i];
+  for (int i = 0; i < N; ++i) x[i] = group_carry[(b * g.gpt + j / NT2) * N + i];
   {
     A s;
-    load(s, run_suf + tile * (int64_t)A::SZ * NT + r, NT);
+    load(s, tile_sufx + tile * (int64_t)A::SZ, 1);  // x at the tile's last node
+    apply(s, x);
+    load(s, run_suf + tile * (int64_t)A::SZ * NT + r, NT);  // x at the run's last node
     apply(s, x);
   }
   R* xo = x_out + b * g.Nn * N;

@@ -1,0 +1,524 @@
+// pmap_lti.cuh -- pass-1 reduce specialised for time-invariant (LTI) linear models.
+//
+// For an LTI model every interior node element is E_i = (A, b, C, eta_i, J) with
+// only eta_i = K y_i - K r depending on the data (R-ELEM).  The combination rule
+// P:395-407 is affine in the data parts (b, eta) with coefficient matrices that
+// depend only on the matrix parts (A, C, J) of the two operands:
+//   b   = [A2 M] b1 + [A2 M C1] eta2 + b2
+//   eta = [A1^T M^T] eta2 - [A1^T M^T J2] b1 + eta1,      M = (I + C1 J2)^-1.
+// In an interior tile (all runs full, node 0 not included) the matrix parts of
+// every run fold prefix and of every Kogge-Stone span are therefore identical
+// across runs and tiles: they are computed once at plan time by k_lti_setup (a
+// one-thread device kernel; model-only data, O(K + NT) combines), and the
+// per-solve reduce k_p1_reduce_lti only propagates the data parts: ~40 FMA per
+// node (fold) + 4 N x N mat-vecs per Kogge-Stone round, instead of one general
+// combine (580 FMA at nx = 4) per node.  Boundary tiles (the one holding node 0,
+// a ragged last tile) use the general k_p1_reduce.  Output format (run_incl,
+// tile_agg) is identical to k_p1_reduce, so every later kernel is shared.
+#pragma once
+#include "pmap_kernels.cuh"
+
+namespace pmap {
+
+template <typename R, int N, int NT, int K>
+struct LtiTables {
+  static constexpr int NS = Dim<N>::NS;
+  // run fold, step m = 1..K-1 (index m):  b' = b + Wb eta + cb ;  eta' = We eta + ce + eta_m
+  R Wb[K][N][N];
+  R cb[K][N];
+  R We[K][N][N];
+  R ce[K][N];
+  // matrix parts of the fold prefix of m + 1 nodes, m = 0..K-1
+  R PA[K][N][N];
+  R PC[K][NS];
+  R PJ[K][NS];
+  // matrix parts of a span of l full runs, l = 1..NT (index l-1)
+  R SA[NT][N][N];
+  R SC[NT][NS];
+  R SJ[NT][NS];
+  // the same, field-major: SF[f][l-1] (f over A, C, J) so lane r reads column r coalesced
+  R SF[N * N + 2 * NS][NT];
+  // Kogge-Stone round d (1, 2, 4, ..), partner span l2 in 1..d: index d + l2 - 2
+  R U1[NT - 1][N][N];
+  R U2[NT - 1][N][N];
+  R U3[NT - 1][N][N];
+  R U4[NT - 1][N][N];
+};
+
+// M = (I + C1 J2)^-1 explicitly (plan-time only), via the pivoted LU of pmap_algebra.
+template <typename R, int N>
+PM_INLINE void inv_ICJ(const R (&C1)[Dim<N>::NS], const R (&J2)[Dim<N>::NS], R (&M)[N][N]) {
+  LUF<R, N> f;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = (i == j) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(C1[sidx(i, k, N)], J2[sidx(k, j, N)], s);
+      f.a[i][j] = s;
+    }
+  bool ok = true;
+  lu_factor(f, ok);
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    R t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = (i == c) ? R(1) : R(0);
+    lu_solve(f, t);
+#pragma unroll
+    for (int i = 0; i < N; ++i) M[i][c] = t[i];
+  }
+}
+
+template <typename R, int N>
+PM_INLINE void matmul(const R (&X)[N][N], const R (&Y)[N][N], R (&Z)[N][N]) {
+  R T[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(X[i][k], Y[k][j], s);
+      T[i][j] = s;
+    }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) Z[i][j] = T[i][j];
+}
+
+template <typename R, int N>
+PM_INLINE void unpack(const R (&P)[Dim<N>::NS], R (&M)[N][N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) M[i][j] = P[sidx(i, j, N)];
+}
+
+// Matrix parts of an interior LTI node element and its measurement map.
+template <typename R, int N, int NY>
+struct LtiNode {
+  R A[N][N];
+  R b[N];
+  R C[Dim<N>::NS];
+  R J[Dim<N>::NS];
+  R K[N][NY];  // eta_i = K y_i + h0
+  R h0[N];
+};
+
+// Kernel-parameter copy of the node data and the run-fold tables: read through the
+// constant bank, so the fully unrolled fold uses them as DFMA constant operands
+// (no load instructions; ~10.7 KB at nx = 4, within the 32 KB parameter limit).
+template <typename R, int N, int NY, int K>
+struct LtiFoldParams {
+  LtiNode<R, N, NY> node;
+  R Wb[K][N][N];
+  R cb[K][N];
+  R We[K][N][N];
+  R ce[K][N];
+};
+
+// Plan-time tables (one thread; model-only quantities).
+template <typename R, int N, int NY, int NT, int K>
+__global__ void k_lti_setup(const LtiNode<R, N, NY> src, LtiTables<R, N, NT, K>* tab, int* okflag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  using E = Elem<R, N>;
+  bool ok = true;
+  E node;  // interior node element with zero data parts
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) node.A[i][j] = src.A[i][j];
+    node.b[i] = src.b[i];
+    node.h[i] = R(0);
+  }
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) {
+    node.C[k] = src.C[k];
+    node.J[k] = src.J[k];
+  }
+  R Am[N][N], Cm[N][N];
+  unpack<R, N>(node.C, Cm);
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) Am[i][j] = node.A[i][j];
+  E acc = node;
+  auto put_prefix = [&](int m) {
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) tab->PA[m][i][j] = acc.A[i][j];
+    for (int k = 0; k < Dim<N>::NS; ++k) {
+      tab->PC[m][k] = acc.C[k];
+      tab->PJ[m][k] = acc.J[k];
+    }
+  };
+  put_prefix(0);
+  for (int m = 1; m < K; ++m) {
+    R M[N][N], A2M[N][N], T[N][N], J2m[N][N];
+    inv_ICJ<R, N>(node.C, acc.J, M);
+    matmul<R, N>(acc.A, M, A2M);
+    matmul<R, N>(A2M, Cm, T);
+    unpack<R, N>(acc.J, J2m);
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+      for (int k = 0; k < N; ++k) s = fma(A2M[i][k], node.b[k], s);
+      tab->cb[m][i] = s;
+      for (int j = 0; j < N; ++j) tab->Wb[m][i][j] = T[i][j];
+    }
+    // We = A^T M^T ;  ce = -A^T M^T J2 b
+    R AtMt[N][N];
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        R s = R(0);
+        for (int k = 0; k < N; ++k) s = fma(Am[k][i], M[j][k], s);
+        AtMt[i][j] = s;
+      }
+    R J2b[N];
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+      for (int k = 0; k < N; ++k) s = fma(J2m[i][k], node.b[k], s);
+      J2b[i] = s;
+    }
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+      for (int k = 0; k < N; ++k) s = fma(-AtMt[i][k], J2b[k], s);
+      tab->ce[m][i] = s;
+      for (int j = 0; j < N; ++j) tab->We[m][i][j] = AtMt[i][j];
+    }
+    combine(node, acc, acc, ok);
+    put_prefix(m);
+  }
+  // spans of l full runs (flipped: later span on the left)
+  E run = acc, span = acc;
+  for (int l = 1; l <= NT; ++l) {
+    if (l > 1) combine(run, span, span, ok);
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) tab->SA[l - 1][i][j] = span.A[i][j];
+    for (int k = 0; k < Dim<N>::NS; ++k) {
+      tab->SC[l - 1][k] = span.C[k];
+      tab->SJ[l - 1][k] = span.J[k];
+    }
+    int f = 0;
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) tab->SF[f++][l - 1] = span.A[i][j];
+    for (int k = 0; k < Dim<N>::NS; ++k) tab->SF[f++][l - 1] = span.C[k];
+    for (int k = 0; k < Dim<N>::NS; ++k) tab->SF[f++][l - 1] = span.J[k];
+  }
+  // Kogge-Stone coefficient sets: own span d (left), partner span l2 (right)
+  for (int d = 1; d < NT; d <<= 1) {
+    for (int l2 = 1; l2 <= d; ++l2) {
+      const int idx = d + l2 - 2;
+      R C1[Dim<N>::NS], J2[Dim<N>::NS], A1[N][N], A2[N][N], C1m[N][N], J2m[N][N], M[N][N], A2M[N][N], T[N][N];
+      for (int k = 0; k < Dim<N>::NS; ++k) {
+        C1[k] = tab->SC[d - 1][k];
+        J2[k] = tab->SJ[l2 - 1][k];
+      }
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          A1[i][j] = tab->SA[d - 1][i][j];
+          A2[i][j] = tab->SA[l2 - 1][i][j];
+        }
+      unpack<R, N>(C1, C1m);
+      unpack<R, N>(J2, J2m);
+      inv_ICJ<R, N>(C1, J2, M);
+      matmul<R, N>(A2, M, A2M);
+      matmul<R, N>(A2M, C1m, T);
+      R AtMt[N][N], U4[N][N];
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          R s = R(0);
+          for (int k = 0; k < N; ++k) s = fma(A1[k][i], M[j][k], s);
+          AtMt[i][j] = s;
+        }
+      matmul<R, N>(AtMt, J2m, U4);
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          tab->U1[idx][i][j] = A2M[i][j];
+          tab->U2[idx][i][j] = T[i][j];
+          tab->U3[idx][i][j] = AtMt[i][j];
+          tab->U4[idx][i][j] = U4[i][j];
+        }
+    }
+  }
+  *okflag = ok ? 1 : 0;
+}
+
+template <typename R, int N>
+PM_INLINE void matvec_acc(const R* __restrict__ M, const R (&x)[N], R (&y)[N]) {  // y += M x (row-major)
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = y[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(__ldg(M + i * N + k), x[k], s);
+    y[i] = s;
+  }
+}
+
+// Interior tiles only: blockIdx.x -> (trajectory b, tile j = j_lo + blockIdx.x % n_int).
+// REV: reversed node order (two-filter pass B over mirrored elements).
+// The tile's y block is staged through shared memory (coalesced global reads, a
+// padded row per run so the per-run reads are bank-conflict free).
+template <typename R, int N, int NY, int NT, int K, bool REV>
+__global__ void __launch_bounds__(NT) k_p1_reduce_lti(const __grid_constant__ LtiFoldParams<R, N, NY, K> fp,
+                                                      const Geom g, int64_t j_lo, int64_t n_int,
+                                                      const R* __restrict__ y,
+                                                      const LtiTables<R, N, NT, K>* __restrict__ tab,
+                                                      R* __restrict__ run_incl, R* __restrict__ tile_agg) {
+  using E = Elem<R, N>;
+  // padded run row in shared memory: 16-byte aligned rows, consecutive runs 4 banks apart
+  constexpr int ROW = ((K * NY * (int)sizeof(R) + 15) / 16 * 16 + 16) / (int)sizeof(R);
+  __shared__ __align__(16) R ys[NT * ROW];
+  __shared__ R sh[2 * N][NT];
+  const LtiNode<R, N, NY>& src = fp.node;
+  const int64_t b = blockIdx.x / n_int;
+  const int64_t j = j_lo + blockIdx.x % n_int;
+  const int64_t tile = b * g.tpt + j;
+  const int r = threadIdx.x;
+  // stage y: the tile covers local nodes [j NT K, (j+1) NT K) (REV: mirrored).
+  // One cp.async (LDGSTS) per node row: all in flight at once, padded destination.
+  {
+    const int64_t base = REV ? (g.Nn - (j + 1) * (int64_t)NT * K) : j * (int64_t)NT * K;
+    const R* src_y = y + (b * g.Nn + base) * NY;
+    constexpr int BYTES = NY * (int)sizeof(R);
+    static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16 || BYTES % 16 == 0, "row size");
+#pragma unroll 4
+    for (int node = r; node < NT * K; node += NT) {
+      const int tnode = REV ? NT * K - 1 - node : node;  // reversed order within the tile
+      const int run = tnode / K, m = tnode - run * K;
+      R* dst = ys + run * ROW + m * NY;
+      const R* srcp = src_y + (int64_t)node * NY;
+      const unsigned sdst = (unsigned)__cvta_generic_to_shared(dst);
+      if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 16; ++c)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + 16 * c), "l"(srcp + c * (16 / sizeof(R))));
+      } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sdst), "l"(srcp), "n"(BYTES));
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  }
+  __syncthreads();
+  const R* yr = ys + r * ROW;
+  R bb[N], hh[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = src.h0[i];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], yr[k], s);
+    hh[i] = s;
+    bb[i] = src.b[i];
+  }
+#pragma unroll
+  for (int m = 1; m < K; ++m) {
+    R yv[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) yv[k] = yr[m * NY + k];
+    R nb[N], nh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = bb[i] + fp.cb[m][i];
+      R t = src.h0[i] + fp.ce[m][i];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) t = fma(src.K[i][k], yv[k], t);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s = fma(fp.Wb[m][i][k], hh[k], s);
+        t = fma(fp.We[m][i][k], hh[k], t);
+      }
+      nb[i] = s;
+      nh[i] = t;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = nb[i];
+      hh[i] = nh[i];
+    }
+  }
+  // Kogge-Stone over runs, data parts only
+#pragma unroll 1
+  for (int d = 1; d < NT; d <<= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      sh[i][r] = bb[i];
+      sh[N + i][r] = hh[i];
+    }
+    __syncthreads();
+    if (r >= d) {
+      const int l2 = min(r - d + 1, d);
+      const int idx = d + l2 - 2;
+      R b2[N], h2[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        b2[i] = sh[i][r - d];
+        h2[i] = sh[N + i][r - d];
+      }
+      R nb[N], nh[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        nb[i] = b2[i];
+        nh[i] = hh[i];
+      }
+      matvec_acc<R, N>(&tab->U1[idx][0][0], bb, nb);
+      matvec_acc<R, N>(&tab->U2[idx][0][0], h2, nb);
+      matvec_acc<R, N>(&tab->U3[idx][0][0], h2, nh);
+      R mb[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) mb[i] = -bb[i];
+      matvec_acc<R, N>(&tab->U4[idx][0][0], mb, nh);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        bb[i] = nb[i];
+        hh[i] = nh[i];
+      }
+    }
+    __syncthreads();
+  }
+  // write the full inclusive prefix element: matrix parts of a span of r + 1 runs
+  // (field-major table: coalesced across the warp)
+  R* out = run_incl + tile * (int64_t)E::SZ * NT + r;
+  int f = 0, t = 0;
+#pragma unroll
+  for (int i = 0; i < N * N; ++i) out[(f++) * NT] = __ldg(&tab->SF[t++][r]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[(f++) * NT] = bb[i];
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) out[(f++) * NT] = __ldg(&tab->SF[t++][r]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[(f++) * NT] = hh[i];
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) out[(f++) * NT] = __ldg(&tab->SF[t++][r]);
+  if (r == NT - 1) {
+    E e;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) e.A[i][jj] = tab->SA[NT - 1][i][jj];
+      e.b[i] = bb[i];
+      e.h[i] = hh[i];
+    }
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) {
+      e.C[k] = tab->SC[NT - 1][k];
+      e.J[k] = tab->SJ[NT - 1][k];
+    }
+    store(e, tile_agg + tile * (int64_t)E::SZ, 1);
+  }
+}
+
+// Data parts (b, eta) of the fold of q consecutive interior nodes whose first row is
+// yrow(0) (LTI recurrence, steps 1..q-1 of the tables).
+template <typename R, int N, int NY, int NT, int K, class YRow>
+PM_INLINE void lti_fold_data(const LtiNode<R, N, NY>& src, const LtiTables<R, N, NT, K>* __restrict__ tab, int q,
+                             YRow yrow, R (&bb)[N], R (&hh)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = src.h0[i];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], yrow(0)[k], s);
+    hh[i] = s;
+    bb[i] = src.b[i];
+  }
+  for (int m = 1; m < q; ++m) {
+    R yv[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) yv[k] = yrow(m)[k];
+    R nb[N], nh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = bb[i] + __ldg(&tab->cb[m][i]);
+      R t = src.h0[i] + __ldg(&tab->ce[m][i]);
+#pragma unroll
+      for (int k = 0; k < NY; ++k) t = fma(src.K[i][k], yv[k], t);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s = fma(__ldg(&tab->Wb[m][i][k]), hh[k], s);
+        t = fma(__ldg(&tab->We[m][i][k]), hh[k], t);
+      }
+      nb[i] = s;
+      nh[i] = t;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = nb[i];
+      hh[i] = nh[i];
+    }
+  }
+}
+
+// Boundary tiles of an LTI model (the tile holding node 0 / the terminal node, a
+// ragged last tile): run elements from the LTI data recurrence and the fold-prefix
+// matrix tables (plus one general combine with E_0 / M_T for the run holding it),
+// then a general Kogge-Stone over the runs.  blockIdx.x -> (b, jsel[k]).
+template <typename R, int N, int NY, int NT, int K, class Src, bool REV>
+__global__ void __launch_bounds__(NT) k_p1_reduce_lti_edge(const __grid_constant__ Src gsrc,
+                                                           const __grid_constant__ LtiNode<R, N, NY> src, const Geom g,
+                                                           int nsel, int64_t jsel0, int64_t jsel1,
+                                                           const R* __restrict__ y,
+                                                           const LtiTables<R, N, NT, K>* __restrict__ tab,
+                                                           R* __restrict__ run_incl, R* __restrict__ tile_agg,
+                                                           unsigned long long* flag) {
+  using E = Elem<R, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sh = reinterpret_cast<R*>(smem_raw);  // [E::SZ][NT]
+  const int64_t b = blockIdx.x / nsel;
+  const int64_t j = (blockIdx.x % nsel == 0) ? jsel0 : jsel1;
+  const int64_t tile = b * g.tpt + j;
+  const int r = threadIdx.x;
+  const int64_t l0 = (j * NT + r) * (int64_t)K;
+  const R* yb = y + b * g.Nn * NY;
+  auto lidx = [&](int64_t lr) { return REV ? (g.Nn - 1 - lr) : lr; };
+  const int64_t rem = g.Nn - l0;
+  const int q = rem <= 0 ? 0 : (rem >= K ? K : (int)rem);
+  const bool first = (l0 == 0) && (REV || g.node0 == 0);  // run holds E_0 (or M_T)
+  bool ok = true;
+  E acc;
+  set_identity(acc);
+  if (q > 0) {
+    const int qf = first ? q - 1 : q;  // interior nodes of the run
+    const int64_t s0 = first ? l0 + 1 : l0;
+    if (qf > 0) {
+      R bb[N], hh[N];
+      lti_fold_data<R, N, NY, NT, K>(src, tab, qf, [&](int m) { return yb + lidx(s0 + m) * NY; }, bb, hh);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) acc.A[i][jj] = tab->PA[qf - 1][i][jj];
+        acc.b[i] = bb[i];
+        acc.h[i] = hh[i];
+      }
+#pragma unroll
+      for (int k = 0; k < Dim<N>::NS; ++k) {
+        acc.C[k] = tab->PC[qf - 1][k];
+        acc.J[k] = tab->PJ[qf - 1][k];
+      }
+    }
+    if (first) {
+      const int64_t l = lidx(l0);
+      E e0;
+      gsrc.node(g.node0 + l, yb + l * NY, (const R*)nullptr, e0);
+      if (qf > 0)
+        combine(acc, e0, acc, ok);  // later nodes on the left (R-FLIP)
+      else
+        acc = e0;
+    }
+  }
+#pragma unroll 1
+  for (int d = 1; d < NT; d <<= 1) {
+    store(acc, sh + r, NT);
+    __syncthreads();
+    if (r >= d) {
+      E p;
+      load(p, sh + r - d, NT);
+      combine(acc, p, acc, ok);
+    }
+    __syncthreads();
+  }
+  store(acc, run_incl + tile * (int64_t)E::SZ * NT + r, NT);
+  if (r == NT - 1) store(acc, tile_agg + tile * (int64_t)E::SZ, 1);
+  if (!ok) atomicMin(flag, (unsigned long long)(g.node0 + l0));
+}
+
+}  // namespace pmap

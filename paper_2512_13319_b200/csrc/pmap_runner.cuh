@@ -16,6 +16,9 @@
 #include "../../include/pmap.h"
 #include "pmap_kernels.cuh"
 #include "pmap_tf.cuh"
+#include "pmap_lti.cuh"
+#include <cstdlib>
+#include <type_traits>
 
 using namespace pmap;
 
@@ -63,7 +66,7 @@ inline bool h_is_finite(const double* a, int n) {
 template <typename R, int N>
 struct WsLayout {
   size_t run_incl, tile_agg1, tile_incl1, group_agg1, group_carry1, total1, sv, run_suf, tile_agg2,
-      tile_carry2, total2, carry_in, xend, tf_run, tf_tile, tf_tincl, tf_gagg, tf_gcarry, bytes;
+      tile_sufx2, group_agg2, group_carry2, total2, carry_in, xend, tf_run, tf_tile, tf_tincl, tf_gagg, tf_gcarry, bytes;
   void plan(const Geom& g, bool tf) {
     using E = Elem<R, N>;
     using V = VF<R, N>;
@@ -84,7 +87,9 @@ struct WsLayout {
     sv = take(nt * V::SZ * kK * kNT);
     run_suf = take(nt * A::SZ * kNT);
     tile_agg2 = take(nt * A::SZ);
-    tile_carry2 = take(nt * N);
+    tile_sufx2 = take(nt * A::SZ);
+    group_agg2 = take(ng * A::SZ);
+    group_carry2 = take(ng * N);
     total2 = take(B * (A::SZ + N));
     carry_in = take(B * V::SZ);
     xend = take(B * N);
@@ -108,6 +113,8 @@ struct Runner {
   virtual ~Runner() {}
   virtual size_t ws_bytes(const Geom& g, bool tf) const = 0;
   virtual void set_attrs() = 0;
+  // plan-time device preparation (LTI tables); returns false on failure
+  virtual bool prepare(PlanState& p) = 0;
   // one parallel-RTS solve (pass 1 + pass 2); xbar only for nonlinear sources
   virtual void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) = 0;
   virtual void two_filter(PlanState& p, const void* y, void* x) = 0;
@@ -159,7 +166,9 @@ struct PlanState {
   int64_t graph_launches = 0;
   size_t elem_real = 8;
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
+  cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_edge0 = nullptr, ev_edge1 = nullptr, ev_edge2 = nullptr, ev_edge3 = nullptr;
   // per-kernel CUDA-event profiling (map_profile_enable / map_profile_read)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -177,13 +186,14 @@ struct PlanState {
 };
 
 // kernel classes reported by map_profile_read
-enum KernelId { K_P1_REDUCE = 0, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_DOWN, K_FILTER_OUT,
-                K_TF_REDUCE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD, K_NL_MISC, K_COUNT };
+enum KernelId { K_P1_REDUCE = 0, K_P1_REDUCE_EDGE, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_GROUPS,
+                K_P2_DOWN, K_FILTER_OUT, K_TF_REDUCE, K_TF_REDUCE_EDGE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD,
+                K_NL_MISC, K_COUNT };
 inline const char* kernel_name(int id) {
-  static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_tiles", "k_p1_groups", "k_p1_down", "k_p2_tiles",
-                                       "k_p2_down", "k_filter_out", "k_tf_reduce(k_p1_reduce<Mirror>)",
-                                       "k_tf_tiles(k_p1_tiles)", "k_tf_groups(k_p1_groups)", "k_tf_down",
-                                       "k_shard_*", "k_fill_m0/k_maxdiff"};
+  static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_reduce_lti_edge", "k_p1_tiles", "k_p1_groups",
+                                       "k_p1_down", "k_p2_tiles", "k_p2_groups", "k_p2_down", "k_filter_out",
+                                       "k_tf_reduce", "k_tf_reduce_lti_edge", "k_tf_tiles", "k_tf_groups",
+                                       "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff"};
   return (id >= 0 && id < K_COUNT) ? names[id] : "?";
 }
 
@@ -221,6 +231,62 @@ struct RunnerT : Runner {
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
+  static constexpr bool IS_LTI = std::is_same<Src, SrcLTI<R, N, NY>>::value;
+  using Tab = LtiTables<R, N, kNT, kK>;
+  Tab* tab = nullptr;    // pass-1 tables (LTI only)
+  Tab* tab_m = nullptr;  // mirrored-element tables (two-filter pass B)
+  LtiNode<R, N, NY> lnode{}, lnode_m{};
+  LtiFoldParams<R, N, NY, kK> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
+  bool use_lti = false;
+
+  ~RunnerT() override {
+    cudaFree(tab);
+    cudaFree(tab_m);
+  }
+
+  bool prepare(PlanState& p) override;
+
+  // Pass-1 reduce: LTI-specialised kernel on interior tiles, general kernel on the
+  // boundary tiles (node 0 / terminal node, ragged last tile); all tiles otherwise.
+  template <bool REV, class KS>
+  void reduce1(PlanState& p, cudaStream_t s, int kid, const KS& ksrc, const LtiFoldParams<R, N, NY, kK>& fpar,
+               const Tab* tb, const R* y, const R* xbar, R* run_incl, R* tile_agg) {
+    const LtiNode<R, N, NY>& ln = fpar.node;
+    const Geom& g = p.g;
+    if (!(use_lti && tb)) {
+      PM_LAUNCH(p, s, kid,
+                (k_p1_reduce<R, N, NY, kNT, kK, KS, REV><<<(unsigned)(g.batch * g.tpt), kNT, smem_reduce(), s>>>(
+                    ksrc, g, y, xbar, run_incl, tile_agg, p.dflag, 0, 0, 0)));
+      return;
+    }
+    const int64_t Lt = (int64_t)kNT * kK;
+    const int64_t j_lo = (REV || g.node0 == 0) ? 1 : 0;
+    const int64_t j_hi = g.Nn / Lt;  // full tiles
+    const int64_t n_int = j_hi > j_lo ? j_hi - j_lo : 0;
+    int nsel = 0;
+    int64_t js[2] = {0, 0};
+    if (j_lo == 1) js[nsel++] = 0;
+    if (j_hi < g.tpt && !(nsel == 1 && js[0] == g.tpt - 1)) js[nsel++] = g.tpt - 1;
+    // boundary tiles on a forked stream, concurrently with the interior tiles
+    cudaStream_t se = (s == p.stream) ? p.stream3 : p.stream4;
+    cudaEvent_t e0 = (s == p.stream) ? p.ev_edge0 : p.ev_edge2, e1 = (s == p.stream) ? p.ev_edge1 : p.ev_edge3;
+    if (nsel > 0) {
+      cudaEventRecord(e0, s);
+      cudaStreamWaitEvent(se, e0, 0);
+      PM_LAUNCH(p, se, kid + 1,
+                (k_p1_reduce_lti_edge<R, N, NY, kNT, kK, KS, REV><<<(unsigned)(g.batch * nsel), kNT, smem_reduce(),
+                                                                    se>>>(ksrc, ln, g, nsel, js[0], js[1], y, tb,
+                                                                          run_incl, tile_agg, p.dflag)));
+    }
+    if (n_int > 0)
+      PM_LAUNCH(p, s, kid,
+                (k_p1_reduce_lti<R, N, NY, kNT, kK, REV><<<(unsigned)(g.batch * n_int), kNT, 0, s>>>(
+                    fpar, g, j_lo, n_int, y, tb, run_incl, tile_agg)));
+    if (nsel > 0) {
+      cudaEventRecord(e1, se);
+      cudaStreamWaitEvent(s, e1, 0);
+    }
+  }
 
   size_t ws_bytes(const Geom& g, bool tf) const override {
     WsLayout<R, N> L;
@@ -233,7 +299,8 @@ struct RunnerT : Runner {
   static size_t smem_tiles() { return sizeof(R) * E::SZ * NT2; }
   static size_t smem_groups() { return sizeof(R) * E::SZ * NT3; }
   static size_t smem_down() { return sizeof(R) * (A::SZ * kNT > V::SZ ? A::SZ * kNT : V::SZ); }
-  static size_t smem_p2tiles() { return sizeof(R) * (A::SZ * NT4 + N); }
+  static size_t smem_p2tiles() { return sizeof(R) * A::SZ * NT2; }
+  static size_t smem_p2groups() { return sizeof(R) * (A::SZ * NT4 + N); }
 
   void set_attrs() override {
     cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, kK, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -242,8 +309,15 @@ struct RunnerT : Runner {
     cudaFuncSetAttribute(k_p1_groups<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_groups());
     cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, kK, Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_down());
-    cudaFuncSetAttribute(k_p2_tiles<R, N, kNT, kK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_p2tiles());
+    cudaFuncSetAttribute(k_p2_tiles<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p2tiles());
+    cudaFuncSetAttribute(k_p2_groups<R, N, kNT, kK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_p2groups());
+    if constexpr (IS_LTI) {
+      cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, kK, Src, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
+      cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, kK, Mirror<Src>, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
+    }
     if constexpr (Src::HAS_MIRROR) {
       cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, kK, Mirror<Src>, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
@@ -266,9 +340,7 @@ struct RunnerT : Runner {
     const bool sharded = p.d.world > 1;
     cudaStream_t s = p.stream;
     // ---- pass 1
-    PM_LAUNCH(p, s, K_P1_REDUCE,
-              (k_p1_reduce<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_reduce(), s>>>(
-                  src, g, y, xbar, W(L.run_incl), W(L.tile_agg1), p.dflag)));
+    reduce1<false>(p, s, K_P1_REDUCE, src, fold, tab, y, xbar, W(L.run_incl), W(L.tile_agg1));
     PM_LAUNCH(p, s, K_P1_TILES,
               (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
                   g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
@@ -289,20 +361,24 @@ struct RunnerT : Runner {
                   src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
                   W(L.tile_agg2), p.dflag)));
     // ---- pass 2
+    PM_LAUNCH(p, s, K_P2_TILES,
+              (k_p2_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_p2tiles(), s>>>(
+                  g, W(L.tile_agg2), W(L.tile_sufx2), W(L.group_agg2))));
     const R* xend_in = nullptr;
     if (sharded) {
-      PM_LAUNCH(p, s, K_P2_TILES,
-                (k_p2_tiles<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2tiles(), s>>>(
-                    g, W(L.sv), W(L.tile_agg2), W(L.xend), W(L.tile_carry2), W(L.total2), p.dflag)));
+      PM_LAUNCH(p, s, K_P2_GROUPS,
+                (k_p2_groups<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
+                    g, W(L.sv), W(L.group_agg2), W(L.xend), W(L.group_carry2), W(L.total2), p.dflag)));
       shard_carry2(p, W(L.total2), W(L.xend), W(L.sv));
       xend_in = W(L.xend);
     }
-    PM_LAUNCH(p, s, K_P2_TILES,
-              (k_p2_tiles<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2tiles(), s>>>(
-                  g, W(L.sv), W(L.tile_agg2), xend_in, W(L.tile_carry2), nullptr, p.dflag)));
+    PM_LAUNCH(p, s, K_P2_GROUPS,
+              (k_p2_groups<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
+                  g, W(L.sv), W(L.group_agg2), xend_in, W(L.group_carry2), nullptr, p.dflag)));
     PM_LAUNCH(p, s, K_P2_DOWN,
               (k_p2_down<R, N, kNT, kK, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
-                                                                  W(L.tile_carry2), W(L.carry_in), x, p.dflag)));
+                                                                  W(L.tile_sufx2), W(L.group_carry2),
+                                                                  W(L.carry_in), x, p.dflag)));
     if (fm || fP) {
       const int64_t n = g.batch * g.Nn;
       PM_LAUNCH(p, s, K_FILTER_OUT,
@@ -331,9 +407,7 @@ struct RunnerT : Runner {
       cudaEventRecord(p.ev_fork, s);
       cudaStreamWaitEvent(s2, p.ev_fork, 0);
       // pass A: forward filter (S_i, v_i)
-      PM_LAUNCH(p, s, K_P1_REDUCE,
-                (k_p1_reduce<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_reduce(), s>>>(
-                    src, g, y, nullptr, W(L.run_incl), W(L.tile_agg1), p.dflag)));
+      reduce1<false>(p, s, K_P1_REDUCE, src, fold, tab, y, nullptr, W(L.run_incl), W(L.tile_agg1));
       PM_LAUNCH(p, s, K_P1_TILES,
                 (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
                     g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
@@ -346,9 +420,7 @@ struct RunnerT : Runner {
                     nullptr, p.dflag)));
       // pass B: backward information filter over mirrored elements (reverse node order)
       Mirror<Src> mir{src, g.node0 + g.Nn - 1};
-      PM_LAUNCH(p, s2, K_TF_REDUCE,
-                (k_p1_reduce<R, N, NY, kNT, kK, Mirror<Src>, true><<<ntiles, kNT, smem_reduce(), s2>>>(
-                    mir, g, y, nullptr, W(L.tf_run), W(L.tf_tile), p.dflag)));
+      reduce1<true>(p, s2, K_TF_REDUCE, mir, fold_m, tab_m, y, nullptr, W(L.tf_run), W(L.tf_tile));
       PM_LAUNCH(p, s2, K_TF_TILES,
                 (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s2>>>(
                     g, W(L.tf_tile), W(L.tf_tincl), W(L.tf_gagg), p.dflag)));
@@ -378,6 +450,51 @@ struct RunnerT : Runner {
               (k_maxdiff<R><<<296, 256, 0, p.stream>>>(n, static_cast<const R*>(a), static_cast<const R*>(b), out)));
   }
 };
+
+template <typename R, int N, int NY, class Src>
+bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
+  if constexpr (IS_LTI) {
+    const char* gen = getenv("PMAP_GENERAL");
+    if (gen && gen[0] == '1') return true;  // force the general reduce (A/B checks)
+    auto fill = [&](LtiNode<R, N, NY>& ln, bool mirror) {
+      for (int i = 0; i < N; ++i) {
+        for (int j = 0; j < N; ++j) ln.A[i][j] = mirror ? src.Am[i][j] : src.A[i][j];
+        ln.b[i] = mirror ? src.bm[i] : src.b[i];
+        ln.h0[i] = src.h0[i];
+        for (int k = 0; k < NY; ++k) ln.K[i][k] = src.K[i][k];
+      }
+      for (int k = 0; k < Dim<N>::NS; ++k) {
+        ln.C[k] = mirror ? src.Cm[k] : src.C[k];
+        ln.J[k] = src.J[k];
+      }
+    };
+    fill(lnode, false);
+    fill(lnode_m, true);
+    int* dok = nullptr;
+    if (cudaMalloc(&tab, sizeof(Tab)) != cudaSuccess || cudaMalloc(&tab_m, sizeof(Tab)) != cudaSuccess ||
+        cudaMalloc(&dok, 2 * sizeof(int)) != cudaSuccess)
+      return false;
+    k_lti_setup<R, N, NY, kNT, kK><<<1, 1>>>(lnode, tab, dok);
+    k_lti_setup<R, N, NY, kNT, kK><<<1, 1>>>(lnode_m, tab_m, dok + 1);
+    int ok[2] = {0, 0};
+    cudaError_t e = cudaMemcpy(ok, dok, sizeof ok, cudaMemcpyDeviceToHost);
+    cudaFree(dok);
+    if (e != cudaSuccess) return false;
+    use_lti = ok[0] && ok[1];  // a failed setup (singular pivot) falls back to the general kernels
+    if (use_lti) {
+      auto pull = [&](LtiFoldParams<R, N, NY, kK>& fpp, const LtiNode<R, N, NY>& ln, const Tab* t) {
+        fpp.node = ln;
+        return cudaMemcpy(fpp.Wb, t->Wb, sizeof fpp.Wb, cudaMemcpyDeviceToHost) == cudaSuccess &&
+               cudaMemcpy(fpp.cb, t->cb, sizeof fpp.cb, cudaMemcpyDeviceToHost) == cudaSuccess &&
+               cudaMemcpy(fpp.We, t->We, sizeof fpp.We, cudaMemcpyDeviceToHost) == cudaSuccess &&
+               cudaMemcpy(fpp.ce, t->ce, sizeof fpp.ce, cudaMemcpyDeviceToHost) == cudaSuccess;
+      };
+      if (!pull(fold, lnode, tab) || !pull(fold_m, lnode_m, tab_m)) return false;
+    }
+  }
+  (void)p;
+  return true;
+}
 
 // shard exchange helpers (host-side sequencing; the folds run in tiny kernels)
 template <typename R, int N>

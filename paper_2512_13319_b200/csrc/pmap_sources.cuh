@@ -78,6 +78,24 @@ struct SrcLTI {
       e.J[k] = first ? J0[k] : J[k];
     }
   }
+  // element of a node gi >= 1 (no node-0 selects: constants stay constant-bank operands)
+  PM_INLINE void node_interior(int64_t /*gi*/, const R* yrow, const R* /*xrow*/, Elem<R, N>& e) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = h0[i];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) s = fma(K[i][k], yrow[k], s);
+      e.h[i] = s;
+#pragma unroll
+      for (int j = 0; j < N; ++j) e.A[i][j] = A[i][j];
+      e.b[i] = b[i];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      e.C[k] = C[k];
+      e.J[k] = J[k];
+    }
+  }
   PM_INLINE void trans(int64_t /*gi*/, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -198,6 +216,9 @@ struct SrcTV {
 #pragma unroll
       for (int k = 0; k < NS; ++k) e.C[k] = dt * Q[k];
     }
+  }
+  PM_INLINE void node_interior(int64_t gi, const R* yrow, const R* xrow, Elem<R, N>& e) const {
+    node(gi, yrow, xrow, e);
   }
   PM_INLINE void trans(int64_t gi, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
     R Ft[N][N], ct[N], Q[NS];
@@ -421,6 +442,9 @@ struct SrcNL {
 #pragma unroll
       for (int k = 0; k < NS; ++k) e.C[k] = C[k];
     }
+  }
+  PM_INLINE void node_interior(int64_t gi, const R* yrow, const R* xrow, Elem<R, N>& e) const {
+    node(gi, yrow, xrow, e);
   }
   PM_INLINE void trans(int64_t /*gi*/, const R* xrow, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
     R x[N];

@@ -64,7 +64,7 @@ def random_lti(nx, ny, seed, offsets=True):
     return wl.LinearSpec("random", F, L, W, H, R, m0, P0, c=c, r=r, t0=0.0, tf=2.0)
 
 
-@pytest.mark.parametrize("T", [1, 2, 63, 2047, 2048, 2049, 5000, 300_000])
+@pytest.mark.parametrize("T", [1, 2, 63, 2047, 2048, 2049, 4095, 5000, 6143, 300_000])
 def test_wiener_rts_sizes(torch_cuda, T):
     torch = torch_cuda
     spec = wl.wiener_velocity()
@@ -285,3 +285,24 @@ def test_errors(torch_cuda):
     with pytest.raises(pm.MapError) as e:
         plan.solve_nonlinear(to_dev(torch, y2[None]))
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("T", [4095, 10_000, 123_457])
+def test_lti_specialised_reduce_matches_general(torch_cuda, T, monkeypatch):
+    """The LTI-specialised pass-1 reduce (plan-time tables, data-part propagation) and the
+    general reduce give the same trajectory (and both match the oracle)."""
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    spec.r = np.array([0.5, -0.25])
+    _, y = wl.simulate_linear(spec, T, seed=T, batch=3)
+    yd = to_dev(torch, y)
+    x_lti = gpu_plan(spec, T, batch=3).solve_linear(yd).cpu().numpy()
+    xt_lti = gpu_plan(spec, T, batch=3).two_filter(yd).cpu().numpy()
+    monkeypatch.setenv("PMAP_GENERAL", "1")
+    x_gen = gpu_plan(spec, T, batch=3).solve_linear(yd).cpu().numpy()
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
+    for b in range(3):
+        assert rel(x_lti[b], x_gen[b]) < 1e-11
+        assert rel(x_lti[b], xo[b]) < TOL64
+        assert rel(xt_lti[b], xo[b]) < TOL64
