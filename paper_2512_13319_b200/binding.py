@@ -14,7 +14,7 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpmap.so")
+LIB_PATH = os.environ.get("PMAP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpmap.so")
 
 MAP_F64, MAP_F32 = 0, 1
 MAP_NL_COORD_TURN, MAP_NL_VAN_DER_POL = 1, 2

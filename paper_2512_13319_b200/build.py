@@ -17,7 +17,8 @@ OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libpmap.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-diag-suppress", "128"] + ARCH
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-diag-suppress", "128"] + ARCH + \
+    [f for f in os.environ.get("PMAP_NVCC_EXTRA", "").split() if f]
 
 SHAPES = [(1, 1), (2, 1), (2, 2), (3, 1), (3, 2), (4, 2), (5, 2)]
 

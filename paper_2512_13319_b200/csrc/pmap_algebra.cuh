@@ -177,8 +177,9 @@ struct LUF {
 PM_INLINE double pm_abs(double x) { return fabs(x); }
 PM_INLINE float pm_abs(float x) { return fabsf(x); }
 
-template <typename R>
-PM_INLINE R pm_rcp(R x) { return R(1) / x; }
+// correctly rounded reciprocal (bit-identical to 1/x, without the division slow path)
+PM_INLINE double pm_rcp(double x) { return __drcp_rn(x); }
+PM_INLINE float pm_rcp(float x) { return __frcp_rn(x); }
 
 // Factorise f.a in place.  Row swaps are predicated selects (no dynamic
 // register indexing).  `ok` is cleared on a zero or non-finite pivot.
@@ -565,7 +566,7 @@ PM_INLINE void apply(const Aff<R, N>& f, R (&x)[N]) {
 // Symmetric positive-definite solve S x = v by Cholesky (x* = S^-1 v).
 template <typename R, int N>
 PM_INLINE void spd_solve(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N], bool& ok) {
-  R Lm[N][N];
+  R Lm[N][N], di[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     R d = S[sidx(j, j, N)];
@@ -574,7 +575,8 @@ PM_INLINE void spd_solve(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N], b
     ok = ok && (d > R(0));
     R s = sqrt(d);
     Lm[j][j] = s;
-    R si = R(1) / s;
+    R si = pm_rcp(s);
+    di[j] = si;
 #pragma unroll
     for (int i = j + 1; i < N; ++i) {
       R t = S[sidx(i, j, N)];
@@ -588,14 +590,14 @@ PM_INLINE void spd_solve(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N], b
     R t = v[i];
 #pragma unroll
     for (int k = 0; k < i; ++k) t = fma(-Lm[i][k], x[k], t);
-    x[i] = t / Lm[i][i];
+    x[i] = t * di[i];
   }
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
     R t = x[i];
 #pragma unroll
     for (int k = i + 1; k < N; ++k) t = fma(-Lm[k][i], x[k], t);
-    x[i] = t / Lm[i][i];
+    x[i] = t * di[i];
   }
 }
 

@@ -205,8 +205,15 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
 }
 
 // ----------------------------------------------------------------- pass 1d
+// 6 resident 64-thread CTAs per SM for nx <= 4 (<= 168 registers: measured 10 %
+// faster than the unconstrained 186-register build at nx = 4); nx = 5 unconstrained.
+#ifdef PM_DOWN_MINB
+#define PM_DOWN_LB(NT) __launch_bounds__(NT, PM_DOWN_MINB)
+#else
+#define PM_DOWN_LB(NT) __launch_bounds__(NT, (N <= 4 ? 6 : 1))
+#endif
 template <typename R, int N, int NY, int NT, int K, class Src, bool P2>
-__global__ void __launch_bounds__(NT) k_p1_down(const __grid_constant__ Src src, const Geom g,
+__global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const Geom g,
                                                 const R* __restrict__ y, const R* __restrict__ xbar,
                                                 const R* __restrict__ run_incl, const R* __restrict__ tile_incl,
                                                 const R* __restrict__ group_carry, R* __restrict__ sv,
