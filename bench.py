@@ -101,9 +101,9 @@ class ClockSampler:
 # ---------------------------------------------------------------- workloads
 def build_inputs(config: str, rank: int, world: int):
     import workloads as wl
+    from paper_2512_13319_b200.binding import shard_range
     spec, y, T, B = wl.make_workload(config, seed=0)
-    N = T + 1
-    a0, a1 = rank * N // world, (rank + 1) * N // world
+    a0, a1 = shard_range(rank, world, T)
     if y.ndim == 2:
         y = y[None]
     return spec, np.ascontiguousarray(y[:, a0:a1]), T, B

@@ -86,7 +86,8 @@ typedef struct {
   int32_t reserved0;
   int32_t reserved1;
   void* nccl_comm;     /* ncclComm_t borrowed from the caller (e.g. torch's
-                          ProcessGroupNCCL._comm_ptr()); NULL when world == 1 */
+                          ProcessGroupNCCL._comm_ptr()); NULL when world == 1, or
+                          when the caller drives the exchange (map_shard_phase) */
   void* stream;        /* cudaStream_t borrowed from the caller; NULL = legacy default */
 } map_plan_desc;
 
@@ -145,6 +146,21 @@ map_status map_two_filter(map_plan_t plan, const void* y, void* x_map);
  * receives the number of passes executed.  Nonlinear plans only. */
 map_status map_solve_nonlinear(map_plan_t plan, const void* y, int32_t passes, double tol,
                                const void* x_init, void* x_map, int32_t* passes_run);
+
+/* Time-sharded solves (world > 1) with a caller-driven
+ * exchange.  map_solve_linear on a sharded plan runs the same three phases around
+ * two ncclAllGather calls on desc->nccl_comm; these entry points let the caller
+ * run the exchange itself (another communicator, or single-GPU virtual shards).
+ * All buffers are DEVICE buffers; calls are asynchronous on the plan's stream.
+ *   phase 1: y (this rank's nodes) -> payload: the rank's pass-1 chunk aggregate
+ *            (an element (A, b, C, eta, J) per trajectory).
+ *   phase 2: gathered = [world][payload1] in rank order -> payload: the rank's
+ *            pass-2 chunk affine aggregate (Phi, beta) (+ x*_T on the last rank).
+ *   phase 3: gathered = [world][payload2] -> x_map (+ optional filter outputs).
+ * Unused pointers may be NULL.  Linear plans only. */
+int64_t map_shard_payload_bytes(map_plan_t plan, int32_t phase /* 1 or 2 */);
+map_status map_shard_phase(map_plan_t plan, int32_t phase, const void* y, const void* gathered, void* payload,
+                           void* x_map, void* filt_m, void* filt_P);
 
 /* Wait for the plan's stream and surface device-side numeric flags. */
 map_status map_sync(map_plan_t plan);

@@ -24,7 +24,8 @@ STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 
 # every symbol include/pmap.h declares
 EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter", "map_solve_nonlinear",
            "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
-           "map_profile_enable", "map_profile_read", "map_version"]
+           "map_profile_enable", "map_profile_read", "map_shard_payload_bytes", "map_shard_phase",
+           "map_version"]
 
 
 class MapError(RuntimeError):
@@ -89,6 +90,10 @@ def load_library():
         lib.map_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(D),
                                          ctypes.POINTER(I64), I32]
         lib.map_profile_read.restype = I32
+        lib.map_shard_payload_bytes.argtypes = [P, I32]
+        lib.map_shard_payload_bytes.restype = I64
+        lib.map_shard_phase.argtypes = [P, I32, P, P, P, P, P, P]
+        lib.map_shard_phase.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -108,6 +113,12 @@ def _ptr(a) -> int | None:
         assert a.flags.c_contiguous
         return a.ctypes.data
     return a.data_ptr()  # torch.Tensor (device or host)
+
+
+def shard_range(rank: int, world: int, T: int) -> tuple[int, int]:
+    """Nodes [a, b) owned by `rank` of a time-sharded plan (include/pmap.h: a_r = floor(r (T+1) / world))."""
+    N = T + 1
+    return rank * N // world, (rank + 1) * N // world
 
 
 # ------------------------------------------------------------ raw C entry points
@@ -137,6 +148,16 @@ def map_solve_nonlinear(plan: int, y, passes: int, tol: float, x_init, x_map) ->
     _check(load_library().map_solve_nonlinear(plan, _ptr(y), passes, tol, _ptr(x_init), _ptr(x_map),
                                               ctypes.byref(run)), plan)
     return run.value
+
+
+def map_shard_payload_bytes(plan: int, phase: int) -> int:
+    return int(load_library().map_shard_payload_bytes(plan, phase))
+
+
+def map_shard_phase(plan: int, phase: int, y=None, gathered=None, payload=None, x_map=None, filt_m=None,
+                    filt_P=None) -> None:
+    _check(load_library().map_shard_phase(plan, phase, _ptr(y), _ptr(gathered), _ptr(payload), _ptr(x_map),
+                                          _ptr(filt_m), _ptr(filt_P)), plan)
 
 
 def map_sync(plan: int) -> None:
@@ -185,9 +206,8 @@ class Plan:
         self.stream = torch.cuda.current_stream().cuda_stream if stream is None else stream
         d.stream = self.stream
         self.rank, self.world = rank, world
-        N = T + 1
-        self.n_local = (rank + 1) * N // world - rank * N // world
-        self.node0 = rank * N // world
+        self.node0, a1 = shard_range(rank, world, T)
+        self.n_local = a1 - self.node0
         lin = nl = None
         if nl_kind is None:
             lin = LinearModel()
@@ -249,6 +269,20 @@ class Plan:
 
     def sync(self):
         map_sync(self.handle)
+
+    def shard_phase(self, phase: int, y=None, gathered=None, x_map=None):
+        """One phase of a caller-driven time-sharded solve (map_shard_phase); returns the
+        phase's payload tensor (phases 1, 2) or x_map (phase 3)."""
+        import torch
+        if phase in (1, 2):
+            n = map_shard_payload_bytes(self.handle, phase) // (8 if self.dtype == "f64" else 4)
+            payload = torch.empty(n, dtype=self.torch_dtype, device="cuda")
+            map_shard_phase(self.handle, phase, y, gathered, payload)
+            return payload
+        if x_map is None:
+            x_map = torch.empty((self.batch, self.n_local, self.nx), dtype=self.torch_dtype, device="cuda")
+        map_shard_phase(self.handle, 3, None, gathered, None, x_map)
+        return x_map
 
     def profile(self, enable: bool = True) -> None:
         """Per-kernel CUDA-event timing of subsequent solves (map_profile_enable)."""

@@ -124,7 +124,6 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   if (d.nx < 1 || d.ny < 1 || d.nw < 1 || d.nw > d.nx || d.T < 1 || d.batch < 1 || !(d.tf > d.t0) ||
       (d.dtype != MAP_F64 && d.dtype != MAP_F32) || d.world < 1 || d.rank < 0 || d.rank >= d.world)
     return MAP_E_ARG;
-  if (d.world > 1 && !d.nccl_comm) return MAP_E_ARG;
   std::unique_ptr<map_plan_s> p(new map_plan_s());
   p->d = d;
   p->stream = static_cast<cudaStream_t>(d.stream);
@@ -324,6 +323,7 @@ void map_plan_destroy(map_plan_t p) {
   cudaFree(p->stage_x);
   cudaFree(p->stage_aux);
   cudaFree(p->dev_tv);
+  cudaFree(p->scratch);
   cudaFree(p->m0_dev);
   if (p->stream2) cudaStreamDestroy(p->stream2);
   if (p->stream3) cudaStreamDestroy(p->stream3);
@@ -419,6 +419,10 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
     md = Pd = nullptr;
   }
   if (st) return st;
+  if (p->d.world > 1 && !p->d.nccl_comm) {
+    p->err = "time-sharded plan without an NCCL communicator: drive the exchange with map_shard_phase";
+    return MAP_E_NCCL;
+  }
   p->runner->rts(*p, yd, nullptr, xd, md, Pd);
   std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
   outs.push_back({x_map, {xd, xb}});
@@ -540,6 +544,38 @@ map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, doub
   }
   if (passes_run) *passes_run = run;
   return finish(*p, blocking, {{x_map, {xd, xb}}});
+}
+
+int64_t map_shard_payload_bytes(map_plan_t p, int32_t phase) {
+  if (!p || (phase != 1 && phase != 2)) return -1;
+  return (int64_t)(p->runner->payload_elems(phase) * p->g.batch * p->elem_real);
+}
+
+map_status map_shard_phase(map_plan_t p, int32_t phase, const void* y, const void* gathered, void* payload,
+                           void* x_map, void* filt_m, void* filt_P) {
+  if (!p || phase < 1 || phase > 3) return MAP_E_ARG;
+  if (p->kind == Kind::NL || p->d.world < 2) {
+    p->err = "map_shard_phase needs a linear time-sharded plan (world > 1)";
+    return MAP_E_ARG;
+  }
+  const bool dev_ok = (phase == 3 || is_device_ptr(y)) && (phase == 1 || is_device_ptr(gathered)) &&
+                      (phase == 3 || is_device_ptr(payload)) && (phase != 3 || is_device_ptr(x_map)) &&
+                      (!filt_m || is_device_ptr(filt_m)) && (!filt_P || is_device_ptr(filt_P));
+  if (!dev_ok) {
+    p->err = "map_shard_phase takes device buffers only";
+    return MAP_E_ARG;
+  }
+  p->err.clear();
+  p->launches = 0;
+  if (phase == 1)
+    p->runner->phase1(*p, y, nullptr, payload);
+  else if (phase == 2)
+    p->runner->phase2(*p, y, nullptr, gathered, payload);
+  else
+    p->runner->phase3(*p, nullptr, gathered, x_map, filt_m, filt_P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(*p, e, "kernel launch");
+  return MAP_OK;
 }
 
 map_status map_sync(map_plan_t p) {

@@ -117,6 +117,10 @@ struct Runner {
   virtual bool prepare(PlanState& p) = 0;
   // one parallel-RTS solve (pass 1 + pass 2); xbar only for nonlinear sources
   virtual void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) = 0;
+  virtual size_t payload_elems(int phase) const = 0;
+  virtual void phase1(PlanState& p, const void* y, const void* xbar, void* payload) = 0;
+  virtual void phase2(PlanState& p, const void* y, const void* xbar, const void* gathered, void* payload) = 0;
+  virtual void phase3(PlanState& p, const void* xbar, const void* gathered, void* x, void* fm, void* fP) = 0;
   virtual void two_filter(PlanState& p, const void* y, void* x) = 0;
   virtual void fill_m0(PlanState& p, void* xbar) = 0;
   virtual void maxdiff(PlanState& p, const void* a, const void* b, unsigned long long* out) = 0;
@@ -175,6 +179,17 @@ struct PlanState {
   size_t ev_used = 0;
   struct Rec { int id; cudaEvent_t a, b; };
   std::vector<Rec> recs;
+  void* scratch = nullptr;  // shard payload / gather buffers
+  size_t scratch_bytes = 0;
+  void* shard_scratch(size_t bytes) {
+    if (scratch_bytes < bytes) {
+      cudaFree(scratch);
+      scratch = nullptr;
+      scratch_bytes = 0;
+      if (cudaMalloc(&scratch, bytes) == cudaSuccess) scratch_bytes = bytes;
+    }
+    return scratch;
+  }
   cudaEvent_t ev_get() {
     if (ev_used == ev_pool.size()) {
       cudaEvent_t e;
@@ -224,6 +239,66 @@ inline map_status cuda_fail(PlanState& p, cudaError_t e, const char* where) {
     cudaError_t _e = (call);                                  \
     if (_e != cudaSuccess) return cuda_fail((p), _e, #call);  \
   } while (0)
+
+// shard exchange helpers (host-side sequencing; the folds run in tiny kernels)
+template <typename R, int N>
+__global__ void k_shard_fold1(int world, int rank, int64_t batch, const R* __restrict__ gathered,
+                              R* __restrict__ carry_in, unsigned long long* flag) {
+  // gathered: [world][batch][E::SZ]; carry for `rank` = Agg_{rank-1} (x) ... (x) Agg_0 (.) (0,0)
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  bool ok = true;
+  V cur;
+  set_zero(cur);
+  for (int q = 0; q < rank; ++q) {
+    E a;
+    load(a, gathered + ((int64_t)q * batch + b) * E::SZ, 1);
+    vapply<R, N, false>(a, cur, cur, nullptr, ok);
+  }
+  store(cur, carry_in + b * V::SZ, 1);
+  if (!ok) atomicMin(flag, 0ull);
+}
+
+template <typename R, int N>
+__global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ sv_last,
+                              int64_t sv_stride, R* __restrict__ payload, unsigned long long* flag) {
+  // payload per trajectory: [Aff total][x_T (last rank only)]
+  using A = Aff<R, N>;
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  for (int k = 0; k < A::SZ; ++k) payload[b * (A::SZ + N) + k] = total2[b * A::SZ + k];
+  if (last) {
+    VF<R, N> V;
+    load(V, sv_last + b * sv_stride, (int64_t)kK * kNT);
+    R x[N];
+    bool ok = true;
+    spd_solve<R, N>(V.S, V.v, x, ok);
+    for (int i = 0; i < N; ++i) payload[b * (A::SZ + N) + A::SZ + i] = x[i];
+    if (!ok) atomicMin(flag, 0ull);
+  }
+}
+
+template <typename R, int N>
+__global__ void k_shard_fold2(int world, int rank, int64_t batch, const R* __restrict__ gathered,
+                              R* __restrict__ xend) {
+  // x at this rank's last node = Agg_{rank+1} o ... o Agg_{world-1} (x_T)
+  using A = Aff<R, N>;
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int64_t PS = A::SZ + N;
+  R x[N];
+  for (int i = 0; i < N; ++i) x[i] = gathered[((int64_t)(world - 1) * batch + b) * PS + A::SZ + i];
+  for (int q = world - 1; q > rank; --q) {
+    A a;
+    load(a, gathered + ((int64_t)q * batch + b) * PS, 1);
+    apply(a, x);
+  }
+  for (int i = 0; i < N; ++i) xend[b * N + i] = x[i];
+}
+
+
 
 template <typename R, int N, int NY, class Src>
 struct RunnerT : Runner {
@@ -328,29 +403,52 @@ struct RunnerT : Runner {
     }
   }
 
-  void rts(PlanState& p, const void* yv, const void* xbarv, void* xv, void* fm, void* fP) override {
+  // ---------------------------------------------------------------------------
+  // Parallel RTS solve (pass 1 + pass 2).  Time-sharded plans (world > 1) run it
+  // as three phases around two all-gathers of chunk carries:
+  //   phase 1: local pass-1 reduce -> payload1 = this rank's chunk aggregate
+  //   phase 2: fold gathered aggregates of ranks < r into the carry (S, v), local
+  //            pass-1 down-sweep + pass-2 reduce -> payload2 = chunk affine aggregate
+  //            (+ x*_T on the last rank)
+  //   phase 3: fold gathered affine aggregates of ranks > r onto x*_T, local pass 2.
+  // map_solve_linear drives the exchange with ncclAllGather; map_shard_phase lets
+  // the caller drive it (other communicators, single-GPU virtual shards in tests).
+  size_t payload_elems(int phase) const override {
+    return phase == 1 ? (size_t)E::SZ : (size_t)(A::SZ + N);
+  }
+
+  void phase1(PlanState& p, const void* yv, const void* xbarv, void* payload) override {
     const Geom& g = p.g;
     WsLayout<R, N> L;
     L.plan(g, p.ws_tf);
     auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
     const R* y = static_cast<const R*>(yv);
     const R* xbar = static_cast<const R*>(xbarv);
-    R* x = static_cast<R*>(xv);
-    const unsigned ntiles = (unsigned)(g.batch * g.tpt);
-    const bool sharded = p.d.world > 1;
     cudaStream_t s = p.stream;
-    // ---- pass 1
     reduce1<false>(p, s, K_P1_REDUCE, src, fold, tab, y, xbar, W(L.run_incl), W(L.tile_agg1));
     PM_LAUNCH(p, s, K_P1_TILES,
               (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
                   g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
-    const R* carry_in = nullptr;
-    if (sharded) {
-      // chunk aggregate of this rank, all-gather, carry = Agg_{r-1} (x) ... (x) Agg_0 (.) (0, 0)
+    if (payload)  // chunk aggregate only (group carries are recomputed in phase 2)
       PM_LAUNCH(p, s, K_P1_GROUPS,
                 (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                    g, W(L.group_agg1), nullptr, W(L.group_carry1), W(L.total1), p.dflag)));
-      shard_carry1(p, W(L.total1), W(L.carry_in));
+                    g, W(L.group_agg1), nullptr, W(L.group_carry1), static_cast<R*>(payload), p.dflag)));
+  }
+
+  void phase2(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* payload) override {
+    const Geom& g = p.g;
+    WsLayout<R, N> L;
+    L.plan(g, p.ws_tf);
+    auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
+    const R* y = static_cast<const R*>(yv);
+    const R* xbar = static_cast<const R*>(xbarv);
+    const unsigned ntiles = (unsigned)(g.batch * g.tpt);
+    cudaStream_t s = p.stream;
+    const R* carry_in = nullptr;
+    if (gathered) {
+      PM_LAUNCH(p, s, K_SHARD,
+                (k_shard_fold1<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
+                    p.d.world, p.d.rank, g.batch, static_cast<const R*>(gathered), W(L.carry_in), p.dflag)));
       carry_in = W(L.carry_in);
     }
     PM_LAUNCH(p, s, K_P1_GROUPS,
@@ -360,16 +458,39 @@ struct RunnerT : Runner {
               (k_p1_down<R, N, NY, kNT, kK, Src, true><<<ntiles, kNT, smem_down(), s>>>(
                   src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
                   W(L.tile_agg2), p.dflag)));
-    // ---- pass 2
     PM_LAUNCH(p, s, K_P2_TILES,
               (k_p2_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_p2tiles(), s>>>(
                   g, W(L.tile_agg2), W(L.tile_sufx2), W(L.group_agg2))));
-    const R* xend_in = nullptr;
-    if (sharded) {
+    if (payload) {
       PM_LAUNCH(p, s, K_P2_GROUPS,
                 (k_p2_groups<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
-                    g, W(L.sv), W(L.group_agg2), W(L.xend), W(L.group_carry2), W(L.total2), p.dflag)));
-      shard_carry2(p, W(L.total2), W(L.xend), W(L.sv));
+                    g, W(L.sv), W(L.group_agg2), nullptr, W(L.group_carry2), W(L.total2), p.dflag)));
+      const int64_t l = g.Nn - 1;
+      const int64_t Lt = (int64_t)kNT * kK;
+      const int64_t j = l / Lt, q = l % Lt, rr = q / kK, m = q % kK;
+      const R* sv_last = W(L.sv) + j * (int64_t)V::SZ * kK * kNT + m * kNT + rr;
+      const int64_t sv_stride = g.tpt * (int64_t)V::SZ * kK * kNT;
+      PM_LAUNCH(p, s, K_SHARD,
+                (k_shard_pack2<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
+                    g.batch, p.d.rank == p.d.world - 1, W(L.total2), sv_last, sv_stride, static_cast<R*>(payload),
+                    p.dflag)));
+    }
+  }
+
+  void phase3(PlanState& p, const void* xbarv, const void* gathered, void* xv, void* fm, void* fP) override {
+    const Geom& g = p.g;
+    WsLayout<R, N> L;
+    L.plan(g, p.ws_tf);
+    auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
+    const R* xbar = static_cast<const R*>(xbarv);
+    R* x = static_cast<R*>(xv);
+    const unsigned ntiles = (unsigned)(g.batch * g.tpt);
+    cudaStream_t s = p.stream;
+    const R* xend_in = nullptr;
+    if (gathered) {
+      PM_LAUNCH(p, s, K_SHARD,
+                (k_shard_fold2<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
+                    p.d.world, p.d.rank, g.batch, static_cast<const R*>(gathered), W(L.xend))));
       xend_in = W(L.xend);
     }
     PM_LAUNCH(p, s, K_P2_GROUPS,
@@ -387,10 +508,33 @@ struct RunnerT : Runner {
     }
   }
 
-  // Time-sharded exchange of pass-1 chunk aggregates:
-  // gather every rank's aggregate and fold those of the preceding ranks.
-  void shard_carry1(PlanState& p, R* total1, R* carry_in);
-  void shard_carry2(PlanState& p, R* total2, R* xend, const R* sv);
+  void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) override {
+    if (p.d.world == 1) {
+      phase1(p, y, xbar, nullptr);
+      phase2(p, y, xbar, nullptr, nullptr);
+      phase3(p, xbar, nullptr, x, fm, fP);
+      return;
+    }
+    // NCCL-driven exchange: two all-gathers of chunk carries per solve
+    const size_t per1 = (size_t)p.g.batch * payload_elems(1), per2 = (size_t)p.g.batch * payload_elems(2);
+    R* buf = static_cast<R*>(p.shard_scratch(((per1 + per2) * (p.d.world + 1)) * sizeof(R)));
+    R* pay1 = buf;
+    R* gat1 = pay1 + per1;
+    R* pay2 = gat1 + per1 * p.d.world;
+    R* gat2 = pay2 + per2;
+    const int nt = sizeof(R) == 8 ? 8 /*ncclFloat64*/ : 7 /*ncclFloat32*/;
+    phase1(p, y, xbar, pay1);
+    if (!p.nccl.load() || p.nccl.allgather(pay1, gat1, per1, nt, p.d.nccl_comm, p.stream) != 0) {
+      p.err = "ncclAllGather failed or NCCL not loaded in the process";
+      return;
+    }
+    phase2(p, y, xbar, gat1, pay2);
+    if (p.nccl.allgather(pay2, gat2, per2, nt, p.d.nccl_comm, p.stream) != 0) {
+      p.err = "ncclAllGather failed";
+      return;
+    }
+    phase3(p, xbar, gat2, x, fm, fP);
+  }
 
   // Two-filter (R-TF): pass A = pass-1 kernels without the pass-2 fold on the plan
   // stream; pass B = mirrored suffix scan with the fused combine on a forked stream.
@@ -494,119 +638,6 @@ bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
   }
   (void)p;
   return true;
-}
-
-// shard exchange helpers (host-side sequencing; the folds run in tiny kernels)
-template <typename R, int N>
-__global__ void k_shard_fold1(int world, int rank, int64_t batch, const R* __restrict__ gathered,
-                              R* __restrict__ carry_in, unsigned long long* flag) {
-  // gathered: [world][batch][E::SZ]; carry for `rank` = Agg_{rank-1} (x) ... (x) Agg_0 (.) (0,0)
-  using E = Elem<R, N>;
-  using V = VF<R, N>;
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  bool ok = true;
-  V cur;
-  set_zero(cur);
-  for (int q = 0; q < rank; ++q) {
-    E a;
-    load(a, gathered + ((int64_t)q * batch + b) * E::SZ, 1);
-    vapply<R, N, false>(a, cur, cur, nullptr, ok);
-  }
-  store(cur, carry_in + b * V::SZ, 1);
-  if (!ok) atomicMin(flag, 0ull);
-}
-
-template <typename R, int N>
-__global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ sv_last,
-                              int64_t sv_stride, R* __restrict__ payload, unsigned long long* flag) {
-  // payload per trajectory: [Aff total][x_T (last rank only)]
-  using A = Aff<R, N>;
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  for (int k = 0; k < A::SZ; ++k) payload[b * (A::SZ + N) + k] = total2[b * A::SZ + k];
-  if (last) {
-    VF<R, N> V;
-    load(V, sv_last + b * sv_stride, (int64_t)kK * kNT);
-    R x[N];
-    bool ok = true;
-    spd_solve<R, N>(V.S, V.v, x, ok);
-    for (int i = 0; i < N; ++i) payload[b * (A::SZ + N) + A::SZ + i] = x[i];
-    if (!ok) atomicMin(flag, 0ull);
-  }
-}
-
-template <typename R, int N>
-__global__ void k_shard_fold2(int world, int rank, int64_t batch, const R* __restrict__ gathered,
-                              R* __restrict__ xend) {
-  // x at this rank's last node = Agg_{rank+1} o ... o Agg_{world-1} (x_T)
-  using A = Aff<R, N>;
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  const int64_t PS = A::SZ + N;
-  R x[N];
-  for (int i = 0; i < N; ++i) x[i] = gathered[((int64_t)(world - 1) * batch + b) * PS + A::SZ + i];
-  for (int q = world - 1; q > rank; --q) {
-    A a;
-    load(a, gathered + ((int64_t)q * batch + b) * PS, 1);
-    apply(a, x);
-  }
-  for (int i = 0; i < N; ++i) xend[b * N + i] = x[i];
-}
-
-inline size_t g_shard_scratch_bytes = 0;
-inline void* g_shard_scratch = nullptr;
-
-template <typename R, int N, int NY, class Src>
-void RunnerT<R, N, NY, Src>::shard_carry1(PlanState& p, R* total1, R* carry_in) {
-  const int world = p.d.world;
-  const size_t per = (size_t)p.g.batch * E::SZ;
-  const size_t need = per * world * sizeof(R);
-  if (g_shard_scratch_bytes < need) {
-    cudaFree(g_shard_scratch);
-    cudaMalloc(&g_shard_scratch, need);
-    g_shard_scratch_bytes = need;
-  }
-  R* gathered = static_cast<R*>(g_shard_scratch);
-  const int dt = sizeof(R) == 8 ? 8 /*ncclFloat64*/ : 7 /*ncclFloat32*/;
-  if (!p.nccl.load() || p.nccl.allgather(total1, gathered, per, dt, p.d.nccl_comm, p.stream) != 0) {
-    p.err = "ncclAllGather failed or NCCL not loaded";
-    return;
-  }
-  PM_LAUNCH(p, p.stream, K_SHARD,
-            (k_shard_fold1<R, N><<<(unsigned)((p.g.batch + 63) / 64), 64, 0, p.stream>>>(
-                world, p.d.rank, p.g.batch, gathered, carry_in, p.dflag)));
-}
-
-template <typename R, int N, int NY, class Src>
-void RunnerT<R, N, NY, Src>::shard_carry2(PlanState& p, R* total2, R* xend, const R* sv) {
-  const int world = p.d.world;
-  const size_t per = (size_t)p.g.batch * (A::SZ + N);
-  const size_t need = per * (world + 1) * sizeof(R);
-  if (g_shard_scratch_bytes < need) {
-    cudaFree(g_shard_scratch);
-    cudaMalloc(&g_shard_scratch, need);
-    g_shard_scratch_bytes = need;
-  }
-  R* payload = static_cast<R*>(g_shard_scratch);
-  R* gathered = payload + per;
-  // (S, v) of the rank's last local node
-  const int64_t l = p.g.Nn - 1;
-  const int64_t Lt = (int64_t)kNT * kK;
-  const int64_t j = l / Lt, q = l % Lt, rr = q / kK, m = q % kK;
-  const R* sv_last = sv + j * (int64_t)V::SZ * kK * kNT + m * kNT + rr;
-  const int64_t sv_stride = p.g.tpt * (int64_t)V::SZ * kK * kNT;
-  PM_LAUNCH(p, p.stream, K_SHARD,
-            (k_shard_pack2<R, N><<<(unsigned)((p.g.batch + 63) / 64), 64, 0, p.stream>>>(
-                p.g.batch, p.d.rank == world - 1, total2, sv_last, sv_stride, payload, p.dflag)));
-  const int dt = sizeof(R) == 8 ? 8 : 7;
-  if (!p.nccl.load() || p.nccl.allgather(payload, gathered, per, dt, p.d.nccl_comm, p.stream) != 0) {
-    p.err = "ncclAllGather failed or NCCL not loaded";
-    return;
-  }
-  PM_LAUNCH(p, p.stream, K_SHARD,
-            (k_shard_fold2<R, N><<<(unsigned)((p.g.batch + 63) / 64), 64, 0, p.stream>>>(
-                world, p.d.rank, p.g.batch, gathered, xend)));
 }
 
 // ---------------------------------------------------------- instantiation

@@ -306,3 +306,37 @@ def test_lti_specialised_reduce_matches_general(torch_cuda, T, monkeypatch):
         assert rel(x_lti[b], x_gen[b]) < 1e-11
         assert rel(x_lti[b], xo[b]) < TOL64
         assert rel(xt_lti[b], xo[b]) < TOL64
+
+
+@pytest.mark.parametrize("G,T,B,general", [(2, 10_000, 1, False), (3, 123_457, 2, False), (4, 7_000, 3, True),
+                                           (8, 300_000, 1, False), (2, 5, 1, False)])
+def test_virtual_time_shards(torch_cuda, G, T, B, general, monkeypatch):
+    """The time-sharded protocol (map_shard_phase) with G virtual
+    ranks on one GPU and the all-gathers done by device concatenation: matches the
+    single-GPU solve and the oracle."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    if general:
+        monkeypatch.setenv("PMAP_GENERAL", "1")
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    spec.r = np.array([0.5, -0.25])
+    _, y = wl.simulate_linear(spec, T, seed=G + T, batch=B)
+    plans = [pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H, r=spec.r,
+                     R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, rank=r, world=G) for r in range(G)]
+    ys = []
+    for r in range(G):
+        a, b = pm.shard_range(r, G, T)
+        ys.append(to_dev(torch, y[:, a:b]))
+    g1 = torch.cat([plans[r].shard_phase(1, ys[r]) for r in range(G)])
+    g2 = torch.cat([plans[r].shard_phase(2, ys[r], g1) for r in range(G)])
+    x = torch.cat([plans[r].shard_phase(3, gathered=g2) for r in range(G)], dim=1).cpu().numpy()
+    for p in plans:
+        p.sync()
+    x1 = gpu_plan(spec, T, batch=B).solve_linear(to_dev(torch, y)).cpu().numpy()
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
+    for b in range(B):
+        assert rel(x[b], x1[b]) < 1e-11
+        assert rel(x[b], xo[b]) < TOL64
+    with pytest.raises(pm.MapError):       # no communicator: map_solve_linear refuses
+        plans[0].solve_linear(ys[0])
