@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src sr
     else
       combine(e, acc, acc, ok);  // acc = E_l (x) acc   (R-FLIP)
   }
+  // the run's own aggregate (pass 2 derives its transition from it, R-RUNAGG)
+  store(acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);
   // inclusive Kogge-Stone scan over the runs of the tile: In_r = In_r (x) In_{r-d}
 #pragma unroll 1
   for (int d = 1; d < NT; d <<= 1) {
@@ -218,7 +220,8 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
                                                 const R* __restrict__ run_incl, const R* __restrict__ tile_incl,
                                                 const R* __restrict__ group_carry, R* __restrict__ sv,
                                                 R* __restrict__ run_suf, R* __restrict__ tile_agg2,
-                                                unsigned long long* flag) {
+                                                unsigned long long* flag, const R* __restrict__ span1,
+                                                int64_t j_lo, int64_t j_hi) {
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
@@ -252,8 +255,32 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     load(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), NT);
     vapply<R, N, false>(p, cur, cur, nullptr, ok);
   }
+  // Pass-2 aggregate of the run (maps x*_e -> x*_{s-1}), R-RUNAGG: by dynamic
+  // programming it is the argmin of V_{s-1}(x) + R(x_e; x) over x for the run's own
+  // aggregate element R, i.e. the transition of vapply(R, V_{s-1}) -- one solve per
+  // run instead of one affine composition per node.  The run holding global node 0
+  // (no transition into it) composes per node instead.
   A agg;
-  set_identity(agg);
+  const bool node0_run = (g.node0 + l0 == 0);
+  if (P2 && !node0_run) {
+    E ra;
+    const R* pa = run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r;
+    if (span1 && j >= j_lo && j < j_hi) {
+      // LTI interior tile: matrix parts of one full run from the plan table, data parts stored
+      load(ra, span1, 1);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        ra.b[i] = pa[(N * N + i) * NT];
+        ra.h[i] = pa[(N * N + N + Dim<N>::NS + i) * NT];
+      }
+    } else {
+      load(ra, pa, NT);
+    }
+    V vend;
+    vapply<R, N, true>(ra, cur, vend, &agg, ok);
+  } else {
+    set_identity(agg);
+  }
   R* svt = sv + tile * (int64_t)V::SZ * K * NT;
 #pragma unroll 1
   for (int m = 0; m < K; ++m) {
@@ -267,11 +294,11 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
       for (int k = 0; k < Dim<N>::NS; ++k) cur.S[k] = e.J[k];
 #pragma unroll
       for (int i = 0; i < N; ++i) cur.v[i] = e.h[i];
-    } else if (P2) {
+    } else if (P2 && node0_run) {
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       A tr;
       vapply<R, N, true>(e, cur, cur, &tr, ok);
-      compose(agg, tr, agg);  // run aggregate maps x*_{l} -> x*_{l0 - 1}
+      compose(agg, tr, agg);  // run aggregate maps x*_{l} -> x*_{0}
     } else {
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       vapply<R, N, false>(e, cur, cur, nullptr, ok);
@@ -427,6 +454,9 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
 }
 
 // ----------------------------------------------------------------- pass 2b
+// Backward sweep of each run.  (S, v) of the next node is prefetched one step
+// ahead (coalesced SoA loads), and x is staged through shared memory in chunks of
+// KC nodes so that it leaves as contiguous 8*KC*N-byte segments per run.
 template <typename R, int N, int NT, int K, class Src>
 __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src, const Geom g,
                                                 const R* __restrict__ xbar, const R* __restrict__ sv,
@@ -435,6 +465,9 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
                                                 R* __restrict__ x_out, unsigned long long* flag) {
   using V = VF<R, N>;
   using A = Aff<R, N>;
+  constexpr int KC = 8;  // nodes per staged chunk
+  static_assert(K % KC == 0, "chunking");
+  __shared__ R xs[NT][KC * N + 1];
   const int64_t tile = blockIdx.x;
   const int64_t b = tile / g.tpt, j = tile % g.tpt;
   const int r = threadIdx.x;
@@ -452,22 +485,48 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
     apply(s, x);
   }
   R* xo = x_out + b * g.Nn * N;
-#pragma unroll 1
-  for (int m = K - 1; m >= 0; --m) {
+  const R* svt = sv + tile * (int64_t)V::SZ * K * NT;
+  // (S, v) of node l-1 for step m (m >= 1: same run, SoA slot m-1)
+  auto fetch = [&](int m, V& Vp) {
     const int64_t l = l0 + m;
-    if (l >= g.Nn) continue;
-#pragma unroll
-    for (int i = 0; i < N; ++i) xo[l * N + i] = x[i];
-    const int64_t gi = g.node0 + l;
-    if (gi == 0) continue;
-    V Vp;
-    if (l > 0)
+    if (m >= 1) {
+      load(Vp, svt + (m - 1) * NT + r, (int64_t)K * NT);
+    } else if (l > 0) {
       load_sv<R, N, NT, K>(sv, g, b, l - 1, Vp);
-    else
+    } else {
       load(Vp, carry_in + b * V::SZ, 1);  // previous rank's last node (time shard)
-    R At[N][N], bt[N], Ct[Dim<N>::NS];
-    src.trans(gi, Src::NEEDS_XBAR ? xb + l * N : nullptr, At, bt, Ct);
-    trans_step<R, N>(At, bt, Ct, Vp, x, ok);
+    }
+  };
+  V Vn;
+  fetch(K - 1, Vn);
+#pragma unroll 1
+  for (int c = K / KC - 1; c >= 0; --c) {
+#pragma unroll 1
+    for (int mm = KC - 1; mm >= 0; --mm) {
+      const int m = c * KC + mm;
+      const int64_t l = l0 + m;
+      const bool valid = l < g.Nn;
+      V Vp = Vn;
+      if (m > 0) fetch(m - 1, Vn);  // prefetch the next step's (S, v)
+#pragma unroll
+      for (int i = 0; i < N; ++i) xs[r][mm * N + i] = x[i];
+      const int64_t gi = g.node0 + l;
+      if (valid && gi != 0) {
+        R At[N][N], bt[N], Ct[Dim<N>::NS];
+        src.trans(gi, Src::NEEDS_XBAR ? xb + l * N : nullptr, At, bt, Ct);
+        trans_step<R, N>(At, bt, Ct, Vp, x, ok);
+      }
+    }
+    __syncthreads();
+    // cooperative store of the chunk: one run's KC*N contiguous doubles per pass
+    for (int rr = r >> 5; rr < NT; rr += NT / 32) {
+      const int64_t lb = (j * NT + rr) * (int64_t)K + c * KC;
+      for (int q = r & 31; q < KC * N; q += 32) {
+        const int64_t node = lb + q / N;
+        if (node < g.Nn) xo[lb * N + q] = xs[rr][q];
+      }
+    }
+    __syncthreads();
   }
   R s = R(0);
 #pragma unroll

@@ -28,6 +28,9 @@ struct LtiTables {
   R cb[K][N];
   R We[K][N][N];
   R ce[K][N];
+  // the fold is linear in the measurements: (b, eta)_run = crun + sum_m GK[m] y_m
+  R GK[K][2 * N][8];  // [m][state][measurement] (NY <= 8)
+  R crun[2 * N];
   // matrix parts of the fold prefix of m + 1 nodes, m = 0..K-1
   R PA[K][N][N];
   R PC[K][NS];
@@ -36,8 +39,15 @@ struct LtiTables {
   R SA[NT][N][N];
   R SC[NT][NS];
   R SJ[NT][NS];
+  // one full run as an element in the Elem field order (data parts zero)
+  R E1[N * N + 2 * N + 2 * NS];
   // the same, field-major: SF[f][l-1] (f over A, C, J) so lane r reads column r coalesced
   R SF[N * N + 2 * NS][NT];
+  // warp-synchronous Kogge-Stone, lane-indexed (coalesced) coefficient sets:
+  //   UW[lg][u][i][k][lane]: round d = 2^lg (< 32), own span d, partner span min(lane-d+1, d)
+  //   UX[u][i][k][lane]:     cross-warp step, own span lane+1 (in warp 1), partner span 32
+  R UW[5][4][N][N][32];
+  R UX[4][N][N][32];
   // Kogge-Stone round d (1, 2, 4, ..), partner span l2 in 1..d: index d + l2 - 2
   R U1[NT - 1][N][N];
   R U2[NT - 1][N][N];
@@ -111,13 +121,19 @@ struct LtiNode {
 // Kernel-parameter copy of the node data and the run-fold tables: read through the
 // constant bank, so the fully unrolled fold uses them as DFMA constant operands
 // (no load instructions; ~10.7 KB at nx = 4, within the 32 KB parameter limit).
-template <typename R, int N, int NY, int K>
+template <typename R, int N, int NY, int K, int LOGNT>
 struct LtiFoldParams {
   LtiNode<R, N, NY> node;
-  R Wb[K][N][N];
-  R cb[K][N];
-  R We[K][N][N];
-  R ce[K][N];
+  R GK[K][2 * N][NY];  // impulse response of the run fold to y_m
+  R crun[2 * N];       // the fold of a run with y = 0
+  // Kogge-Stone coefficient sets of round 2^k with a full partner span (the
+  // common case): U1..U4 of table index 2 * 2^k - 2
+  R Uf[LOGNT][4][N][N];
+};
+
+template <int NT>
+struct Log2 {
+  static constexpr int value = NT <= 1 ? 0 : 1 + Log2<NT / 2>::value;
 };
 
 // Plan-time tables (one thread; model-only quantities).
@@ -190,6 +206,72 @@ __global__ void k_lti_setup(const LtiNode<R, N, NY> src, LtiTables<R, N, NT, K>*
     combine(node, acc, acc, ok);
     put_prefix(m);
   }
+  // impulse response of the run fold (state s = (b, eta), s' = T_m s + [0; eta_m] + c_m,
+  // T_m = [[I, Wb_m], [0, We_m]]):  G_m = (T_{K-1} ... T_{m+1})[:, N:2N],  GK_m = G_m K.
+  {
+    R P[2 * N][2 * N];
+    for (int i = 0; i < 2 * N; ++i)
+      for (int j = 0; j < 2 * N; ++j) P[i][j] = (i == j) ? R(1) : R(0);
+    for (int m = K - 1; m >= 0; --m) {
+      for (int i = 0; i < 2 * N; ++i)
+        for (int k = 0; k < NY; ++k) {
+          R sacc = R(0);
+          for (int j = 0; j < N; ++j) sacc = fma(P[i][N + j], src.K[j][k], sacc);
+          tab->GK[m][i][k] = sacc;
+        }
+      if (m >= 1) {  // P <- P T_m
+        R Q[2 * N][2 * N];
+        for (int i = 0; i < 2 * N; ++i)
+          for (int j = 0; j < 2 * N; ++j) {
+            R sacc = R(0);
+            if (j < N) {
+              sacc = P[i][j];  // T_m[:, j] = e_j for the b columns
+            } else {
+              const int jj = j - N;
+              for (int k = 0; k < N; ++k) sacc = fma(P[i][k], tab->Wb[m][k][jj], sacc);
+              for (int k = 0; k < N; ++k) sacc = fma(P[i][N + k], tab->We[m][k][jj], sacc);
+            }
+            Q[i][j] = sacc;
+          }
+        for (int i = 0; i < 2 * N; ++i)
+          for (int j = 0; j < 2 * N; ++j) P[i][j] = Q[i][j];
+      }
+    }
+    // constant part: the data fold with y = 0
+    R bb[N], hh[N];
+    for (int i = 0; i < N; ++i) {
+      bb[i] = src.b[i];
+      hh[i] = src.h0[i];
+    }
+    for (int m = 1; m < K; ++m) {
+      R nb[N], nh[N];
+      for (int i = 0; i < N; ++i) {
+        R s1 = bb[i] + tab->cb[m][i], t1 = src.h0[i] + tab->ce[m][i];
+        for (int k = 0; k < N; ++k) {
+          s1 = fma(tab->Wb[m][i][k], hh[k], s1);
+          t1 = fma(tab->We[m][i][k], hh[k], t1);
+        }
+        nb[i] = s1;
+        nh[i] = t1;
+      }
+      for (int i = 0; i < N; ++i) {
+        bb[i] = nb[i];
+        hh[i] = nh[i];
+      }
+    }
+    for (int i = 0; i < N; ++i) {
+      tab->crun[i] = bb[i];
+      tab->crun[N + i] = hh[i];
+    }
+  }
+  {
+    E e1 = acc;
+    for (int i = 0; i < N; ++i) {
+      e1.b[i] = R(0);
+      e1.h[i] = R(0);
+    }
+    store(e1, tab->E1, 1);
+  }
   // spans of l full runs (flipped: later span on the left)
   E run = acc, span = acc;
   for (int l = 1; l <= NT; ++l) {
@@ -242,6 +324,60 @@ __global__ void k_lti_setup(const LtiNode<R, N, NY> src, LtiTables<R, N, NT, K>*
         }
     }
   }
+  // lane-indexed copies for the warp-synchronous scan
+  auto coeff = [&](int l1, int l2, int lane, R (*dst)[N][N][32]) {
+    // own span l1 (left), partner span l2 (right): U1 = A2 M, U2 = A2 M C1, U3 = A1^T M^T, U4 = A1^T M^T J2
+    R C1[Dim<N>::NS], J2[Dim<N>::NS], A1[N][N], A2[N][N], C1m[N][N], J2m[N][N], M[N][N], A2M[N][N], T[N][N];
+    for (int k = 0; k < Dim<N>::NS; ++k) {
+      C1[k] = tab->SC[l1 - 1][k];
+      J2[k] = tab->SJ[l2 - 1][k];
+    }
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        A1[i][j] = tab->SA[l1 - 1][i][j];
+        A2[i][j] = tab->SA[l2 - 1][i][j];
+      }
+    unpack<R, N>(C1, C1m);
+    unpack<R, N>(J2, J2m);
+    inv_ICJ<R, N>(C1, J2, M);
+    matmul<R, N>(A2, M, A2M);
+    matmul<R, N>(A2M, C1m, T);
+    R AtMt[N][N], U4[N][N];
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        R sacc = R(0);
+        for (int k = 0; k < N; ++k) sacc = fma(A1[k][i], M[j][k], sacc);
+        AtMt[i][j] = sacc;
+      }
+    matmul<R, N>(AtMt, J2m, U4);
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        dst[0][i][j][lane] = A2M[i][j];
+        dst[1][i][j][lane] = T[i][j];
+        dst[2][i][j][lane] = AtMt[i][j];
+        dst[3][i][j][lane] = U4[i][j];
+      }
+  };
+  for (int lg = 0; lg < 5; ++lg) {
+    const int d = 1 << lg;
+    for (int lane = 0; lane < 32; ++lane) {
+      if (lane < d || d > NT / 2) {
+        for (int u = 0; u < 4; ++u)
+          for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) tab->UW[lg][u][i][j][lane] = R(0);
+        continue;
+      }
+      coeff(d, min(lane - d + 1, d), lane, tab->UW[lg]);
+    }
+  }
+  for (int lane = 0; lane < 32; ++lane) {
+    if (NT > 32)
+      coeff(lane + 1, 32, lane, tab->UX);
+    else
+      for (int u = 0; u < 4; ++u)
+        for (int i = 0; i < N; ++i)
+          for (int j = 0; j < N; ++j) tab->UX[u][i][j][lane] = R(0);
+  }
   *okflag = ok ? 1 : 0;
 }
 
@@ -261,7 +397,7 @@ PM_INLINE void matvec_acc(const R* __restrict__ M, const R (&x)[N], R (&y)[N]) {
 // The tile's y block is staged through shared memory (coalesced global reads, a
 // padded row per run so the per-run reads are bank-conflict free).
 template <typename R, int N, int NY, int NT, int K, bool REV>
-__global__ void __launch_bounds__(NT) k_p1_reduce_lti(const __grid_constant__ LtiFoldParams<R, N, NY, K> fp,
+__global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__ LtiFoldParams<R, N, NY, K, Log2<NT>::value> fp,
                                                       const Geom g, int64_t j_lo, int64_t n_int,
                                                       const R* __restrict__ y,
                                                       const LtiTables<R, N, NT, K>* __restrict__ tab,
@@ -270,7 +406,6 @@ __global__ void __launch_bounds__(NT) k_p1_reduce_lti(const __grid_constant__ Lt
   // padded run row in shared memory: 16-byte aligned rows, consecutive runs 4 banks apart
   constexpr int ROW = ((K * NY * (int)sizeof(R) + 15) / 16 * 16 + 16) / (int)sizeof(R);
   __shared__ __align__(16) R ys[NT * ROW];
-  __shared__ R sh[2 * N][NT];
   const LtiNode<R, N, NY>& src = fp.node;
   const int64_t b = blockIdx.x / n_int;
   const int64_t j = j_lo + blockIdx.x % n_int;
@@ -302,79 +437,103 @@ __global__ void __launch_bounds__(NT) k_p1_reduce_lti(const __grid_constant__ Lt
   }
   __syncthreads();
   const R* yr = ys + r * ROW;
+  // run fold as a sum of independent terms: (b, eta) = crun + sum_m GK[m] y_m
+  R acc0[2 * N], acc1[2 * N];
+#pragma unroll
+  for (int i = 0; i < 2 * N; ++i) {
+    acc0[i] = fp.crun[i];
+    acc1[i] = R(0);
+  }
+#pragma unroll
+  for (int m = 0; m < K; m += 2) {
+    R y0[NY], y1[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) {
+      y0[k] = yr[m * NY + k];
+      y1[k] = yr[(m + 1) * NY + k];
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * N; ++i)
+#pragma unroll
+      for (int k = 0; k < NY; ++k) {
+        acc0[i] = fma(fp.GK[m][i][k], y0[k], acc0[i]);
+        acc1[i] = fma(fp.GK[m + 1][i][k], y1[k], acc1[i]);
+      }
+  }
   R bb[N], hh[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    R s = src.h0[i];
-#pragma unroll
-    for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], yr[k], s);
-    hh[i] = s;
-    bb[i] = src.b[i];
+    bb[i] = acc0[i] + acc1[i];
+    hh[i] = acc0[N + i] + acc1[N + i];
   }
+  // the run's own aggregate, R-RUNAGG: data parts only (the matrix parts of a full
+  // interior run are the plan constant tab->SA[0] etc., read by k_p1_down)
+  {
+    R* oa = run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r;
 #pragma unroll
-  for (int m = 1; m < K; ++m) {
-    R yv[NY];
-#pragma unroll
-    for (int k = 0; k < NY; ++k) yv[k] = yr[m * NY + k];
+    for (int i = 0; i < N; ++i) {
+      oa[(N * N + i) * NT] = bb[i];
+      oa[(N * N + N + Dim<N>::NS + i) * NT] = hh[i];
+    }
+  }
+  // Scan over the runs, data parts only: warp-synchronous Kogge-Stone with shuffles
+  // (lane-indexed coefficient tables -> coalesced loads, no divergence), then one
+  // cross-warp step with warp 0's total.
+  static_assert(NT == 32 || NT == 64, "tile of one or two warps");
+  const int lane = r & 31;
+  const unsigned FULL = 0xffffffffu;
+  auto step = [&](const R* __restrict__ U, const R (&b2)[N], const R (&h2)[N]) {
+    // U = [4][N][N][32] (lane-indexed): b = U1 b1 + U2 eta2 + b2 ; eta = U3 eta2 - U4 b1 + eta1
     R nb[N], nh[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      R s = bb[i] + fp.cb[m][i];
-      R t = src.h0[i] + fp.ce[m][i];
-#pragma unroll
-      for (int k = 0; k < NY; ++k) t = fma(src.K[i][k], yv[k], t);
+      R sb = b2[i], sh_ = hh[i];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        s = fma(fp.Wb[m][i][k], hh[k], s);
-        t = fma(fp.We[m][i][k], hh[k], t);
+        sb = fma(__ldg(U + ((0 * N + i) * N + k) * 32 + lane), bb[k], sb);
+        sb = fma(__ldg(U + ((1 * N + i) * N + k) * 32 + lane), h2[k], sb);
+        sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * 32 + lane), h2[k], sh_);
+        sh_ = fma(-__ldg(U + ((3 * N + i) * N + k) * 32 + lane), bb[k], sh_);
       }
-      nb[i] = s;
-      nh[i] = t;
+      nb[i] = sb;
+      nh[i] = sh_;
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       bb[i] = nb[i];
       hh[i] = nh[i];
     }
-  }
-  // Kogge-Stone over runs, data parts only
-#pragma unroll 1
-  for (int d = 1; d < NT; d <<= 1) {
+  };
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {
+    const int d = 1 << lg;
+    R b2[N], h2[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      sh[i][r] = bb[i];
-      sh[N + i][r] = hh[i];
+      b2[i] = __shfl_up_sync(FULL, bb[i], d);
+      h2[i] = __shfl_up_sync(FULL, hh[i], d);
+    }
+    if (lane >= d) step(&tab->UW[lg][0][0][0][0], b2, h2);
+  }
+  if (NT == 64) {
+    __shared__ R tot[2 * N];
+    if (r == 31) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        tot[i] = bb[i];
+        tot[N + i] = hh[i];
+      }
     }
     __syncthreads();
-    if (r >= d) {
-      const int l2 = min(r - d + 1, d);
-      const int idx = d + l2 - 2;
+    if (r >= 32) {
       R b2[N], h2[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        b2[i] = sh[i][r - d];
-        h2[i] = sh[N + i][r - d];
+        b2[i] = tot[i];
+        h2[i] = tot[N + i];
       }
-      R nb[N], nh[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        nb[i] = b2[i];
-        nh[i] = hh[i];
-      }
-      matvec_acc<R, N>(&tab->U1[idx][0][0], bb, nb);
-      matvec_acc<R, N>(&tab->U2[idx][0][0], h2, nb);
-      matvec_acc<R, N>(&tab->U3[idx][0][0], h2, nh);
-      R mb[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) mb[i] = -bb[i];
-      matvec_acc<R, N>(&tab->U4[idx][0][0], mb, nh);
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        bb[i] = nb[i];
-        hh[i] = nh[i];
-      }
+      step(&tab->UX[0][0][0][0], b2, h2);
     }
-    __syncthreads();
   }
   // write the full inclusive prefix element: matrix parts of a span of r + 1 runs
   // (field-major table: coalesced across the warp)
@@ -505,6 +664,7 @@ __global__ void __launch_bounds__(NT) k_p1_reduce_lti_edge(const __grid_constant
         acc = e0;
     }
   }
+  store(acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);  // run aggregate
 #pragma unroll 1
   for (int d = 1; d < NT; d <<= 1) {
     store(acc, sh + r, NT);

@@ -78,7 +78,7 @@ struct WsLayout {
       off += ((elems * sizeof(R) + 255) / 256) * 256;
       return o;
     };
-    run_incl = take(nt * E::SZ * kNT);
+    run_incl = take(2 * nt * E::SZ * kNT);  // [inclusive prefixes | run aggregates]
     tile_agg1 = take(nt * E::SZ);
     tile_incl1 = take(nt * E::SZ);
     group_agg1 = take(ng * E::SZ);
@@ -94,7 +94,7 @@ struct WsLayout {
     carry_in = take(B * V::SZ);
     xend = take(B * N);
     if (tf) {
-      tf_run = take(nt * E::SZ * kNT);
+      tf_run = take(2 * nt * E::SZ * kNT);
       tf_tile = take(nt * E::SZ);
       tf_tincl = take(nt * E::SZ);
       tf_gagg = take(ng * E::SZ);
@@ -311,7 +311,7 @@ struct RunnerT : Runner {
   Tab* tab = nullptr;    // pass-1 tables (LTI only)
   Tab* tab_m = nullptr;  // mirrored-element tables (two-filter pass B)
   LtiNode<R, N, NY> lnode{}, lnode_m{};
-  LtiFoldParams<R, N, NY, kK> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
+  LtiFoldParams<R, N, NY, kK, Log2<kNT>::value> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
   bool use_lti = false;
 
   ~RunnerT() override {
@@ -321,10 +321,15 @@ struct RunnerT : Runner {
 
   bool prepare(PlanState& p) override;
 
+  // interior (LTI-specialised) tile range [j_lo, j_hi) of a trajectory
+  static int64_t lti_jlo(const Geom& g, bool rev) { return (rev || g.node0 == 0) ? 1 : 0; }
+  static int64_t lti_jhi(const Geom& g) { return g.Nn / ((int64_t)kNT * kK); }
+
   // Pass-1 reduce: LTI-specialised kernel on interior tiles, general kernel on the
   // boundary tiles (node 0 / terminal node, ragged last tile); all tiles otherwise.
   template <bool REV, class KS>
-  void reduce1(PlanState& p, cudaStream_t s, int kid, const KS& ksrc, const LtiFoldParams<R, N, NY, kK>& fpar,
+  void reduce1(PlanState& p, cudaStream_t s, int kid, const KS& ksrc,
+               const LtiFoldParams<R, N, NY, kK, Log2<kNT>::value>& fpar,
                const Tab* tb, const R* y, const R* xbar, R* run_incl, R* tile_agg) {
     const LtiNode<R, N, NY>& ln = fpar.node;
     const Geom& g = p.g;
@@ -334,9 +339,8 @@ struct RunnerT : Runner {
                     ksrc, g, y, xbar, run_incl, tile_agg, p.dflag, 0, 0, 0)));
       return;
     }
-    const int64_t Lt = (int64_t)kNT * kK;
-    const int64_t j_lo = (REV || g.node0 == 0) ? 1 : 0;
-    const int64_t j_hi = g.Nn / Lt;  // full tiles
+    const int64_t j_lo = lti_jlo(g, REV);
+    const int64_t j_hi = lti_jhi(g);
     const int64_t n_int = j_hi > j_lo ? j_hi - j_lo : 0;
     int nsel = 0;
     int64_t js[2] = {0, 0};
@@ -457,7 +461,8 @@ struct RunnerT : Runner {
     PM_LAUNCH(p, s, K_P1_DOWN,
               (k_p1_down<R, N, NY, kNT, kK, Src, true><<<ntiles, kNT, smem_down(), s>>>(
                   src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
-                  W(L.tile_agg2), p.dflag)));
+                  W(L.tile_agg2), p.dflag, (use_lti && tab) ? tab->E1 : nullptr, lti_jlo(g, false),
+                  lti_jhi(g))));
     PM_LAUNCH(p, s, K_P2_TILES,
               (k_p2_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_p2tiles(), s>>>(
                   g, W(L.tile_agg2), W(L.tile_sufx2), W(L.group_agg2))));
@@ -561,7 +566,7 @@ struct RunnerT : Runner {
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
-                    nullptr, p.dflag)));
+                    nullptr, p.dflag, nullptr, 0, 0)));
       // pass B: backward information filter over mirrored elements (reverse node order)
       Mirror<Src> mir{src, g.node0 + g.Nn - 1};
       reduce1<true>(p, s2, K_TF_REDUCE, mir, fold_m, tab_m, y, nullptr, W(L.tf_run), W(L.tf_tile));
@@ -626,12 +631,24 @@ bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
     if (e != cudaSuccess) return false;
     use_lti = ok[0] && ok[1];  // a failed setup (singular pivot) falls back to the general kernels
     if (use_lti) {
-      auto pull = [&](LtiFoldParams<R, N, NY, kK>& fpp, const LtiNode<R, N, NY>& ln, const Tab* t) {
+      auto pull = [&](LtiFoldParams<R, N, NY, kK, Log2<kNT>::value>& fpp, const LtiNode<R, N, NY>& ln,
+                      const Tab* t) {
         fpp.node = ln;
-        return cudaMemcpy(fpp.Wb, t->Wb, sizeof fpp.Wb, cudaMemcpyDeviceToHost) == cudaSuccess &&
-               cudaMemcpy(fpp.cb, t->cb, sizeof fpp.cb, cudaMemcpyDeviceToHost) == cudaSuccess &&
-               cudaMemcpy(fpp.We, t->We, sizeof fpp.We, cudaMemcpyDeviceToHost) == cudaSuccess &&
-               cudaMemcpy(fpp.ce, t->ce, sizeof fpp.ce, cudaMemcpyDeviceToHost) == cudaSuccess;
+        bool okc = true;
+        for (int lg = 0; lg < Log2<kNT>::value; ++lg) {
+          const int idx = 2 * (1 << lg) - 2;
+          okc = okc && cudaMemcpy(fpp.Uf[lg][0], t->U1[idx], sizeof(R) * N * N, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                cudaMemcpy(fpp.Uf[lg][1], t->U2[idx], sizeof(R) * N * N, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                cudaMemcpy(fpp.Uf[lg][2], t->U3[idx], sizeof(R) * N * N, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                cudaMemcpy(fpp.Uf[lg][3], t->U4[idx], sizeof(R) * N * N, cudaMemcpyDeviceToHost) == cudaSuccess;
+        }
+        if (!okc || cudaMemcpy(fpp.crun, t->crun, sizeof fpp.crun, cudaMemcpyDeviceToHost) != cudaSuccess)
+          return false;
+        for (int m = 0; m < kK; ++m)
+          for (int i = 0; i < 2 * N; ++i)
+            if (cudaMemcpy(fpp.GK[m][i], t->GK[m][i], sizeof(R) * NY, cudaMemcpyDeviceToHost) != cudaSuccess)
+              return false;
+        return true;
       };
       if (!pull(fold, lnode, tab) || !pull(fold_m, lnode_m, tab_m)) return false;
     }
