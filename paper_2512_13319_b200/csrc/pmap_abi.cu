@@ -127,6 +127,10 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   std::unique_ptr<map_plan_s> p(new map_plan_s());
   p->d = d;
   p->stream = static_cast<cudaStream_t>(d.stream);
+  {
+    const char* fs = getenv("PMAP_FORCE_SHARD");
+    p->force_shard = fs && fs[0] == '1' && d.nccl_comm;
+  }
   const int nx = d.nx, ny = d.ny, nw = d.nw;
   const int NS = nx * (nx + 1) / 2;
   const double dt = (d.tf - d.t0) / (double)d.T;
@@ -483,7 +487,7 @@ map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, doub
   if (tol == 0.0) {
     // fixed number of passes, no host synchronisation: one CUDA graph
     const void* key[4] = {yd, xd, (const void*)(intptr_t)passes, nullptr};
-    const bool capture = p->d.world == 1;
+    const bool capture = p->d.world == 1 && !p->force_shard;
     if (capture && !(p->graph && memcmp(key, p->graph_key, sizeof key) == 0)) {
       if (p->graph) {
         cudaGraphExecDestroy(p->graph);

@@ -169,6 +169,7 @@ struct PlanState {
   int graph_passes = -1;
   int64_t graph_launches = 0;
   size_t elem_real = 8;
+  bool force_shard = false;  // PMAP_FORCE_SHARD=1 with a communicator: run the NCCL path at world == 1 (tests)
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
   cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -514,7 +515,7 @@ struct RunnerT : Runner {
   }
 
   void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) override {
-    if (p.d.world == 1) {
+    if (p.d.world == 1 && !p.force_shard) {
       phase1(p, y, xbar, nullptr);
       phase2(p, y, xbar, nullptr, nullptr);
       phase3(p, xbar, nullptr, x, fm, fP);

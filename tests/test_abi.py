@@ -65,3 +65,16 @@ def test_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f
+
+
+def test_nccl_symbol_lookup_strategy():
+    """libpmap resolves ncclAllGather from the NCCL that torch already loaded (dlsym on
+    RTLD_DEFAULT, else dlopen("libnccl.so.2", RTLD_NOLOAD)); check that lookup works in a
+    torch process (no GPU needed)."""
+    import torch  # noqa: F401  (loads libtorch_cuda -> libnccl.so.2)
+    import torch.distributed as dist
+    if not dist.is_nccl_available():
+        pytest.skip("torch built without NCCL")
+    RTLD_NOLOAD = 4
+    h = ctypes.CDLL("libnccl.so.2", mode=RTLD_NOLOAD)
+    assert hasattr(h, "ncclAllGather")

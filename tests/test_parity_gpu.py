@@ -340,3 +340,37 @@ def test_virtual_time_shards(torch_cuda, G, T, B, general, monkeypatch):
         assert rel(x[b], xo[b]) < TOL64
     with pytest.raises(pm.MapError):       # no communicator: map_solve_linear refuses
         plans[0].solve_linear(ys[0])
+
+
+def test_nccl_exchange_path_single_rank(torch_cuda, monkeypatch):
+    """The library's own NCCL all-gather path (map_solve_linear on a time-sharded plan),
+    exercised on one GPU with a 1-rank NCCL process group (PMAP_FORCE_SHARD=1 routes a
+    world-1 plan through the phases + ncclAllGather): equals the unsharded solve."""
+    import socket
+    import torch.distributed as dist
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    monkeypatch.setenv("MASTER_ADDR", "127.0.0.1")
+    monkeypatch.setenv("MASTER_PORT", str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        dist.barrier()
+        comm = dist.group.WORLD._get_backend(torch.device("cuda", 0))._comm_ptr()
+        spec = wl.wiener_velocity()
+        T = 50_000
+        _, y = wl.simulate_linear(spec, T, seed=3)
+        yd = to_dev(torch, y[None])
+        x_ref = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+        monkeypatch.setenv("PMAP_FORCE_SHARD", "1")
+        plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                       P0=spec.P0, nccl_comm=comm)
+        x = plan.solve_linear(yd)
+        plan.sync()
+        assert plan.launches >= 9  # phases + shard folds ran
+        assert rel(x.cpu().numpy(), x_ref) < 1e-12
+    finally:
+        dist.destroy_process_group()
