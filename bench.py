@@ -35,27 +35,29 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 # ----------------------------------------------------------- algorithmic counts
-def alg_counts(nx: int, ny: int, K: int = 32):
+def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True):
     """Algorithmic FP64 flops (FMA = 2) and HBM bytes per node of each kernel class
-    (DESIGN.md "Roofline"): the operations the parallel method performs per node,
-    excluding this implementation's intra-tile scan overheads."""
+    (DESIGN.md section 6): the arithmetic each kernel's per-node recurrence performs
+    in this decomposition, excluding the intra-tile scan overheads (Kogge-Stone
+    rounds, carries), which are implementation cost."""
     N = nx
     lu = sum((N - k - 1) + (N - k - 1) ** 2 for k in range(N))
     solve = N * N
     combine = N ** 3 + lu + 2 * N * solve + (N * N + solve) * 2 + N ** 3 + N * N + (N ** 3 + N * N * (N + 1) // 2) * 2 + N * N
-    vapply_tr = N ** 3 + lu + N * solve + (N * N + solve) * 2 + N ** 3 + N * N * (N + 1) // 2 + N * N
-    compose = N ** 3 + N * N
+    vapply = N ** 3 + lu + N * solve + (N * N + solve) + N ** 3 + N * N * (N + 1) // 2 + N * N
+    vapply_tr = vapply + (N * N + solve)
     trans = N ** 3 + lu + 2 * N * N + solve
     ns = N * (N + 1) // 2
     esz = N * N + 2 * N + 2 * ns
     vsz = ns + N
     asz = N * N + N
     d = 8
+    reduce_fl = 2 * N * ny if lti else combine  # LTI: impulse-response fold (y_m -> (b, eta))
     return {
-        "k_p1_reduce": (2 * combine, d * (ny + esz / K)),
-        "k_p1_down": (2 * (vapply_tr + compose), d * (ny + esz / K + vsz + asz / K)),
+        "k_p1_reduce": (2 * reduce_fl, d * (ny + esz / K)),
+        "k_p1_down": (2 * (vapply + vapply_tr / K), d * (ny + esz / K + vsz + asz / K)),
         "k_p2_down": (2 * trans, d * (vsz + nx + asz / K)),
-        "solve": (2 * (combine + vapply_tr + compose + trans), d * (ny + 2 * vsz + nx)),
+        "solve": (2 * (reduce_fl + vapply + vapply_tr / K + trans), d * (ny + 2 * vsz + nx)),
     }
 
 
@@ -311,7 +313,7 @@ def main():
         return
 
     # roofline of the dominant kernel (FP64-ALU bound)
-    counts = alg_counts(plan.nx, plan.ny)
+    counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1")
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl

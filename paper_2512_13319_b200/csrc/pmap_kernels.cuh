@@ -78,8 +78,10 @@ __global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src sr
   const R* yb = y + b * g.Nn * NY;
   const R* xb = Src::NEEDS_XBAR ? xbar + b * g.Nn * N : nullptr;
   bool ok = true;
-  E acc;
+  E acc, acc_x0;  // acc_x0: the run's fold without global node 0 (pass-2 aggregate of that run)
   set_identity(acc);
+  set_identity(acc_x0);
+  const bool has_node0 = !REV && (g.node0 + l0 == 0);
 #pragma unroll 1
   for (int m = 0; m < K; ++m) {
     const int64_t lr = l0 + m;
@@ -91,9 +93,15 @@ __global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src sr
       acc = e;
     else
       combine(e, acc, acc, ok);  // acc = E_l (x) acc   (R-FLIP)
+    if (has_node0 && m >= 1) {
+      if (m == 1)
+        acc_x0 = e;
+      else
+        combine(e, acc_x0, acc_x0, ok);
+    }
   }
   // the run's own aggregate (pass 2 derives its transition from it, R-RUNAGG)
-  store(acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);
+  store(has_node0 ? acc_x0 : acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);
   // inclusive Kogge-Stone scan over the runs of the tile: In_r = In_r (x) In_{r-d}
 #pragma unroll 1
   for (int d = 1; d < NT; d <<= 1) {
@@ -260,9 +268,9 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
   // aggregate element R, i.e. the transition of vapply(R, V_{s-1}) -- one solve per
   // run instead of one affine composition per node.  The run holding global node 0
   // (no transition into it) composes per node instead.
-  A agg;
   const bool node0_run = (g.node0 + l0 == 0);
-  if (P2 && !node0_run) {
+  if (P2) {
+    A agg;
     E ra;
     const R* pa = run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r;
     if (span1 && j >= j_lo && j < j_hi) {
@@ -274,12 +282,20 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
         ra.h[i] = pa[(N * N + N + Dim<N>::NS + i) * NT];
       }
     } else {
-      load(ra, pa, NT);
+      load(ra, pa, NT);  // (the run holding node 0 stores its fold without node 0)
+    }
+    V vin = cur;
+    if (node0_run) {  // no transition into node 0: the DP starts from V_0 = E_0 (.) (0, 0)
+      E e0;
+      src.node(0, yb, Src::NEEDS_XBAR ? xb : nullptr, e0);
+#pragma unroll
+      for (int k = 0; k < Dim<N>::NS; ++k) vin.S[k] = e0.J[k];
+#pragma unroll
+      for (int i = 0; i < N; ++i) vin.v[i] = e0.h[i];
     }
     V vend;
-    vapply<R, N, true>(ra, cur, vend, &agg, ok);
-  } else {
-    set_identity(agg);
+    vapply<R, N, true>(ra, vin, vend, &agg, ok);
+    store(agg, sh + r, NT);  // parked in shared memory across the node loop
   }
   R* svt = sv + tile * (int64_t)V::SZ * K * NT;
 #pragma unroll 1
@@ -294,11 +310,6 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
       for (int k = 0; k < Dim<N>::NS; ++k) cur.S[k] = e.J[k];
 #pragma unroll
       for (int i = 0; i < N; ++i) cur.v[i] = e.h[i];
-    } else if (P2 && node0_run) {
-      src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
-      A tr;
-      vapply<R, N, true>(e, cur, cur, &tr, ok);
-      compose(agg, tr, agg);  // run aggregate maps x*_{l} -> x*_{0}
     } else {
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       vapply<R, N, false>(e, cur, cur, nullptr, ok);
@@ -311,6 +322,9 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     return;
   }
   // exclusive suffix scan of the run aggregates within the tile
+  A agg;
+  load(agg, sh + r, NT);
+  __syncthreads();
 #pragma unroll 1
   for (int d = 1; d < NT; d <<= 1) {
     store(agg, sh + r, NT);

@@ -654,6 +654,9 @@ __global__ void __launch_bounds__(NT) k_p1_reduce_lti_edge(const __grid_constant
         acc.J[k] = tab->PJ[qf - 1][k];
       }
     }
+    // run aggregate for pass 2 (R-RUNAGG): the run holding node 0 stores its fold
+    // without node 0 (no transition into node 0)
+    store(acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);
     if (first) {
       const int64_t l = lidx(l0);
       E e0;
@@ -663,8 +666,9 @@ __global__ void __launch_bounds__(NT) k_p1_reduce_lti_edge(const __grid_constant
       else
         acc = e0;
     }
+  } else {
+    store(acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);
   }
-  store(acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);  // run aggregate
 #pragma unroll 1
   for (int d = 1; d < NT; d <<= 1) {
     store(acc, sh + r, NT);
