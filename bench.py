@@ -321,8 +321,17 @@ def main():
     nodes_per_launch = B * plan.n_local
     fl, by = counts.get(dname, counts["solve"])
     achieved_tflops = fl * nodes_per_launch / (per_launch_ms * 1e-3) / 1e12
+    traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from a committed ncu capture
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        rec = tr.get("kernels", {}).get(dname)
+        if rec and tr.get("nodes") == B * plan.n_local:
+            traffic = rec["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     roofline = {"bound": "alu", "kernel": dname, "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
-                "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS_DERIVED, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS_DERIVED, "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)" if traffic else None,
                 "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (MEASURED_PEAKS.json has no FP64; "
                                "DFMA microbenchmark measured 34.2 TF/s, profiles/r01_fp64_peak_probe.log)",
                 "alg_flops_per_node": fl, "alg_bytes_per_node": by, "kernel_ms_per_launch": per_launch_ms,
