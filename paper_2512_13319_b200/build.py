@@ -23,16 +23,21 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-diag-suppres
 SHAPES = [(1, 1), (2, 1), (2, 2), (3, 1), (3, 2), (4, 2), (5, 2)]
 
 
+RUN_LENGTHS = (32, 8)  # nodes per run (tile = 64 runs): large / small problems
+
+
 def units(f64_only: bool = False):
     out = []
     for R in (("double",) if f64_only else ("double", "float")):
         tag = "f64" if R == "double" else "f32"
-        for kind in (0, 1):
-            for nx, ny in SHAPES:
-                out.append((f"inst_{tag}_k{kind}_{nx}{ny}", ["-DPM_R=" + R, f"-DPM_NX={nx}", f"-DPM_NY={ny}",
-                                                            f"-DPM_KIND={kind}"], "inst.cu"))
-        out.append((f"inst_{tag}_ct", ["-DPM_R=" + R, "-DPM_NX=5", "-DPM_NY=2", "-DPM_KIND=2"], "inst.cu"))
-        out.append((f"inst_{tag}_vdp", ["-DPM_R=" + R, "-DPM_NX=2", "-DPM_NY=1", "-DPM_KIND=3"], "inst.cu"))
+        for K in RUN_LENGTHS:
+            base = ["-DPM_R=" + R, f"-DPM_K={K}"]
+            for kind in (0, 1):
+                for nx, ny in SHAPES:
+                    out.append((f"inst_{tag}_K{K}_k{kind}_{nx}{ny}",
+                                base + [f"-DPM_NX={nx}", f"-DPM_NY={ny}", f"-DPM_KIND={kind}"], "inst.cu"))
+            out.append((f"inst_{tag}_K{K}_ct", base + ["-DPM_NX=5", "-DPM_NY=2", "-DPM_KIND=2"], "inst.cu"))
+            out.append((f"inst_{tag}_K{K}_vdp", base + ["-DPM_NX=2", "-DPM_NY=1", "-DPM_KIND=3"], "inst.cu"))
     out.append(("pmap_abi", [], "pmap_abi.cu"))
     return out
 

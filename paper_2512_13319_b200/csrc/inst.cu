@@ -1,20 +1,20 @@
 // inst.cu -- one explicit instantiation of the solver per translation unit.
-// Compiled once per (PM_R, PM_NX, PM_NY, PM_KIND) by the build (see build.py):
+// Compiled once per (PM_R, PM_NX, PM_NY, PM_KIND, PM_K) by the build (see build.py):
 //   PM_KIND 0 = LTI linear, 1 = time-varying linear, 2 = coordinated turn, 3 = Van der Pol.
 #include "pmap_make.cuh"
 
 namespace pmap_rt {
 #if PM_KIND == 0
-template Runner* make_lti<PM_R, PM_NX, PM_NY>(const double*, const double*, const double*, const double*,
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K>(const double*, const double*, const double*, const double*,
                                               const double*, const double*, const double*, const double*,
                                               const double*, const double*, const double*);
 #elif PM_KIND == 1
-template Runner* make_tv<PM_R, PM_NX, PM_NY>(const PM_R*, const PM_R*, const PM_R*, const PM_R*, const PM_R*,
+template Runner* make_tv<PM_R, PM_NX, PM_NY, PM_K>(const PM_R*, const PM_R*, const PM_R*, const PM_R*, const PM_R*,
                                              const PM_R*, const PM_R*, const int64_t*, int, double, const double*,
                                              const double*);
 #elif PM_KIND == 2
-template Runner* make_nl<PM_R, 5, 2, 1>(double, double, const double*, const double*, const double*, const double*);
+template Runner* make_nl<PM_R, 5, 2, 1, PM_K>(double, double, const double*, const double*, const double*, const double*);
 #elif PM_KIND == 3
-template Runner* make_nl<PM_R, 2, 1, 2>(double, double, const double*, const double*, const double*, const double*);
+template Runner* make_nl<PM_R, 2, 1, 2, PM_K>(double, double, const double*, const double*, const double*, const double*);
 #endif
 }  // namespace pmap_rt

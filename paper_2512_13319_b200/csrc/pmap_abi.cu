@@ -29,33 +29,51 @@ namespace {
 
 // ------------------------------------------------------------- dispatch
 template <typename R>
-static Runner* dispatch_lti(int nx, int ny, const double* A, const double* b, const double* C, const double* J,
-                            const double* K, const double* h0, const double* J0, const double* h00,
+static Runner* dispatch_lti(int kr, int nx, int ny, const double* A, const double* b, const double* C,
+                            const double* J, const double* K, const double* h0, const double* J0, const double* h00,
                             const double* Am, const double* bm, const double* Cm) {
-#define PM_CASE(NXV, NYV) \
-  if (nx == NXV && ny == NYV) return make_lti<R, NXV, NYV>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm);
+#define PM_CASE(NXV, NYV)                                                                                    \
+  if (nx == NXV && ny == NYV)                                                                                \
+    return kr == kKBig ? make_lti<R, NXV, NYV, kKBig>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm)                \
+                       : make_lti<R, NXV, NYV, kKSmall>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm);
   PM_SHAPES(PM_CASE)
 #undef PM_CASE
   return nullptr;
 }
 
 template <typename R>
-static Runner* dispatch_tv(int nx, int ny, const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r,
-                           const R* Rm, const int64_t* str, int nw, double dt, const double* P0i,
+static Runner* dispatch_tv(int kr, int nx, int ny, const R* F, const R* c, const R* L, const R* Wm, const R* H,
+                           const R* r, const R* Rm, const int64_t* str, int nw, double dt, const double* P0i,
                            const double* P0im0) {
-#define PM_CASE(NXV, NYV) \
-  if (nx == NXV && ny == NYV) return make_tv<R, NXV, NYV>(F, c, L, Wm, H, r, Rm, str, nw, dt, P0i, P0im0);
+#define PM_CASE(NXV, NYV)                                                                                    \
+  if (nx == NXV && ny == NYV)                                                                                \
+    return kr == kKBig ? make_tv<R, NXV, NYV, kKBig>(F, c, L, Wm, H, r, Rm, str, nw, dt, P0i, P0im0)         \
+                       : make_tv<R, NXV, NYV, kKSmall>(F, c, L, Wm, H, r, Rm, str, nw, dt, P0i, P0im0);
   PM_SHAPES(PM_CASE)
 #undef PM_CASE
   return nullptr;
 }
 
 template <typename R>
-static Runner* dispatch_nl(int kind, double dt, double mu, const double* C, const double* Ri, const double* P0i,
-                           const double* P0im0) {
-  if (kind == MAP_NL_COORD_TURN) return make_nl<R, 5, 2, 1>(dt, mu, C, Ri, P0i, P0im0);
-  if (kind == MAP_NL_VAN_DER_POL) return make_nl<R, 2, 1, 2>(dt, mu, C, Ri, P0i, P0im0);
+static Runner* dispatch_nl(int kr, int kind, double dt, double mu, const double* C, const double* Ri,
+                           const double* P0i, const double* P0im0) {
+  if (kind == MAP_NL_COORD_TURN)
+    return kr == kKBig ? make_nl<R, 5, 2, 1, kKBig>(dt, mu, C, Ri, P0i, P0im0)
+                       : make_nl<R, 5, 2, 1, kKSmall>(dt, mu, C, Ri, P0i, P0im0);
+  if (kind == MAP_NL_VAN_DER_POL)
+    return kr == kKBig ? make_nl<R, 2, 1, 2, kKBig>(dt, mu, C, Ri, P0i, P0im0)
+                       : make_nl<R, 2, 1, 2, kKSmall>(dt, mu, C, Ri, P0i, P0im0);
   return nullptr;
+}
+
+// Run length: 2048-node tiles when they give >= 4 tiles per SM-slot-row of the GPU
+// (148 SMs), else 512-node tiles so small problems still fill the machine.
+static int choose_run_length(int64_t Nn, int64_t batch) {
+  const char* e = getenv("PMAP_K");
+  if (e && atoi(e) == kKSmall) return kKSmall;
+  if (e && atoi(e) == kKBig) return kKBig;
+  const int64_t tiles_big = batch * ((Nn + (int64_t)kNT * kKBig - 1) / ((int64_t)kNT * kKBig));
+  return tiles_big >= 4 * 148 ? kKBig : kKSmall;
 }
 
 static bool is_device_ptr(const void* ptr) {
@@ -143,7 +161,8 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   g.Nn = a1 - a0;
   g.node0 = a0;
   g.batch = d.batch;
-  const int64_t L = (int64_t)kNT * kK;
+  const int kr = choose_run_length(g.Nn, g.batch);
+  const int64_t L = (int64_t)kNT * kr;
   g.tpt = (g.Nn + L - 1) / L;
   g.gpt = (g.tpt + NT2 - 1) / NT2;
   if (g.Nn < 1) return MAP_E_ARG;
@@ -204,9 +223,9 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
         for (int j = 0; j < nx; ++j)
           for (int k = 0; k < nx; ++k) Cmf[i * nx + j] += T1[i * nx + k] * Am[j * nx + k];
       sym_pack(Cmf.data(), Cmp.data());
-      rn = f32 ? dispatch_lti<float>(nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
+      rn = f32 ? dispatch_lti<float>(kr, nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
                                      J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data())
-               : dispatch_lti<double>(nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
+               : dispatch_lti<double>(kr, nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
                                       J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data());
     } else {
       p->kind = Kind::TV;
@@ -239,11 +258,11 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
         off += len[k];
       }
       if (f32)
-        rn = dispatch_tv<float>(nx, ny, (const float*)dptr[0], (const float*)dptr[1], (const float*)dptr[2],
+        rn = dispatch_tv<float>(kr, nx, ny, (const float*)dptr[0], (const float*)dptr[1], (const float*)dptr[2],
                                 (const float*)dptr[3], (const float*)dptr[4], (const float*)dptr[5],
                                 (const float*)dptr[6], str, nw, dt, P0ip.data(), P0im0.data());
       else
-        rn = dispatch_tv<double>(nx, ny, (const double*)dptr[0], (const double*)dptr[1], (const double*)dptr[2],
+        rn = dispatch_tv<double>(kr, nx, ny, (const double*)dptr[0], (const double*)dptr[1], (const double*)dptr[2],
                                  (const double*)dptr[3], (const double*)dptr[4], (const double*)dptr[5],
                                  (const double*)dptr[6], str, nw, dt, P0ip.data(), P0im0.data());
     }
@@ -262,8 +281,8 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     sym_pack(Q.data(), Cp.data());
     if (!h_inv(ny, nl->R, Ri.data())) return MAP_E_ARG;
     const double mu = (nl->nparams >= 1 && nl->params) ? nl->params[0] : 0.0;
-    rn = f32 ? dispatch_nl<float>(nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data())
-             : dispatch_nl<double>(nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data());
+    rn = f32 ? dispatch_nl<float>(kr, nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data())
+             : dispatch_nl<double>(kr, nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data());
   }
   if (!rn) return MAP_E_UNSUPPORTED;
   p->runner.reset(rn);
@@ -487,7 +506,7 @@ map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, doub
   if (tol == 0.0) {
     // fixed number of passes, no host synchronisation: one CUDA graph
     const void* key[4] = {yd, xd, (const void*)(intptr_t)passes, nullptr};
-    const bool capture = p->d.world == 1 && !p->force_shard;
+    const bool capture = p->d.world == 1 && !p->force_shard && !p->prof;  // profiling: plain launches
     if (capture && !(p->graph && memcmp(key, p->graph_key, sizeof key) == 0)) {
       if (p->graph) {
         cudaGraphExecDestroy(p->graph);

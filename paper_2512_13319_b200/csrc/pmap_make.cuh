@@ -4,11 +4,11 @@
 
 namespace pmap_rt {
 
-template <typename R, int N, int NY>
+template <typename R, int N, int NY, int KR>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
                         const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
                         const double* Cm) {
-  auto* rn = new RunnerT<R, N, NY, SrcLTI<R, N, NY>>();
+  auto* rn = new RunnerT<R, N, NY, SrcLTI<R, N, NY>, KR>();
   auto& s = rn->src;
   constexpr int NS = Dim<N>::NS;
   for (int i = 0; i < N; ++i) {
@@ -31,10 +31,10 @@ Runner* make_lti(const double* A, const double* b, const double* C, const double
   return rn;
 }
 
-template <typename R, int N, int NY>
+template <typename R, int N, int NY, int KR>
 Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r, const R* Rm,
                        const int64_t* str, int nw, double dt, const double* P0i, const double* P0im0) {
-  auto* rn = new RunnerT<R, N, NY, SrcTV<R, N, NY>>();
+  auto* rn = new RunnerT<R, N, NY, SrcTV<R, N, NY>, KR>();
   auto& s = rn->src;
   s.F = F; s.c = c; s.L = L; s.W = Wm; s.H = H; s.r = r; s.Rm = Rm;
   s.sF = str[0]; s.sc = str[1]; s.sL = str[2]; s.sW = str[3]; s.sH = str[4]; s.sr = str[5]; s.sR = str[6];
@@ -45,10 +45,10 @@ Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, con
   return rn;
 }
 
-template <typename R, int N, int NY, int KIND>
+template <typename R, int N, int NY, int KIND, int KR>
 Runner* make_nl(double dt, double mu, const double* C, const double* Ri, const double* P0i,
                        const double* P0im0) {
-  auto* rn = new RunnerT<R, N, NY, SrcNL<R, N, NY, KIND>>();
+  auto* rn = new RunnerT<R, N, NY, SrcNL<R, N, NY, KIND>, KR>();
   auto& s = rn->src;
   s.dt = (R)dt;
   s.mu = (R)mu;

@@ -25,7 +25,10 @@ using namespace pmap;
 namespace pmap_rt {
 
 constexpr int kNT = 64;  // runs (threads) per tile
-constexpr int kK = 32;   // nodes per run
+// nodes per run K is a template parameter of the runner: 32 (tiles of 2048 nodes) for
+// large problems, 8 (512-node tiles) when that leaves too few tiles to fill the GPU
+constexpr int kKBig = 32;
+constexpr int kKSmall = 8;
 
 enum class Kind { LTI, TV, NL };
 
@@ -63,7 +66,7 @@ inline bool h_is_finite(const double* a, int n) {
 }
 
 // ---------------------------------------------------------------- workspace
-template <typename R, int N>
+template <typename R, int N, int K>
 struct WsLayout {
   size_t run_incl, tile_agg1, tile_incl1, group_agg1, group_carry1, total1, sv, run_suf, tile_agg2,
       tile_sufx2, group_agg2, group_carry2, total2, carry_in, xend, tf_run, tf_tile, tf_tincl, tf_gagg, tf_gcarry, bytes;
@@ -84,7 +87,7 @@ struct WsLayout {
     group_agg1 = take(ng * E::SZ);
     group_carry1 = take(ng * V::SZ);
     total1 = take(B * E::SZ);
-    sv = take(nt * V::SZ * kK * kNT);
+    sv = take(nt * V::SZ * K * kNT);
     run_suf = take(nt * A::SZ * kNT);
     tile_agg2 = take(nt * A::SZ);
     tile_sufx2 = take(nt * A::SZ);
@@ -262,7 +265,7 @@ __global__ void k_shard_fold1(int world, int rank, int64_t batch, const R* __res
   if (!ok) atomicMin(flag, 0ull);
 }
 
-template <typename R, int N>
+template <typename R, int N, int K>
 __global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ sv_last,
                               int64_t sv_stride, R* __restrict__ payload, unsigned long long* flag) {
   // payload per trajectory: [Aff total][x_T (last rank only)]
@@ -272,7 +275,7 @@ __global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ to
   for (int k = 0; k < A::SZ; ++k) payload[b * (A::SZ + N) + k] = total2[b * A::SZ + k];
   if (last) {
     VF<R, N> V;
-    load(V, sv_last + b * sv_stride, (int64_t)kK * kNT);
+    load(V, sv_last + b * sv_stride, (int64_t)K * kNT);
     R x[N];
     bool ok = true;
     spd_solve<R, N>(V.S, V.v, x, ok);
@@ -301,18 +304,18 @@ __global__ void k_shard_fold2(int world, int rank, int64_t batch, const R* __res
 
 
 
-template <typename R, int N, int NY, class Src>
+template <typename R, int N, int NY, class Src, int K>
 struct RunnerT : Runner {
   Src src;
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
   static constexpr bool IS_LTI = std::is_same<Src, SrcLTI<R, N, NY>>::value;
-  using Tab = LtiTables<R, N, kNT, kK>;
+  using Tab = LtiTables<R, N, kNT, K>;
   Tab* tab = nullptr;    // pass-1 tables (LTI only)
   Tab* tab_m = nullptr;  // mirrored-element tables (two-filter pass B)
   LtiNode<R, N, NY> lnode{}, lnode_m{};
-  LtiFoldParams<R, N, NY, kK, Log2<kNT>::value> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
+  LtiFoldParams<R, N, NY, K, Log2<kNT>::value> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
   bool use_lti = false;
 
   ~RunnerT() override {
@@ -324,19 +327,19 @@ struct RunnerT : Runner {
 
   // interior (LTI-specialised) tile range [j_lo, j_hi) of a trajectory
   static int64_t lti_jlo(const Geom& g, bool rev) { return (rev || g.node0 == 0) ? 1 : 0; }
-  static int64_t lti_jhi(const Geom& g) { return g.Nn / ((int64_t)kNT * kK); }
+  static int64_t lti_jhi(const Geom& g) { return g.Nn / ((int64_t)kNT * K); }
 
   // Pass-1 reduce: LTI-specialised kernel on interior tiles, general kernel on the
   // boundary tiles (node 0 / terminal node, ragged last tile); all tiles otherwise.
   template <bool REV, class KS>
   void reduce1(PlanState& p, cudaStream_t s, int kid, const KS& ksrc,
-               const LtiFoldParams<R, N, NY, kK, Log2<kNT>::value>& fpar,
+               const LtiFoldParams<R, N, NY, K, Log2<kNT>::value>& fpar,
                const Tab* tb, const R* y, const R* xbar, R* run_incl, R* tile_agg) {
     const LtiNode<R, N, NY>& ln = fpar.node;
     const Geom& g = p.g;
     if (!(use_lti && tb)) {
       PM_LAUNCH(p, s, kid,
-                (k_p1_reduce<R, N, NY, kNT, kK, KS, REV><<<(unsigned)(g.batch * g.tpt), kNT, smem_reduce(), s>>>(
+                (k_p1_reduce<R, N, NY, kNT, K, KS, REV><<<(unsigned)(g.batch * g.tpt), kNT, smem_reduce(), s>>>(
                     ksrc, g, y, xbar, run_incl, tile_agg, p.dflag, 0, 0, 0)));
       return;
     }
@@ -354,13 +357,13 @@ struct RunnerT : Runner {
       cudaEventRecord(e0, s);
       cudaStreamWaitEvent(se, e0, 0);
       PM_LAUNCH(p, se, kid + 1,
-                (k_p1_reduce_lti_edge<R, N, NY, kNT, kK, KS, REV><<<(unsigned)(g.batch * nsel), kNT, smem_reduce(),
+                (k_p1_reduce_lti_edge<R, N, NY, kNT, K, KS, REV><<<(unsigned)(g.batch * nsel), kNT, smem_reduce(),
                                                                     se>>>(ksrc, ln, g, nsel, js[0], js[1], y, tb,
                                                                           run_incl, tile_agg, p.dflag)));
     }
     if (n_int > 0)
       PM_LAUNCH(p, s, kid,
-                (k_p1_reduce_lti<R, N, NY, kNT, kK, REV><<<(unsigned)(g.batch * n_int), kNT, 0, s>>>(
+                (k_p1_reduce_lti<R, N, NY, kNT, K, REV><<<(unsigned)(g.batch * n_int), kNT, 0, s>>>(
                     fpar, g, j_lo, n_int, y, tb, run_incl, tile_agg)));
     if (nsel > 0) {
       cudaEventRecord(e1, se);
@@ -369,7 +372,7 @@ struct RunnerT : Runner {
   }
 
   size_t ws_bytes(const Geom& g, bool tf) const override {
-    WsLayout<R, N> L;
+    WsLayout<R, N, K> L;
     L.plan(g, tf);
     return L.bytes;
   }
@@ -383,27 +386,27 @@ struct RunnerT : Runner {
   static size_t smem_p2groups() { return sizeof(R) * (A::SZ * NT4 + N); }
 
   void set_attrs() override {
-    cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, kK, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, K, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_reduce());
     cudaFuncSetAttribute(k_p1_tiles<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tiles());
     cudaFuncSetAttribute(k_p1_groups<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_groups());
-    cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, kK, Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, K, Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_down());
     cudaFuncSetAttribute(k_p2_tiles<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p2tiles());
-    cudaFuncSetAttribute(k_p2_groups<R, N, kNT, kK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_p2_groups<R, N, kNT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_p2groups());
     if constexpr (IS_LTI) {
-      cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, kK, Src, false>,
+      cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, K, Src, false>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
-      cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, kK, Mirror<Src>, true>,
+      cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, K, Mirror<Src>, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
     }
     if constexpr (Src::HAS_MIRROR) {
-      cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, kK, Mirror<Src>, true>,
+      cudaFuncSetAttribute(k_p1_reduce<R, N, NY, kNT, K, Mirror<Src>, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
-      cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, kK, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_p1_down<R, N, NY, kNT, K, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem_down());
-      cudaFuncSetAttribute(k_tf_down<R, N, NY, kNT, kK, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_tf_down<R, N, NY, kNT, K, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem_down());
     }
   }
@@ -424,7 +427,7 @@ struct RunnerT : Runner {
 
   void phase1(PlanState& p, const void* yv, const void* xbarv, void* payload) override {
     const Geom& g = p.g;
-    WsLayout<R, N> L;
+    WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
     auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
     const R* y = static_cast<const R*>(yv);
@@ -442,7 +445,7 @@ struct RunnerT : Runner {
 
   void phase2(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* payload) override {
     const Geom& g = p.g;
-    WsLayout<R, N> L;
+    WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
     auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
     const R* y = static_cast<const R*>(yv);
@@ -460,7 +463,7 @@ struct RunnerT : Runner {
               (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
                   g, W(L.group_agg1), carry_in, W(L.group_carry1), nullptr, p.dflag)));
     PM_LAUNCH(p, s, K_P1_DOWN,
-              (k_p1_down<R, N, NY, kNT, kK, Src, true><<<ntiles, kNT, smem_down(), s>>>(
+              (k_p1_down<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, smem_down(), s>>>(
                   src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
                   W(L.tile_agg2), p.dflag, (use_lti && tab) ? tab->E1 : nullptr, lti_jlo(g, false),
                   lti_jhi(g))));
@@ -469,15 +472,15 @@ struct RunnerT : Runner {
                   g, W(L.tile_agg2), W(L.tile_sufx2), W(L.group_agg2))));
     if (payload) {
       PM_LAUNCH(p, s, K_P2_GROUPS,
-                (k_p2_groups<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
+                (k_p2_groups<R, N, kNT, K><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
                     g, W(L.sv), W(L.group_agg2), nullptr, W(L.group_carry2), W(L.total2), p.dflag)));
       const int64_t l = g.Nn - 1;
-      const int64_t Lt = (int64_t)kNT * kK;
-      const int64_t j = l / Lt, q = l % Lt, rr = q / kK, m = q % kK;
-      const R* sv_last = W(L.sv) + j * (int64_t)V::SZ * kK * kNT + m * kNT + rr;
-      const int64_t sv_stride = g.tpt * (int64_t)V::SZ * kK * kNT;
+      const int64_t Lt = (int64_t)kNT * K;
+      const int64_t j = l / Lt, q = l % Lt, rr = q / K, m = q % K;
+      const R* sv_last = W(L.sv) + j * (int64_t)V::SZ * K * kNT + m * kNT + rr;
+      const int64_t sv_stride = g.tpt * (int64_t)V::SZ * K * kNT;
       PM_LAUNCH(p, s, K_SHARD,
-                (k_shard_pack2<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
+                (k_shard_pack2<R, N, K><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
                     g.batch, p.d.rank == p.d.world - 1, W(L.total2), sv_last, sv_stride, static_cast<R*>(payload),
                     p.dflag)));
     }
@@ -485,7 +488,7 @@ struct RunnerT : Runner {
 
   void phase3(PlanState& p, const void* xbarv, const void* gathered, void* xv, void* fm, void* fP) override {
     const Geom& g = p.g;
-    WsLayout<R, N> L;
+    WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
     auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
     const R* xbar = static_cast<const R*>(xbarv);
@@ -500,16 +503,16 @@ struct RunnerT : Runner {
       xend_in = W(L.xend);
     }
     PM_LAUNCH(p, s, K_P2_GROUPS,
-              (k_p2_groups<R, N, kNT, kK><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
+              (k_p2_groups<R, N, kNT, K><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
                   g, W(L.sv), W(L.group_agg2), xend_in, W(L.group_carry2), nullptr, p.dflag)));
     PM_LAUNCH(p, s, K_P2_DOWN,
-              (k_p2_down<R, N, kNT, kK, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
+              (k_p2_down<R, N, kNT, K, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
                                                                   W(L.tile_sufx2), W(L.group_carry2),
                                                                   W(L.carry_in), x, p.dflag)));
     if (fm || fP) {
       const int64_t n = g.batch * g.Nn;
       PM_LAUNCH(p, s, K_FILTER_OUT,
-                (k_filter_out<R, N, kNT, kK><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, W(L.sv), (R*)fm,
+                (k_filter_out<R, N, kNT, K><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, W(L.sv), (R*)fm,
                                                                                         (R*)fP, p.dflag)));
     }
   }
@@ -547,7 +550,7 @@ struct RunnerT : Runner {
   void two_filter(PlanState& p, const void* yv, void* xv) override {
     if constexpr (Src::HAS_MIRROR) {
       const Geom& g = p.g;
-      WsLayout<R, N> L;
+      WsLayout<R, N, K> L;
       L.plan(g, true);
       auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
       const R* y = static_cast<const R*>(yv);
@@ -565,7 +568,7 @@ struct RunnerT : Runner {
                 (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
                     g, W(L.group_agg1), nullptr, W(L.group_carry1), nullptr, p.dflag)));
       PM_LAUNCH(p, s, K_P1_DOWN,
-                (k_p1_down<R, N, NY, kNT, kK, Src, false><<<ntiles, kNT, smem_down(), s>>>(
+                (k_p1_down<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
                     nullptr, p.dflag, nullptr, 0, 0)));
       // pass B: backward information filter over mirrored elements (reverse node order)
@@ -580,7 +583,7 @@ struct RunnerT : Runner {
       cudaEventRecord(p.ev_join, s);
       cudaStreamWaitEvent(s2, p.ev_join, 0);
       PM_LAUNCH(p, s2, K_TF_DOWN,
-                (k_tf_down<R, N, NY, kNT, kK, Src><<<ntiles, kNT, smem_down(), s2>>>(
+                (k_tf_down<R, N, NY, kNT, K, Src><<<ntiles, kNT, smem_down(), s2>>>(
                     mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, p.dflag)));
       cudaEventRecord(p.ev_fork, s2);
       cudaStreamWaitEvent(s, p.ev_fork, 0);
@@ -601,8 +604,8 @@ struct RunnerT : Runner {
   }
 };
 
-template <typename R, int N, int NY, class Src>
-bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
+template <typename R, int N, int NY, class Src, int K>
+bool RunnerT<R, N, NY, Src, K>::prepare(PlanState& p) {
   if constexpr (IS_LTI) {
     const char* gen = getenv("PMAP_GENERAL");
     if (gen && gen[0] == '1') return true;  // force the general reduce (A/B checks)
@@ -624,15 +627,15 @@ bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
     if (cudaMalloc(&tab, sizeof(Tab)) != cudaSuccess || cudaMalloc(&tab_m, sizeof(Tab)) != cudaSuccess ||
         cudaMalloc(&dok, 2 * sizeof(int)) != cudaSuccess)
       return false;
-    k_lti_setup<R, N, NY, kNT, kK><<<1, 1>>>(lnode, tab, dok);
-    k_lti_setup<R, N, NY, kNT, kK><<<1, 1>>>(lnode_m, tab_m, dok + 1);
+    k_lti_setup<R, N, NY, kNT, K><<<1, 1>>>(lnode, tab, dok);
+    k_lti_setup<R, N, NY, kNT, K><<<1, 1>>>(lnode_m, tab_m, dok + 1);
     int ok[2] = {0, 0};
     cudaError_t e = cudaMemcpy(ok, dok, sizeof ok, cudaMemcpyDeviceToHost);
     cudaFree(dok);
     if (e != cudaSuccess) return false;
     use_lti = ok[0] && ok[1];  // a failed setup (singular pivot) falls back to the general kernels
     if (use_lti) {
-      auto pull = [&](LtiFoldParams<R, N, NY, kK, Log2<kNT>::value>& fpp, const LtiNode<R, N, NY>& ln,
+      auto pull = [&](LtiFoldParams<R, N, NY, K, Log2<kNT>::value>& fpp, const LtiNode<R, N, NY>& ln,
                       const Tab* t) {
         fpp.node = ln;
         bool okc = true;
@@ -645,7 +648,7 @@ bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
         }
         if (!okc || cudaMemcpy(fpp.crun, t->crun, sizeof fpp.crun, cudaMemcpyDeviceToHost) != cudaSuccess)
           return false;
-        for (int m = 0; m < kK; ++m)
+        for (int m = 0; m < K; ++m)
           for (int i = 0; i < 2 * N; ++i)
             if (cudaMemcpy(fpp.GK[m][i], t->GK[m][i], sizeof(R) * NY, cudaMemcpyDeviceToHost) != cudaSuccess)
               return false;
@@ -661,14 +664,14 @@ bool RunnerT<R, N, NY, Src>::prepare(PlanState& p) {
 // ---------------------------------------------------------- instantiation
 // Factories are declared here and explicitly instantiated, one (dtype, shape,
 // model kind) per translation unit, in inst.cu (see pmap_make.cuh).
-template <typename R, int N, int NY>
+template <typename R, int N, int NY, int KR>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
                  const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
                  const double* Cm);
-template <typename R, int N, int NY>
+template <typename R, int N, int NY, int KR>
 Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r, const R* Rm,
                 const int64_t* str, int nw, double dt, const double* P0i, const double* P0im0);
-template <typename R, int N, int NY, int KIND>
+template <typename R, int N, int NY, int KIND, int KR>
 Runner* make_nl(double dt, double mu, const double* C, const double* Ri, const double* P0i, const double* P0im0);
 
 #define PM_SHAPES(X) X(1, 1) X(2, 1) X(2, 2) X(3, 1) X(3, 2) X(4, 2) X(5, 2)

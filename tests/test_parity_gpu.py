@@ -374,3 +374,48 @@ def test_nccl_exchange_path_single_rank(torch_cuda, monkeypatch):
         assert rel(x.cpu().numpy(), x_ref) < 1e-12
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("K", ["8", "32"])
+@pytest.mark.parametrize("case", ["lti", "lti_tf", "tv", "ct", "shard3"])
+def test_both_run_lengths(torch_cuda, K, case, monkeypatch):
+    """Both compiled tile geometries (64 runs x 8 nodes and 64 runs x 32 nodes, PMAP_K)
+    on multi-tile problems with ragged tails, for each model kind."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    monkeypatch.setenv("PMAP_K", K)
+    if case in ("lti", "lti_tf", "shard3"):
+        spec = wl.wiener_velocity()
+        spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+        spec.r = np.array([0.5, -0.25])
+        T, B = 9_001, 2
+        _, y = wl.simulate_linear(spec, T, seed=21, batch=B)
+        xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
+        if case == "shard3":
+            G = 3
+            plans = [pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H,
+                             r=spec.r, R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, rank=r, world=G) for r in range(G)]
+            ys = [to_dev(torch, y[:, slice(*pm.shard_range(r, G, T))]) for r in range(G)]
+            g1 = torch.cat([plans[r].shard_phase(1, ys[r]) for r in range(G)])
+            g2 = torch.cat([plans[r].shard_phase(2, ys[r], g1) for r in range(G)])
+            x = torch.cat([plans[r].shard_phase(3, gathered=g2) for r in range(G)], dim=1).cpu().numpy()
+        else:
+            plan = gpu_plan(spec, T, batch=B)
+            x = (plan.two_filter if case == "lti_tf" else plan.solve_linear)(to_dev(torch, y)).cpu().numpy()
+        for b in range(B):
+            assert rel(x[b], xo[b]) < TOL64
+    elif case == "tv":
+        T = 5_000
+        spec = tv_spec(T, 4, 2)
+        y = np.random.default_rng(2).standard_normal((T + 1, 2))
+        xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+        x = gpu_plan(spec, T).solve_linear(to_dev(torch, y[None]))
+        assert rel(x[0].cpu().numpy(), xo) < TOL64
+    else:
+        s = wl.coordinated_turn()
+        T = 6_000
+        _, y = wl.simulate_nonlinear(s, T, seed=8)
+        xo, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=4)
+        plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1)
+        x, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=4)
+        assert rel(x[0].cpu().numpy(), xo) < TOL64
