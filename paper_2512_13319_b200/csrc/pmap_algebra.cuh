@@ -190,6 +190,49 @@ PM_INLINE float pm_rcp(float x) { return __frcp_rn(x); }
 // dominant for small dt; general aggregates fall back to the pivoted path.
 template <typename R, int N>
 PM_INLINE void lu_factor(LUF<R, N>& f, bool& ok) {
+#ifdef PM_LU_SPEC
+  // speculative unpivoted factorisation; the dominance test runs alongside it and
+  // only a non-dominant matrix (rare) is refactorised with pivoting
+  R orig[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) orig[i][j] = f.a[i][j];
+  bool okf = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    f.piv[k] = k;
+    R d = f.a[k][k];
+    okf = okf && (d != R(0)) && (d == d);
+    R di = pm_rcp(d);
+    f.dinv[k] = di;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      R l = f.a[i][k] * di;
+      f.a[i][k] = l;
+#pragma unroll
+      for (int j = k + 1; j < N; ++j) f.a[i][j] = fma(-l, f.a[k][j], f.a[i][j]);
+    }
+  }
+  bool dom = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    R off = R(0);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (i != k) off += pm_abs(orig[i][k]);
+    dom = dom && (pm_abs(orig[k][k]) >= off);
+  }
+  f.nopiv = dom;
+  if (dom) {
+    ok = ok && okf;
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) f.a[i][j] = orig[i][j];
+#else
   bool dom = true;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -218,6 +261,7 @@ PM_INLINE void lu_factor(LUF<R, N>& f, bool& ok) {
     }
     return;
   }
+#endif
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     int p = k;

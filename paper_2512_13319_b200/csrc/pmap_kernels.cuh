@@ -35,6 +35,10 @@ struct Geom {
   int64_t batch;
 };
 
+#ifndef PM_DOWN_UNROLL
+#define PM_DOWN_UNROLL 1
+#endif
+constexpr int kDownUnroll = PM_DOWN_UNROLL;  // node-loop unroll of k_p1_down
 constexpr int NT2 = 128;  // tiles per group (k_p1_tiles block size)
 constexpr int NT3 = 128;  // k_p1_groups block size
 constexpr int NT4 = 256;  // k_p2_groups block size
@@ -298,7 +302,7 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     store(agg, sh + r, NT);  // parked in shared memory across the node loop
   }
   R* svt = sv + tile * (int64_t)V::SZ * K * NT;
-#pragma unroll 1
+#pragma unroll kDownUnroll
   for (int m = 0; m < K; ++m) {
     const int64_t l = l0 + m;
     if (l >= g.Nn) break;
