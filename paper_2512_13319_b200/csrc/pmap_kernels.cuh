@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(NT2) k_p1_tiles(const Geom g, const R* __restr
   const int t = threadIdx.x;
   const int64_t jt = gg * NT2 + t;
   const bool valid = jt < g.tpt;
+  const int cnt = (int)min((int64_t)NT2, g.tpt - gg * NT2);  // valid tiles in this group
   bool ok = true;
   E acc;
   if (valid)
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(NT2) k_p1_tiles(const Geom g, const R* __restr
   else
     set_identity(acc);
 #pragma unroll 1
-  for (int d = 1; d < NT2; d <<= 1) {
+  for (int d = 1; d < cnt; d <<= 1) {
     store(acc, sh + t, NT2);
     __syncthreads();
     if (t >= d) {
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(NT2) k_p1_tiles(const Geom g, const R* __restr
     __syncthreads();
   }
   if (valid) store(acc, tile_incl + (b * g.tpt + jt) * E::SZ, 1);
-  if (t == NT2 - 1) store(acc, group_agg + grp * E::SZ, 1);
+  if (t == cnt - 1) store(acc, group_agg + grp * E::SZ, 1);
   if (!ok) flag_node(flag, g.node0 + jt);
 }
 
@@ -174,16 +175,20 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
   const int t = threadIdx.x;
   const int64_t c = (g.gpt + NT3 - 1) / NT3;
   const int64_t k0 = t * c, k1 = min(g.gpt, k0 + c);
+  const int nact = (int)((g.gpt + c - 1) / c);  // threads holding groups
   bool ok = true;
   E acc;
   set_identity(acc);
   for (int64_t k = k0; k < k1; ++k) {
     E p;
     load(p, group_agg + (b * g.gpt + k) * E::SZ, 1);
-    combine(p, acc, acc, ok);
+    if (k == k0)
+      acc = p;
+    else
+      combine(p, acc, acc, ok);
   }
 #pragma unroll 1
-  for (int d = 1; d < NT3; d <<= 1) {
+  for (int d = 1; d < nact; d <<= 1) {
     store(acc, sh + t, NT3);
     __syncthreads();
     if (t >= d) {
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
     load(cin, carry_in + b * V::SZ, 1);
   else
     set_zero(cin);
-  if (t == NT3 - 1 && total_agg) store(acc, total_agg + b * E::SZ, 1);
+  if (t == nact - 1 && total_agg) store(acc, total_agg + b * E::SZ, 1);
   V cur = cin;
   if (t > 0) {
     E p;
@@ -374,13 +379,14 @@ __global__ void __launch_bounds__(NT2) k_p2_tiles(const Geom g, const R* __restr
   const int t = threadIdx.x;
   const int64_t jt = gg * NT2 + t;
   const bool valid = jt < g.tpt;
+  const int cnt = (int)min((int64_t)NT2, g.tpt - gg * NT2);
   A acc;
   if (valid)
     load(acc, tile_agg2 + (b * g.tpt + jt) * A::SZ, 1);
   else
     set_identity(acc);
 #pragma unroll 1
-  for (int d = 1; d < NT2; d <<= 1) {
+  for (int d = 1; d < cnt; d <<= 1) {
     store(acc, sh + t, NT2);
     __syncthreads();
     if (t + d < NT2) {
@@ -432,6 +438,7 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
   }
   const int64_t c = (g.gpt + NT4 - 1) / NT4;
   const int64_t k0 = t * c, k1 = min(g.gpt, k0 + c);
+  const int nact = (int)((g.gpt + c - 1) / c);
   A acc;
   set_identity(acc);
   for (int64_t k = k1 - 1; k >= k0; --k) {
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
     compose(p, acc, acc);
   }
 #pragma unroll 1
-  for (int d = 1; d < NT4; d <<= 1) {
+  for (int d = 1; d < nact; d <<= 1) {
     store(acc, sh + t, NT4);
     __syncthreads();
     if (t + d < NT4) {

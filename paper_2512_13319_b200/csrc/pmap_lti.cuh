@@ -403,26 +403,39 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
                                                       const LtiTables<R, N, NT, K>* __restrict__ tab,
                                                       R* __restrict__ run_incl, R* __restrict__ tile_agg) {
   using E = Elem<R, N>;
-  // padded run row in shared memory: 16-byte aligned rows, consecutive runs 4 banks apart
-  constexpr int ROW = ((K * NY * (int)sizeof(R) + 15) / 16 * 16 + 16) / (int)sizeof(R);
+  // The tile's y block is staged in two halves (KH nodes of every run at a time) to keep
+  // shared memory small (more CTAs per SM and room in L1 for the scan tables).
+  // Padded run rows: 16-byte aligned, consecutive runs 4 banks apart.
+  constexpr int KH = K / 2;
+  static_assert(K % 4 == 0, "run length");
+  constexpr int ROW = ((KH * NY * (int)sizeof(R) + 15) / 16 * 16 + 16) / (int)sizeof(R);
   __shared__ __align__(16) R ys[NT * ROW];
   const LtiNode<R, N, NY>& src = fp.node;
   const int64_t b = blockIdx.x / n_int;
   const int64_t j = j_lo + blockIdx.x % n_int;
   const int64_t tile = b * g.tpt + j;
   const int r = threadIdx.x;
-  // stage y: the tile covers local nodes [j NT K, (j+1) NT K) (REV: mirrored).
-  // One cp.async (LDGSTS) per node row: all in flight at once, padded destination.
-  {
-    const int64_t base = REV ? (g.Nn - (j + 1) * (int64_t)NT * K) : j * (int64_t)NT * K;
-    const R* src_y = y + (b * g.Nn + base) * NY;
-    constexpr int BYTES = NY * (int)sizeof(R);
-    static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16 || BYTES % 16 == 0, "row size");
+  const int64_t base = REV ? (g.Nn - (j + 1) * (int64_t)NT * K) : j * (int64_t)NT * K;
+  const R* src_y = y + (b * g.Nn + base) * NY;
+  constexpr int BYTES = NY * (int)sizeof(R);
+  static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16 || BYTES % 16 == 0, "row size");
+  const R* yr = ys + r * ROW;
+  // run fold as a sum of independent terms: (b, eta) = crun + sum_m GK[m] y_m
+  R acc0[2 * N], acc1[2 * N];
+#pragma unroll
+  for (int i = 0; i < 2 * N; ++i) {
+    acc0[i] = fp.crun[i];
+    acc1[i] = R(0);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    // one cp.async (LDGSTS) per node row, all in flight at once
 #pragma unroll 4
-    for (int node = r; node < NT * K; node += NT) {
-      const int tnode = REV ? NT * K - 1 - node : node;  // reversed order within the tile
-      const int run = tnode / K, m = tnode - run * K;
-      R* dst = ys + run * ROW + m * NY;
+    for (int q = r; q < NT * KH; q += NT) {
+      const int run = q / KH, mm = q - run * KH;
+      const int tpos = run * K + h * KH + mm;            // position in tile (scan order)
+      const int node = REV ? NT * K - 1 - tpos : tpos;   // position in memory
+      R* dst = ys + run * ROW + mm * NY;
       const R* srcp = src_y + (int64_t)node * NY;
       const unsigned sdst = (unsigned)__cvta_generic_to_shared(dst);
       if constexpr (BYTES % 16 == 0) {
@@ -434,31 +447,25 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
       }
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  }
-  __syncthreads();
-  const R* yr = ys + r * ROW;
-  // run fold as a sum of independent terms: (b, eta) = crun + sum_m GK[m] y_m
-  R acc0[2 * N], acc1[2 * N];
+    __syncthreads();
 #pragma unroll
-  for (int i = 0; i < 2 * N; ++i) {
-    acc0[i] = fp.crun[i];
-    acc1[i] = R(0);
-  }
-#pragma unroll
-  for (int m = 0; m < K; m += 2) {
-    R y0[NY], y1[NY];
-#pragma unroll
-    for (int k = 0; k < NY; ++k) {
-      y0[k] = yr[m * NY + k];
-      y1[k] = yr[(m + 1) * NY + k];
-    }
-#pragma unroll
-    for (int i = 0; i < 2 * N; ++i)
+    for (int mm = 0; mm < KH; mm += 2) {
+      const int m = h * KH + mm;
+      R y0[NY], y1[NY];
 #pragma unroll
       for (int k = 0; k < NY; ++k) {
-        acc0[i] = fma(fp.GK[m][i][k], y0[k], acc0[i]);
-        acc1[i] = fma(fp.GK[m + 1][i][k], y1[k], acc1[i]);
+        y0[k] = yr[mm * NY + k];
+        y1[k] = yr[(mm + 1) * NY + k];
       }
+#pragma unroll
+      for (int i = 0; i < 2 * N; ++i)
+#pragma unroll
+        for (int k = 0; k < NY; ++k) {
+          acc0[i] = fma(fp.GK[m][i][k], y0[k], acc0[i]);
+          acc1[i] = fma(fp.GK[m + 1][i][k], y1[k], acc1[i]);
+        }
+    }
+    if (h == 0) __syncthreads();  // the buffer is refilled by the second half
   }
   R bb[N], hh[N];
 #pragma unroll
