@@ -645,4 +645,42 @@ PM_INLINE void spd_solve(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N], b
   }
 }
 
+// Symmetric positive-definite solve S x = v by LDL^T (no square roots).
+template <typename R, int N>
+PM_INLINE void spd_solve_ldl(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N], bool& ok) {
+  R Lm[N][N], D[N], Di[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    R d = S[sidx(j, j, N)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = fma(-Lm[j][k] * D[k], Lm[j][k], d);
+    ok = ok && (d > R(0));
+    D[j] = d;
+    Di[j] = pm_rcp(d);
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      R t = S[sidx(i, j, N)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t = fma(-Lm[i][k] * D[k], Lm[j][k], t);
+      Lm[i][j] = t * Di[j];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R t = v[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) t = fma(-Lm[i][k], x[k], t);
+    x[i] = t;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] *= Di[i];
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    R t = x[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) t = fma(-Lm[k][i], x[k], t);
+    x[i] = t;
+  }
+}
+
 }  // namespace pmap

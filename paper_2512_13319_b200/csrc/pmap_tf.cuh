@@ -68,24 +68,43 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
     load(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), NT);
     vapply<R, N, false>(p, cur, cur, nullptr, ok);
   }
+  // x is staged in shared memory in chunks of KC nodes and stored as contiguous segments
+  constexpr int KC = 8;
+  static_assert(K % KC == 0, "chunking");
+  __shared__ R xs[NT][KC * N + 1];
 #pragma unroll 1
-  for (int m = 0; m < K; ++m) {
-    const int64_t lr = l0 + m;
-    if (lr >= g.Nn) break;
-    const int64_t l = g.Nn - 1 - lr;
-    E e;
-    mir.template node<R, N>(g.node0 + l, yb + l * NY, nullptr, e);
-    vapply<R, N, false>(e, cur, cur, nullptr, ok);  // (Lam_l, xi_l)
-    V Va;
-    load_sv<R, N, NT, K>(sv, g, b, l, Va);
-    R Ssum[Dim<N>::NS], rhs[N], xv[N];
+  for (int c = 0; c < K / KC; ++c) {
+#pragma unroll 1
+    for (int mm = 0; mm < KC; ++mm) {
+      const int64_t lr = l0 + c * KC + mm;
+      if (lr < g.Nn) {
+        const int64_t l = g.Nn - 1 - lr;
+        V Va;
+        load_sv<R, N, NT, K>(sv, g, b, l, Va);  // issued early: independent of the recursion
+        E e;
+        mir.template node<R, N>(g.node0 + l, yb + l * NY, nullptr, e);
+        vapply<R, N, false>(e, cur, cur, nullptr, ok);  // (Lam_l, xi_l)
+        R Ssum[Dim<N>::NS], rhs[N], xv[N];
 #pragma unroll
-    for (int k = 0; k < Dim<N>::NS; ++k) Ssum[k] = Va.S[k] + (cur.S[k] - e.J[k]);
+        for (int k = 0; k < Dim<N>::NS; ++k) Ssum[k] = Va.S[k] + (cur.S[k] - e.J[k]);
 #pragma unroll
-    for (int i = 0; i < N; ++i) rhs[i] = Va.v[i] + (cur.v[i] - e.h[i]);
-    spd_solve<R, N>(Ssum, rhs, xv, ok);
+        for (int i = 0; i < N; ++i) rhs[i] = Va.v[i] + (cur.v[i] - e.h[i]);
+        spd_solve_ldl<R, N>(Ssum, rhs, xv, ok);
 #pragma unroll
-    for (int i = 0; i < N; ++i) xo[l * N + i] = xv[i];
+        for (int i = 0; i < N; ++i) xs[r][mm * N + i] = xv[i];
+      }
+    }
+    __syncthreads();
+    // run rr's chunk holds nodes Nn-1-(l0_rr + c KC + mm), mm = 0..KC-1 (descending)
+    for (int rr = r >> 5; rr < NT; rr += NT / 32) {
+      const int64_t lrb = (j * NT + rr) * (int64_t)K + c * KC;
+      for (int q = r & 31; q < KC * N; q += 32) {
+        const int mm = q / N, i = q - mm * N;
+        const int64_t lr = lrb + mm;
+        if (lr < g.Nn) xo[(g.Nn - 1 - lr) * N + i] = xs[rr][q];
+      }
+    }
+    __syncthreads();
   }
   if (!ok) flag_node(flag, g.node0 + g.Nn - 1 - l0);
 }
