@@ -5,9 +5,14 @@
 
 namespace pmap_rt {
 #if PM_KIND == 0
-template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K>(const double*, const double*, const double*, const double*,
-                                              const double*, const double*, const double*, const double*,
-                                              const double*, const double*, const double*);
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 0>(const double*, const double*, const double*, const double*,
+                                                     const double*, const double*, const double*, const double*,
+                                                     const double*, const double*, const double*, const double*);
+#if PM_NX == 4 && PM_NY == 2  // rank-2 diffusion (Wiener velocity): Woodbury node update
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2>(const double*, const double*, const double*, const double*,
+                                                     const double*, const double*, const double*, const double*,
+                                                     const double*, const double*, const double*, const double*);
+#endif
 #elif PM_KIND == 1
 template Runner* make_tv<PM_R, PM_NX, PM_NY, PM_K>(const PM_R*, const PM_R*, const PM_R*, const PM_R*, const PM_R*,
                                              const PM_R*, const PM_R*, const int64_t*, int, double, const double*,

@@ -29,13 +29,17 @@ namespace {
 
 // ------------------------------------------------------------- dispatch
 template <typename R>
-static Runner* dispatch_lti(int kr, int nx, int ny, const double* A, const double* b, const double* C,
-                            const double* J, const double* K, const double* h0, const double* J0, const double* h00,
-                            const double* Am, const double* bm, const double* Cm) {
+static Runner* dispatch_lti(int kr, int nx, int ny, int lowrank, const double* A, const double* b,
+                            const double* C, const double* J, const double* K, const double* h0, const double* J0,
+                            const double* h00, const double* Am, const double* bm, const double* Cm,
+                            const double* U) {
+  if (nx == 4 && ny == 2 && lowrank == 2)
+    return kr == kKBig ? make_lti<R, 4, 2, kKBig, 2>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U)
+                       : make_lti<R, 4, 2, kKSmall, 2>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
 #define PM_CASE(NXV, NYV)                                                                                    \
   if (nx == NXV && ny == NYV)                                                                                \
-    return kr == kKBig ? make_lti<R, NXV, NYV, kKBig>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm)                \
-                       : make_lti<R, NXV, NYV, kKSmall>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm);
+    return kr == kKBig ? make_lti<R, NXV, NYV, kKBig, 0>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U)          \
+                       : make_lti<R, NXV, NYV, kKSmall, 0>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
   PM_SHAPES(PM_CASE)
 #undef PM_CASE
   return nullptr;
@@ -223,10 +227,32 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
         for (int j = 0; j < nx; ++j)
           for (int k = 0; k < nx; ++k) Cmf[i * nx + j] += T1[i * nx + k] * Am[j * nx + k];
       sym_pack(Cmf.data(), Cmp.data());
-      rn = f32 ? dispatch_lti<float>(kr, nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
-                                     J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data())
-               : dispatch_lti<double>(kr, nx, ny, A.data(), b.data(), Cp.data(), Jp.data(), K.data(), h0.data(),
-                                      J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data());
+      // low-rank diffusion factor U = sqrt(dt) L chol(W) (dt Q = U U^T), R-LOWRANK
+      std::vector<double> Lw(nw * nw, 0.0), U(nx * nw, 0.0);
+      bool wpd = true;
+      for (int j = 0; j < nw && wpd; ++j) {
+        double d = lin->W[j * nw + j];
+        for (int k = 0; k < j; ++k) d -= Lw[j * nw + k] * Lw[j * nw + k];
+        if (!(d > 0)) { wpd = false; break; }
+        Lw[j * nw + j] = std::sqrt(d);
+        for (int i = j + 1; i < nw; ++i) {
+          double t = lin->W[i * nw + j];
+          for (int k = 0; k < j; ++k) t -= Lw[i * nw + k] * Lw[j * nw + k];
+          Lw[i * nw + j] = t / Lw[j * nw + j];
+        }
+      }
+      for (int i = 0; i < nx; ++i)
+        for (int a = 0; a < nw; ++a) {
+          double t = 0;
+          for (int k = 0; k < nw; ++k) t += lin->L[i * nw + k] * Lw[k * nw + a];
+          U[i * nw + a] = std::sqrt(dt) * t;
+        }
+      const char* nlr = getenv("PMAP_NO_LOWRANK");
+      const int lowrank = (wpd && nw < nx && !(nlr && nlr[0] == '1')) ? nw : 0;
+      rn = f32 ? dispatch_lti<float>(kr, nx, ny, lowrank, A.data(), b.data(), Cp.data(), Jp.data(), K.data(),
+                                     h0.data(), J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data(), U.data())
+               : dispatch_lti<double>(kr, nx, ny, lowrank, A.data(), b.data(), Cp.data(), Jp.data(), K.data(),
+                                      h0.data(), J0.data(), h00.data(), Am.data(), bm.data(), Cmp.data(), U.data());
     } else {
       p->kind = Kind::TV;
       // copy node arrays (global node indexing) to the device in the plan dtype

@@ -540,6 +540,128 @@ PM_INLINE void vapply(const Elem<R, N>& e1, const VF<R, N>& V, VF<R, N>& out, Af
   out = o;
 }
 
+// vapply without transition for a node element whose C = U U^T has rank NW < N
+// (R-LOWRANK, Woodbury):  (I + C S)^-1 = I - U G^-1 U^T S,  G = I + U^T S U  (NW x NW, SPD),
+//   S' = A^T S A - M^T G^-1 M + J,  M = U^T S A,
+//   v' = A^T [w - S U G^-1 U^T w] + eta,  w = v - S b.
+// Same value function as vapply (up to rounding); the N x N pivoted LU becomes an NW x NW
+// Cholesky, which shortens the per-node dependency chain.
+template <typename R, int N, int NW>
+PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const VF<R, N>& V, VF<R, N>& out,
+                              bool& ok) {
+  R SU[N][NW];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int a = 0; a < NW; ++a) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], U[k][a], s);
+      SU[i][a] = s;
+    }
+  // G = I + U^T S U, Cholesky G = Lg Lg^T
+  R Lg[NW][NW], dg[NW];
+#pragma unroll
+  for (int a = 0; a < NW; ++a)
+#pragma unroll
+    for (int c = 0; c <= a; ++c) {
+      R s = (a == c) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(U[k][a], SU[k][c], s);
+      Lg[a][c] = s;
+    }
+#pragma unroll
+  for (int c = 0; c < NW; ++c) {
+    R d = Lg[c][c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) d = fma(-Lg[c][k], Lg[c][k], d);
+    ok = ok && (d > R(0));
+    const R sd = sqrt(d);
+    Lg[c][c] = sd;
+    dg[c] = pm_rcp(sd);
+#pragma unroll
+    for (int a = c + 1; a < NW; ++a) {
+      R t = Lg[a][c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) t = fma(-Lg[a][k], Lg[c][k], t);
+      Lg[a][c] = t * dg[c];
+    }
+  }
+  // SA = S A ; M = U^T S A = (SU)^T A ; W2 = Lg^-1 M  (so M^T G^-1 M = W2^T W2)
+  R SA[N][N], W2[NW][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], e1.A[k][j], s);
+      SA[i][j] = s;
+    }
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+#pragma unroll
+    for (int a = 0; a < NW; ++a) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(SU[k][a], e1.A[k][j], s);
+#pragma unroll
+      for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], W2[c][j], s);
+      W2[a][j] = s * dg[a];
+    }
+  }
+  // w = v - S b ; q = Lg^-T Lg^-1 U^T w ; w2 = w - SU q
+  R w[N], q[NW];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = V.v[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(-V.S[sidx(i, k, N)], e1.b[k], s);
+    w[i] = s;
+  }
+#pragma unroll
+  for (int a = 0; a < NW; ++a) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(U[k][a], w[k], s);
+#pragma unroll
+    for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], q[c], s);
+    q[a] = s * dg[a];
+  }
+#pragma unroll
+  for (int a = NW - 1; a >= 0; --a) {
+    R s = q[a];
+#pragma unroll
+    for (int c = a + 1; c < NW; ++c) s = fma(-Lg[c][a], q[c], s);
+    q[a] = s * dg[a];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = w[i];
+#pragma unroll
+    for (int a = 0; a < NW; ++a) s = fma(-SU[i][a], q[a], s);
+    w[i] = s;
+  }
+  VF<R, N> o;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i; j < N; ++j) {
+      R s = e1.J[sidx(i, j, N)];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], SA[k][j], s);
+#pragma unroll
+      for (int a = 0; a < NW; ++a) s = fma(-W2[a][i], W2[a][j], s);
+      o.S[sidx(i, j, N)] = s;
+    }
+    R s = e1.h[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], w[k], s);
+    o.v[i] = s;
+  }
+  out = o;
+}
+
 // Pass-2 single step (P:456-459 with the transition of vapply):
 //   x_{i-1} = (I + C_i S_{i-1})^-1 (A_i x_i + b_i + C_i v_{i-1}).
 template <typename R, int N>

@@ -321,7 +321,10 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
       for (int i = 0; i < N; ++i) cur.v[i] = e.h[i];
     } else {
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
-      vapply<R, N, false>(e, cur, cur, nullptr, ok);
+      if constexpr (Src::LOWRANK > 0)
+        vapply_lowrank<R, N, Src::LOWRANK>(e, src.U, cur, cur, ok);
+      else
+        vapply<R, N, false>(e, cur, cur, nullptr, ok);
     }
     store(cur, svt + m * NT + r, (int64_t)K * NT);
   }

@@ -4,11 +4,11 @@
 
 namespace pmap_rt {
 
-template <typename R, int N, int NY, int KR>
+template <typename R, int N, int NY, int KR, int NWC>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
-                        const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
-                        const double* Cm) {
-  auto* rn = new RunnerT<R, N, NY, SrcLTI<R, N, NY>, KR>();
+                 const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
+                 const double* Cm, const double* U) {
+  auto* rn = new RunnerT<R, N, NY, SrcLTI<R, N, NY, NWC>, KR>();
   auto& s = rn->src;
   constexpr int NS = Dim<N>::NS;
   for (int i = 0; i < N; ++i) {
@@ -27,6 +27,7 @@ Runner* make_lti(const double* A, const double* b, const double* C, const double
   for (int i = 0; i < N; ++i) {
     s.bm[i] = (R)bm[i];
     for (int jj = 0; jj < N; ++jj) s.Am[i][jj] = (R)Am[i * N + jj];
+    for (int a = 0; a < (NWC > 0 ? NWC : 1); ++a) s.U[i][a] = NWC > 0 ? (R)U[i * NWC + a] : R(0);
   }
   return rn;
 }

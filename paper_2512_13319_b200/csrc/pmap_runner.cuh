@@ -310,7 +310,7 @@ struct RunnerT : Runner {
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
-  static constexpr bool IS_LTI = std::is_same<Src, SrcLTI<R, N, NY>>::value;
+  static constexpr bool IS_LTI = Src::IS_LTI_SRC;
   using Tab = LtiTables<R, N, kNT, K>;
   Tab* tab = nullptr;    // pass-1 tables (LTI only)
   Tab* tab_m = nullptr;  // mirrored-element tables (two-filter pass B)
@@ -664,10 +664,10 @@ bool RunnerT<R, N, NY, Src, K>::prepare(PlanState& p) {
 // ---------------------------------------------------------- instantiation
 // Factories are declared here and explicitly instantiated, one (dtype, shape,
 // model kind) per translation unit, in inst.cu (see pmap_make.cuh).
-template <typename R, int N, int NY, int KR>
+template <typename R, int N, int NY, int KR, int NWC>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
                  const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
-                 const double* Cm);
+                 const double* Cm, const double* U);
 template <typename R, int N, int NY, int KR>
 Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r, const R* Rm,
                 const int64_t* str, int nw, double dt, const double* P0i, const double* P0im0);

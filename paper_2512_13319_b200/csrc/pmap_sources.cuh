@@ -16,9 +16,13 @@ namespace pmap {
 // ---------------------------------------------------------------- LTI model
 // F, c, L, W, H, r, R constant in time (all strides 0).  Everything but the
 // y-dependent eta is precomputed on the host at plan time.
-template <typename R, int N, int NY>
+// NWC > 0: the diffusion has low rank, C = dt Q = U U^T with U (N x NWC), and the
+// per-node value-function update uses the Woodbury form (vapply_lowrank, R-LOWRANK).
+template <typename R, int N, int NY, int NWC = 0>
 struct SrcLTI {
   static constexpr int NS = Dim<N>::NS;
+  static constexpr bool IS_LTI_SRC = true;
+  static constexpr int LOWRANK = NWC;
   static constexpr int NXB = N;  // row width of the nominal trajectory (unused)
   static constexpr bool NEEDS_XBAR = false;
   R A[N][N];
@@ -32,6 +36,7 @@ struct SrcLTI {
   R Am[N][N];  // (I - dt F)^-1             (two-filter mirrored element, R-TF)
   R bm[N];     // (I - dt F)^-1 dt c
   R Cm[NS];    // (I - dt F)^-1 dt Q (I - dt F)^-T
+  R U[N][NWC > 0 ? NWC : 1];  // dt Q = U U^T (NWC > 0)
   static constexpr bool HAS_MIRROR = true;
 
   // Mirrored element M_i of node gi (R-TF); the terminal node Tg has no transition.
@@ -113,6 +118,8 @@ struct SrcLTI {
 template <typename R, int N, int NY>
 struct SrcTV {
   static constexpr int NS = Dim<N>::NS;
+  static constexpr bool IS_LTI_SRC = false;
+  static constexpr int LOWRANK = 0;
   static constexpr bool NEEDS_XBAR = false;
   static constexpr bool HAS_MIRROR = true;
   const R *F, *c, *L, *W, *H, *r, *Rm;
@@ -321,6 +328,8 @@ PM_INLINE R wrap_pi(R a) {  // to (-pi, pi]
 template <typename R, int N, int NY, int KIND>
 struct SrcNL {
   static constexpr int NS = Dim<N>::NS;
+  static constexpr bool IS_LTI_SRC = false;
+  static constexpr int LOWRANK = 0;
   static constexpr bool NEEDS_XBAR = true;
   static constexpr bool HAS_MIRROR = false;
   R dt;

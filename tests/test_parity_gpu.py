@@ -419,3 +419,22 @@ def test_both_run_lengths(torch_cuda, K, case, monkeypatch):
         plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1)
         x, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=4)
         assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+@pytest.mark.parametrize("lowrank", ["0", "1"])
+def test_lowrank_node_update(torch_cuda, lowrank, monkeypatch):
+    """Rank-2 diffusion (Wiener velocity): the Woodbury node update (R-LOWRANK) and the
+    pivoted-LU update agree with each other and with the oracle."""
+    torch = torch_cuda
+    if lowrank == "0":
+        monkeypatch.setenv("PMAP_NO_LOWRANK", "1")
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    T = 70_000
+    _, y = wl.simulate_linear(spec, T, seed=77)
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    plan = gpu_plan(spec, T)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    xt = plan.two_filter(to_dev(torch, y[None]))
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    assert rel(xt[0].cpu().numpy(), xo) < TOL64
