@@ -27,7 +27,12 @@ Runner* make_lti(const double* A, const double* b, const double* C, const double
   for (int i = 0; i < N; ++i) {
     s.bm[i] = (R)bm[i];
     for (int jj = 0; jj < N; ++jj) s.Am[i][jj] = (R)Am[i * N + jj];
-    for (int a = 0; a < (NWC > 0 ? NWC : 1); ++a) s.U[i][a] = NWC > 0 ? (R)U[i * NWC + a] : R(0);
+    for (int a = 0; a < (NWC > 0 ? NWC : 1); ++a) {
+      s.U[i][a] = NWC > 0 ? (R)U[i * NWC + a] : R(0);
+      double t = 0;
+      for (int k = 0; k < N && NWC > 0; ++k) t += Am[i * N + k] * U[k * (NWC > 0 ? NWC : 1) + a];
+      s.Um[i][a] = (R)t;
+    }
   }
   return rn;
 }

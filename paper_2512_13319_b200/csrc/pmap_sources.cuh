@@ -36,7 +36,8 @@ struct SrcLTI {
   R Am[N][N];  // (I - dt F)^-1             (two-filter mirrored element, R-TF)
   R bm[N];     // (I - dt F)^-1 dt c
   R Cm[NS];    // (I - dt F)^-1 dt Q (I - dt F)^-T
-  R U[N][NWC > 0 ? NWC : 1];  // dt Q = U U^T (NWC > 0)
+  R U[N][NWC > 0 ? NWC : 1];   // dt Q = U U^T (NWC > 0)
+  R Um[N][NWC > 0 ? NWC : 1];  // mirrored: Cm = (Am U)(Am U)^T
   static constexpr bool HAS_MIRROR = true;
 
   // Mirrored element M_i of node gi (R-TF); the terminal node Tg has no transition.

@@ -83,7 +83,14 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
         load_sv<R, N, NT, K>(sv, g, b, l, Va);  // issued early: independent of the recursion
         E e;
         mir.template node<R, N>(g.node0 + l, yb + l * NY, nullptr, e);
-        vapply<R, N, false>(e, cur, cur, nullptr, ok);  // (Lam_l, xi_l)
+        if constexpr (Src::LOWRANK > 0) {  // mirrored diffusion Cm = (Am U)(Am U)^T
+          if (g.node0 + l != mir.Tg)
+            vapply_lowrank<R, N, Src::LOWRANK>(e, mir.s.Um, cur, cur, ok);
+          else
+            vapply<R, N, false>(e, cur, cur, nullptr, ok);
+        } else {
+          vapply<R, N, false>(e, cur, cur, nullptr, ok);  // (Lam_l, xi_l)
+        }
         R Ssum[Dim<N>::NS], rhs[N], xv[N];
 #pragma unroll
         for (int k = 0; k < Dim<N>::NS; ++k) Ssum[k] = Va.S[k] + (cur.S[k] - e.J[k]);
