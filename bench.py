@@ -35,11 +35,12 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 # ----------------------------------------------------------- algorithmic counts
-def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True):
+def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0):
     """Algorithmic FP64 flops (FMA = 2) and HBM bytes per node of each kernel class
     (DESIGN.md section 6): the arithmetic each kernel's per-node recurrence performs
     in this decomposition, excluding the intra-tile scan overheads (Kogge-Stone
-    rounds, carries), which are implementation cost."""
+    rounds, carries), which are implementation cost.  nw > 0: low-rank diffusion
+    (R-LOWRANK node update, R-P2REC pass-2 records of nw (nx + 1) values)."""
     N = nx
     lu = sum((N - k - 1) + (N - k - 1) ** 2 for k in range(N))
     solve = N * N
@@ -53,10 +54,20 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True):
     asz = N * N + N
     d = 8
     reduce_fl = 2 * N * ny if lti else combine  # LTI: impulse-response fold (y_m -> (b, eta))
+    vsz2 = vsz  # per-node values pass 1 stores for pass 2
+    if nw > 0:  # R-LOWRANK node update (vapply_lowrank), R-P2REC records when smaller than (S, v)
+        r = nw
+        chol = r * (r + 1) // 2 * N + r * (r - 1) // 2 * (r + 1) + r
+        vapply = (N * r * N + chol + N * N * N + r * N * N + r * (r - 1) // 2 * N + N * N + r * N + r * r
+                  + N * r + ns * (N + r) + N * N)
+        if r * (N + 1) < vsz:
+            vsz2 = r * (N + 1)
+            vapply += r * N  # U^T v
+            trans = N * N + N * r + chol + r * N + r * r + N * r
     return {
         "k_p1_reduce": (2 * reduce_fl, d * (ny + esz / K)),
-        "k_p1_down": (2 * (vapply + vapply_tr / K), d * (ny + esz / K + vsz + asz / K)),
-        "k_p2_down": (2 * trans, d * (vsz + nx + asz / K)),
+        "k_p1_down": (2 * (vapply + vapply_tr / K), d * (ny + esz / K + vsz2 + asz / K)),
+        "k_p2_down": (2 * trans, d * (vsz2 + nx + asz / K)),
         "solve": (2 * (reduce_fl + vapply + vapply_tr / K + trans), d * (ny + 2 * vsz + nx)),
     }
 
@@ -313,7 +324,12 @@ def main():
         return
 
     # roofline of the dominant kernel (FP64-ALU bound)
-    counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1")
+    import workloads as wl
+    lowrank = 0
+    if (isinstance(spec, wl.LinearSpec) and spec.L.shape[1] < spec.nx and os.environ.get("PMAP_NO_LOWRANK") != "1"
+            and os.environ.get("PMAP_GENERAL") != "1"):
+        lowrank = spec.L.shape[1]
+    counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank)
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl

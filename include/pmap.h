@@ -157,6 +157,9 @@ map_status map_solve_nonlinear(map_plan_t plan, const void* y, int32_t passes, d
  *   phase 2: gathered = [world][payload1] in rank order -> payload: the rank's
  *            pass-2 chunk affine aggregate (Phi, beta) (+ x*_T on the last rank).
  *   phase 3: gathered = [world][payload2] -> x_map (+ optional filter outputs).
+ * Filter outputs (filt_m, filt_P) are written at phase 3 and must also be passed
+ * (non-NULL) at phase 2: without them phase 2 of a low-rank-diffusion model keeps only
+ * the pass-2 records (DESIGN.md R-P2REC) and phase 3 then fails with MAP_E_ARG.
  * Unused pointers may be NULL.  Linear plans only. */
 int64_t map_shard_payload_bytes(map_plan_t plan, int32_t phase /* 1 or 2 */);
 map_status map_shard_phase(map_plan_t plan, int32_t phase, const void* y, const void* gathered, void* payload,

@@ -270,18 +270,19 @@ class Plan:
     def sync(self):
         map_sync(self.handle)
 
-    def shard_phase(self, phase: int, y=None, gathered=None, x_map=None):
+    def shard_phase(self, phase: int, y=None, gathered=None, x_map=None, filt_m=None, filt_P=None):
         """One phase of a caller-driven time-sharded solve (map_shard_phase); returns the
-        phase's payload tensor (phases 1, 2) or x_map (phase 3)."""
+        phase's payload tensor (phases 1, 2) or x_map (phase 3).  Filter outputs are
+        written at phase 3 and must be passed at phase 2 too (full (S, v) storage)."""
         import torch
         if phase in (1, 2):
             n = map_shard_payload_bytes(self.handle, phase) // (8 if self.dtype == "f64" else 4)
             payload = torch.empty(n, dtype=self.torch_dtype, device="cuda")
-            map_shard_phase(self.handle, phase, y, gathered, payload)
+            map_shard_phase(self.handle, phase, y, gathered, payload, None, filt_m, filt_P)
             return payload
         if x_map is None:
             x_map = torch.empty((self.batch, self.n_local, self.nx), dtype=self.torch_dtype, device="cuda")
-        map_shard_phase(self.handle, 3, None, gathered, None, x_map)
+        map_shard_phase(self.handle, 3, None, gathered, None, x_map, filt_m, filt_P)
         return x_map
 
     def profile(self, enable: bool = True) -> None:

@@ -152,6 +152,8 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   {
     const char* fs = getenv("PMAP_FORCE_SHARD");
     p->force_shard = fs && fs[0] == '1' && d.nccl_comm;
+    const char* nr = getenv("PMAP_NO_P2REC");
+    p->no_rec = nr && nr[0] == '1';
   }
   const int nx = d.nx, ny = d.ny, nw = d.nw;
   const int NS = nx * (nx + 1) / 2;
@@ -618,10 +620,13 @@ map_status map_shard_phase(map_plan_t p, int32_t phase, const void* y, const voi
   p->launches = 0;
   if (phase == 1)
     p->runner->phase1(*p, y, nullptr, payload);
-  else if (phase == 2)
+  else if (phase == 2) {
+    p->want_filter = filt_m || filt_P;
     p->runner->phase2(*p, y, nullptr, gathered, payload);
-  else
+  } else {
     p->runner->phase3(*p, nullptr, gathered, x_map, filt_m, filt_P);
+    if (!p->err.empty()) return MAP_E_ARG;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(*p, e, "kernel launch");
   return MAP_OK;

@@ -548,7 +548,7 @@ PM_INLINE void vapply(const Elem<R, N>& e1, const VF<R, N>& V, VF<R, N>& out, Af
 // Cholesky, which shortens the per-node dependency chain.
 template <typename R, int N, int NW>
 PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const VF<R, N>& V, VF<R, N>& out,
-                              bool& ok) {
+                              bool& ok, R* rec = nullptr, int64_t rstride = 0) {
   R SU[N][NW];
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -559,6 +559,19 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], U[k][a], s);
       SU[i][a] = s;
     }
+  if (rec) {  // pass-2 record of the input value function (R-P2REC): [S U | U^T v]
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int a = 0; a < NW; ++a) rec[(i * NW + a) * rstride] = SU[i][a];
+#pragma unroll
+    for (int a = 0; a < NW; ++a) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(U[k][a], V.v[k], s);
+      rec[(N * NW + a) * rstride] = s;
+    }
+  }
   // G = I + U^T S U, Cholesky G = Lg Lg^T
   R Lg[NW][NW], dg[NW];
 #pragma unroll
@@ -692,6 +705,73 @@ PM_INLINE void trans_step(const R (&A)[N][N], const R (&b)[N], const R (&C)[Dim<
   lu_solve(f, t);
 #pragma unroll
   for (int i = 0; i < N; ++i) x[i] = t[i];
+}
+
+// Pass-2 step from the low-rank record of V_{i-1} (R-P2REC, C_i = U U^T):
+//   w = A_i x_i + b_i + U (U^T v_{i-1}),  x_{i-1} = w - U G^-1 (S U)^T w,  G = I + U^T (S U),
+// which is (I + C_i S_{i-1})^-1 (A_i x_i + b_i + C_i v_{i-1}) by the Woodbury identity.
+template <typename R, int N, int NW>
+PM_INLINE void trans_step_rec(const R (&A)[N][N], const R (&b)[N], const R (&U)[N][NW], const R (&SU)[N][NW],
+                              const R (&u)[NW], R (&x)[N], bool& ok) {
+  R w[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = b[i];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(A[i][k], x[k], s);
+#pragma unroll
+    for (int a = 0; a < NW; ++a) s = fma(U[i][a], u[a], s);
+    w[i] = s;
+  }
+  R Lg[NW][NW], dg[NW], q[NW];
+#pragma unroll
+  for (int a = 0; a < NW; ++a)
+#pragma unroll
+    for (int c = 0; c <= a; ++c) {
+      R s = (a == c) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(U[k][a], SU[k][c], s);
+      Lg[a][c] = s;
+    }
+#pragma unroll
+  for (int c = 0; c < NW; ++c) {
+    R d = Lg[c][c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) d = fma(-Lg[c][k], Lg[c][k], d);
+    ok = ok && (d > R(0));
+    const R sd = sqrt(d);
+    dg[c] = pm_rcp(sd);
+#pragma unroll
+    for (int a = c + 1; a < NW; ++a) {
+      R t = Lg[a][c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) t = fma(-Lg[a][k], Lg[c][k], t);
+      Lg[a][c] = t * dg[c];
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NW; ++a) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(SU[k][a], w[k], s);
+#pragma unroll
+    for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], q[c], s);
+    q[a] = s * dg[a];
+  }
+#pragma unroll
+  for (int a = NW - 1; a >= 0; --a) {
+    R s = q[a];
+#pragma unroll
+    for (int c = a + 1; c < NW; ++c) s = fma(-Lg[c][a], q[c], s);
+    q[a] = s * dg[a];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = w[i];
+#pragma unroll
+    for (int a = 0; a < NW; ++a) s = fma(-U[i][a], q[a], s);
+    x[i] = s;
+  }
 }
 
 // (f o g)(x) = f(g(x)):  (P_f P_g, P_f q_g + q_f).

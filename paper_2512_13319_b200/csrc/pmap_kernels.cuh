@@ -231,14 +231,18 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
 #else
 #define PM_DOWN_LB(NT) __launch_bounds__(NT, (N <= 4 ? 6 : 1))
 #endif
-template <typename R, int N, int NY, int NT, int K, class Src, bool P2>
+// REC (low-rank sources only, R-P2REC): instead of (S_i, v_i) store at node i the
+// pass-2 record [S_{i-1} U | U^T v_{i-1}] of the value function the node consumes
+// (N*NW + NW values instead of N(N+1)/2 + N); (S, v) of the last node always goes to svl.
+template <typename R, int N, int NY, int NT, int K, class Src, bool P2, bool REC = false>
 __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const Geom g,
                                                 const R* __restrict__ y, const R* __restrict__ xbar,
                                                 const R* __restrict__ run_incl, const R* __restrict__ tile_incl,
                                                 const R* __restrict__ group_carry, R* __restrict__ sv,
                                                 R* __restrict__ run_suf, R* __restrict__ tile_agg2,
                                                 unsigned long long* flag, const R* __restrict__ span1,
-                                                int64_t j_lo, int64_t j_hi) {
+                                                int64_t j_lo, int64_t j_hi, R* __restrict__ svl) {
+  static_assert(!REC || Src::LOWRANK > 0, "pass-2 records need a low-rank source");
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
@@ -322,11 +326,13 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     } else {
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       if constexpr (Src::LOWRANK > 0)
-        vapply_lowrank<R, N, Src::LOWRANK>(e, src.U, cur, cur, ok);
+        vapply_lowrank<R, N, Src::LOWRANK>(e, src.U, cur, cur, ok, REC ? svt + m * NT + r : nullptr,
+                                           (int64_t)K * NT);
       else
         vapply<R, N, false>(e, cur, cur, nullptr, ok);
     }
-    store(cur, svt + m * NT + r, (int64_t)K * NT);
+    if (!REC) store(cur, svt + m * NT + r, (int64_t)K * NT);
+    if (l == g.Nn - 1 && svl) store(cur, svl + b * V::SZ, 1);
   }
   if (!finite_vf(cur)) ok = false;
   if (!P2) {
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(NT2) k_p2_tiles(const Geom g, const R* __restr
 // x* at the last node of every tile group (exclusive suffix over group aggregates,
 // seeded with x_end = S_T^-1 v_T on the rank holding node T, or the shard carry).
 template <typename R, int N, int NT, int K>
-__global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __restrict__ sv,
+__global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __restrict__ svl,
                                                    const R* __restrict__ group_agg2, const R* __restrict__ xend_in,
                                                    R* __restrict__ group_carry, R* __restrict__ total_agg2,
                                                    unsigned long long* flag) {
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
       for (int i = 0; i < N; ++i) x[i] = xend_in[b * N + i];
     } else {
       VF<R, N> V;
-      load_sv<R, N, NT, K>(sv, g, b, g.Nn - 1, V);
+      load(V, svl + b * VF<R, N>::SZ, 1);
       spd_solve<R, N>(V.S, V.v, x, ok);  // x*_T = S_T^-1 v_T
     }
 #pragma unroll
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
 // Backward sweep of each run.  (S, v) of the next node is prefetched one step
 // ahead (coalesced SoA loads), and x is staged through shared memory in chunks of
 // KC nodes so that it leaves as contiguous 8*KC*N-byte segments per run.
-template <typename R, int N, int NT, int K, class Src>
+template <typename R, int N, int NT, int K, class Src, bool REC = false>
 __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src, const Geom g,
                                                 const R* __restrict__ xbar, const R* __restrict__ sv,
                                                 const R* __restrict__ run_suf, const R* __restrict__ tile_sufx,
@@ -514,6 +520,53 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
   }
   R* xo = x_out + b * g.Nn * N;
   const R* svt = sv + tile * (int64_t)V::SZ * K * NT;
+  if constexpr (REC) {
+    // pass-2 records (R-P2REC): the record of step m sits in the run's own slot m
+    constexpr int NW = Src::LOWRANK > 0 ? Src::LOWRANK : 1;
+    constexpr int RS = N * NW + NW;
+    R rn[RS];
+    auto fetch_rec = [&](int m, R (&rr)[RS]) {
+#pragma unroll
+      for (int f = 0; f < RS; ++f) rr[f] = svt[(int64_t)f * K * NT + m * NT + r];
+    };
+    fetch_rec(K - 1, rn);
+#pragma unroll 1
+    for (int c = K / KC - 1; c >= 0; --c) {
+#pragma unroll 1
+      for (int mm = KC - 1; mm >= 0; --mm) {
+        const int m = c * KC + mm;
+        const int64_t l = l0 + m;
+        const bool valid = l < g.Nn;
+        R rc[RS];
+#pragma unroll
+        for (int f = 0; f < RS; ++f) rc[f] = rn[f];
+        if (m > 0) fetch_rec(m - 1, rn);
+#pragma unroll
+        for (int i = 0; i < N; ++i) xs[r][mm * N + i] = x[i];
+        const int64_t gi = g.node0 + l;
+        if (valid && gi != 0) {
+          R At[N][N], bt[N], Ct[Dim<N>::NS], SU[N][NW], u[NW];
+          src.trans(gi, nullptr, At, bt, Ct);
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int a = 0; a < NW; ++a) SU[i][a] = rc[i * NW + a];
+#pragma unroll
+          for (int a = 0; a < NW; ++a) u[a] = rc[N * NW + a];
+          trans_step_rec<R, N, NW>(At, bt, src.U, SU, u, x, ok);
+        }
+      }
+      __syncthreads();
+      for (int rr = r >> 5; rr < NT; rr += NT / 32) {
+        const int64_t lb = (j * NT + rr) * (int64_t)K + c * KC;
+        for (int q = r & 31; q < KC * N; q += 32) {
+          const int64_t node = lb + q / N;
+          if (node < g.Nn) xo[lb * N + q] = xs[rr][q];
+        }
+      }
+      __syncthreads();
+    }
+  } else {
   // (S, v) of node l-1 for step m (m >= 1: same run, SoA slot m-1)
   auto fetch = [&](int m, V& Vp) {
     const int64_t l = l0 + m;
@@ -555,6 +608,7 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
       }
     }
     __syncthreads();
+  }
   }
   R s = R(0);
 #pragma unroll

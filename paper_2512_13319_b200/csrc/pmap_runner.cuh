@@ -69,7 +69,7 @@ inline bool h_is_finite(const double* a, int n) {
 template <typename R, int N, int K>
 struct WsLayout {
   size_t run_incl, tile_agg1, tile_incl1, group_agg1, group_carry1, total1, sv, run_suf, tile_agg2,
-      tile_sufx2, group_agg2, group_carry2, total2, carry_in, xend, tf_run, tf_tile, tf_tincl, tf_gagg, tf_gcarry, bytes;
+      tile_sufx2, group_agg2, group_carry2, total2, carry_in, xend, svl, tf_run, tf_tile, tf_tincl, tf_gagg, tf_gcarry, bytes;
   void plan(const Geom& g, bool tf) {
     using E = Elem<R, N>;
     using V = VF<R, N>;
@@ -96,6 +96,7 @@ struct WsLayout {
     total2 = take(B * (A::SZ + N));
     carry_in = take(B * V::SZ);
     xend = take(B * N);
+    svl = take(B * V::SZ);  // (S, v) of every trajectory's last local node
     if (tf) {
       tf_run = take(2 * nt * E::SZ * kNT);
       tf_tile = take(nt * E::SZ);
@@ -172,6 +173,9 @@ struct PlanState {
   int graph_passes = -1;
   int64_t graph_launches = 0;
   size_t elem_real = 8;
+  bool want_filter = false;  // filter outputs requested for the current solve (full (S, v) storage)
+  bool rec_done = false;     // phase 2 stored low-rank pass-2 records (R-P2REC) instead of (S, v)
+  bool no_rec = false;       // PMAP_NO_P2REC=1: always store (S, v) (A/B checks)
   bool force_shard = false;  // PMAP_FORCE_SHARD=1 with a communicator: run the NCCL path at world == 1 (tests)
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
   cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
@@ -265,9 +269,9 @@ __global__ void k_shard_fold1(int world, int rank, int64_t batch, const R* __res
   if (!ok) atomicMin(flag, 0ull);
 }
 
-template <typename R, int N, int K>
-__global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ sv_last,
-                              int64_t sv_stride, R* __restrict__ payload, unsigned long long* flag) {
+template <typename R, int N>
+__global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ svl,
+                              R* __restrict__ payload, unsigned long long* flag) {
   // payload per trajectory: [Aff total][x_T (last rank only)]
   using A = Aff<R, N>;
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -275,7 +279,7 @@ __global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ to
   for (int k = 0; k < A::SZ; ++k) payload[b * (A::SZ + N) + k] = total2[b * A::SZ + k];
   if (last) {
     VF<R, N> V;
-    load(V, sv_last + b * sv_stride, (int64_t)K * kNT);
+    load(V, svl + b * VF<R, N>::SZ, 1);
     R x[N];
     bool ok = true;
     spd_solve<R, N>(V.S, V.v, x, ok);
@@ -311,6 +315,8 @@ struct RunnerT : Runner {
   using V = VF<R, N>;
   using A = Aff<R, N>;
   static constexpr bool IS_LTI = Src::IS_LTI_SRC;
+  // low-rank pass-2 records (R-P2REC) when they are smaller than (S, v)
+  static constexpr bool kRec = Src::LOWRANK > 0 && Src::LOWRANK * (N + 1) < VF<R, N>::SZ;
   using Tab = LtiTables<R, N, kNT, K>;
   Tab* tab = nullptr;    // pass-1 tables (LTI only)
   Tab* tab_m = nullptr;  // mirrored-element tables (two-filter pass B)
@@ -462,26 +468,31 @@ struct RunnerT : Runner {
     PM_LAUNCH(p, s, K_P1_GROUPS,
               (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
                   g, W(L.group_agg1), carry_in, W(L.group_carry1), nullptr, p.dflag)));
-    PM_LAUNCH(p, s, K_P1_DOWN,
-              (k_p1_down<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, smem_down(), s>>>(
-                  src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
-                  W(L.tile_agg2), p.dflag, (use_lti && tab) ? tab->E1 : nullptr, lti_jlo(g, false),
-                  lti_jhi(g))));
+    const R* span1 = (use_lti && tab) ? tab->E1 : nullptr;
+    p.rec_done = false;
+    if constexpr (kRec) p.rec_done = !p.want_filter && !p.no_rec;
+    if (p.rec_done) {
+      if constexpr (kRec)
+        PM_LAUNCH(p, s, K_P1_DOWN,
+                  (k_p1_down<R, N, NY, kNT, K, Src, true, true><<<ntiles, kNT, smem_down(), s>>>(
+                      src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
+                      W(L.tile_agg2), p.dflag, span1, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
+    } else {
+      PM_LAUNCH(p, s, K_P1_DOWN,
+                (k_p1_down<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, smem_down(), s>>>(
+                    src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
+                    W(L.tile_agg2), p.dflag, span1, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
+    }
     PM_LAUNCH(p, s, K_P2_TILES,
               (k_p2_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_p2tiles(), s>>>(
                   g, W(L.tile_agg2), W(L.tile_sufx2), W(L.group_agg2))));
     if (payload) {
       PM_LAUNCH(p, s, K_P2_GROUPS,
                 (k_p2_groups<R, N, kNT, K><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
-                    g, W(L.sv), W(L.group_agg2), nullptr, W(L.group_carry2), W(L.total2), p.dflag)));
-      const int64_t l = g.Nn - 1;
-      const int64_t Lt = (int64_t)kNT * K;
-      const int64_t j = l / Lt, q = l % Lt, rr = q / K, m = q % K;
-      const R* sv_last = W(L.sv) + j * (int64_t)V::SZ * K * kNT + m * kNT + rr;
-      const int64_t sv_stride = g.tpt * (int64_t)V::SZ * K * kNT;
+                    g, W(L.svl), W(L.group_agg2), nullptr, W(L.group_carry2), W(L.total2), p.dflag)));
       PM_LAUNCH(p, s, K_SHARD,
-                (k_shard_pack2<R, N, K><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
-                    g.batch, p.d.rank == p.d.world - 1, W(L.total2), sv_last, sv_stride, static_cast<R*>(payload),
+                (k_shard_pack2<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
+                    g.batch, p.d.rank == p.d.world - 1, W(L.total2), W(L.svl), static_cast<R*>(payload),
                     p.dflag)));
     }
   }
@@ -504,11 +515,23 @@ struct RunnerT : Runner {
     }
     PM_LAUNCH(p, s, K_P2_GROUPS,
               (k_p2_groups<R, N, kNT, K><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
-                  g, W(L.sv), W(L.group_agg2), xend_in, W(L.group_carry2), nullptr, p.dflag)));
-    PM_LAUNCH(p, s, K_P2_DOWN,
-              (k_p2_down<R, N, kNT, K, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
-                                                                  W(L.tile_sufx2), W(L.group_carry2),
-                                                                  W(L.carry_in), x, p.dflag)));
+                  g, W(L.svl), W(L.group_agg2), xend_in, W(L.group_carry2), nullptr, p.dflag)));
+    if ((fm || fP) && p.rec_done) {
+      p.err = "filter outputs need full (S, v) storage: pass filt_m/filt_P at phase 2 as well";
+      return;
+    }
+    if (p.rec_done) {
+      if constexpr (kRec)
+        PM_LAUNCH(p, s, K_P2_DOWN,
+                  (k_p2_down<R, N, kNT, K, Src, true><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
+                                                                           W(L.tile_sufx2), W(L.group_carry2),
+                                                                           W(L.carry_in), x, p.dflag)));
+    } else {
+      PM_LAUNCH(p, s, K_P2_DOWN,
+                (k_p2_down<R, N, kNT, K, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
+                                                                    W(L.tile_sufx2), W(L.group_carry2),
+                                                                    W(L.carry_in), x, p.dflag)));
+    }
     if (fm || fP) {
       const int64_t n = g.batch * g.Nn;
       PM_LAUNCH(p, s, K_FILTER_OUT,
@@ -518,6 +541,7 @@ struct RunnerT : Runner {
   }
 
   void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) override {
+    p.want_filter = fm || fP;
     if (p.d.world == 1 && !p.force_shard) {
       phase1(p, y, xbar, nullptr);
       phase2(p, y, xbar, nullptr, nullptr);
@@ -570,7 +594,7 @@ struct RunnerT : Runner {
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
-                    nullptr, p.dflag, nullptr, 0, 0)));
+                    nullptr, p.dflag, nullptr, 0, 0, nullptr)));
       // pass B: backward information filter over mirrored elements (reverse node order)
       Mirror<Src> mir{src, g.node0 + g.Nn - 1};
       reduce1<true>(p, s2, K_TF_REDUCE, mir, fold_m, tab_m, y, nullptr, W(L.tf_run), W(L.tf_tile));

@@ -81,6 +81,10 @@ def test_wiener_rts_sizes(torch_cuda, T):
     assert rel(fmd[0].cpu().numpy(), fm) < TOL64
     iu = np.triu_indices(nx)
     assert rel(fPd[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
+    # without filter outputs pass 2 runs from the low-rank records (R-P2REC)
+    x2 = plan.solve_linear(yd)
+    assert rel(x2[0].cpu().numpy(), xo) < TOL64
+    assert rel(x2[0].cpu().numpy(), x[0].cpu().numpy()) < 1e-11
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (2, 1), (2, 2), (3, 1), (3, 2), (4, 2), (5, 2)])
@@ -421,13 +425,46 @@ def test_both_run_lengths(torch_cuda, K, case, monkeypatch):
         assert rel(x[0].cpu().numpy(), xo) < TOL64
 
 
-@pytest.mark.parametrize("lowrank", ["0", "1"])
+def test_shard_filter_outputs(torch_cuda):
+    """Virtual time shards with filter outputs: passed at phases 2 and 3 they match the
+    oracle's filter; passed at phase 3 only (phase 2 stored pass-2 records) they are
+    refused with MAP_E_ARG."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T, G = 20_000, 3
+    _, y = wl.simulate_linear(spec, T, seed=5)
+    xo, fm, fP = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf, want_filter=True)
+    plans = [pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                     P0=spec.P0, rank=r, world=G) for r in range(G)]
+    ys = [to_dev(torch, y[None, slice(*pm.shard_range(r, G, T))]) for r in range(G)]
+    nx = spec.nx
+    fms = [torch.empty((1, p.n_local, nx), dtype=torch.float64, device="cuda") for p in plans]
+    fPs = [torch.empty((1, p.n_local, nx * (nx + 1) // 2), dtype=torch.float64, device="cuda") for p in plans]
+    g1 = torch.cat([plans[r].shard_phase(1, ys[r]) for r in range(G)])
+    g2 = torch.cat([plans[r].shard_phase(2, ys[r], g1, filt_m=fms[r], filt_P=fPs[r]) for r in range(G)])
+    x = torch.cat([plans[r].shard_phase(3, gathered=g2, filt_m=fms[r], filt_P=fPs[r]) for r in range(G)], dim=1)
+    for p in plans:
+        p.sync()
+    iu = np.triu_indices(nx)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    assert rel(torch.cat(fms, dim=1)[0].cpu().numpy(), fm) < TOL64
+    assert rel(torch.cat(fPs, dim=1)[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
+    g2 = torch.cat([plans[r].shard_phase(2, ys[r], g1) for r in range(G)])
+    with pytest.raises(pm.MapError):
+        plans[0].shard_phase(3, gathered=g2, filt_m=fms[0])
+
+
+@pytest.mark.parametrize("lowrank", ["0", "1", "norec"])
 def test_lowrank_node_update(torch_cuda, lowrank, monkeypatch):
-    """Rank-2 diffusion (Wiener velocity): the Woodbury node update (R-LOWRANK) and the
-    pivoted-LU update agree with each other and with the oracle."""
+    """Rank-2 diffusion (Wiener velocity): the Woodbury node update (R-LOWRANK), with and
+    without the low-rank pass-2 records (R-P2REC), and the pivoted-LU update agree with
+    each other and with the oracle."""
     torch = torch_cuda
     if lowrank == "0":
         monkeypatch.setenv("PMAP_NO_LOWRANK", "1")
+    if lowrank == "norec":
+        monkeypatch.setenv("PMAP_NO_P2REC", "1")
     spec = wl.wiener_velocity()
     spec.c = np.array([0.3, -0.2, 0.1, 0.05])
     T = 70_000
