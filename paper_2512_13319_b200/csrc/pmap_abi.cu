@@ -138,6 +138,12 @@ const char* map_status_string(map_status s) {
   return "unknown status";
 }
 
+static int hi_prio() {
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  return hi;
+}
+
 map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, const map_nl_model* nl,
                     map_plan_t* out) {
   if (!desc || !out || (!lin) == (!nl)) return MAP_E_ARG;
@@ -344,8 +350,11 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     }
   }
   if (cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&p->stream3, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&p->stream4, cudaStreamNonBlocking) != cudaSuccess ||
+      // boundary-tile forks at the highest priority: their CTAs are dispatched ahead of
+      // the interior reduce's pending CTAs, keeping the short serial chain off the
+      // critical path of pass 1
+      cudaStreamCreateWithPriority(&p->stream3, cudaStreamNonBlocking, hi_prio()) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&p->stream4, cudaStreamNonBlocking, hi_prio()) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_edge0, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_edge1, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_edge2, cudaEventDisableTiming) != cudaSuccess ||

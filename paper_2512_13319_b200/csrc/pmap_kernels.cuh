@@ -57,6 +57,31 @@ PM_INLINE bool finite_vf(const VF<R, N>& V) {
   return s - s == R(0);
 }
 
+// Inclusive run prefix r of a tile (row pointer already offset by the run): on LTI
+// interior tiles the reduce stores only its data parts and the matrix parts come from
+// the plan table (sf = SF + run, field-major over A, C, J), else the full element.
+template <typename R, int N, int NT>
+PM_INLINE void load_prefix(Elem<R, N>& p, const R* __restrict__ row, const R* __restrict__ sf) {
+  if (sf) {
+    int f = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) p.A[i][j] = __ldg(sf + (f++) * NT);
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) p.C[k] = __ldg(sf + (f++) * NT);
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) p.J[k] = __ldg(sf + (f++) * NT);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      p.b[i] = row[(N * N + i) * NT];
+      p.h[i] = row[(N * N + N + Dim<N>::NS + i) * NT];
+    }
+  } else {
+    load(p, row, NT);
+  }
+}
+
 // ----------------------------------------------------------------- pass 1a
 // nsel > 0: only the listed tiles {jsel0, jsel1} of each trajectory (the boundary
 // tiles left over by the LTI-specialised reduce), else every tile.
@@ -241,7 +266,8 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
                                                 const R* __restrict__ group_carry, R* __restrict__ sv,
                                                 R* __restrict__ run_suf, R* __restrict__ tile_agg2,
                                                 unsigned long long* flag, const R* __restrict__ span1,
-                                                int64_t j_lo, int64_t j_hi, R* __restrict__ svl) {
+                                                const R* __restrict__ sf, int64_t j_lo, int64_t j_hi,
+                                                R* __restrict__ svl) {
   static_assert(!REC || Src::LOWRANK > 0, "pass-2 records need a low-rank source");
   using E = Elem<R, N>;
   using V = VF<R, N>;
@@ -271,9 +297,10 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
   V cur;
   load(cur, sh, 1);
   __syncthreads();
+  const bool interior = sf && j >= j_lo && j < j_hi;
   if (r > 0) {
     E p;
-    load(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), NT);
+    load_prefix<R, N, NT>(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), interior ? sf + (r - 1) : nullptr);
     vapply<R, N, false>(p, cur, cur, nullptr, ok);
   }
   // Pass-2 aggregate of the run (maps x*_e -> x*_{s-1}), R-RUNAGG: by dynamic
@@ -524,12 +551,13 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
     // pass-2 records (R-P2REC): the record of step m sits in the run's own slot m
     constexpr int NW = Src::LOWRANK > 0 ? Src::LOWRANK : 1;
     constexpr int RS = N * NW + NW;
-    R rn[RS];
+    R rn[RS], rn2[RS];  // records of the next two steps (two nodes of loads in flight)
     auto fetch_rec = [&](int m, R (&rr)[RS]) {
 #pragma unroll
       for (int f = 0; f < RS; ++f) rr[f] = svt[(int64_t)f * K * NT + m * NT + r];
     };
     fetch_rec(K - 1, rn);
+    fetch_rec(K - 2, rn2);
 #pragma unroll 1
     for (int c = K / KC - 1; c >= 0; --c) {
 #pragma unroll 1
@@ -539,8 +567,11 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
         const bool valid = l < g.Nn;
         R rc[RS];
 #pragma unroll
-        for (int f = 0; f < RS; ++f) rc[f] = rn[f];
-        if (m > 0) fetch_rec(m - 1, rn);
+        for (int f = 0; f < RS; ++f) {
+          rc[f] = rn[f];
+          rn[f] = rn2[f];
+        }
+        if (m > 1) fetch_rec(m - 2, rn2);
 #pragma unroll
         for (int i = 0; i < N; ++i) xs[r][mm * N + i] = x[i];
         const int64_t gi = g.node0 + l;

@@ -494,16 +494,17 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
     R nb[N], nh[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      R sb = b2[i], sh_ = hh[i];
+      // two independent accumulators per output (halves the dependent FMA chain)
+      R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         sb = fma(__ldg(U + ((0 * N + i) * N + k) * 32 + lane), bb[k], sb);
-        sb = fma(__ldg(U + ((1 * N + i) * N + k) * 32 + lane), h2[k], sb);
+        sb2 = fma(__ldg(U + ((1 * N + i) * N + k) * 32 + lane), h2[k], sb2);
         sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * 32 + lane), h2[k], sh_);
-        sh_ = fma(-__ldg(U + ((3 * N + i) * N + k) * 32 + lane), bb[k], sh_);
+        sh2 = fma(-__ldg(U + ((3 * N + i) * N + k) * 32 + lane), bb[k], sh2);
       }
-      nb[i] = sb;
-      nh[i] = sh_;
+      nb[i] = sb + sb2;
+      nh[i] = sh_ + sh2;
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -542,20 +543,14 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
       step(&tab->UX[0][0][0][0], b2, h2);
     }
   }
-  // write the full inclusive prefix element: matrix parts of a span of r + 1 runs
-  // (field-major table: coalesced across the warp)
+  // the inclusive prefix: data parts only -- its matrix parts (a span of r + 1 runs)
+  // are the plan table SF[.][r], which the consumers (load_prefix) read instead
   R* out = run_incl + tile * (int64_t)E::SZ * NT + r;
-  int f = 0, t = 0;
 #pragma unroll
-  for (int i = 0; i < N * N; ++i) out[(f++) * NT] = __ldg(&tab->SF[t++][r]);
-#pragma unroll
-  for (int i = 0; i < N; ++i) out[(f++) * NT] = bb[i];
-#pragma unroll
-  for (int k = 0; k < Dim<N>::NS; ++k) out[(f++) * NT] = __ldg(&tab->SF[t++][r]);
-#pragma unroll
-  for (int i = 0; i < N; ++i) out[(f++) * NT] = hh[i];
-#pragma unroll
-  for (int k = 0; k < Dim<N>::NS; ++k) out[(f++) * NT] = __ldg(&tab->SF[t++][r]);
+  for (int i = 0; i < N; ++i) {
+    out[(N * N + i) * NT] = bb[i];
+    out[(N * N + N + Dim<N>::NS + i) * NT] = hh[i];
+  }
   if (r == NT - 1) {
     E e;
 #pragma unroll

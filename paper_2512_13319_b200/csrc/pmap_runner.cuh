@@ -469,6 +469,7 @@ struct RunnerT : Runner {
               (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
                   g, W(L.group_agg1), carry_in, W(L.group_carry1), nullptr, p.dflag)));
     const R* span1 = (use_lti && tab) ? tab->E1 : nullptr;
+    const R* sf = (use_lti && tab) ? &tab->SF[0][0] : nullptr;
     p.rec_done = false;
     if constexpr (kRec) p.rec_done = !p.want_filter && !p.no_rec;
     if (p.rec_done) {
@@ -476,12 +477,12 @@ struct RunnerT : Runner {
         PM_LAUNCH(p, s, K_P1_DOWN,
                   (k_p1_down<R, N, NY, kNT, K, Src, true, true><<<ntiles, kNT, smem_down(), s>>>(
                       src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
-                      W(L.tile_agg2), p.dflag, span1, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
+                      W(L.tile_agg2), p.dflag, span1, sf, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
     } else {
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
-                    W(L.tile_agg2), p.dflag, span1, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
+                    W(L.tile_agg2), p.dflag, span1, sf, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
     }
     PM_LAUNCH(p, s, K_P2_TILES,
               (k_p2_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_p2tiles(), s>>>(
@@ -594,7 +595,8 @@ struct RunnerT : Runner {
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
-                    nullptr, p.dflag, nullptr, 0, 0, nullptr)));
+                    nullptr, p.dflag, nullptr, (use_lti && tab) ? &tab->SF[0][0] : nullptr, lti_jlo(g, false),
+                    lti_jhi(g), nullptr)));
       // pass B: backward information filter over mirrored elements (reverse node order)
       Mirror<Src> mir{src, g.node0 + g.Nn - 1};
       reduce1<true>(p, s2, K_TF_REDUCE, mir, fold_m, tab_m, y, nullptr, W(L.tf_run), W(L.tf_tile));
@@ -608,7 +610,8 @@ struct RunnerT : Runner {
       cudaStreamWaitEvent(s2, p.ev_join, 0);
       PM_LAUNCH(p, s2, K_TF_DOWN,
                 (k_tf_down<R, N, NY, kNT, K, Src><<<ntiles, kNT, smem_down(), s2>>>(
-                    mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, p.dflag)));
+                    mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, p.dflag,
+                    (use_lti && tab_m) ? &tab_m->SF[0][0] : nullptr, lti_jlo(g, true), lti_jhi(g))));
       cudaEventRecord(p.ev_fork, s2);
       cudaStreamWaitEvent(s, p.ev_fork, 0);
     } else {

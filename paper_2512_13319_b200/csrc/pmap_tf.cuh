@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
                                                 const R* __restrict__ y, const R* __restrict__ run_incl,
                                                 const R* __restrict__ tile_incl, const R* __restrict__ group_carry,
                                                 const R* __restrict__ sv, R* __restrict__ x_out,
-                                                unsigned long long* flag) {
+                                                unsigned long long* flag, const R* __restrict__ sf, int64_t j_lo,
+                                                int64_t j_hi) {
   using E = Elem<R, N>;
   using V = VF<R, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -65,7 +66,8 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
   load(cur, sh, 1);
   if (r > 0) {
     E p;
-    load(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), NT);
+    const bool interior = sf && j >= j_lo && j < j_hi;
+    load_prefix<R, N, NT>(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), interior ? sf + (r - 1) : nullptr);
     vapply<R, N, false>(p, cur, cur, nullptr, ok);
   }
   // x is staged in shared memory in chunks of KC nodes and stored as contiguous segments
