@@ -181,6 +181,70 @@ PM_INLINE float pm_abs(float x) { return fabsf(x); }
 PM_INLINE double pm_rcp(double x) { return __drcp_rn(x); }
 PM_INLINE float pm_rcp(float x) { return __frcp_rn(x); }
 
+// Reciprocal of a normal number >= 1 (the LDL pivots of G = I + U^T S U): the
+// hardware approximation refined by two Newton steps (error ~1 ulp; no slow path).
+PM_INLINE double pm_rcp_ge1(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+PM_INLINE float pm_rcp_ge1(float x) { return __frcp_rn(x); }
+
+// G = L D L^T of the small SPD matrix G = I + U^T (S U) (NW x NW, pivots >= 1),
+// sqrt-free.  In: SU = S U.  Out: unit lower L (strict part), Dinv = D^-1.
+template <typename R, int N, int NW>
+PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW], R (&Dinv)[NW], bool& ok) {
+  R G[NW][NW];
+#pragma unroll
+  for (int a = 0; a < NW; ++a)
+#pragma unroll
+    for (int c = 0; c <= a; ++c) {
+      R s = (a == c) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(U[k][a], SU[k][c], s);
+      G[a][c] = s;
+    }
+  R D[NW];
+#pragma unroll
+  for (int c = 0; c < NW; ++c) {
+    R d = G[c][c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) d = fma(-L[c][k] * D[k], L[c][k], d);
+    ok = ok && (d > R(0));
+    D[c] = d;
+    Dinv[c] = pm_rcp_ge1(d);
+#pragma unroll
+    for (int a = c + 1; a < NW; ++a) {
+      R t = G[a][c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) t = fma(-L[a][k] * D[k], L[c][k], t);
+      L[a][c] = t * Dinv[c];
+    }
+  }
+}
+
+// q <- G^-1 q with G = L D L^T from ldl_gram.
+template <typename R, int NW>
+PM_INLINE void ldl_solve(const R (&L)[NW][NW], const R (&Dinv)[NW], R (&q)[NW]) {
+#pragma unroll
+  for (int a = 0; a < NW; ++a) {
+    R s = q[a];
+#pragma unroll
+    for (int c = 0; c < a; ++c) s = fma(-L[a][c], q[c], s);
+    q[a] = s;
+  }
+#pragma unroll
+  for (int a = NW - 1; a >= 0; --a) {
+    R s = q[a] * Dinv[a];
+#pragma unroll
+    for (int c = a + 1; c < NW; ++c) s = fma(-L[c][a], q[c], s);
+    q[a] = s;
+  }
+}
+
 // Factorise f.a in place.  Row swaps are predicated selects (no dynamic
 // register indexing).  `ok` is cleared on a zero or non-finite pivot.
 // Fast path: if the matrix is column diagonally dominant, Gaussian elimination
@@ -572,36 +636,11 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       rec[(N * NW + a) * rstride] = s;
     }
   }
-  // G = I + U^T S U, Cholesky G = Lg Lg^T
-  R Lg[NW][NW], dg[NW];
-#pragma unroll
-  for (int a = 0; a < NW; ++a)
-#pragma unroll
-    for (int c = 0; c <= a; ++c) {
-      R s = (a == c) ? R(1) : R(0);
-#pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(U[k][a], SU[k][c], s);
-      Lg[a][c] = s;
-    }
-#pragma unroll
-  for (int c = 0; c < NW; ++c) {
-    R d = Lg[c][c];
-#pragma unroll
-    for (int k = 0; k < c; ++k) d = fma(-Lg[c][k], Lg[c][k], d);
-    ok = ok && (d > R(0));
-    const R sd = sqrt(d);
-    Lg[c][c] = sd;
-    dg[c] = pm_rcp(sd);
-#pragma unroll
-    for (int a = c + 1; a < NW; ++a) {
-      R t = Lg[a][c];
-#pragma unroll
-      for (int k = 0; k < c; ++k) t = fma(-Lg[a][k], Lg[c][k], t);
-      Lg[a][c] = t * dg[c];
-    }
-  }
-  // SA = S A ; M = U^T S A = (SU)^T A ; W2 = Lg^-1 M  (so M^T G^-1 M = W2^T W2)
-  R SA[N][N], W2[NW][N];
+  // G = I + U^T S U = L D L^T
+  R Lg[NW][NW], dinv[NW];
+  ldl_gram<R, N, NW>(U, SU, Lg, dinv, ok);
+  // SA = S A ; M = U^T S A = (SU)^T A ; W2 = L^-1 M, W2s = D^-1 W2 (M^T G^-1 M = W2s^T W2)
+  R SA[N][N], W2[NW][N], W2s[NW][N];
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
@@ -620,10 +659,11 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       for (int k = 0; k < N; ++k) s = fma(SU[k][a], e1.A[k][j], s);
 #pragma unroll
       for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], W2[c][j], s);
-      W2[a][j] = s * dg[a];
+      W2[a][j] = s;
+      W2s[a][j] = s * dinv[a];
     }
   }
-  // w = v - S b ; q = Lg^-T Lg^-1 U^T w ; w2 = w - SU q
+  // w = v - S b ; q = G^-1 U^T w ; w2 = w - SU q
   R w[N], q[NW];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -637,17 +677,9 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     R s = R(0);
 #pragma unroll
     for (int k = 0; k < N; ++k) s = fma(U[k][a], w[k], s);
-#pragma unroll
-    for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], q[c], s);
-    q[a] = s * dg[a];
+    q[a] = s;
   }
-#pragma unroll
-  for (int a = NW - 1; a >= 0; --a) {
-    R s = q[a];
-#pragma unroll
-    for (int c = a + 1; c < NW; ++c) s = fma(-Lg[c][a], q[c], s);
-    q[a] = s * dg[a];
-  }
+  ldl_solve<R, NW>(Lg, dinv, q);
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     R s = w[i];
@@ -664,7 +696,7 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
 #pragma unroll
       for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], SA[k][j], s);
 #pragma unroll
-      for (int a = 0; a < NW; ++a) s = fma(-W2[a][i], W2[a][j], s);
+      for (int a = 0; a < NW; ++a) s = fma(-W2s[a][i], W2[a][j], s);
       o.S[sidx(i, j, N)] = s;
     }
     R s = e1.h[i];
@@ -723,48 +755,16 @@ PM_INLINE void trans_step_rec(const R (&A)[N][N], const R (&b)[N], const R (&U)[
     for (int a = 0; a < NW; ++a) s = fma(U[i][a], u[a], s);
     w[i] = s;
   }
-  R Lg[NW][NW], dg[NW], q[NW];
-#pragma unroll
-  for (int a = 0; a < NW; ++a)
-#pragma unroll
-    for (int c = 0; c <= a; ++c) {
-      R s = (a == c) ? R(1) : R(0);
-#pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(U[k][a], SU[k][c], s);
-      Lg[a][c] = s;
-    }
-#pragma unroll
-  for (int c = 0; c < NW; ++c) {
-    R d = Lg[c][c];
-#pragma unroll
-    for (int k = 0; k < c; ++k) d = fma(-Lg[c][k], Lg[c][k], d);
-    ok = ok && (d > R(0));
-    const R sd = sqrt(d);
-    dg[c] = pm_rcp(sd);
-#pragma unroll
-    for (int a = c + 1; a < NW; ++a) {
-      R t = Lg[a][c];
-#pragma unroll
-      for (int k = 0; k < c; ++k) t = fma(-Lg[a][k], Lg[c][k], t);
-      Lg[a][c] = t * dg[c];
-    }
-  }
+  R Lg[NW][NW], dinv[NW], q[NW];
+  ldl_gram<R, N, NW>(U, SU, Lg, dinv, ok);
 #pragma unroll
   for (int a = 0; a < NW; ++a) {
     R s = R(0);
 #pragma unroll
     for (int k = 0; k < N; ++k) s = fma(SU[k][a], w[k], s);
-#pragma unroll
-    for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], q[c], s);
-    q[a] = s * dg[a];
+    q[a] = s;
   }
-#pragma unroll
-  for (int a = NW - 1; a >= 0; --a) {
-    R s = q[a];
-#pragma unroll
-    for (int c = a + 1; c < NW; ++c) s = fma(-Lg[c][a], q[c], s);
-    q[a] = s * dg[a];
-  }
+  ldl_solve<R, NW>(Lg, dinv, q);
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     R s = w[i];
