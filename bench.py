@@ -35,7 +35,7 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 # ----------------------------------------------------------- algorithmic counts
-def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0):
+def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zero_b: bool = False):
     """Algorithmic FP64 flops (FMA = 2) and HBM bytes per node of each kernel class
     (DESIGN.md section 6): the arithmetic each kernel's per-node recurrence performs
     in this decomposition, excluding the intra-tile scan overheads (Kogge-Stone
@@ -58,8 +58,10 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0):
     if nw > 0:  # R-LOWRANK node update (vapply_lowrank), R-P2REC records when smaller than (S, v)
         r = nw
         chol = r * (r + 1) // 2 * N + r * (r - 1) // 2 * (r + 1) + r
-        vapply = (N * r * N + chol + N * N * N + r * N * N + r * (r - 1) // 2 * N + N * N + r * N + r * r
-                  + N * r + ns * (N + r) + N * N)
+        # S U, Gram + LDL, Y = L^-1 (S U)^T and D^-1 Y, B = S - Ys^T Y, w = v - S b (skipped
+        # when b == 0), q = G^-1 U^T w, w - S U q, B A, A^T (B A) + J, A^T w + eta
+        vapply = (N * r * N + chol + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
+                  + r * N + r * r + N * r + N * N * N + ns * N + N * N)
         if r * (N + 1) < vsz:
             vsz2 = r * (N + 1)
             vapply += r * N  # U^T v
@@ -329,7 +331,8 @@ def main():
     if (isinstance(spec, wl.LinearSpec) and spec.L.shape[1] < spec.nx and os.environ.get("PMAP_NO_LOWRANK") != "1"
             and os.environ.get("PMAP_GENERAL") != "1"):
         lowrank = spec.L.shape[1]
-    counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank)
+    zero_b = isinstance(spec, wl.LinearSpec) and (spec.c is None or not np.any(spec.c))
+    counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank, zero_b=zero_b)
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl

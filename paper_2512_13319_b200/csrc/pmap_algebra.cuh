@@ -605,14 +605,15 @@ PM_INLINE void vapply(const Elem<R, N>& e1, const VF<R, N>& V, VF<R, N>& out, Af
 }
 
 // vapply without transition for a node element whose C = U U^T has rank NW < N
-// (R-LOWRANK, Woodbury):  (I + C S)^-1 = I - U G^-1 U^T S,  G = I + U^T S U  (NW x NW, SPD),
-//   S' = A^T S A - M^T G^-1 M + J,  M = U^T S A,
-//   v' = A^T [w - S U G^-1 U^T w] + eta,  w = v - S b.
-// Same value function as vapply (up to rounding); the N x N pivoted LU becomes an NW x NW
-// Cholesky, which shortens the per-node dependency chain.
+// (R-LOWRANK, Woodbury):  (S^-1 + C)^-1 = S - S U G^-1 U^T S =: B,  G = I + U^T S U
+// (NW x NW, SPD, G = L D L^T), (I + S C)^-1 = I - S U G^-1 U^T, so
+//   S' = A^T B A + J,   v' = A^T [w - S U G^-1 U^T w] + eta,   w = v - S b.
+// Same value function as vapply (up to rounding); the N x N pivoted LU becomes an
+// NW x NW sqrt-free LDL^T.  zero_b: b == 0 (skips S b).  rec (nullable): pass-2
+// record [S U | U^T v] of the input value function (R-P2REC), field stride rstride.
 template <typename R, int N, int NW>
 PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const VF<R, N>& V, VF<R, N>& out,
-                              bool& ok, R* rec = nullptr, int64_t rstride = 0) {
+                              bool& ok, R* rec = nullptr, int64_t rstride = 0, bool zero_b = false) {
   R SU[N][NW];
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -623,7 +624,7 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], U[k][a], s);
       SU[i][a] = s;
     }
-  if (rec) {  // pass-2 record of the input value function (R-P2REC): [S U | U^T v]
+  if (rec) {
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
@@ -636,40 +637,41 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       rec[(N * NW + a) * rstride] = s;
     }
   }
-  // G = I + U^T S U = L D L^T
   R Lg[NW][NW], dinv[NW];
   ldl_gram<R, N, NW>(U, SU, Lg, dinv, ok);
-  // SA = S A ; M = U^T S A = (SU)^T A ; W2 = L^-1 M, W2s = D^-1 W2 (M^T G^-1 M = W2s^T W2)
-  R SA[N][N], W2[NW][N], W2s[NW][N];
+  // Y = L^-1 (S U)^T, Ys = D^-1 Y:  S U G^-1 (S U)^T = Ys^T Y
+  R Y[NW][N], Ys[NW][N];
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int a = 0; a < NW; ++a) {
+      R s = SU[j][a];
+#pragma unroll
+      for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], Y[c][j], s);
+      Y[a][j] = s;
+      Ys[a][j] = s * dinv[a];
+    }
+  // B = S - Ys^T Y (symmetric, full for the product below)
+  R B[N][N];
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      R s = R(0);
+    for (int j = i; j < N; ++j) {
+      R s = V.S[sidx(i, j, N)];
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], e1.A[k][j], s);
-      SA[i][j] = s;
+      for (int a = 0; a < NW; ++a) s = fma(-Ys[a][i], Y[a][j], s);
+      B[i][j] = s;
+      B[j][i] = s;
     }
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-#pragma unroll
-    for (int a = 0; a < NW; ++a) {
-      R s = R(0);
-#pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(SU[k][a], e1.A[k][j], s);
-#pragma unroll
-      for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], W2[c][j], s);
-      W2[a][j] = s;
-      W2s[a][j] = s * dinv[a];
-    }
-  }
-  // w = v - S b ; q = G^-1 U^T w ; w2 = w - SU q
+  // w = v - S b ; q = G^-1 U^T w ; w2 = w - S U q
   R w[N], q[NW];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     R s = V.v[i];
+    if (!zero_b) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) s = fma(-V.S[sidx(i, k, N)], e1.b[k], s);
+      for (int k = 0; k < N; ++k) s = fma(-V.S[sidx(i, k, N)], e1.b[k], s);
+    }
     w[i] = s;
   }
 #pragma unroll
@@ -687,6 +689,17 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     for (int a = 0; a < NW; ++a) s = fma(-SU[i][a], q[a], s);
     w[i] = s;
   }
+  // BA = B A ; S' = A^T (B A) + J (upper triangle) ; v' = A^T w2 + eta
+  R BA[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(B[i][k], e1.A[k][j], s);
+      BA[i][j] = s;
+    }
   VF<R, N> o;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -694,9 +707,7 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     for (int j = i; j < N; ++j) {
       R s = e1.J[sidx(i, j, N)];
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], SA[k][j], s);
-#pragma unroll
-      for (int a = 0; a < NW; ++a) s = fma(-W2s[a][i], W2[a][j], s);
+      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], BA[k][j], s);
       o.S[sidx(i, j, N)] = s;
     }
     R s = e1.h[i];

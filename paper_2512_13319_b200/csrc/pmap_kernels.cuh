@@ -354,7 +354,7 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       if constexpr (Src::LOWRANK > 0)
         vapply_lowrank<R, N, Src::LOWRANK>(e, src.U, cur, cur, ok, REC ? svt + m * NT + r : nullptr,
-                                           (int64_t)K * NT);
+                                           (int64_t)K * NT, src.zero_b != 0);
       else
         vapply<R, N, false>(e, cur, cur, nullptr, ok);
     }

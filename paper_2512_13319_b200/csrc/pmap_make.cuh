@@ -34,6 +34,11 @@ Runner* make_lti(const double* A, const double* b, const double* C, const double
       s.Um[i][a] = (R)t;
     }
   }
+  s.zero_b = s.zero_bm = 1;
+  for (int i = 0; i < N; ++i) {
+    if (s.b[i] != R(0)) s.zero_b = 0;
+    if (s.bm[i] != R(0)) s.zero_bm = 0;
+  }
   return rn;
 }
 

@@ -38,6 +38,7 @@ struct SrcLTI {
   R Cm[NS];    // (I - dt F)^-1 dt Q (I - dt F)^-T
   R U[N][NWC > 0 ? NWC : 1];   // dt Q = U U^T (NWC > 0)
   R Um[N][NWC > 0 ? NWC : 1];  // mirrored: Cm = (Am U)(Am U)^T
+  int zero_b = 0, zero_bm = 0;  // b == 0 / bm == 0 (c == 0): the node updates skip S b
   static constexpr bool HAS_MIRROR = true;
 
   // Mirrored element M_i of node gi (R-TF); the terminal node Tg has no transition.

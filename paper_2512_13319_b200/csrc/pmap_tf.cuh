@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
         mir.template node<R, N>(g.node0 + l, yb + l * NY, nullptr, e);
         if constexpr (Src::LOWRANK > 0) {  // mirrored diffusion Cm = (Am U)(Am U)^T
           if (g.node0 + l != mir.Tg)
-            vapply_lowrank<R, N, Src::LOWRANK>(e, mir.s.Um, cur, cur, ok);
+            vapply_lowrank<R, N, Src::LOWRANK>(e, mir.s.Um, cur, cur, ok, nullptr, 0, mir.s.zero_bm != 0);
           else
             vapply<R, N, false>(e, cur, cur, nullptr, ok);
         } else {
