@@ -229,6 +229,33 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------- sequential GPU baseline (f1)
+def sequential_gpu(plan, config, yd, xd, ms_parallel, torch, stream):
+    """The paper's comparison: the same smoother run sequentially
+    on the same B200 (map_solve_sequential, one thread per trajectory), full workload,
+    timed with CUDA events (after one untimed run unless the run is long)."""
+    from workloads.models import CONFIGS
+    c = CONFIGS[config]
+    method = 1 if c["method"] == "two_filter" else 0
+    passes = c.get("passes", 1)
+    run = lambda: plan.solve_sequential(yd, method=method, passes=passes, x_map=xd)
+    if plan.batch * plan.T * passes < 2_000_000:  # long runs (C3: ~19 s) are timed cold: load cost is noise
+        run()
+        plan.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    plan.sync()
+    ms = e0.elapsed_time(e1)
+    B, T = plan.batch, plan.T
+    return {"value": B * T / (ms * 1e-3), "unit": "steps/s", "ms_per_solve": ms,
+            "method": ("two-filter" if method else "RTS") + (f", {passes} IEKS passes" if "passes" in c else ""),
+            "threads": B, "parallel_speedup": ms / ms_parallel,
+            "what": "map_solve_sequential: one GPU thread per trajectory, same element build and fp64 algebra"}
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -240,6 +267,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-seq", action="store_true", help="skip the sequential on-device baseline (SURVEY f1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -366,6 +394,10 @@ def main():
                  "peak_source": hbm_src, "frac_of_hbm_roofline": sby * B * T / (ms * 1e-3) / 1e9 / hbm,
                  "alg_tflops": sfl * B * T / (ms * 1e-3) / 1e12}
 
+    seq = None
+    if world == 1 and not args.no_seq:
+        seq = sequential_gpu(plan, args.config, yd, xd, ms, torch, stream)
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, cores, sample = oracle_sample(args.config)
@@ -384,6 +416,7 @@ def main():
         "solve_roofline": solve_hbm,
         "kernels_ms_per_step": {k: v[0] / max(1, min(args.steps, 50)) for k, v in prof.items()},
         "cpu_baseline": cpu,
+        "sequential_gpu": seq,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,

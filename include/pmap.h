@@ -132,8 +132,28 @@ map_status map_solve_linear(map_plan_t plan, const void* y, void* x_map, void* f
 /* Linear MAP by the parallel two-filter form (information-form
  * backward filter, DESIGN.md R-TF): the backward-information suffix scan runs
  * concurrently with pass 1 and the per-node combine is fused into its epilogue.
- * Linear plans only; single GPU (world == 1). */
-map_status map_two_filter(map_plan_t plan, const void* y, void* x_map);
+ * smooth_P (nullable) [batch][T+1][nx*(nx+1)/2] (upper triangle, row-major)
+ * receives the smoother covariance (S_i + Lam_i - J_i^m)^-1: the posterior
+ * precision of x_i is the sum of the forward and backward filters' information
+ * (SURVEY f4).  Linear plans only; single GPU (world == 1). */
+map_status map_two_filter(map_plan_t plan, const void* y, void* x_map, void* smooth_P);
+
+/* Sequential on-device baselines: the paper's "sequential counterparts"
+ * of the parallel smoothers, one GPU thread per trajectory,
+ * same element sources and register algebra as the parallel path.
+ *   method 0: value-function recursion V_i = E_i (x) V_{i-1} (Kalman--Bucy filter
+ *             in information form) then the RTS recursion
+ *             x*_{i-1} = (I + C_i S_{i-1})^-1 (A_i x*_i + b_i + C_i v_{i-1})
+ *              from x*_T = S_T^-1 v_T;
+ *   method 1: the same forward recursion and the backward information filter over
+ *             mirrored elements, combined per node (two-filter, R-TF).
+ * smooth_P (nullable, layout as in map_two_filter): smoother covariance
+ * (method 0: P^s_{i-1} = Phi_i P^s_i Phi_i^T + (I + C_i S_{i-1})^-1 C_i; method 1:
+ * (S_i + Lam_i - J_i^m)^-1).  Nonlinear plans: method 0 only, `passes` iterated
+ * linearisation passes from xbar^(0) = m0 (R-INIT); linear plans ignore
+ * `passes`.  Single GPU (world == 1).  MAP_E_ARG on a bad method / plan kind. */
+map_status map_solve_sequential(map_plan_t plan, int32_t method, const void* y, int32_t passes, void* x_map,
+                                void* smooth_P);
 
 /* Nonlinear MAP by iterated Taylor linearisation (IEKS): each pass
  * re-linearises f, h about the previous estimate on the device (F_i = df(xbar_i),

@@ -40,7 +40,7 @@ class OraModel(ctypes.Structure):
         ("T", ctypes.c_long), ("t0", ctypes.c_double), ("tf", ctypes.c_double),
     ] + [(n, ctypes.c_void_p) for n in ("F", "c", "L", "W", "H", "r", "R")] + [
         (n, ctypes.c_long) for n in ("sF", "sc", "sL", "sW", "sH", "sr", "sR")
-    ] + [("m0", ctypes.c_void_p), ("P0", ctypes.c_void_p)]
+    ] + [("m0", ctypes.c_void_p), ("P0", ctypes.c_void_p), ("g", ctypes.c_void_p)]
 
 
 _loaded: dict = {}
@@ -53,6 +53,7 @@ def _lib(long_double: bool = False):
         P = ctypes.c_void_p
         lib.ora_kf_rts.argtypes = [ctypes.POINTER(OraModel), P, P, P, P]
         lib.ora_two_filter.argtypes = [ctypes.POINTER(OraModel), P, P]
+        lib.ora_kf_rts_cov.argtypes = [ctypes.POINTER(OraModel), P, P, P]
         lib.ora_batch.argtypes = [ctypes.POINTER(OraModel), ctypes.c_long, P, P, ctypes.c_int]
         lib.ora_ieks.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long,
                                  ctypes.c_double, ctypes.c_double, P, P, P, P, P, P, ctypes.c_int, P, P, P]
@@ -113,6 +114,7 @@ class LinearModel:
             setattr(s, name, _ptr(a))
             setattr(s, "s" + name, stride(a, nd))
         s.m0, s.P0 = _ptr(self.m0), _ptr(self.P0)
+        s.g = None
         return s
 
 
@@ -132,6 +134,20 @@ def kf_rts(model: LinearModel, y, T: int, t0: float, tf: float, long_double: boo
     if rc:
         raise FloatingPointError(f"oracle kf_rts failed rc={rc}")
     return (x, fm, fP) if want_filter else x
+
+
+def kf_rts_cov(model: LinearModel, y, T: int, t0: float, tf: float, long_double: bool = False):
+    """Discrete KF + RTS MAP and smoother covariances (textbook RTS covariance recursion,
+    SURVEY f4).  Returns (x_map [T+1, nx], smooth_P [T+1, nx, nx])."""
+    y = _f64(y).reshape(T + 1, model.ny)
+    N, nx = T + 1, model.nx
+    x = np.empty((N, nx))
+    P = np.empty((N, nx, nx))
+    s = model._struct(T, t0, tf)
+    rc = _lib(long_double).ora_kf_rts_cov(ctypes.byref(s), _ptr(y), _ptr(x), _ptr(P))
+    if rc:
+        raise FloatingPointError(f"oracle kf_rts_cov failed rc={rc}")
+    return x, P
 
 
 def two_filter(model: LinearModel, y, T: int, t0: float, tf: float, long_double: bool = False):
@@ -159,13 +175,15 @@ def batch(model: LinearModel, y, T: int, t0: float, tf: float, mode: int = 0):
 
 def ieks(kind: int, params, L, W, R, m0, P0, y, T: int, t0: float, tf: float, passes: int,
          x_init=None):
-    """Iterated linearisation MAP (5 passes in P:625). kind 1 = CT, 2 = VdP.
+    """Iterated linearisation MAP (5 passes in P:625). kind 1 = CT, 2 = VdP
+    (params = [mu] or [mu, om_div]; om_div != 0 keeps the OM divergence term of P:66).
 
     Returns (x_map [T+1, nx], per-pass max |dx|)."""
     L, W, R, m0, P0 = map(_f64, (L, W, R, m0, P0))
     nx, nw, ny = L.shape[0], L.shape[1], R.shape[0]
     y = _f64(y).reshape(T + 1, ny)
     params = _f64(params if params is not None else [0.0])
+    params = np.concatenate([params, np.zeros(max(0, 2 - params.size))])  # C reads params[0..1]
     xi = None if x_init is None else _f64(x_init)
     x = np.empty((T + 1, nx))
     delta = np.empty(max(passes, 1))

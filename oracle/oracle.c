@@ -48,6 +48,7 @@ typedef struct {
   const double *F, *c, *L, *W, *H, *r, *R; /* per-node arrays, row-major */
   long sF, sc, sL, sW, sH, sr, sR;          /* element stride between nodes (0 = constant) */
   const double *m0, *P0;
+  const double* g;   /* nullable [T+1][nx]: linear node cost g_i^T x_i (OM divergence term) */
 } ora_model;
 
 /* ---------------- small dense helpers (row-major, n <= MAXN) ---------------- */
@@ -232,29 +233,54 @@ static int kf_forward(const ora_model* md, const double* y, REAL* ms, REAL* Ps) 
       return 1;
     }
     if (update(nx, ny, dt, &nm, y + i * ny, mp, Pp, ms + i * nx, Ps + i * nx * nx)) return 1;
+    if (md->g) {
+      /* a linear cost term g_i^T x_i multiplies the filtering density by exp(-g_i^T x_i):
+       * N(x; m, P) exp(-g^T x) is proportional to N(x; m - P g, P) (completing the square) */
+      REAL t[MAXN], gi[MAXN];
+      load(nx, md->g + i * nx, gi);
+      mat_vec(nx, nx, Ps + i * nx * nx, gi, t);
+      for (int a = 0; a < nx; ++a) ms[i * nx + a] -= t[a];
+    }
   }
   return 0;
 }
 
 /* RTS smoother: x_T = m_T; x_i = m_i + G_i (x_{i+1} - mp_{i+1}),
- * G_i = P_i Phi_{i+1}^T Pp_{i+1}^{-1}  (discrete counterpart of P:219-223). */
-static int rts_backward(const ora_model* md, const REAL* ms, const REAL* Ps, REAL* xs) {
+ * G_i = P_i Phi_{i+1}^T Pp_{i+1}^{-1}  (discrete counterpart of P:219-223).
+ * PsS (nullable): smoother covariances, textbook RTS form
+ * PsS_T = P_T,  PsS_i = P_i + G_i (PsS_{i+1} - Pp_{i+1}) G_i^T. */
+static int rts_backward(const ora_model* md, const REAL* ms, const REAL* Ps, REAL* xs, REAL* PsS) {
   int nx = md->nx;
   REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)md->T;
   REAL mp[MAXN], Pp[MAXN * MAXN], Phi[MAXN * MAXN], Gt[MAXN * MAXN], d[MAXN];
+  REAL D[MAXN * MAXN], DG[MAXN * MAXN];
   node_model nm;
   long T = md->T;
   memcpy(xs + T * nx, ms + T * nx, sizeof(REAL) * nx);
+  if (PsS) memcpy(PsS + T * nx * nx, Ps + T * nx * nx, sizeof(REAL) * nx * nx);
   for (long i = T - 1; i >= 0; --i) {
     model_at(md, i + 1, &nm);
     if (predict(nx, dt, &nm, ms + i * nx, Ps + i * nx * nx, Phi, mp, Pp)) return 1;
     mat_mul_bt(nx, nx, nx, Phi, Ps + i * nx * nx, Gt); /* Phi P_i (P_i symmetric) = (P_i Phi^T)^T */
+    if (PsS)
+      for (int a = 0; a < nx * nx; ++a) D[a] = PsS[(i + 1) * nx * nx + a] - Pp[a];
     if (chol_solve(nx, nx, Pp, Gt)) return 1;          /* Gt = Pp^{-1} Phi P_i = G^T */
     for (int a = 0; a < nx; ++a) d[a] = xs[(i + 1) * nx + a] - mp[a];
     for (int a = 0; a < nx; ++a) {
       REAL s = ms[i * nx + a];
       for (int b = 0; b < nx; ++b) s += Gt[b * nx + a] * d[b];
       xs[i * nx + a] = s;
+    }
+    if (PsS) {
+      /* PsS_i = P_i + G D G^T with G = Gt^T:  DG = D Gt,  PsS_i = P_i + Gt^T DG */
+      mat_mul(nx, nx, nx, D, Gt, DG);
+      for (int a = 0; a < nx; ++a)
+        for (int b = 0; b < nx; ++b) {
+          REAL s = Ps[i * nx * nx + a * nx + b];
+          for (int l = 0; l < nx; ++l) s += Gt[l * nx + a] * DG[l * nx + b];
+          PsS[i * nx * nx + a * nx + b] = s;
+        }
+      symmetrize(nx, PsS + i * nx * nx);
     }
   }
   return 0;
@@ -274,13 +300,32 @@ int ora_kf_rts(const ora_model* md, const double* y, double* x_map, double* filt
   REAL* Ps = malloc(sizeof(REAL) * N * nx * nx);
   REAL* xs = malloc(sizeof(REAL) * N * nx);
   int rc = (!ms || !Ps || !xs) ? 3 : kf_forward(md, y, ms, Ps);
-  if (!rc) rc = rts_backward(md, ms, Ps, xs);
+  if (!rc) rc = rts_backward(md, ms, Ps, xs, NULL);
   if (!rc) {
     store(N * nx, xs, x_map);
     if (filt_m) store(N * nx, ms, filt_m);
     if (filt_P) store(N * nx * nx, Ps, filt_P);
   }
   free(ms); free(Ps); free(xs);
+  return rc;
+}
+
+/* Linear MAP and smoother covariances (RTS form).  smooth_P: [T+1][nx][nx]. */
+int ora_kf_rts_cov(const ora_model* md, const double* y, double* x_map, double* smooth_P) {
+  long N = md->T + 1;
+  int nx = md->nx;
+  if (nx > MAXN || md->ny > MAXN || md->nw > MAXN || md->T < 1) return 2;
+  REAL* ms = malloc(sizeof(REAL) * N * nx);
+  REAL* Ps = malloc(sizeof(REAL) * N * nx * nx);
+  REAL* xs = malloc(sizeof(REAL) * N * nx);
+  REAL* PsS = malloc(sizeof(REAL) * N * nx * nx);
+  int rc = (!ms || !Ps || !xs || !PsS) ? 3 : kf_forward(md, y, ms, Ps);
+  if (!rc) rc = rts_backward(md, ms, Ps, xs, PsS);
+  if (!rc) {
+    store(N * nx, xs, x_map);
+    store(N * nx * nx, PsS, smooth_P);
+  }
+  free(ms); free(Ps); free(xs); free(PsS);
   return rc;
 }
 
@@ -296,7 +341,7 @@ int ora_kf_rts(const ora_model* md, const double* y, double* x_map, double* filt
 int ora_two_filter(const ora_model* md, const double* y, double* x_map) {
   long N = md->T + 1, T = md->T;
   int nx = md->nx, ny = md->ny;
-  if (nx > MAXN || ny > MAXN || md->nw > MAXN || T < 1) return 2;
+  if (nx > MAXN || ny > MAXN || md->nw > MAXN || T < 1 || md->g) return 2;
   REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)T;
   REAL* ms = malloc(sizeof(REAL) * N * nx);
   REAL* Ps = malloc(sizeof(REAL) * N * nx * nx);
@@ -440,7 +485,12 @@ int ora_ieks(int kind, const double* params, int nx, int ny, int nw, long T, dou
   double *F = malloc(sizeof(double) * N * nx * nx), *c = malloc(sizeof(double) * N * nx);
   double *H = malloc(sizeof(double) * N * ny * nx), *r = malloc(sizeof(double) * N * ny);
   double *ye = malloc(sizeof(double) * N * ny), *xb = malloc(sizeof(double) * N * nx);
-  int rc = (!F || !c || !H || !r || !ye || !xb) ? 3 : 0;
+  /* Van der Pol with params[1] != 0: keep the OM divergence term 1/2 div f of
+   * every interval i >= 1, dt/2 mu (1 - x_{i,0}^2), linearised about the nominal: its
+   * gradient dt/2 (-2 mu xbar_{i,0}, 0) becomes a linear node cost. */
+  const int om_div = (kind == 2 && params[1] != 0.0);
+  double* gdiv = om_div ? calloc(N * nx, sizeof(double)) : NULL;
+  int rc = (!F || !c || !H || !r || !ye || !xb || (om_div && !gdiv)) ? 3 : 0;
   for (long i = 0; i < N && !rc; ++i)
     for (int a = 0; a < nx; ++a) xb[i * nx + a] = x_init ? x_init[i * nx + a] : m0[a];
   for (int p = 0; p < passes && !rc; ++p) {
@@ -463,9 +513,10 @@ int ora_ieks(int kind, const double* params, int nx, int ny, int nw, long T, dou
         if (kind == 1 && a == 1) res = wrap_pi(res);
         ye[i * ny + a] = r[i * ny + a] + hx + res;
       }
+      if (om_div && i >= 1) gdiv[i * nx + 0] = 0.5 * ((tf - t0) / T) * (-2.0 * params[0] * xi[0]);
     }
     ora_model md = {nx, ny, nw, T, t0, tf, F, c, L, W, H, r, R,
-                    nx * nx, nx, 0, 0, ny * nx, ny, 0, m0, P0};
+                    nx * nx, nx, 0, 0, ny * nx, ny, 0, m0, P0, gdiv};
     rc = ora_kf_rts(&md, ye, x_map, NULL, NULL);
     if (rc) break;
     double dmax = 0;
@@ -476,7 +527,7 @@ int ora_ieks(int kind, const double* params, int nx, int ny, int nw, long T, dou
     }
     if (delta) delta[p] = dmax;
   }
-  free(F); free(c); free(H); free(r); free(ye); free(xb);
+  free(F); free(c); free(H); free(r); free(ye); free(xb); free(gdiv);
   return rc;
 }
 

@@ -25,7 +25,7 @@ STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 
 EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter", "map_solve_nonlinear",
            "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
            "map_profile_enable", "map_profile_read", "map_shard_payload_bytes", "map_shard_phase",
-           "map_version"]
+           "map_version", "map_solve_sequential"]
 
 
 class MapError(RuntimeError):
@@ -70,8 +70,10 @@ def load_library():
         lib.map_plan_destroy.restype = None
         lib.map_solve_linear.argtypes = [P, P, P, P, P]
         lib.map_solve_linear.restype = ctypes.c_int
-        lib.map_two_filter.argtypes = [P, P, P]
+        lib.map_two_filter.argtypes = [P, P, P, P]
         lib.map_two_filter.restype = ctypes.c_int
+        lib.map_solve_sequential.argtypes = [P, I32, P, I32, P, P]
+        lib.map_solve_sequential.restype = ctypes.c_int
         lib.map_solve_nonlinear.argtypes = [P, P, I32, D, P, P, ctypes.POINTER(I32)]
         lib.map_solve_nonlinear.restype = ctypes.c_int
         lib.map_sync.argtypes = [P]
@@ -139,8 +141,12 @@ def map_solve_linear(plan: int, y, x_map, filt_m=None, filt_P=None) -> None:
     _check(load_library().map_solve_linear(plan, _ptr(y), _ptr(x_map), _ptr(filt_m), _ptr(filt_P)), plan)
 
 
-def map_two_filter(plan: int, y, x_map) -> None:
-    _check(load_library().map_two_filter(plan, _ptr(y), _ptr(x_map)), plan)
+def map_two_filter(plan: int, y, x_map, smooth_P=None) -> None:
+    _check(load_library().map_two_filter(plan, _ptr(y), _ptr(x_map), _ptr(smooth_P)), plan)
+
+
+def map_solve_sequential(plan: int, method: int, y, passes: int, x_map, smooth_P=None) -> None:
+    _check(load_library().map_solve_sequential(plan, method, _ptr(y), passes, _ptr(x_map), _ptr(smooth_P)), plan)
 
 
 def map_solve_nonlinear(plan: int, y, passes: int, tol: float, x_init, x_map) -> int:
@@ -255,10 +261,19 @@ class Plan:
         map_solve_linear(self.handle, y, x_map, filt_m, filt_P)
         return x_map
 
-    def two_filter(self, y, x_map=None):
+    def two_filter(self, y, x_map=None, smooth_P=None):
+        """Parallel two-filter MAP; smooth_P (optional, [batch][T+1][nx(nx+1)/2]) receives
+        the smoother covariances."""
         if x_map is None:
             x_map = self._out(y, self.batch, self.n_local, self.nx)
-        map_two_filter(self.handle, y, x_map)
+        map_two_filter(self.handle, y, x_map, smooth_P)
+        return x_map
+
+    def solve_sequential(self, y, method: int = 0, passes: int = 1, x_map=None, smooth_P=None):
+        """Sequential on-device baseline (map_solve_sequential): method 0 = RTS, 1 = two-filter."""
+        if x_map is None:
+            x_map = self._out(y, self.batch, self.n_local, self.nx)
+        map_solve_sequential(self.handle, method, y, passes, x_map, smooth_P)
         return x_map
 
     def solve_nonlinear(self, y, passes: int = 10, tol: float = 0.0, x_init=None, x_map=None):

@@ -18,8 +18,10 @@ template Runner* make_tv<PM_R, PM_NX, PM_NY, PM_K>(const PM_R*, const PM_R*, con
                                              const PM_R*, const PM_R*, const int64_t*, int, double, const double*,
                                              const double*);
 #elif PM_KIND == 2
-template Runner* make_nl<PM_R, 5, 2, 1, PM_K>(double, double, const double*, const double*, const double*, const double*);
+template Runner* make_nl<PM_R, 5, 2, 1, PM_K>(double, double, double, const double*, const double*, const double*,
+                                              const double*);
 #elif PM_KIND == 3
-template Runner* make_nl<PM_R, 2, 1, 2, PM_K>(double, double, const double*, const double*, const double*, const double*);
+template Runner* make_nl<PM_R, 2, 1, 2, PM_K>(double, double, double, const double*, const double*, const double*,
+                                              const double*);
 #endif
 }  // namespace pmap_rt

@@ -59,14 +59,14 @@ static Runner* dispatch_tv(int kr, int nx, int ny, const R* F, const R* c, const
 }
 
 template <typename R>
-static Runner* dispatch_nl(int kr, int kind, double dt, double mu, const double* C, const double* Ri,
+static Runner* dispatch_nl(int kr, int kind, double dt, double mu, double dv, const double* C, const double* Ri,
                            const double* P0i, const double* P0im0) {
   if (kind == MAP_NL_COORD_TURN)
-    return kr == kKBig ? make_nl<R, 5, 2, 1, kKBig>(dt, mu, C, Ri, P0i, P0im0)
-                       : make_nl<R, 5, 2, 1, kKSmall>(dt, mu, C, Ri, P0i, P0im0);
+    return kr == kKBig ? make_nl<R, 5, 2, 1, kKBig>(dt, mu, dv, C, Ri, P0i, P0im0)
+                       : make_nl<R, 5, 2, 1, kKSmall>(dt, mu, dv, C, Ri, P0i, P0im0);
   if (kind == MAP_NL_VAN_DER_POL)
-    return kr == kKBig ? make_nl<R, 2, 1, 2, kKBig>(dt, mu, C, Ri, P0i, P0im0)
-                       : make_nl<R, 2, 1, 2, kKSmall>(dt, mu, C, Ri, P0i, P0im0);
+    return kr == kKBig ? make_nl<R, 2, 1, 2, kKBig>(dt, mu, dv, C, Ri, P0i, P0im0)
+                       : make_nl<R, 2, 1, 2, kKSmall>(dt, mu, dv, C, Ri, P0i, P0im0);
   return nullptr;
 }
 
@@ -315,8 +315,10 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     sym_pack(Q.data(), Cp.data());
     if (!h_inv(ny, nl->R, Ri.data())) return MAP_E_ARG;
     const double mu = (nl->nparams >= 1 && nl->params) ? nl->params[0] : 0.0;
-    rn = f32 ? dispatch_nl<float>(kr, nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data())
-             : dispatch_nl<double>(kr, nl->kind, dt, mu, Cp.data(), Ri.data(), P0ip.data(), P0im0.data());
+    // Van der Pol params[1] != 0: keep the Onsager--Machlup divergence term
+    const double dv = (nl->kind == MAP_NL_VAN_DER_POL && nl->nparams >= 2 && nl->params) ? nl->params[1] : 0.0;
+    rn = f32 ? dispatch_nl<float>(kr, nl->kind, dt, mu, dv, Cp.data(), Ri.data(), P0ip.data(), P0im0.data())
+             : dispatch_nl<double>(kr, nl->kind, dt, mu, dv, Cp.data(), Ri.data(), P0ip.data(), P0im0.data());
   }
   if (!rn) return MAP_E_UNSUPPORTED;
   p->runner.reset(rn);
@@ -491,7 +493,7 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
   return finish(*p, blocking, outs);
 }
 
-map_status map_two_filter(map_plan_t p, const void* y, void* x_map) {
+map_status map_two_filter(map_plan_t p, const void* y, void* x_map, void* smooth_P) {
   if (!p || !y || !x_map) return MAP_E_ARG;
   if (p->kind == Kind::NL || p->d.world != 1) {
     p->err = "map_two_filter needs a linear single-GPU plan";
@@ -502,14 +504,60 @@ map_status map_two_filter(map_plan_t p, const void* y, void* x_map) {
   const Geom& g = p->g;
   const size_t es = p->elem_real;
   const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  const size_t Pb = (size_t)g.batch * g.Nn * (p->d.nx * (p->d.nx + 1) / 2) * es;
   bool blocking = false;
   const void* yd;
-  void* xd;
+  void *xd, *Pd = nullptr;
   map_status st = stage_in(*p, y, yb, &yd, &blocking);
   if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (!st) st = stage_out_buf(*p, smooth_P, Pb, &p->stage_aux, &p->stage_aux_bytes, &Pd, &blocking);
   if (st) return st;
-  p->runner->two_filter(*p, yd, xd);
-  return finish(*p, blocking, {{x_map, {xd, xb}}});
+  p->runner->two_filter(*p, yd, xd, Pd);
+  std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
+  outs.push_back({x_map, {xd, xb}});
+  if (smooth_P) outs.push_back({smooth_P, {Pd, Pb}});
+  return finish(*p, blocking, outs);
+}
+
+map_status map_solve_sequential(map_plan_t p, int32_t method, const void* y, int32_t passes, void* x_map,
+                                void* smooth_P) {
+  if (!p || !y || !x_map || (method != 0 && method != 1)) return MAP_E_ARG;
+  if (p->d.world != 1) {
+    p->err = "map_solve_sequential needs a single-GPU plan (world == 1)";
+    return MAP_E_ARG;
+  }
+  const bool nl = p->kind == Kind::NL;
+  if (nl && (method != 0 || passes < 1)) {
+    p->err = "nonlinear plans: sequential RTS (method 0) with passes >= 1";
+    return MAP_E_ARG;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  const size_t Pb = (size_t)g.batch * g.Nn * (p->d.nx * (p->d.nx + 1) / 2) * es;
+  bool blocking = false;
+  const void* yd;
+  void *xd, *Pd = nullptr;
+  map_status st = stage_in(*p, y, yb, &yd, &blocking);
+  if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (!st) st = stage_out_buf(*p, smooth_P, Pb, &p->stage_aux, &p->stage_aux_bytes, &Pd, &blocking);
+  if (st) return st;
+  if (!nl) {
+    p->runner->sequential(*p, method, yd, nullptr, xd, Pd);
+  } else {  // sequential IEKS: xbar^(0) = m0 (R-INIT), re-linearised every pass
+    p->runner->fill_m0(*p, p->xbuf[0]);
+    for (int k = 0; k < passes; ++k) {
+      void* out = (k == passes - 1) ? xd : p->xbuf[(k + 1) & 1];
+      p->runner->sequential(*p, 0, yd, p->xbuf[k & 1], out, (k == passes - 1) ? Pd : nullptr);
+    }
+  }
+  if (!p->err.empty()) return MAP_E_ARG;
+  std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
+  outs.push_back({x_map, {xd, xb}});
+  if (smooth_P) outs.push_back({smooth_P, {Pd, Pb}});
+  return finish(*p, blocking, outs);
 }
 
 map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, double tol, const void* x_init,

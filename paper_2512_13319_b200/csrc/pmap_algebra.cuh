@@ -896,4 +896,49 @@ PM_INLINE void spd_solve_ldl(const R (&S)[Dim<N>::NS], const R (&v)[N], R (&x)[N
   }
 }
 
+// Packed inverse of a symmetric positive-definite S (covariance P = S^-1 from an
+// information matrix, P:202 / P:509): one LDL^T factorisation, N unit-vector solves.
+template <typename R, int N>
+PM_INLINE void spd_inverse(const R (&S)[Dim<N>::NS], R (&P)[Dim<N>::NS], bool& ok) {
+  R Lm[N][N], D[N], Di[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    R d = S[sidx(j, j, N)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = fma(-Lm[j][k] * D[k], Lm[j][k], d);
+    ok = ok && (d > R(0));
+    D[j] = d;
+    Di[j] = pm_rcp(d);
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      R t = S[sidx(i, j, N)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t = fma(-Lm[i][k] * D[k], Lm[j][k], t);
+      Lm[i][j] = t * Di[j];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    R x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R t = (i == c) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < i; ++k) t = fma(-Lm[i][k], x[k], t);
+      x[i] = t;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] *= Di[i];
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+      R t = x[i];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) t = fma(-Lm[k][i], x[k], t);
+      x[i] = t;
+    }
+#pragma unroll
+    for (int i = 0; i <= c; ++i) P[sidx(i, c, N)] = x[i];
+  }
+}
+
 }  // namespace pmap

@@ -57,12 +57,13 @@ Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, con
 }
 
 template <typename R, int N, int NY, int KIND, int KR>
-Runner* make_nl(double dt, double mu, const double* C, const double* Ri, const double* P0i,
-                       const double* P0im0) {
+Runner* make_nl(double dt, double mu, double om_div, const double* C, const double* Ri, const double* P0i,
+                const double* P0im0) {
   auto* rn = new RunnerT<R, N, NY, SrcNL<R, N, NY, KIND>, KR>();
   auto& s = rn->src;
   s.dt = (R)dt;
   s.mu = (R)mu;
+  s.om_div = om_div != 0.0 ? 1 : 0;
   for (int k = 0; k < Dim<N>::NS; ++k) { s.C[k] = (R)C[k]; s.P0i[k] = (R)P0i[k]; }
   for (int i = 0; i < N; ++i) s.P0im0[i] = (R)P0im0[i];
   for (int a = 0; a < NY; ++a)

@@ -17,6 +17,7 @@
 #include "pmap_kernels.cuh"
 #include "pmap_tf.cuh"
 #include "pmap_lti.cuh"
+#include "pmap_seq.cuh"
 #include <cstdlib>
 #include <type_traits>
 
@@ -125,7 +126,9 @@ struct Runner {
   virtual void phase1(PlanState& p, const void* y, const void* xbar, void* payload) = 0;
   virtual void phase2(PlanState& p, const void* y, const void* xbar, const void* gathered, void* payload) = 0;
   virtual void phase3(PlanState& p, const void* xbar, const void* gathered, void* x, void* fm, void* fP) = 0;
-  virtual void two_filter(PlanState& p, const void* y, void* x) = 0;
+  virtual void two_filter(PlanState& p, const void* y, void* x, void* Ps) = 0;
+  // sequential on-device baseline: method 0 = RTS, 1 = two-filter
+  virtual void sequential(PlanState& p, int method, const void* y, const void* xbar, void* x, void* Ps) = 0;
   virtual void fill_m0(PlanState& p, void* xbar) = 0;
   virtual void maxdiff(PlanState& p, const void* a, const void* b, unsigned long long* out) = 0;
   virtual int sizeof_real() const = 0;
@@ -211,12 +214,12 @@ struct PlanState {
 // kernel classes reported by map_profile_read
 enum KernelId { K_P1_REDUCE = 0, K_P1_REDUCE_EDGE, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_GROUPS,
                 K_P2_DOWN, K_FILTER_OUT, K_TF_REDUCE, K_TF_REDUCE_EDGE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD,
-                K_NL_MISC, K_COUNT };
+                K_NL_MISC, K_SEQ, K_COUNT };
 inline const char* kernel_name(int id) {
   static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_reduce_lti_edge", "k_p1_tiles", "k_p1_groups",
                                        "k_p1_down", "k_p2_tiles", "k_p2_groups", "k_p2_down", "k_filter_out",
                                        "k_tf_reduce", "k_tf_reduce_lti_edge", "k_tf_tiles", "k_tf_groups",
-                                       "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff"};
+                                       "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff", "k_seq_rts/k_seq_tf"};
   return (id >= 0 && id < K_COUNT) ? names[id] : "?";
 }
 
@@ -572,7 +575,7 @@ struct RunnerT : Runner {
 
   // Two-filter (R-TF): pass A = pass-1 kernels without the pass-2 fold on the plan
   // stream; pass B = mirrored suffix scan with the fused combine on a forked stream.
-  void two_filter(PlanState& p, const void* yv, void* xv) override {
+  void two_filter(PlanState& p, const void* yv, void* xv, void* Psv) override {
     if constexpr (Src::HAS_MIRROR) {
       const Geom& g = p.g;
       WsLayout<R, N, K> L;
@@ -610,12 +613,32 @@ struct RunnerT : Runner {
       cudaStreamWaitEvent(s2, p.ev_join, 0);
       PM_LAUNCH(p, s2, K_TF_DOWN,
                 (k_tf_down<R, N, NY, kNT, K, Src><<<ntiles, kNT, smem_down(), s2>>>(
-                    mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, p.dflag,
+                    mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, static_cast<R*>(Psv), p.dflag,
                     (use_lti && tab_m) ? &tab_m->SF[0][0] : nullptr, lti_jlo(g, true), lti_jhi(g))));
       cudaEventRecord(p.ev_fork, s2);
       cudaStreamWaitEvent(s, p.ev_fork, 0);
     } else {
       p.err = "two-filter not available for this model kind";
+    }
+  }
+  void sequential(PlanState& p, int method, const void* yv, const void* xbarv, void* xv, void* Psv) override {
+    const Geom& g = p.g;
+    WsLayout<R, N, K> L;
+    L.plan(g, p.ws_tf);
+    R* ws = reinterpret_cast<R*>(p.ws + L.sv);  // V_i of every node: [Nn][SZ][batch] fits the (S, v) planes
+    const R* y = static_cast<const R*>(yv);
+    const R* xbar = static_cast<const R*>(xbarv);
+    R* x = static_cast<R*>(xv);
+    R* Ps = static_cast<R*>(Psv);
+    cudaStream_t s = p.stream;
+    const unsigned nb = (unsigned)((g.batch + 31) / 32);
+    const unsigned nt = (unsigned)(g.batch < 32 ? g.batch : 32);
+    if (method == 0) {
+      PM_LAUNCH(p, s, K_SEQ, (k_seq_rts<R, N, NY, Src><<<nb, nt, 0, s>>>(src, g, y, xbar, ws, x, Ps, p.dflag)));
+    } else if constexpr (Src::HAS_MIRROR) {
+      PM_LAUNCH(p, s, K_SEQ, (k_seq_tf<R, N, NY, Src><<<nb, nt, 0, s>>>(src, g, y, ws, x, Ps, p.dflag)));
+    } else {
+      p.err = "sequential two-filter not available for this model kind";
     }
   }
   void fill_m0(PlanState& p, void* xbar) override {
@@ -699,7 +722,8 @@ template <typename R, int N, int NY, int KR>
 Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r, const R* Rm,
                 const int64_t* str, int nw, double dt, const double* P0i, const double* P0im0);
 template <typename R, int N, int NY, int KIND, int KR>
-Runner* make_nl(double dt, double mu, const double* C, const double* Ri, const double* P0i, const double* P0im0);
+Runner* make_nl(double dt, double mu, double om_div, const double* C, const double* Ri, const double* P0i,
+                const double* P0im0);
 
 #define PM_SHAPES(X) X(1, 1) X(2, 1) X(2, 2) X(3, 1) X(3, 2) X(4, 2) X(5, 2)
 

@@ -336,6 +336,7 @@ struct SrcNL {
   static constexpr bool HAS_MIRROR = false;
   R dt;
   R mu;           // Van der Pol parameter
+  int om_div = 0;  // keep the OM divergence term 1/2 div f linearised into eta
   R C[NS];        // dt Q, Q = L W L^T
   R Ri[NY][NY];   // R^-1
   R P0i[NS];
@@ -427,6 +428,12 @@ struct SrcNL {
         for (int a = 0; a < NY; ++a) t = fma(Kt[i][a], H[a][j], t);
         e.J[sidx(i, j, N)] = t;
       }
+    }
+    if (KIND == 2 && om_div && !first) {
+      // OM cost of interval i: + dt/2 div f(x_i), div f = mu (1 - x_0^2) for VdP.  Its
+      // Taylor linearisation about xbar_i adds dt/2 grad(div f)(xbar_i)^T x_i to the node
+      // cost, i.e. eta_i -= dt/2 grad(div f) = eta_i + (dt mu xbar_0, 0).
+      e.h[0] = fma(dt * mu, x[0], e.h[0]);
     }
     if (first) {
 #pragma unroll

@@ -10,7 +10,9 @@
 // whose suffix products acc_i = M_i (x) acc_{i+1} carry in (J, eta) the backward
 // information filter (Lam_i, xi_i) of y_i..y_T.  The two filters are combined per
 // node (P:462-466 in information form, C_bar = Lam^-1, b_bar = Lam^-1 xi):
-//   x_i = (S_i + Lam_i - J_i^m)^-1 (v_i + xi_i - eta_i^m)   (y_i counted once, R-TF).
+//   x_i = (S_i + Lam_i - J_i^m)^-1 (v_i + xi_i - eta_i^m)   (y_i counted once, R-TF),
+// and, optionally, the smoother covariance P^s_i = (S_i + Lam_i - J_i^m)^-1 (the
+// posterior precision of x_i is the sum of both filters' information).
 // Pass A (forward filter, the pass-1 kernels without the pass-2 fold) and pass B
 // (this suffix scan, with the combine fused into its epilogue) are independent
 // and run on two streams.
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
                                                 const R* __restrict__ y, const R* __restrict__ run_incl,
                                                 const R* __restrict__ tile_incl, const R* __restrict__ group_carry,
                                                 const R* __restrict__ sv, R* __restrict__ x_out,
-                                                unsigned long long* flag, const R* __restrict__ sf, int64_t j_lo,
+                                                R* __restrict__ Ps_out, unsigned long long* flag, const R* __restrict__ sf, int64_t j_lo,
                                                 int64_t j_hi) {
   using E = Elem<R, N>;
   using V = VF<R, N>;
@@ -101,6 +103,13 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
         spd_solve_ldl<R, N>(Ssum, rhs, xv, ok);
 #pragma unroll
         for (int i = 0; i < N; ++i) xs[r][mm * N + i] = xv[i];
+        if (Ps_out) {  // smoother covariance (S_l + Lam_l - J_l^m)^-1
+          R P[Dim<N>::NS];
+          spd_inverse<R, N>(Ssum, P, ok);
+          R* po = Ps_out + (b * g.Nn + l) * Dim<N>::NS;
+#pragma unroll
+          for (int k = 0; k < Dim<N>::NS; ++k) po[k] = P[k];
+        }
       }
     }
     __syncthreads();

@@ -1,0 +1,164 @@
+"""GPU parity of the SURVEY §8(f) rows built after (a)-(e):
+
+f1  sequential on-device baselines (map_solve_sequential: RTS and two-filter, one
+    thread per trajectory; sequential IEKS for nonlinear plans) vs the CPU oracle;
+f4  smoother covariances (parallel two-filter combine, sequential RTS covariance
+    recursion, sequential two-filter) vs the oracle's textbook RTS covariance
+    recursion (itself pinned to dense Gaussian conditioning, test_oracle_pins P1-cov).
+
+Tolerance as in test_parity_gpu.py: <= 1e-9 relative (inf-norm, per trajectory) in fp64.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+from test_parity_gpu import TOL64, TOL32, gpu_plan, ora_model, random_lti, rel, to_dev, torch_cuda, tv_spec  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def packed(P):
+    """[N, nx, nx] -> [N, nx(nx+1)/2] upper triangle, row-major (include/pmap.h layout)."""
+    nx = P.shape[-1]
+    iu = np.triu_indices(nx)
+    return P[..., iu[0], iu[1]]
+
+
+@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("case", ["wiener", "ou", "tv", "random52"])
+def test_sequential_matches_oracle(torch_cuda, case, method):
+    torch = torch_cuda
+    T = 3001
+    if case == "wiener":
+        spec = wl.wiener_velocity()
+        _, y = wl.simulate_linear(spec, T, seed=4)
+    elif case == "ou":
+        spec = wl.ornstein_uhlenbeck()
+        _, y = wl.simulate_linear(spec, T, seed=5)
+    elif case == "tv":
+        spec = tv_spec(T)
+        y = np.random.default_rng(2).standard_normal((T + 1, spec.ny))
+    else:
+        spec = random_lti(5, 2, seed=52)
+        y = np.random.default_rng(3).standard_normal((T + 1, 2))
+    xo, Po = oracle.kf_rts_cov(ora_model(spec), y, T, spec.t0, spec.tf)
+    plan = gpu_plan(spec, T)
+    nx = spec.nx
+    Pd = torch.empty((1, T + 1, nx * (nx + 1) // 2), dtype=torch.float64, device="cuda")
+    x = plan.solve_sequential(to_dev(torch, y[None]), method=method, smooth_P=Pd)
+    plan.sync()
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    assert rel(Pd[0].cpu().numpy(), packed(Po)) < TOL64
+
+
+def test_sequential_batch_matches_parallel(torch_cuda):
+    """Batched sequential baseline (one thread per trajectory, C5-shaped) = oracle, both methods."""
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    T, B = 2000, 40
+    _, y = wl.simulate_linear(spec, T, seed=12, batch=B)
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
+    plan = gpu_plan(spec, T, batch=B)
+    yd = to_dev(torch, y)
+    for method in (0, 1):
+        x = plan.solve_sequential(yd, method=method).cpu().numpy()
+        for b in range(B):
+            assert rel(x[b], xo[b]) < TOL64
+
+
+@pytest.mark.parametrize("case", ["wiener", "tv", "c5_small_batch"])
+def test_parallel_two_filter_smoother_covariance(torch_cuda, case):
+    torch = torch_cuda
+    if case == "c5_small_batch":
+        spec = wl.wiener_velocity()
+        T, B = 10_000, 3
+        _, y = wl.simulate_linear(spec, T, seed=21, batch=B)
+    else:
+        T, B = 5000, 1
+        if case == "wiener":
+            spec = wl.wiener_velocity()
+            _, y = wl.simulate_linear(spec, T, seed=7)
+        else:
+            spec = tv_spec(T)
+            y = np.random.default_rng(8).standard_normal((T + 1, spec.ny))
+        y = y[None]
+    nx = spec.nx
+    plan = gpu_plan(spec, T, batch=B)
+    Pd = torch.empty((B, T + 1, nx * (nx + 1) // 2), dtype=torch.float64, device="cuda")
+    x = plan.two_filter(to_dev(torch, y), smooth_P=Pd)
+    plan.sync()
+    for b in range(B):
+        xo, Po = oracle.kf_rts_cov(ora_model(spec), y[b], T, spec.t0, spec.tf)
+        assert rel(x[b].cpu().numpy(), xo) < TOL64
+        assert rel(Pd[b].cpu().numpy(), packed(Po)) < TOL64
+
+
+def test_sequential_fp32(torch_cuda):
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 4000
+    _, y = wl.simulate_linear(spec, T, seed=31)
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    plan = gpu_plan(spec, T, dtype="f32")
+    for method in (0, 1):
+        x = plan.solve_sequential(to_dev(torch, y[None], torch.float32), method=method)
+        assert rel(x[0].cpu().numpy(), xo) < TOL32
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_sequential_ieks(torch_cuda, kind):
+    """Sequential on-device IEKS (f1, the paper's nonlinear comparison P:625) = oracle per iterate."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    T = 2500
+    s = wl.coordinated_turn() if kind == 1 else wl.van_der_pol()
+    _, y = wl.simulate_nonlinear(s, T, seed=3)
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=kind,
+                   params=s.params)
+    yd = to_dev(torch, y[None])
+    for passes in (1, 4):
+        xo, _ = oracle.ieks(kind, s.params, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=passes)
+        x = plan.solve_sequential(yd, method=0, passes=passes)
+        assert rel(x[0].cpu().numpy(), xo) < TOL64
+        xp, _ = plan.solve_nonlinear(yd, passes=passes)
+        assert rel(xp[0].cpu().numpy(), x[0].cpu().numpy()) < TOL64
+
+
+def test_sequential_errors(torch_cuda):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = wl.coordinated_turn()
+    T = 100
+    _, y = wl.simulate_nonlinear(s, T, seed=1)
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1)
+    with pytest.raises(pm.MapError):  # no sequential two-filter for nonlinear plans
+        plan.solve_sequential(to_dev(torch, y[None]), method=1)
+    spec = wl.wiener_velocity()
+    lp = gpu_plan(spec, T)
+    with pytest.raises(pm.MapError):
+        lp.solve_sequential(to_dev(torch, np.zeros((1, T + 1, 2))), method=2)
+
+
+@pytest.mark.parametrize("T", [3000, 100_000])
+def test_vdp_om_divergence(torch_cuda, T):
+    """f3: Van der Pol with the OM divergence term (params = [mu, 1]) = oracle per iterate
+    (parallel and sequential); the term changes the answer (it is not silently dropped)."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = wl.van_der_pol(mu=1.5)
+    _, y = wl.simulate_nonlinear(s, T, seed=17)
+    yd = to_dev(torch, y[None])
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=2,
+                   params=np.array([1.5, 1.0]))
+    plan0 = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=2,
+                    params=np.array([1.5]))
+    for passes in (2, 10):
+        xo, _ = oracle.ieks(2, [1.5, 1.0], s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=passes)
+        x, _ = plan.solve_nonlinear(yd, passes=passes)
+        assert rel(x[0].cpu().numpy(), xo) < TOL64
+        xs = plan.solve_sequential(yd, method=0, passes=passes)
+        assert rel(xs[0].cpu().numpy(), xo) < TOL64
+    x0, _ = plan0.solve_nonlinear(yd, passes=10)
+    assert rel(x0[0].cpu().numpy(), xo) > 1e-6

@@ -113,6 +113,34 @@ def test_P1_dense_conditioning(case):
         assert rel_inf(fP[i], P_i) < 1e-10
 
 
+@pytest.mark.parametrize("case", ["wiener", "tv_offsets", "ou"])
+def test_P1_smoother_covariance_dense(case):
+    """P1-cov -- oracle RTS smoother covariances = the exact posterior
+    covariance Cov[x_i | y_0..y_T] of the discrete model by dense conditioning."""
+    T, t0, tf = 40, 0.0, 2.0
+    if case == "wiener":
+        s = wl.wiener_velocity()
+        md = oracle.LinearModel(s.F, s.L, s.W, s.H, s.R, s.m0, s.P0)
+        _, y = wl.simulate_linear(s, T, seed=1)
+    elif case == "ou":
+        s = wl.ornstein_uhlenbeck()
+        md = oracle.LinearModel(s.F, s.L, s.W, s.H, s.R, s.m0, s.P0)
+        _, y = wl.simulate_linear(s, T, seed=2)
+    else:
+        md = tv_model(T)
+        y = np.random.default_rng(5).standard_normal((T + 1, md.ny))
+    x, Ps = oracle.kf_rts_cov(md, y, T, t0, tf)
+    assert rel_inf(x, oracle.kf_rts(md, y, T, t0, tf)) == 0.0
+    SX, Hb, SY, mu, my = dense_conditioning(md, y, T, t0, tf)
+    post_cov = SX - SX @ Hb.T @ np.linalg.solve(SY, Hb @ SX)
+    nx = md.nx
+    for i in range(T + 1):
+        blk = post_cov[i * nx:(i + 1) * nx, i * nx:(i + 1) * nx]
+        assert np.abs(Ps[i] - blk).max() <= 1e-11 * np.abs(blk).max(), i
+        assert np.array_equal(Ps[i], Ps[i].T)
+        assert np.linalg.eigvalsh(Ps[i]).min() > 0
+
+
 def test_P2_discretised_objective_minimiser():
     """P2 -- x_map minimises the discretised OM/LQT objective
     J(x) = 1/2|x0-m0|^2_{P0^-1} + sum_i 1/2|x_{i-1} - A_i x_i - b_i|^2_{(dt Q_i)^-1}
@@ -360,6 +388,44 @@ def test_P11_ieks_fixed_point_is_stationary():
     scale = np.abs(np.linalg.inv(dt * L @ L.T)).max() * np.abs(x).max()
     assert g.abs().max().item() < 1e-9 * scale
 
+
+@pytest.mark.parametrize("om_div", [0.0, 1.0])
+def test_P12_om_divergence_fixed_point_is_stationary(om_div):
+    """P12 -- with params = [mu, 1] the iterated-linearisation fixed point is a
+    stationary point of the discretised Onsager--Machlup functional INCLUDING the
+    divergence term 1/2 int div f dt, sum_{i>=1} dt/2 mu (1 - x_{i,0}^2) for Van der
+    Pol; with params = [mu, 0] it is stationary for the functional without it (IEKS),
+    and each is NOT stationary for the other (so a dropped term or a sign error fails).
+    Full-rank diffusion so the objective is unconstrained; torch autograd."""
+    import torch
+    s = wl.van_der_pol()
+    mu = 1.5
+    L = np.diag([0.3, 1.0])
+    W = np.array([[0.5]])[0, 0] * np.eye(2)
+    T, tf = 200, 2.0
+    spec = wl.models.NonlinearSpec("vdp", 2, 2, 1, L, W, s.R, s.m0, s.P0, params=np.array([mu]), tf=tf)
+    _, y = wl.simulate_nonlinear(spec, T, seed=9)
+    x, delta = oracle.ieks(2, [mu, om_div], L, W, s.R, s.m0, s.P0, y, T, 0.0, tf, passes=40)
+    assert delta[-1] < 1e-11
+    dt = tf / T
+    X = torch.tensor(x, requires_grad=True)
+    Y = torch.tensor(y).reshape(T + 1, 1)
+    Qi = torch.tensor(np.linalg.inv(dt * L @ W @ L.T))
+    Ri = torch.tensor(dt * np.linalg.inv(s.R))
+    P0i = torch.tensor(np.linalg.inv(s.P0))
+    m0 = torch.tensor(s.m0)
+    f = torch.stack([X[:, 1], mu * (1 - X[:, 0] ** 2) * X[:, 1] - X[:, 0]], 1)
+    e = X[:-1] - X[1:] + dt * f[1:]
+    res = Y - X[:, :1]
+    d0 = X[0] - m0
+    J = 0.5 * d0 @ P0i @ d0 + 0.5 * torch.einsum("ia,ab,ib->", e, Qi, e) + 0.5 * torch.einsum("ia,ab,ib->", res, Ri, res)
+    div = 0.5 * dt * torch.sum(mu * (1 - X[1:, 0] ** 2))
+    scale = np.abs(Qi.numpy()).max() * np.abs(x).max()
+    (g_with,) = torch.autograd.grad(J + div, X, retain_graph=True)
+    (g_without,) = torch.autograd.grad(J, X)
+    g_ok, g_other = (g_with, g_without) if om_div else (g_without, g_with)
+    assert g_ok.abs().max().item() < 1e-9 * scale
+    assert g_other.abs().max().item() > 1e-6 * scale
 
 def test_golden_model_parameters():
     """The workload generator uses the paper's printed parameters."""
