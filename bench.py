@@ -35,12 +35,15 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 # ----------------------------------------------------------- algorithmic counts
-def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zero_b: bool = False):
+def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zero_b: bool = False,
+               euler_n: int = 0):
     """Algorithmic FP64 flops (FMA = 2) and HBM bytes per node of each kernel class
     (DESIGN.md section 6): the arithmetic each kernel's per-node recurrence performs
     in this decomposition, excluding the intra-tile scan overheads (Kogge-Stone
     rounds, carries), which are implementation cost.  nw > 0: low-rank diffusion
-    (R-LOWRANK node update, R-P2REC pass-2 records of nw (nx + 1) values)."""
+    (R-LOWRANK node update, R-P2REC pass-2 records of nw (nx + 1) values).  euler_n > 0:
+    Euler blocks (R-EULER): y rows of euler_n * ny values, element data parts b, eta built
+    from them (2 * nx * euler_n * ny FMA per build: reduce, down; nx * euler_n * ny in pass 2)."""
     N = nx
     lu = sum((N - k - 1) + (N - k - 1) ** 2 for k in range(N))
     solve = N * N
@@ -66,6 +69,16 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
             vsz2 = r * (N + 1)
             vapply += r * N  # U^T v
             trans = N * N + N * r + chol + r * N + r * r + N * r
+    if euler_n > 0:
+        ny_row = euler_n * ny
+        build = 2 * N * ny_row
+        return {
+            "k_p1_reduce": (2 * (combine + build), d * (ny_row + esz / K)),
+            "k_p1_down": (2 * (vapply + build + vapply_tr / K), d * (ny_row + esz / K + vsz + asz / K)),
+            "k_p2_down": (2 * (trans + build // 2), d * (ny_row + vsz + nx + asz / K)),
+            "solve": (2 * (combine + 2 * build + vapply + vapply_tr / K + trans + build // 2),
+                      d * (3 * ny_row + 2 * vsz + nx)),
+        }
     return {
         "k_p1_reduce": (2 * reduce_fl, d * (ny + esz / K)),
         "k_p1_down": (2 * (vapply + vapply_tr / K), d * (ny + esz / K + vsz2 + asz / K)),
@@ -124,12 +137,12 @@ def build_inputs(config: str, rank: int, world: int):
     return spec, np.ascontiguousarray(y[:, a0:a1]), T, B
 
 
-def make_plan(pm, spec, T, B, rank, world, comm):
+def make_plan(pm, spec, T, B, rank, world, comm, substeps=1):
     import workloads as wl
     if isinstance(spec, wl.LinearSpec):
         return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H,
                        r=spec.r, R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, rank=rank, world=world,
-                       nccl_comm=comm)
+                       nccl_comm=comm, substeps=substeps)
     return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, L=spec.L, W=spec.W, R=spec.R, m0=spec.m0, P0=spec.P0,
                    nl_kind=spec.kind, params=spec.params, batch=B, rank=rank, world=world, nccl_comm=comm)
 
@@ -148,7 +161,8 @@ def solve_fn(plan, config):
 def workload_name(config, T, B):
     from workloads.models import CONFIGS
     c = CONFIGS[config]
-    return f"{config}: {c['model']} {c['method']} T={T} batch={B}" + (f" passes={c['passes']}" if "passes" in c else "")
+    return (f"{config}: {c['model']} {c['method']} T={T} batch={B}" + (f" passes={c['passes']}" if "passes" in c else "")
+            + (f" euler_substeps={c['substeps']} (T blocks, n*T fine steps)" if "substeps" in c else ""))
 
 
 # ---------------------------------------------------------------- CPU oracle
@@ -168,6 +182,13 @@ def oracle_sample(config: str, budget_s: float = 12.0):
         return T / dt, 1, f"coordinated turn T={T}, {c['passes']} passes, 1 thread (full run is T={c['T']})"
     spec = wl.wiener_velocity() if c["model"] == "wiener_velocity" else wl.ornstein_uhlenbeck()
     md = oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0)
+    if "substeps" in c:
+        n, T = c["substeps"], c["T"]
+        _, yf = wl.simulate_linear(spec, n * T, seed=0)
+        t = time.perf_counter()
+        oracle.euler_rts(md, yf, T, n, spec.t0, spec.tf)
+        dt = time.perf_counter() - t
+        return T / dt, 1, f"Euler blocks T={T} x n={n} (full workload), sequential, 1 thread"
     if c["method"] == "two_filter":
         B, T = 64, c["T"]
         _, y = wl.simulate_linear(spec, T, seed=0, batch=B)
@@ -200,6 +221,12 @@ def run_reference(args):
         step = lambda: oracle.ieks(1, None, spec.L, spec.W, spec.R, spec.m0, spec.P0, y, T, spec.t0, spec.tf,
                                    passes=c["passes"])
         units, cores, sample = T, 1, f"coordinated turn T={T} x {c['passes']} passes per step"
+    elif "substeps" in c:
+        n, T = c["substeps"], c["T"]
+        md = oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0)
+        _, yf = wl.simulate_linear(spec, n * T, seed=0)
+        step = lambda: oracle.euler_rts(md, yf, T, n, spec.t0, spec.tf)
+        units, cores, sample = T, 1, f"Euler blocks T={T} x n={n} per step (full workload), sequential"
     elif c["method"] == "two_filter":
         B, T = 32, c["T"]
         md = oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0)
@@ -262,7 +289,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5", "C2E"])
     ap.add_argument("--impl", default="pmap", choices=["pmap", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -288,8 +315,10 @@ def main():
         comm = be._comm_ptr()
     import paper_2512_13319_b200 as pm
 
+    from workloads.models import CONFIGS
+    substeps = CONFIGS[args.config].get("substeps", 1)
     spec, y_host, T, B = build_inputs(args.config, rank, world)
-    plan = make_plan(pm, spec, T, B, rank, world, comm)
+    plan = make_plan(pm, spec, T, B, rank, world, comm, substeps)
     solve = solve_fn(plan, args.config)
     dev = torch.device("cuda", local)
     yd = torch.from_numpy(y_host).to(dev)
@@ -360,7 +389,10 @@ def main():
             and os.environ.get("PMAP_GENERAL") != "1"):
         lowrank = spec.L.shape[1]
     zero_b = isinstance(spec, wl.LinearSpec) and (spec.c is None or not np.any(spec.c))
-    counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank, zero_b=zero_b)
+    if substeps > 1:  # Euler blocks: general kernels, element build from n*ny measurements
+        counts = alg_counts(plan.nx, plan.ny, lti=False, euler_n=substeps)
+    else:
+        counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank, zero_b=zero_b)
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl

@@ -83,7 +83,16 @@ typedef struct {
   int64_t batch;       /* independent trajectories sharing the model (>= 1) */
   double t0, tf;       /* time span [t0, tf], tf > t0 */
   int32_t rank, world; /* time shard index / count (world == 1: single GPU) */
-  int32_t reserved0;
+  int32_t substeps;    /* 0 or 1: one exact element per grid interval (DESIGN.md R-ELEM).
+                          n > 1: the paper's Euler blocks (DESIGN.md R-EULER):
+                          each interval is n explicit Euler substeps of the element ODEs
+                          P:416-427 (dA/ds sign corrected) with a measurement at
+                          every substep, so y rows hold n*ny values ([batch][T+1][n][ny],
+                          block i's substep k = fine time t_{i-1} + (k+1) dt/n; row 0 holds
+                          y(t_0) in its last sub-slot).  LTI linear models, world == 1, RTS
+                          form (map_solve_linear / map_solve_sequential); compiled for n = 10
+                          at (nx, ny) = (1, 1), (4, 2) (else MAP_E_UNSUPPORTED).  x_map is
+                          returned at the block boundaries t_i. */
   int32_t reserved1;
   void* nccl_comm;     /* ncclComm_t borrowed from the caller (e.g. torch's
                           ProcessGroupNCCL._comm_ptr()); NULL when world == 1, or

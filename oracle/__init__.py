@@ -54,6 +54,7 @@ def _lib(long_double: bool = False):
         lib.ora_kf_rts.argtypes = [ctypes.POINTER(OraModel), P, P, P, P]
         lib.ora_two_filter.argtypes = [ctypes.POINTER(OraModel), P, P]
         lib.ora_kf_rts_cov.argtypes = [ctypes.POINTER(OraModel), P, P, P]
+        lib.ora_euler_rts.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P, ctypes.c_int]
         lib.ora_batch.argtypes = [ctypes.POINTER(OraModel), ctypes.c_long, P, P, ctypes.c_int]
         lib.ora_ieks.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long,
                                  ctypes.c_double, ctypes.c_double, P, P, P, P, P, P, ctypes.c_int, P, P, P]
@@ -148,6 +149,21 @@ def kf_rts_cov(model: LinearModel, y, T: int, t0: float, tf: float, long_double:
     if rc:
         raise FloatingPointError(f"oracle kf_rts_cov failed rc={rc}")
     return x, P
+
+
+def euler_rts(model: LinearModel, y_fine, T: int, nsub: int, t0: float, tf: float, g6_printed: bool = False,
+              long_double: bool = False):
+    """Paper-faithful Euler blocks: T blocks of nsub explicit Euler
+    substeps of the element ODEs P:416-427, sequential value-function fold and RTS
+    transitions.  y_fine [nsub*T+1, ny]; returns x_map [T+1, nx] at the block boundaries.
+    g6_printed: use the printed dA/ds = -A Q J^T - A F -- pins only."""
+    y = _f64(y_fine).reshape(nsub * T + 1, model.ny)
+    x = np.empty((T + 1, model.nx))
+    s = model._struct(T, t0, tf)
+    rc = _lib(long_double).ora_euler_rts(ctypes.byref(s), nsub, _ptr(y), _ptr(x), 1 if g6_printed else 0)
+    if rc:
+        raise FloatingPointError(f"oracle euler_rts failed rc={rc}")
+    return x
 
 
 def two_filter(model: LinearModel, y, T: int, t0: float, tf: float, long_double: bool = False):

@@ -531,6 +531,164 @@ int ora_ieks(int kind, const double* params, int nx, int ny, int nw, long T, dou
   return rc;
 }
 
+/* ------------------------------------------------------------------------
+ * Paper-faithful Euler blocks (DESIGN.md R-EULER).  Followed step by
+ * step in the paper's order and notation:
+ *  1. each grid interval (t_{i-1}, t_i], i = 1..T, is a block; its conditional value
+ *     function element (A, b, C, eta, J) is obtained by n explicit Euler substeps in s of
+ *     the backward ODEs P:416-427 from the boundary A = I, b = C = eta = J = 0,
+ *     with F~ = -F, c~ = -c, Q~ = Q and dA/ds = A Q~ J - A F~
+ *     (the printed -A Q~ J^T is kept behind `g6_printed` only so the pins can
+ *     show that they detect it).  Substep k uses y at the fine time t_{i-1} + (k+1) delta.
+ *  2. the terminal element a_T at node 0: (0, 0, 0, P0^-1 m0 + delta H^T R^-1 (y_0 - r),
+ *     P0^-1 + delta H^T R^-1 H);
+ *  3. value functions at the block boundaries, V_i = E_i (x) V_{i-1} (P:333-336 with the
+ *     combination rule P:395-407, right operand a value function), sequentially;
+ *  4. x_T = S_T^-1 v_T, x_{i-1} = (I + C_i S_{i-1})^-1 (A_i x_i + b_i + C_i v_{i-1})
+ *     (DESIGN.md R-TRANS).
+ * y_fine: [n T + 1][ny]; x_map: [T + 1][nx] at the block boundaries.  LTI models only. */
+static void mm_(int n, const REAL* X, const REAL* Y, REAL* Z) { mat_mul(n, n, n, X, Y, Z); }
+
+int ora_euler_rts(const ora_model* md, int nsub, const double* y_fine, double* x_map, int g6_printed) {
+  int nx = md->nx, ny = md->ny;
+  long T = md->T, N = T + 1;
+  if (nx > MAXN || ny > MAXN || md->nw > MAXN || T < 1 || nsub < 1 || md->g || md->sF || md->sc || md->sL ||
+      md->sW || md->sH || md->sr || md->sR)
+    return 2;
+  REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)T, de = dt / nsub;
+  node_model nm;
+  model_at(md, 0, &nm);
+  REAL Ft[MAXN * MAXN], ct[MAXN], Ri[MAXN * MAXN], HRi[MAXN * MAXN], HRH[MAXN * MAXN];
+  for (int a = 0; a < nx * nx; ++a) Ft[a] = -nm.F[a];
+  for (int a = 0; a < nx; ++a) ct[a] = -nm.c[a];
+  for (int a = 0; a < ny * ny; ++a) Ri[a] = (a % (ny + 1) == 0) ? 1 : 0;
+  { REAL Rc[MAXN * MAXN]; memcpy(Rc, nm.R, sizeof Rc); if (lu_solve(ny, ny, Rc, Ri)) return 1; }
+  for (int a = 0; a < nx; ++a)            /* H^T R^-1 (nx x ny) */
+    for (int q = 0; q < ny; ++q) {
+      REAL s = 0;
+      for (int l = 0; l < ny; ++l) s += nm.H[l * nx + a] * Ri[l * ny + q];
+      HRi[a * ny + q] = s;
+    }
+  mat_mul(nx, ny, nx, HRi, nm.H, HRH);
+  REAL* EA = malloc(sizeof(REAL) * N * nx * nx);
+  REAL* Eb = malloc(sizeof(REAL) * N * nx);
+  REAL* EC = malloc(sizeof(REAL) * N * nx * nx);
+  REAL* Vs = malloc(sizeof(REAL) * N * nx * nx);
+  REAL* Vv = malloc(sizeof(REAL) * N * nx);
+  REAL* xs = malloc(sizeof(REAL) * N * nx);
+  int rc = (!EA || !Eb || !EC || !Vs || !Vv || !xs) ? 3 : 0;
+  /* node 0: a_T of P:329 plus the measurement at t_0 */
+  if (!rc) {
+    REAL P0[MAXN * MAXN], P0i[MAXN * MAXN], m0[MAXN], e[MAXN];
+    load(nx * nx, md->P0, P0);
+    load(nx, md->m0, m0);
+    for (int a = 0; a < nx * nx; ++a) P0i[a] = (a % (nx + 1) == 0) ? 1 : 0;
+    if (lu_solve(nx, nx, P0, P0i)) rc = 1;
+    for (int q = 0; q < ny; ++q) e[q] = (REAL)y_fine[q] - nm.r[q];
+    for (int a = 0; a < nx && !rc; ++a) {
+      REAL s = 0;
+      for (int c = 0; c < nx; ++c) s += P0i[a * nx + c] * m0[c];
+      for (int q = 0; q < ny; ++q) s += de * HRi[a * ny + q] * e[q];
+      Vv[a] = s;                                   /* V_0 = E_0 (x) 0: v_0 = eta_0, S_0 = J_0 */
+      for (int c = 0; c < nx; ++c) Vs[a * nx + c] = P0i[a * nx + c] + de * HRH[a * nx + c];
+    }
+    symmetrize(nx, Vs);
+  }
+  for (long i = 1; i <= T && !rc; ++i) {
+    /* 1. block element by n Euler substeps of P:416-427 (backwards in s from the boundary) */
+    REAL A[MAXN * MAXN], b[MAXN] = {0}, C[MAXN * MAXN] = {0}, eta[MAXN] = {0}, J[MAXN * MAXN] = {0};
+    for (int a = 0; a < nx * nx; ++a) A[a] = (a % (nx + 1) == 0) ? 1 : 0;
+    for (int k = 0; k < nsub; ++k) {
+      const double* yk = y_fine + ((i - 1) * nsub + k + 1) * ny;
+      REAL AQ[MAXN * MAXN], JQ[MAXN * MAXN], t1[MAXN * MAXN], t2[MAXN * MAXN], JT[MAXN * MAXN];
+      REAL dA[MAXN * MAXN], db[MAXN], dC[MAXN * MAXN], deta[MAXN], dJ[MAXN * MAXN], u[MAXN];
+      mm_(nx, A, nm.Q, AQ);
+      mm_(nx, J, nm.Q, JQ);
+      for (int a = 0; a < nx; ++a)
+        for (int c = 0; c < nx; ++c) JT[a * nx + c] = J[c * nx + a];
+      mm_(nx, AQ, g6_printed ? JT : J, t1);
+      mm_(nx, A, Ft, t2);
+      for (int a = 0; a < nx * nx; ++a) dA[a] = (g6_printed ? -t1[a] : t1[a]) - t2[a];   /* dA/ds */
+      mat_vec(nx, nx, AQ, eta, u);
+      mat_vec(nx, nx, A, ct, db);
+      for (int a = 0; a < nx; ++a) db[a] = -u[a] - db[a];                               /* db/ds */
+      mat_mul_bt(nx, nx, nx, AQ, A, dC);
+      for (int a = 0; a < nx * nx; ++a) dC[a] = -dC[a];                                 /* dC/ds */
+      for (int a = 0; a < nx; ++a) {                                                    /* deta/ds */
+        REAL s = 0;
+        for (int c = 0; c < nx; ++c) s += JQ[a * nx + c] * eta[c] - Ft[c * nx + a] * eta[c] + J[a * nx + c] * ct[c];
+        for (int q = 0; q < ny; ++q) s -= HRi[a * ny + q] * ((REAL)yk[q] - nm.r[q]);
+        deta[a] = s;
+      }
+      mm_(nx, JQ, J, t1);                                                               /* dJ/ds */
+      mm_(nx, J, Ft, t2);
+      for (int a = 0; a < nx; ++a)
+        for (int c = 0; c < nx; ++c) {
+          REAL s = t1[a * nx + c] - t2[a * nx + c] - HRH[a * nx + c];
+          for (int l = 0; l < nx; ++l) s -= Ft[l * nx + a] * J[l * nx + c];
+          dJ[a * nx + c] = s;
+        }
+      for (int a = 0; a < nx * nx; ++a) { A[a] -= de * dA[a]; C[a] -= de * dC[a]; J[a] -= de * dJ[a]; }
+      for (int a = 0; a < nx; ++a) { b[a] -= de * db[a]; eta[a] -= de * deta[a]; }
+    }
+    symmetrize(nx, C);
+    symmetrize(nx, J);
+    memcpy(EA + i * nx * nx, A, sizeof(REAL) * nx * nx);
+    memcpy(Eb + i * nx, b, sizeof(REAL) * nx);
+    memcpy(EC + i * nx * nx, C, sizeof(REAL) * nx * nx);
+    /* 3. V_i = E_i (x) V_{i-1}:  S = A^T S (I + C S)^-1 A + J,  v = A^T (I + S C)^-1 (v - S b) + eta */
+    const REAL* S = Vs + (i - 1) * nx * nx;
+    const REAL* v = Vv + (i - 1) * nx;
+    REAL M[MAXN * MAXN], Mt[MAXN * MAXN], X[MAXN * MAXN], w[MAXN * MAXN], Sb[MAXN], t[MAXN * MAXN];
+    mm_(nx, C, S, M);
+    for (int a = 0; a < nx * nx; ++a) M[a] += (a % (nx + 1) == 0) ? 1 : 0;               /* I + C S */
+    for (int a = 0; a < nx; ++a)
+      for (int c = 0; c < nx; ++c) Mt[a * nx + c] = M[c * nx + a];                      /* I + S C */
+    memcpy(X, A, sizeof A);
+    if (lu_solve(nx, nx, M, X)) { rc = 1; break; }                                      /* (I + C S)^-1 A */
+    mm_(nx, S, X, t);
+    for (int a = 0; a < nx; ++a)
+      for (int c = 0; c < nx; ++c) {
+        REAL s = J[a * nx + c];
+        for (int l = 0; l < nx; ++l) s += A[l * nx + a] * t[l * nx + c];
+        Vs[i * nx * nx + a * nx + c] = s;
+      }
+    symmetrize(nx, Vs + i * nx * nx);
+    mat_vec(nx, nx, S, b, Sb);
+    for (int a = 0; a < nx; ++a) w[a] = v[a] - Sb[a];
+    if (lu_solve(nx, 1, Mt, w)) { rc = 1; break; }
+    for (int a = 0; a < nx; ++a) {
+      REAL s = eta[a];
+      for (int l = 0; l < nx; ++l) s += A[l * nx + a] * w[l];
+      Vv[i * nx + a] = s;
+    }
+  }
+  /* 4. x_T = S_T^-1 v_T, then the transitions backwards */
+  if (!rc) {
+    REAL Sc[MAXN * MAXN], xv[MAXN];
+    memcpy(Sc, Vs + T * nx * nx, sizeof(REAL) * nx * nx);
+    memcpy(xv, Vv + T * nx, sizeof(REAL) * nx);
+    if (chol_solve(nx, 1, Sc, xv)) rc = 1;
+    memcpy(xs + T * nx, xv, sizeof(REAL) * nx);
+  }
+  for (long i = T; i >= 1 && !rc; --i) {
+    const REAL* S = Vs + (i - 1) * nx * nx;
+    const REAL* v = Vv + (i - 1) * nx;
+    const REAL *A = EA + i * nx * nx, *b = Eb + i * nx, *C = EC + i * nx * nx;
+    REAL M[MAXN * MAXN], r_[MAXN], Ax[MAXN], Cv[MAXN];
+    mm_(nx, C, S, M);
+    for (int a = 0; a < nx * nx; ++a) M[a] += (a % (nx + 1) == 0) ? 1 : 0;
+    mat_vec(nx, nx, A, xs + i * nx, Ax);
+    mat_vec(nx, nx, C, v, Cv);
+    for (int a = 0; a < nx; ++a) r_[a] = Ax[a] + b[a] + Cv[a];
+    if (lu_solve(nx, 1, M, r_)) { rc = 1; break; }
+    memcpy(xs + (i - 1) * nx, r_, sizeof(REAL) * nx);
+  }
+  if (!rc) store(N * nx, xs, x_map);
+  free(EA); free(Eb); free(EC); free(Vs); free(Vv); free(xs);
+  return rc;
+}
+
 /* Batched linear MAP: `batch` independent trajectories sharing the model;
  * y: [batch][T+1][ny], x_map: [batch][T+1][nx].  mode 0 = RTS, 1 = two-filter.
  * OpenMP over trajectories (each recursion is sequential).  Returns the

@@ -37,7 +37,7 @@ class MapError(RuntimeError):
 class PlanDesc(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nw", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("T", ctypes.c_int64), ("batch", ctypes.c_int64), ("t0", ctypes.c_double), ("tf", ctypes.c_double),
-                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("substeps", ctypes.c_int32),
                 ("reserved1", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
@@ -179,6 +179,19 @@ def map_version() -> str:
 
 
 # ------------------------------------------------------------------ convenience
+def euler_rows(y_fine: np.ndarray, n: int) -> np.ndarray:
+    """Lay out fine-grid measurements [..., n*T+1, ny] as the Euler-block rows
+    [..., T+1, n*ny] of include/pmap.h (row 0: y(t_0) in its last sub-slot).  Layout only."""
+    y_fine = np.asarray(y_fine)
+    *lead, nf, ny = y_fine.shape
+    T = (nf - 1) // n
+    assert nf == n * T + 1, "fine grid must have n*T+1 points"
+    out = np.zeros((*lead, T + 1, n, ny), dtype=y_fine.dtype)
+    out[..., 0, n - 1, :] = y_fine[..., 0, :]
+    out[..., 1:, :, :] = y_fine[..., 1:, :].reshape(*lead, T, n, ny)
+    return out.reshape(*lead, T + 1, n * ny)
+
+
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
@@ -189,11 +202,13 @@ class Plan:
     linear model: pass F, L, W, H, R, m0, P0 (and optionally c, r); each array is
     either constant or carries a leading node axis of length T+1 (time-varying).
     nonlinear model: pass nl_kind (1 = coordinated turn, 2 = Van der Pol), L, W, R,
-    m0, P0 and params."""
+    m0, P0 and params.  substeps = n > 1: the paper's Euler blocks (include/pmap.h), y
+    as [batch][T+1][n*ny] (see euler_rows)."""
 
     def __init__(self, *, T: int, t0: float, tf: float, m0, P0, L, W, R, F=None, H=None, c=None, r=None,
                  batch: int = 1, dtype: str = "f64", nl_kind: int | None = None, params=None,
-                 rank: int = 0, world: int = 1, nccl_comm: int | None = None, stream: int | None = None):
+                 rank: int = 0, world: int = 1, nccl_comm: int | None = None, stream: int | None = None,
+                 substeps: int = 1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2512_13319_b200 needs a CUDA device (no CPU fallback)")
@@ -208,6 +223,8 @@ class Plan:
         d.nx, d.ny, d.nw, d.dtype = nx, ny, nw, MAP_F64 if dtype == "f64" else MAP_F32
         d.T, d.batch, d.t0, d.tf = T, batch, t0, tf
         d.rank, d.world = rank, world
+        d.substeps = substeps
+        self.substeps = substeps
         d.nccl_comm = nccl_comm
         self.stream = torch.cuda.current_stream().cuda_stream if stream is None else stream
         d.stream = self.stream

@@ -23,6 +23,9 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-diag-suppres
 SHAPES = [(1, 1), (2, 1), (2, 2), (3, 1), (3, 2), (4, 2), (5, 2)]
 
 
+EULER_SHAPES = [(1, 1), (4, 2)]  # OU (C1) and Wiener velocity
+EULER_NSUB = 10                  # substeps per block
+
 RUN_LENGTHS = (32, 8)  # nodes per run (tile = 64 runs): large / small problems
 
 
@@ -38,6 +41,9 @@ def units(f64_only: bool = False):
                                 base + [f"-DPM_NX={nx}", f"-DPM_NY={ny}", f"-DPM_KIND={kind}"], "inst.cu"))
             out.append((f"inst_{tag}_K{K}_ct", base + ["-DPM_NX=5", "-DPM_NY=2", "-DPM_KIND=2"], "inst.cu"))
             out.append((f"inst_{tag}_K{K}_vdp", base + ["-DPM_NX=2", "-DPM_NY=1", "-DPM_KIND=3"], "inst.cu"))
+            for nx, ny in EULER_SHAPES:  # paper-faithful Euler blocks
+                out.append((f"inst_{tag}_K{K}_eu{nx}{ny}", base + [f"-DPM_NX={nx}", f"-DPM_NY={ny}", "-DPM_KIND=4",
+                                                                   f"-DPM_NSUB={EULER_NSUB}"], "inst.cu"))
     out.append(("pmap_abi", [], "pmap_abi.cu"))
     return out
 

@@ -1,6 +1,7 @@
 // inst.cu -- one explicit instantiation of the solver per translation unit.
 // Compiled once per (PM_R, PM_NX, PM_NY, PM_KIND, PM_K) by the build (see build.py):
-//   PM_KIND 0 = LTI linear, 1 = time-varying linear, 2 = coordinated turn, 3 = Van der Pol.
+//   PM_KIND 0 = LTI linear, 1 = time-varying linear, 2 = coordinated turn, 3 = Van der Pol,
+//   4 = LTI linear with paper-faithful Euler blocks of PM_NSUB substeps.
 #include "pmap_make.cuh"
 
 namespace pmap_rt {
@@ -20,6 +21,11 @@ template Runner* make_tv<PM_R, PM_NX, PM_NY, PM_K>(const PM_R*, const PM_R*, con
 #elif PM_KIND == 2
 template Runner* make_nl<PM_R, 5, 2, 1, PM_K>(double, double, double, const double*, const double*, const double*,
                                               const double*);
+#elif PM_KIND == 4  // Euler blocks (f2), n = PM_NSUB substeps, LTI
+template Runner* make_euler<PM_R, PM_NX, PM_NY, PM_NSUB, PM_K>(const double*, const double*, const double*,
+                                                             const double*, const double*, const double*,
+                                                             const double*, const double*, const double*,
+                                                             const double*);
 #elif PM_KIND == 3
 template Runner* make_nl<PM_R, 2, 1, 2, PM_K>(double, double, double, const double*, const double*, const double*,
                                               const double*);

@@ -46,6 +46,117 @@ static Runner* dispatch_lti(int kr, int nx, int ny, int lowrank, const double* A
 }
 
 template <typename R>
+static Runner* dispatch_euler(int kr, int nx, int ny, int nsub, const double* A, const double* C, const double* J,
+                              const double* b0, const double* h0, const double* Kb, const double* Ke,
+                              const double* J0, const double* h00, const double* K0) {
+  if (nsub != 10) return nullptr;  // compiled for the paper's n = 10 (build.py EULER_NSUB)
+#define PM_CASE(NXV, NYV)                                                                                    \
+  if (nx == NXV && ny == NYV)                                                                                \
+    return kr == kKBig ? make_euler<R, NXV, NYV, 10, kKBig>(A, C, J, b0, h0, Kb, Ke, J0, h00, K0)            \
+                       : make_euler<R, NXV, NYV, 10, kKSmall>(A, C, J, b0, h0, Kb, Ke, J0, h00, K0);
+  PM_CASE(1, 1)
+  PM_CASE(4, 2)
+#undef PM_CASE
+  return nullptr;
+}
+
+// Euler-block element of one grid interval (DESIGN.md R-EULER): NSUB explicit
+// Euler substeps, in s, of the element ODEs P:416-427 (dA/ds sign corrected)
+// from the boundary (I, 0, 0, 0, 0) of P:427, for an LTI model (F~ = -F, c~ = -c, Q~ = Q).
+// b and eta are affine in the block's measurements: carried as nx x (1 + nsub*ny)
+// matrices whose column 0 is the data-free part and column 1 + k*ny + a the coefficient
+// of measurement component a at substep k (fine time t_{i-1} + (k+1) delta).
+static void euler_block(int nx, int ny, int nsub, double dt, const double* F, const double* c, const double* Q,
+                        const double* H, const double* r, const double* Ri, std::vector<double>& A,
+                        std::vector<double>& C, std::vector<double>& J, std::vector<double>& B,
+                        std::vector<double>& E) {
+  const int M = 1 + nsub * ny;
+  const double de = dt / nsub;
+  auto I = [&](int i, int j) { return i == j ? 1.0 : 0.0; };
+  A.assign(nx * nx, 0.0);
+  for (int i = 0; i < nx; ++i) A[i * nx + i] = 1.0;
+  C.assign(nx * nx, 0.0);
+  J.assign(nx * nx, 0.0);
+  B.assign(nx * M, 0.0);
+  E.assign(nx * M, 0.0);
+  std::vector<double> Ft(nx * nx), ct(nx), HRi(nx * ny, 0.0), HRH(nx * nx, 0.0), HRr(nx, 0.0);
+  for (int i = 0; i < nx * nx; ++i) Ft[i] = -F[i];
+  for (int i = 0; i < nx; ++i) ct[i] = c ? -c[i] : 0.0;
+  for (int i = 0; i < nx; ++i)
+    for (int a = 0; a < ny; ++a)
+      for (int q = 0; q < ny; ++q) HRi[i * ny + a] += H[q * nx + i] * Ri[q * ny + a];
+  for (int i = 0; i < nx; ++i) {
+    for (int j = 0; j < nx; ++j)
+      for (int a = 0; a < ny; ++a) HRH[i * nx + j] += HRi[i * ny + a] * H[a * nx + j];
+    for (int a = 0; a < ny; ++a) HRr[i] += HRi[i * ny + a] * (r ? r[a] : 0.0);
+  }
+  auto mm = [&](const std::vector<double>& X, const double* Y, int m, std::vector<double>& Z) {  // Z = X Y, Y nx x m
+    Z.assign(nx * m, 0.0);
+    for (int i = 0; i < nx; ++i)
+      for (int k = 0; k < nx; ++k)
+        for (int j = 0; j < m; ++j) Z[i * m + j] += X[i * nx + k] * Y[k * m + j];
+  };
+  std::vector<double> AQ, JQ, dA(nx * nx), dB(nx * M), dC(nx * nx), dE(nx * M), dJ(nx * nx), t1, t2;
+  for (int k = 0; k < nsub; ++k) {
+    mm(A, Q, nx, AQ);
+    mm(J, Q, nx, JQ);
+    // dA/ds = A Q~ J - A F~
+    mm(AQ, J.data(), nx, t1);
+    mm(A, Ft.data(), nx, t2);
+    for (int i = 0; i < nx * nx; ++i) dA[i] = t1[i] - t2[i];
+    // db/ds = -A Q~ eta - A c~
+    mm(AQ, E.data(), M, t1);
+    for (int i = 0; i < nx * M; ++i) dB[i] = -t1[i];
+    for (int i = 0; i < nx; ++i) {
+      double s = 0;
+      for (int j = 0; j < nx; ++j) s += A[i * nx + j] * ct[j];
+      dB[i * M] -= s;
+    }
+    // dC/ds = -A Q~ A^T
+    for (int i = 0; i < nx; ++i)
+      for (int j = 0; j < nx; ++j) {
+        double s = 0;
+        for (int q = 0; q < nx; ++q) s += AQ[i * nx + q] * A[j * nx + q];
+        dC[i * nx + j] = -s;
+      }
+    // deta/ds = J Q~ eta - F~^T eta - H^T R^-1 (y - r) + J c~
+    mm(JQ, E.data(), M, t1);
+    for (int i = 0; i < nx; ++i)
+      for (int j = 0; j < M; ++j) {
+        double s = t1[i * M + j];
+        for (int q = 0; q < nx; ++q) s -= Ft[q * nx + i] * E[q * M + j];
+        dE[i * M + j] = s;
+      }
+    for (int i = 0; i < nx; ++i) {
+      double s = HRr[i];
+      for (int j = 0; j < nx; ++j) s += J[i * nx + j] * ct[j];
+      dE[i * M] += s;
+      for (int a = 0; a < ny; ++a) dE[i * M + 1 + k * ny + a] -= HRi[i * ny + a];
+    }
+    // dJ/ds = J Q~ J - J F~ - F~^T J - H^T R^-1 H
+    mm(JQ, J.data(), nx, t1);
+    mm(J, Ft.data(), nx, t2);
+    for (int i = 0; i < nx; ++i)
+      for (int j = 0; j < nx; ++j) {
+        double s = t1[i * nx + j] - t2[i * nx + j] - HRH[i * nx + j];
+        for (int q = 0; q < nx; ++q) s -= Ft[q * nx + i] * J[q * nx + j];
+        dJ[i * nx + j] = s;
+      }
+    // explicit Euler step backwards in s: X(s - delta) = X(s) - delta dX/ds
+    for (int i = 0; i < nx * nx; ++i) {
+      A[i] -= de * dA[i];
+      C[i] -= de * dC[i];
+      J[i] -= de * dJ[i];
+    }
+    for (int i = 0; i < nx * M; ++i) {
+      B[i] -= de * dB[i];
+      E[i] -= de * dE[i];
+    }
+  }
+  (void)I;
+}
+
+template <typename R>
 static Runner* dispatch_tv(int kr, int nx, int ny, const R* F, const R* c, const R* L, const R* Wm, const R* H,
                            const R* r, const R* Rm, const int64_t* str, int nw, double dt, const double* P0i,
                            const double* P0im0) {
@@ -152,8 +263,10 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   if (d.nx < 1 || d.ny < 1 || d.nw < 1 || d.nw > d.nx || d.T < 1 || d.batch < 1 || !(d.tf > d.t0) ||
       (d.dtype != MAP_F64 && d.dtype != MAP_F32) || d.world < 1 || d.rank < 0 || d.rank >= d.world)
     return MAP_E_ARG;
+  if (d.substeps < 0 || (d.substeps > 1 && (!lin || d.world != 1))) return MAP_E_ARG;
   std::unique_ptr<map_plan_s> p(new map_plan_s());
   p->d = d;
+  p->ny_row = d.ny;
   p->stream = static_cast<cudaStream_t>(d.stream);
   {
     const char* fs = getenv("PMAP_FORCE_SHARD");
@@ -198,7 +311,51 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   if (lin) {
     if (!lin->F || !lin->L || !lin->W || !lin->H || !lin->R) return MAP_E_ARG;
     const bool tv = lin->sF || lin->sc || lin->sL || lin->sW || lin->sH || lin->sr || lin->sR;
-    if (!tv) {
+    if (!tv && d.substeps > 1) {  // paper-faithful Euler blocks of d.substeps substeps
+      p->kind = Kind::LTI;
+      p->euler = true;
+      const int nsub = d.substeps;
+      const double de = dt / nsub;
+      std::vector<double> Q(nx * nx, 0.0), Ri(ny * ny), A, C, J, B, E, Cp(NS), Jp(NS);
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j)
+          for (int a = 0; a < nw; ++a)
+            for (int c = 0; c < nw; ++c) Q[i * nx + j] += lin->L[i * nw + a] * lin->W[a * nw + c] * lin->L[j * nw + c];
+      if (!h_inv(ny, lin->R, Ri.data())) return MAP_E_ARG;
+      euler_block(nx, ny, nsub, dt, lin->F, lin->c, Q.data(), lin->H, lin->r, Ri.data(), A, C, J, B, E);
+      sym_pack(C.data(), Cp.data());
+      sym_pack(J.data(), Jp.data());
+      const int M = 1 + nsub * ny, NR = nsub * ny;
+      std::vector<double> b0(nx), h0(nx), Kb(nx * NR), Ke(nx * NR), K0(nx * ny, 0.0), J0f(nx * nx, 0.0), J0(NS),
+          h00(nx);
+      for (int i = 0; i < nx; ++i) {
+        b0[i] = B[i * M];
+        h0[i] = E[i * M];
+        for (int k = 0; k < NR; ++k) {
+          Kb[i * NR + k] = B[i * M + 1 + k];
+          Ke[i * NR + k] = E[i * M + 1 + k];
+        }
+      }
+      // node 0: prior and the measurement at t_0 with the fine weight delta
+      for (int i = 0; i < nx; ++i)
+        for (int a = 0; a < ny; ++a)
+          for (int q = 0; q < ny; ++q) K0[i * ny + a] += de * lin->H[q * nx + i] * Ri[q * ny + a];
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j) {
+          J0f[i * nx + j] = P0i[i * nx + j];
+          for (int a = 0; a < ny; ++a) J0f[i * nx + j] += K0[i * ny + a] * lin->H[a * nx + j];
+        }
+      sym_pack(J0f.data(), J0.data());
+      for (int i = 0; i < nx; ++i) {
+        h00[i] = P0im0[i];
+        for (int a = 0; a < ny; ++a) h00[i] -= K0[i * ny + a] * (lin->r ? lin->r[a] : 0.0);
+      }
+      p->ny_row = NR;
+      rn = f32 ? dispatch_euler<float>(kr, nx, ny, nsub, A.data(), Cp.data(), Jp.data(), b0.data(), h0.data(),
+                                       Kb.data(), Ke.data(), J0.data(), h00.data(), K0.data())
+               : dispatch_euler<double>(kr, nx, ny, nsub, A.data(), Cp.data(), Jp.data(), b0.data(), h0.data(),
+                                        Kb.data(), Ke.data(), J0.data(), h00.data(), K0.data());
+    } else if (!tv) {
       p->kind = Kind::LTI;
       std::vector<double> A(nx * nx), b(nx, 0.0), Q(nx * nx, 0.0), Cp(NS), Ri(ny * ny), K(nx * ny, 0.0),
           Jf(nx * nx, 0.0), Jp(NS), h0(nx, 0.0), J0(NS), h00(nx);
@@ -461,7 +618,7 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
   const Geom& g = p->g;
   const size_t es = p->elem_real;
   const int nx = p->d.nx, ny = p->d.ny;
-  const size_t yb = (size_t)g.batch * g.Nn * ny * es, xb = (size_t)g.batch * g.Nn * nx * es;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xb = (size_t)g.batch * g.Nn * nx * es;
   const size_t mb = xb, Pb = (size_t)g.batch * g.Nn * (nx * (nx + 1) / 2) * es;
   bool blocking = false;
   const void* yd;
@@ -495,6 +652,10 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
 
 map_status map_two_filter(map_plan_t p, const void* y, void* x_map, void* smooth_P) {
   if (!p || !y || !x_map) return MAP_E_ARG;
+  if (p->euler) {
+    p->err = "two-filter is not available with Euler blocks (the block element mixes dynamics and measurements)";
+    return MAP_E_UNSUPPORTED;
+  }
   if (p->kind == Kind::NL || p->d.world != 1) {
     p->err = "map_two_filter needs a linear single-GPU plan";
     return MAP_E_ARG;
@@ -503,7 +664,7 @@ map_status map_two_filter(map_plan_t p, const void* y, void* x_map, void* smooth
   p->launches = 0;
   const Geom& g = p->g;
   const size_t es = p->elem_real;
-  const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
   const size_t Pb = (size_t)g.batch * g.Nn * (p->d.nx * (p->d.nx + 1) / 2) * es;
   bool blocking = false;
   const void* yd;
@@ -535,7 +696,7 @@ map_status map_solve_sequential(map_plan_t p, int32_t method, const void* y, int
   p->launches = 0;
   const Geom& g = p->g;
   const size_t es = p->elem_real;
-  const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
   const size_t Pb = (size_t)g.batch * g.Nn * (p->d.nx * (p->d.nx + 1) / 2) * es;
   bool blocking = false;
   const void* yd;
@@ -571,7 +732,7 @@ map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, doub
   p->launches = 0;
   const Geom& g = p->g;
   const size_t es = p->elem_real;
-  const size_t yb = (size_t)g.batch * g.Nn * p->d.ny * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
   bool blocking = false;
   const void* yd;
   void* xd;
@@ -681,7 +842,7 @@ map_status map_shard_phase(map_plan_t p, int32_t phase, const void* y, const voi
     p->want_filter = filt_m || filt_P;
     p->runner->phase2(*p, y, nullptr, gathered, payload);
   } else {
-    p->runner->phase3(*p, nullptr, gathered, x_map, filt_m, filt_P);
+    p->runner->phase3(*p, y, nullptr, gathered, x_map, filt_m, filt_P);
     if (!p->err.empty()) return MAP_E_ARG;
   }
   cudaError_t e = cudaGetLastError();

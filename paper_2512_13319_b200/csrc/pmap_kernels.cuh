@@ -520,7 +520,8 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
 // KC nodes so that it leaves as contiguous 8*KC*N-byte segments per run.
 template <typename R, int N, int NT, int K, class Src, bool REC = false>
 __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src, const Geom g,
-                                                const R* __restrict__ xbar, const R* __restrict__ sv,
+                                                const R* __restrict__ y, const R* __restrict__ xbar,
+                                                const R* __restrict__ sv,
                                                 const R* __restrict__ run_suf, const R* __restrict__ tile_sufx,
                                                 const R* __restrict__ group_carry, const R* __restrict__ carry_in,
                                                 R* __restrict__ x_out, unsigned long long* flag) {
@@ -534,6 +535,7 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
   const int r = threadIdx.x;
   const int64_t l0 = (j * NT + r) * (int64_t)K;
   const R* xb = Src::NEEDS_XBAR ? xbar + b * g.Nn * N : nullptr;
+  const R* yb = Src::TRANS_Y ? y + b * g.Nn * Src::NYROW : nullptr;
   bool ok = true;
   R x[N];
 #pragma unroll
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
         const int64_t gi = g.node0 + l;
         if (valid && gi != 0) {
           R At[N][N], bt[N], Ct[Dim<N>::NS], SU[N][NW], u[NW];
-          src.trans(gi, nullptr, At, bt, Ct);
+          src.trans(gi, nullptr, nullptr, At, bt, Ct);
 #pragma unroll
           for (int i = 0; i < N; ++i)
 #pragma unroll
@@ -625,7 +627,8 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
       const int64_t gi = g.node0 + l;
       if (valid && gi != 0) {
         R At[N][N], bt[N], Ct[Dim<N>::NS];
-        src.trans(gi, Src::NEEDS_XBAR ? xb + l * N : nullptr, At, bt, Ct);
+        src.trans(gi, Src::TRANS_Y ? yb + l * Src::NYROW : nullptr, Src::NEEDS_XBAR ? xb + l * N : nullptr, At, bt,
+                  Ct);
         trans_step<R, N>(At, bt, Ct, Vp, x, ok);
       }
     }

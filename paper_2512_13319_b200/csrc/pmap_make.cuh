@@ -72,4 +72,30 @@ Runner* make_nl(double dt, double mu, double om_div, const double* C, const doub
 }
 
 
+template <typename R, int N, int NYM, int NSUB, int KR>
+Runner* make_euler(const double* A, const double* C, const double* J, const double* b0, const double* h0,
+                   const double* Kb, const double* Ke, const double* J0, const double* h00, const double* K0) {
+  using S = SrcEulerLTI<R, N, NYM, NSUB>;
+  auto* rn = new RunnerT<R, N, S::NYROW, S, KR>();
+  auto& s = rn->src;
+  constexpr int NS = Dim<N>::NS;
+  for (int i = 0; i < N; ++i) {
+    for (int j = 0; j < N; ++j) s.A[i][j] = (R)A[i * N + j];
+    s.b0[i] = (R)b0[i];
+    s.h0[i] = (R)h0[i];
+    s.h00[i] = (R)h00[i];
+    for (int k = 0; k < S::NYROW; ++k) {
+      s.Kb[i][k] = (R)Kb[i * S::NYROW + k];
+      s.Ke[i][k] = (R)Ke[i * S::NYROW + k];
+    }
+    for (int a = 0; a < NYM; ++a) s.K0[i][a] = (R)K0[i * NYM + a];
+  }
+  for (int k = 0; k < NS; ++k) {
+    s.C[k] = (R)C[k];
+    s.J[k] = (R)J[k];
+    s.J0[k] = (R)J0[k];
+  }
+  return rn;
+}
+
 }  // namespace pmap_rt

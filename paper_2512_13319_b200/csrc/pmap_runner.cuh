@@ -125,7 +125,8 @@ struct Runner {
   virtual size_t payload_elems(int phase) const = 0;
   virtual void phase1(PlanState& p, const void* y, const void* xbar, void* payload) = 0;
   virtual void phase2(PlanState& p, const void* y, const void* xbar, const void* gathered, void* payload) = 0;
-  virtual void phase3(PlanState& p, const void* xbar, const void* gathered, void* x, void* fm, void* fP) = 0;
+  virtual void phase3(PlanState& p, const void* y, const void* xbar, const void* gathered, void* x, void* fm,
+                      void* fP) = 0;
   virtual void two_filter(PlanState& p, const void* y, void* x, void* Ps) = 0;
   // sequential on-device baseline: method 0 = RTS, 1 = two-filter
   virtual void sequential(PlanState& p, int method, const void* y, const void* xbar, void* x, void* Ps) = 0;
@@ -179,6 +180,8 @@ struct PlanState {
   bool want_filter = false;  // filter outputs requested for the current solve (full (S, v) storage)
   bool rec_done = false;     // phase 2 stored low-rank pass-2 records (R-P2REC) instead of (S, v)
   bool no_rec = false;       // PMAP_NO_P2REC=1: always store (S, v) (A/B checks)
+  bool euler = false;        // paper-faithful Euler blocks: y rows of ny_row = substeps * ny
+  int ny_row = 0;            // doubles of y per node
   bool force_shard = false;  // PMAP_FORCE_SHARD=1 with a communicator: run the NCCL path at world == 1 (tests)
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
   cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
@@ -344,7 +347,6 @@ struct RunnerT : Runner {
   void reduce1(PlanState& p, cudaStream_t s, int kid, const KS& ksrc,
                const LtiFoldParams<R, N, NY, K, Log2<kNT>::value>& fpar,
                const Tab* tb, const R* y, const R* xbar, R* run_incl, R* tile_agg) {
-    const LtiNode<R, N, NY>& ln = fpar.node;
     const Geom& g = p.g;
     if (!(use_lti && tb)) {
       PM_LAUNCH(p, s, kid,
@@ -352,6 +354,8 @@ struct RunnerT : Runner {
                     ksrc, g, y, xbar, run_incl, tile_agg, p.dflag, 0, 0, 0)));
       return;
     }
+    if constexpr (IS_LTI) {
+    const LtiNode<R, N, NY>& ln = fpar.node;
     const int64_t j_lo = lti_jlo(g, REV);
     const int64_t j_hi = lti_jhi(g);
     const int64_t n_int = j_hi > j_lo ? j_hi - j_lo : 0;
@@ -377,6 +381,7 @@ struct RunnerT : Runner {
     if (nsel > 0) {
       cudaEventRecord(e1, se);
       cudaStreamWaitEvent(s, e1, 0);
+    }
     }
   }
 
@@ -501,12 +506,14 @@ struct RunnerT : Runner {
     }
   }
 
-  void phase3(PlanState& p, const void* xbarv, const void* gathered, void* xv, void* fm, void* fP) override {
+  void phase3(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* xv, void* fm,
+              void* fP) override {
     const Geom& g = p.g;
     WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
     auto W = [&](size_t off) { return reinterpret_cast<R*>(p.ws + off); };
     const R* xbar = static_cast<const R*>(xbarv);
+    const R* y = static_cast<const R*>(yv);
     R* x = static_cast<R*>(xv);
     const unsigned ntiles = (unsigned)(g.batch * g.tpt);
     cudaStream_t s = p.stream;
@@ -527,12 +534,12 @@ struct RunnerT : Runner {
     if (p.rec_done) {
       if constexpr (kRec)
         PM_LAUNCH(p, s, K_P2_DOWN,
-                  (k_p2_down<R, N, kNT, K, Src, true><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
+                  (k_p2_down<R, N, kNT, K, Src, true><<<ntiles, kNT, 0, s>>>(src, g, y, xbar, W(L.sv), W(L.run_suf),
                                                                            W(L.tile_sufx2), W(L.group_carry2),
                                                                            W(L.carry_in), x, p.dflag)));
     } else {
       PM_LAUNCH(p, s, K_P2_DOWN,
-                (k_p2_down<R, N, kNT, K, Src><<<ntiles, kNT, 0, s>>>(src, g, xbar, W(L.sv), W(L.run_suf),
+                (k_p2_down<R, N, kNT, K, Src><<<ntiles, kNT, 0, s>>>(src, g, y, xbar, W(L.sv), W(L.run_suf),
                                                                     W(L.tile_sufx2), W(L.group_carry2),
                                                                     W(L.carry_in), x, p.dflag)));
     }
@@ -549,7 +556,7 @@ struct RunnerT : Runner {
     if (p.d.world == 1 && !p.force_shard) {
       phase1(p, y, xbar, nullptr);
       phase2(p, y, xbar, nullptr, nullptr);
-      phase3(p, xbar, nullptr, x, fm, fP);
+      phase3(p, y, xbar, nullptr, x, fm, fP);
       return;
     }
     // NCCL-driven exchange: two all-gathers of chunk carries per solve
@@ -570,7 +577,7 @@ struct RunnerT : Runner {
       p.err = "ncclAllGather failed";
       return;
     }
-    phase3(p, xbar, gat2, x, fm, fP);
+    phase3(p, y, xbar, gat2, x, fm, fP);
   }
 
   // Two-filter (R-TF): pass A = pass-1 kernels without the pass-2 fold on the plan
@@ -721,6 +728,9 @@ Runner* make_lti(const double* A, const double* b, const double* C, const double
 template <typename R, int N, int NY, int KR>
 Runner* make_tv(const R* F, const R* c, const R* L, const R* Wm, const R* H, const R* r, const R* Rm,
                 const int64_t* str, int nw, double dt, const double* P0i, const double* P0im0);
+template <typename R, int N, int NYM, int NSUB, int KR>
+Runner* make_euler(const double* A, const double* C, const double* J, const double* b0, const double* h0,
+                   const double* Kb, const double* Ke, const double* J0, const double* h00, const double* K0);
 template <typename R, int N, int NY, int KIND, int KR>
 Runner* make_nl(double dt, double mu, double om_div, const double* C, const double* Ri, const double* P0i,
                 const double* P0im0);

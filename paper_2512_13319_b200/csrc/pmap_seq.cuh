@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(32) k_seq_rts(const __grid_constant__ Src src,
     const V Vp = Vn;
     if (l >= 2) load(Vn, ws + ((l - 2) * V::SZ) * B + b, B);
     R At[N][N], bt[N], Ct[NS];
-    src.trans(g.node0 + l, xb ? xb + l * N : nullptr, At, bt, Ct);
+    src.trans(g.node0 + l, yb + l * NY, xb ? xb + l * N : nullptr, At, bt, Ct);
     rts_back_step<R, N>(At, bt, Ct, Vp, x, po ? Ps : nullptr, ok);
 #pragma unroll
     for (int i = 0; i < N; ++i) xo[(l - 1) * N + i] = x[i];

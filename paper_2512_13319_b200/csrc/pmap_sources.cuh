@@ -25,6 +25,8 @@ struct SrcLTI {
   static constexpr int LOWRANK = NWC;
   static constexpr int NXB = N;  // row width of the nominal trajectory (unused)
   static constexpr bool NEEDS_XBAR = false;
+  static constexpr int NYROW = NY;         // doubles of y per node
+  static constexpr bool TRANS_Y = false;   // the pass-2 transition does not depend on y
   R A[N][N];
   R b[N];
   R C[NS];
@@ -103,7 +105,8 @@ struct SrcLTI {
       e.J[k] = J[k];
     }
   }
-  PM_INLINE void trans(int64_t /*gi*/, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
+  PM_INLINE void trans(int64_t /*gi*/, const R* /*yrow*/, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N],
+                       R (&Ct)[NS]) const {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll
@@ -124,6 +127,8 @@ struct SrcTV {
   static constexpr int LOWRANK = 0;
   static constexpr bool NEEDS_XBAR = false;
   static constexpr bool HAS_MIRROR = true;
+  static constexpr int NYROW = NY;
+  static constexpr bool TRANS_Y = false;
   const R *F, *c, *L, *W, *H, *r, *Rm;
   int64_t sF, sc, sL, sW, sH, sr, sR;
   int nw;
@@ -229,7 +234,8 @@ struct SrcTV {
   PM_INLINE void node_interior(int64_t gi, const R* yrow, const R* xrow, Elem<R, N>& e) const {
     node(gi, yrow, xrow, e);
   }
-  PM_INLINE void trans(int64_t gi, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
+  PM_INLINE void trans(int64_t gi, const R* /*yrow*/, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N],
+                       R (&Ct)[NS]) const {
     R Ft[N][N], ct[N], Q[NS];
     model(gi, Ft, ct, Q);
 #pragma unroll
@@ -334,6 +340,8 @@ struct SrcNL {
   static constexpr int LOWRANK = 0;
   static constexpr bool NEEDS_XBAR = true;
   static constexpr bool HAS_MIRROR = false;
+  static constexpr int NYROW = NY;
+  static constexpr bool TRANS_Y = false;
   R dt;
   R mu;           // Van der Pol parameter
   int om_div = 0;  // keep the OM divergence term 1/2 div f linearised into eta
@@ -464,7 +472,8 @@ struct SrcNL {
   PM_INLINE void node_interior(int64_t gi, const R* yrow, const R* xrow, Elem<R, N>& e) const {
     node(gi, yrow, xrow, e);
   }
-  PM_INLINE void trans(int64_t /*gi*/, const R* xrow, R (&At)[N][N], R (&bt)[N], R (&Ct)[NS]) const {
+  PM_INLINE void trans(int64_t /*gi*/, const R* /*yrow*/, const R* xrow, R (&At)[N][N], R (&bt)[N],
+                       R (&Ct)[NS]) const {
     R x[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) x[i] = xrow[i];
@@ -480,6 +489,97 @@ struct SrcNL {
       }
       bt[i] = -dt * c;
     }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) Ct[k] = C[k];
+  }
+};
+
+// ------------------------------------------- paper-faithful Euler blocks (f2)
+// Each grid interval (t_{i-1}, t_i] is a block of NSUB explicit Euler substeps
+// (n = 10) of the element ODEs P:416-427 in s (tau time), integrated from the
+// boundary (I, 0, 0, 0, 0) of P:427 with the sign of dA/ds corrected (SURVEY G6:
+// dA/ds = +A Q J - A F~).  Substep k (k = 0..NSUB-1) uses the measurement at the fine
+// time t_{i-1} + (k+1) dt/NSUB (DESIGN.md R-EULER); node 0 carries the prior and y(t_0).
+// For LTI models A, C, J of a block are data independent and (b, eta) are affine in
+// the block's NSUB measurements, so the plan integrates the ODEs once (host, fp64) into
+// constants plus data-coefficient matrices (the same superposition as R-LTI); the
+// kernels evaluate b = b0 + Kb y_blk, eta = h0 + Ke y_blk.  y rows hold NSUB*NYM
+// values: [NSUB][NYM] per block, node 0's y(t_0) in its last sub-slot.
+template <typename R, int N, int NYM, int NSUB>
+struct SrcEulerLTI {
+  static constexpr int NS = Dim<N>::NS;
+  static constexpr int NYROW = NSUB * NYM;
+  static constexpr bool IS_LTI_SRC = false;
+  static constexpr int LOWRANK = 0;
+  static constexpr bool NEEDS_XBAR = false;
+  static constexpr bool HAS_MIRROR = false;
+  static constexpr bool TRANS_Y = true;  // b of a block depends on its measurements
+  R A[N][N];
+  R C[NS];
+  R J[NS];
+  R b0[N];
+  R h0[N];
+  R Kb[N][NYROW];
+  R Ke[N][NYROW];
+  R J0[NS];     // P0^-1 + delta H^T R^-1 H
+  R h00[N];     // P0^-1 m0 - delta H^T R^-1 r
+  R K0[N][NYM]; // delta H^T R^-1
+
+  PM_INLINE void data_parts(const R* yrow, R (&b)[N], R (&h)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R sb = b0[i], sh = h0[i];
+#pragma unroll
+      for (int k = 0; k < NYROW; ++k) {
+        const R yk = yrow[k];
+        sb = fma(Kb[i][k], yk, sb);
+        sh = fma(Ke[i][k], yk, sh);
+      }
+      b[i] = sb;
+      h[i] = sh;
+    }
+  }
+  PM_INLINE void node(int64_t gi, const R* yrow, const R* /*xrow*/, Elem<R, N>& e) const {
+    if (gi == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R s = h00[i];
+#pragma unroll
+        for (int a = 0; a < NYM; ++a) s = fma(K0[i][a], yrow[(NSUB - 1) * NYM + a], s);
+        e.h[i] = s;
+        e.b[i] = R(0);
+#pragma unroll
+        for (int j = 0; j < N; ++j) e.A[i][j] = R(0);
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        e.C[k] = R(0);
+        e.J[k] = J0[k];
+      }
+      return;
+    }
+    data_parts(yrow, e.b, e.h);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) e.A[i][j] = A[i][j];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      e.C[k] = C[k];
+      e.J[k] = J[k];
+    }
+  }
+  PM_INLINE void node_interior(int64_t gi, const R* yrow, const R* xrow, Elem<R, N>& e) const {
+    node(gi, yrow, xrow, e);
+  }
+  PM_INLINE void trans(int64_t /*gi*/, const R* yrow, const R* /*xrow*/, R (&At)[N][N], R (&bt)[N],
+                       R (&Ct)[NS]) const {
+    R h[N];
+    data_parts(yrow, bt, h);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) At[i][j] = A[i][j];
 #pragma unroll
     for (int k = 0; k < NS; ++k) Ct[k] = C[k];
   }

@@ -162,3 +162,45 @@ def test_vdp_om_divergence(torch_cuda, T):
         assert rel(xs[0].cpu().numpy(), xo) < TOL64
     x0, _ = plan0.solve_nonlinear(yd, passes=10)
     assert rel(x0[0].cpu().numpy(), xo) > 1e-6
+
+
+@pytest.mark.parametrize("case,T,B", [("wiener", 3000, 1), ("wiener", 100_000, 1), ("wiener_c", 20_000, 3),
+                                       ("ou", 4097, 2)])
+def test_euler_blocks(torch_cuda, case, T, B):
+    """f2: the paper's Euler blocks (n = 10 substeps per grid interval) on the GPU
+    (parallel scan and sequential baseline) = the step-by-step Euler-block oracle."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    n = 10
+    if case.startswith("wiener"):
+        spec = wl.wiener_velocity()
+        if case == "wiener_c":
+            spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+            spec.r = np.array([0.5, -0.25])
+    else:
+        spec = wl.ornstein_uhlenbeck()
+    _, yf = wl.simulate_linear(spec, n * T, seed=T, batch=B)
+    yf = yf.reshape(B, n * T + 1, spec.ny)
+    plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H, r=spec.r,
+                   R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, substeps=n)
+    yd = to_dev(torch, pm.binding.euler_rows(yf, n))
+    x = plan.solve_linear(yd).cpu().numpy()
+    xs = plan.solve_sequential(yd, method=0).cpu().numpy()
+    for b in range(B):
+        xo = oracle.euler_rts(ora_model(spec), yf[b], T, n, spec.t0, spec.tf)
+        assert rel(x[b], xo) < TOL64
+        assert rel(xs[b], xo) < TOL64
+
+
+def test_euler_blocks_errors(torch_cuda):
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 100
+    plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                   P0=spec.P0, substeps=10)
+    with pytest.raises(pm.MapError):  # two-filter needs separable measurements
+        plan.two_filter(to_dev(torch, np.zeros((1, T + 1, 20))))
+    with pytest.raises(pm.MapError):  # only n = 10 is compiled
+        pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                P0=spec.P0, substeps=7)

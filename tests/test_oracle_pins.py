@@ -217,6 +217,33 @@ def test_P3_ou_continuous_limit_first_order():
     assert errs[-1] < 5e-4
 
 
+
+def test_P13_euler_blocks():
+    """P13 -- the paper-faithful Euler-block oracle (T blocks of n
+    Euler substeps of P:416-427): (a) n = 1 is the exact discrete model (= the
+    covariance-form KF/RTS, <= 1e-12); (b) at fixed T the block-boundary MAP converges at
+    first order in the substep (ratio in [1.9, 2.1] per doubling of n) to the continuous
+    OU Euler--Lagrange closed form; (c) with the printed sign of dA/ds it does
+    not converge, so the pin detects that error."""
+    s = wl.wiener_velocity()
+    md = oracle.LinearModel(s.F, s.L, s.W, s.H, s.R, s.m0, s.P0, c=np.array([0.3, -0.2, 0.1, 0.05]))
+    T = 300
+    _, y = wl.simulate_linear(s, T, seed=1)
+    assert rel_inf(oracle.euler_rts(md, y, T, 1, 0.0, 5.0), oracle.kf_rts(md, y, T, 0.0, 5.0)) < 1e-12
+    o = wl.ornstein_uhlenbeck()
+    mo = oracle.LinearModel(o.F, o.L, o.W, o.H, o.R, o.m0, o.P0)
+    th, q, R, m0, P0, yc, tf = 1.0, 2.0, 0.1, 1.0, 1.0, 0.7, 5.0
+    T = 100
+    xc = ou_closed_form(th, q, R, m0, P0, yc, tf, np.linspace(0, tf, T + 1))
+    for printed in (False, True):
+        errs = np.array([np.abs(oracle.euler_rts(mo, np.full((n * T + 1, 1), yc), T, n, 0.0, tf,
+                                                 g6_printed=printed)[:, 0] - xc).max() for n in (4, 8, 16, 32, 64)])
+        ratios = errs[:-1] / errs[1:]
+        if printed:
+            assert errs[-1] > 0.05 and np.all(ratios < 1.5), (errs, ratios)
+        else:
+            assert np.all((ratios > 1.9) & (ratios < 2.1)) and errs[-1] < 1e-3, (errs, ratios)
+
 def test_P4_scalar_moebius_closed_form():
     """P4 -- scalar discrete filter variance = linear-fractional (Moebius) power:
     P_i = M^i (P_{0|0}, 1), M = [[R_d Phi^2, R_d Q_d], [Phi^2, Q_d + R_d]],

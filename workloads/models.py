@@ -102,4 +102,7 @@ CONFIGS = {
     "C3": dict(model="wiener_velocity", T=10_000_000, batch=1, method="rts"),
     "C4": dict(model="coordinated_turn", T=100_000, batch=1, method="ieks", passes=10),
     "C5": dict(model="wiener_velocity", T=10_000, batch=1024, method="two_filter"),
+    # not a BASELINE config: the paper's own discretisation of its linear experiment
+    # (T blocks of n = 10 Euler substeps, a measurement at every substep), SURVEY f2
+    "C2E": dict(model="wiener_velocity", T=100_000, batch=1, method="rts", substeps=10),
 }

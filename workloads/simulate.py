@@ -95,7 +95,19 @@ def make_workload(config: str, seed: int = 0, T: int | None = None, batch: int |
         spec = coordinated_turn()
     else:
         spec = van_der_pol()
-    if isinstance(spec, LinearSpec):
+    n = cfg.get("substeps", 1)
+    if isinstance(spec, LinearSpec) and n > 1:
+        # Euler blocks: simulate on the fine grid of n*T steps, then lay the rows out as
+        # include/pmap.h expects ([T+1][n*ny], row 0 = y(t_0) in its last sub-slot)
+        _, yf = simulate_linear(spec, n * T, seed=seed, batch=(B if B > 1 else None))
+        yf = yf.reshape(B, n * T + 1, spec.ny)
+        y = np.zeros((B, T + 1, n, spec.ny))
+        y[:, 0, n - 1] = yf[:, 0]
+        y[:, 1:] = yf[:, 1:].reshape(B, T, n, spec.ny)
+        y = y.reshape(B, T + 1, n * spec.ny)
+        if B == 1:
+            y = y[0]
+    elif isinstance(spec, LinearSpec):
         _, y = simulate_linear(spec, T, seed=seed, batch=(B if B > 1 else None))
     else:
         _, y = simulate_nonlinear(spec, T, seed=seed)
