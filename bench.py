@@ -36,14 +36,16 @@ FALLBACK_HBM_GBS = 6650.0
 
 # ----------------------------------------------------------- algorithmic counts
 def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zero_b: bool = False,
-               euler_n: int = 0):
+               euler_n: int = 0, amask=None, umask=None):
     """Algorithmic FP64 flops (FMA = 2) and HBM bytes per node of each kernel class
     (DESIGN.md section 6): the arithmetic each kernel's per-node recurrence performs
     in this decomposition, excluding the intra-tile scan overheads (Kogge-Stone
     rounds, carries), which are implementation cost.  nw > 0: low-rank diffusion
     (R-LOWRANK node update, R-P2REC pass-2 records of nw (nx + 1) values).  euler_n > 0:
     Euler blocks (R-EULER): y rows of euler_n * ny values, element data parts b, eta built
-    from them (2 * nx * euler_n * ny FMA per build: reduce, down; nx * euler_n * ny in pass 2)."""
+    from them (2 * nx * euler_n * ny FMA per build: reduce, down; nx * euler_n * ny in pass 2).
+    amask / umask (bool arrays, R-MASK): structural non-zeros of A (nx x nx) and U (nx x nw)
+    the specialised kernels exploit -- terms with a structurally zero factor are not counted."""
     N = nx
     lu = sum((N - k - 1) + (N - k - 1) ** 2 for k in range(N))
     solve = N * N
@@ -60,15 +62,20 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
     vsz2 = vsz  # per-node values pass 1 stores for pass 2
     if nw > 0:  # R-LOWRANK node update (vapply_lowrank), R-P2REC records when smaller than (S, v)
         r = nw
-        chol = r * (r + 1) // 2 * N + r * (r - 1) // 2 * (r + 1) + r
+        am = np.ones((N, N), bool) if amask is None else np.asarray(amask, bool)
+        um = np.ones((N, r), bool) if umask is None else np.asarray(umask, bool)
+        nA, nU = int(am.sum()), int(um.sum())
+        gram = sum((a + 1) * int(um[:, a].sum()) for a in range(r))
+        chol = gram + r * (r - 1) // 2 * (r + 1) + r
+        ata = sum(int(am[:, i].sum()) * (N - i) for i in range(N))  # A^T (B A), upper triangle
         # S U, Gram + LDL, Y = L^-1 (S U)^T and D^-1 Y, B = S - Ys^T Y, w = v - S b (skipped
         # when b == 0), q = G^-1 U^T w, w - S U q, B A, A^T (B A) + J, A^T w + eta
-        vapply = (N * r * N + chol + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
-                  + r * N + r * r + N * r + N * N * N + ns * N + N * N)
+        vapply = (N * nU + chol + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
+                  + nU + r * r + N * r + N * nA + ata + nA)
         if r * (N + 1) < vsz:
             vsz2 = r * (N + 1)
-            vapply += r * N  # U^T v
-            trans = N * N + N * r + chol + r * N + r * r + N * r
+            vapply += nU  # U^T v
+            trans = nA + nU + chol + r * N + r * r + nU
     if euler_n > 0:
         ny_row = euler_n * ny
         build = 2 * N * ny_row
@@ -85,6 +92,22 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         "k_p2_down": (2 * trans, d * (vsz2 + nx + asz / K)),
         "solve": (2 * (reduce_fl + vapply + vapply_tr / K + trans), d * (ny + 2 * vsz + nx)),
     }
+
+
+def structural_masks(spec, T):
+    """Structural non-zeros of A = I - dt F and U = sqrt(dt) L chol(W) the library's
+    specialised kernels use (R-MASK; the compiled Wiener-velocity masks), else dense."""
+    dt = (spec.tf - spec.t0) / T
+    A = np.eye(spec.nx) - dt * spec.F
+    U = np.sqrt(dt) * spec.L @ np.linalg.cholesky(spec.W)
+    wa = np.zeros((4, 4), bool)
+    for i, j in ((0, 0), (0, 2), (1, 1), (1, 3), (2, 2), (3, 3)):
+        wa[i, j] = True
+    wu = np.zeros((4, 2), bool)
+    wu[2, 0] = wu[3, 1] = True
+    if A.shape == (4, 4) and U.shape == (4, 2) and not np.any((A != 0) & ~wa) and not np.any((U != 0) & ~wu):
+        return wa, wu
+    return None, None
 
 
 # ---------------------------------------------------------------- clocks
@@ -389,10 +412,14 @@ def main():
             and os.environ.get("PMAP_GENERAL") != "1"):
         lowrank = spec.L.shape[1]
     zero_b = isinstance(spec, wl.LinearSpec) and (spec.c is None or not np.any(spec.c))
+    amask = umask = None
+    if lowrank and os.environ.get("PMAP_NO_MASK") != "1":
+        amask, umask = structural_masks(spec, T)
     if substeps > 1:  # Euler blocks: general kernels, element build from n*ny measurements
         counts = alg_counts(plan.nx, plan.ny, lti=False, euler_n=substeps)
     else:
-        counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank, zero_b=zero_b)
+        counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank, zero_b=zero_b,
+                            amask=amask, umask=umask)
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl
@@ -400,6 +427,7 @@ def main():
     nodes_per_launch = B * plan.n_local
     fl, by = counts.get(dname, counts["solve"])
     achieved_tflops = fl * nodes_per_launch / (per_launch_ms * 1e-3) / 1e12
+    achieved_gbs = by * nodes_per_launch / (per_launch_ms * 1e-3) / 1e9
     traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from a committed ncu capture
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -408,19 +436,33 @@ def main():
             traffic = rec["dram_bytes_per_launch"]
     except Exception:
         traffic = None
-    roofline = {"bound": "alu", "kernel": dname, "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
-                "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS_DERIVED, "traffic": traffic,
-                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)" if traffic else None,
-                "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (MEASURED_PEAKS.json has no FP64; "
-                               "DFMA microbenchmark measured 34.2 TF/s, profiles/r01_fp64_peak_probe.log)",
-                "alg_flops_per_node": fl, "alg_bytes_per_node": by, "kernel_ms_per_launch": per_launch_ms,
-                "kernel_share_of_step": dms / max(1e-9, sum(v[0] for v in prof.values()))}
     try:
         peaks = json.load(open(PEAKS_PATH))
         hbm = float(peaks["hbm_gbs"])
         hbm_src = "measured"
     except Exception:
         hbm, hbm_src = FALLBACK_HBM_GBS, "fallback"
+    # the binding roof of the dominant kernel: FP64 ALU (DFMA pipe) or HBM, whichever
+    # fraction is larger; the other is reported alongside
+    alu_frac = achieved_tflops / FP64_PEAK_TFLOPS_DERIVED
+    hbm_frac = achieved_gbs / hbm
+    alu_src = ("derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (MEASURED_PEAKS.json has no FP64; "
+               "DFMA microbenchmark measured 34.2 TF/s, profiles/r01_fp64_peak_probe.log)")
+    hbm_desc = f"{hbm_src}: MEASURED_PEAKS.json hbm_gbs" if hbm_src == "measured" else "fallback (B200_PROFILING.md)"
+    if hbm_frac >= alu_frac:
+        roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": hbm_frac, "peak_source": hbm_desc,
+                    "other_roof": {"bound": "alu", "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
+                                   "unit": "TFLOP/s", "frac": alu_frac, "peak_source": alu_src}}
+    else:
+        roofline = {"bound": "alu", "kernel": dname, "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
+                    "unit": "TFLOP/s", "frac": alu_frac, "peak_source": alu_src,
+                    "other_roof": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                                   "frac": hbm_frac, "peak_source": hbm_desc}}
+    roofline.update({"traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)" if traffic else None,
+                     "alg_flops_per_node": fl, "alg_bytes_per_node": by, "kernel_ms_per_launch": per_launch_ms,
+                     "kernel_share_of_step": dms / max(1e-9, sum(v[0] for v in prof.values()))})
     sfl, sby = counts["solve"]
     solve_hbm = {"alg_bytes_per_node": sby, "achieved_gbs": sby * B * T / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
                  "peak_source": hbm_src, "frac_of_hbm_roofline": sby * B * T / (ms * 1e-3) / 1e9 / hbm,

@@ -6,13 +6,18 @@
 
 namespace pmap_rt {
 #if PM_KIND == 0
-template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 0>(const double*, const double*, const double*, const double*,
-                                                     const double*, const double*, const double*, const double*,
-                                                     const double*, const double*, const double*, const double*);
-#if PM_NX == 4 && PM_NY == 2  // rank-2 diffusion (Wiener velocity): Woodbury node update
-template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2>(const double*, const double*, const double*, const double*,
-                                                     const double*, const double*, const double*, const double*,
-                                                     const double*, const double*, const double*, const double*);
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 0, ~0u, ~0u>(const double*, const double*, const double*,
+                                                               const double*, const double*, const double*,
+                                                               const double*, const double*, const double*,
+                                                               const double*, const double*, const double*);
+#if PM_NX == 4 && PM_NY == 2  // rank-2 diffusion (Wiener velocity): Woodbury node update, dense and masked
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2, ~0u, ~0u>(const double*, const double*, const double*,
+                                                               const double*, const double*, const double*,
+                                                               const double*, const double*, const double*,
+                                                               const double*, const double*, const double*);
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2, pmap_rt::kWienerAMask, pmap_rt::kWienerUMask>(
+    const double*, const double*, const double*, const double*, const double*, const double*, const double*,
+    const double*, const double*, const double*, const double*, const double*);
 #endif
 #elif PM_KIND == 1
 template Runner* make_tv<PM_R, PM_NX, PM_NY, PM_K>(const PM_R*, const PM_R*, const PM_R*, const PM_R*, const PM_R*,

@@ -33,13 +33,24 @@ static Runner* dispatch_lti(int kr, int nx, int ny, int lowrank, const double* A
                             const double* C, const double* J, const double* K, const double* h0, const double* J0,
                             const double* h00, const double* Am, const double* bm, const double* Cm,
                             const double* U) {
-  if (nx == 4 && ny == 2 && lowrank == 2)
-    return kr == kKBig ? make_lti<R, 4, 2, kKBig, 2>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U)
-                       : make_lti<R, 4, 2, kKSmall, 2>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
+  if (nx == 4 && ny == 2 && lowrank == 2) {
+    // structural zeros (R-MASK): specialised kernels when the model's zeros cover the mask's
+    uint32_t am = 0, um = 0;
+    for (int i = 0; i < 16; ++i) am |= (A[i] != 0.0 ? 1u : 0u) << i;
+    for (int i = 0; i < 8; ++i) um |= (U[i] != 0.0 ? 1u : 0u) << i;
+    const char* nm = getenv("PMAP_NO_MASK");
+    if (!(nm && nm[0] == '1') && (am & ~kWienerAMask) == 0 && (um & ~kWienerUMask) == 0)
+      return kr == kKBig ? make_lti<R, 4, 2, kKBig, 2, kWienerAMask, kWienerUMask>(A, b, C, J, K, h0, J0, h00, Am,
+                                                                                   bm, Cm, U)
+                         : make_lti<R, 4, 2, kKSmall, 2, kWienerAMask, kWienerUMask>(A, b, C, J, K, h0, J0, h00,
+                                                                                     Am, bm, Cm, U);
+    return kr == kKBig ? make_lti<R, 4, 2, kKBig, 2, ~0u, ~0u>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U)
+                       : make_lti<R, 4, 2, kKSmall, 2, ~0u, ~0u>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
+  }
 #define PM_CASE(NXV, NYV)                                                                                    \
   if (nx == NXV && ny == NYV)                                                                                \
-    return kr == kKBig ? make_lti<R, NXV, NYV, kKBig, 0>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U)          \
-                       : make_lti<R, NXV, NYV, kKSmall, 0>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
+    return kr == kKBig ? make_lti<R, NXV, NYV, kKBig, 0, ~0u, ~0u>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U) \
+                       : make_lti<R, NXV, NYV, kKSmall, 0, ~0u, ~0u>(A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
   PM_SHAPES(PM_CASE)
 #undef PM_CASE
   return nullptr;

@@ -22,6 +22,12 @@ namespace pmap {
 
 #define PM_INLINE __device__ __forceinline__
 
+// Structural-zero masks (DESIGN.md R-MASK): bit (i * cols + j) set = entry (i, j) may be
+// non-zero.  Inside fully unrolled loops the test folds at compile time, so the terms
+// of entries that are structurally zero are never issued -- bit-identical results
+// (fma(x, 0, s) == s for finite x), fewer FP64 instructions.  ~0u = dense.
+__host__ __device__ constexpr bool mask_nz(uint32_t m, int bit) { return ((m >> bit) & 1u) != 0u; }
+
 template <int N>
 struct Dim {
   static constexpr int NS = N * (N + 1) / 2;
@@ -195,7 +201,7 @@ PM_INLINE float pm_rcp_ge1(float x) { return __frcp_rn(x); }
 
 // G = L D L^T of the small SPD matrix G = I + U^T (S U) (NW x NW, pivots >= 1),
 // sqrt-free.  In: SU = S U.  Out: unit lower L (strict part), Dinv = D^-1.
-template <typename R, int N, int NW>
+template <typename R, int N, int NW, uint32_t UM = ~0u>
 PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW], R (&Dinv)[NW], bool& ok) {
   R G[NW][NW];
 #pragma unroll
@@ -204,7 +210,8 @@ PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW
     for (int c = 0; c <= a; ++c) {
       R s = (a == c) ? R(1) : R(0);
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(U[k][a], SU[k][c], s);
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(UM, k * NW + a)) s = fma(U[k][a], SU[k][c], s);
       G[a][c] = s;
     }
   R D[NW];
@@ -611,7 +618,7 @@ PM_INLINE void vapply(const Elem<R, N>& e1, const VF<R, N>& V, VF<R, N>& out, Af
 // Same value function as vapply (up to rounding); the N x N pivoted LU becomes an
 // NW x NW sqrt-free LDL^T.  zero_b: b == 0 (skips S b).  rec (nullable): pass-2
 // record [S U | U^T v] of the input value function (R-P2REC), field stride rstride.
-template <typename R, int N, int NW>
+template <typename R, int N, int NW, uint32_t AM = ~0u, uint32_t UM = ~0u>
 PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const VF<R, N>& V, VF<R, N>& out,
                               bool& ok, R* rec = nullptr, int64_t rstride = 0, bool zero_b = false) {
   R SU[N][NW];
@@ -620,8 +627,13 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
 #pragma unroll
     for (int a = 0; a < NW; ++a) {
       R s = R(0);
+      bool first = true;
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(V.S[sidx(i, k, N)], U[k][a], s);
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(UM, k * NW + a)) {
+          s = first ? V.S[sidx(i, k, N)] * U[k][a] : fma(V.S[sidx(i, k, N)], U[k][a], s);
+          first = false;
+        }
       SU[i][a] = s;
     }
   if (rec) {
@@ -633,12 +645,13 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     for (int a = 0; a < NW; ++a) {
       R s = R(0);
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(U[k][a], V.v[k], s);
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(UM, k * NW + a)) s = fma(U[k][a], V.v[k], s);
       rec[(N * NW + a) * rstride] = s;
     }
   }
   R Lg[NW][NW], dinv[NW];
-  ldl_gram<R, N, NW>(U, SU, Lg, dinv, ok);
+  ldl_gram<R, N, NW, UM>(U, SU, Lg, dinv, ok);
   // Y = L^-1 (S U)^T, Ys = D^-1 Y:  S U G^-1 (S U)^T = Ys^T Y
   R Y[NW][N], Ys[NW][N];
 #pragma unroll
@@ -678,7 +691,8 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
   for (int a = 0; a < NW; ++a) {
     R s = R(0);
 #pragma unroll
-    for (int k = 0; k < N; ++k) s = fma(U[k][a], w[k], s);
+    for (int k = 0; k < N; ++k)
+      if (mask_nz(UM, k * NW + a)) s = fma(U[k][a], w[k], s);
     q[a] = s;
   }
   ldl_solve<R, NW>(Lg, dinv, q);
@@ -697,7 +711,8 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     for (int j = 0; j < N; ++j) {
       R s = R(0);
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(B[i][k], e1.A[k][j], s);
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(AM, k * N + j)) s = fma(B[i][k], e1.A[k][j], s);
       BA[i][j] = s;
     }
   VF<R, N> o;
@@ -707,12 +722,14 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     for (int j = i; j < N; ++j) {
       R s = e1.J[sidx(i, j, N)];
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], BA[k][j], s);
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(AM, k * N + i)) s = fma(e1.A[k][i], BA[k][j], s);
       o.S[sidx(i, j, N)] = s;
     }
     R s = e1.h[i];
 #pragma unroll
-    for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], w[k], s);
+    for (int k = 0; k < N; ++k)
+      if (mask_nz(AM, k * N + i)) s = fma(e1.A[k][i], w[k], s);
     o.v[i] = s;
   }
   out = o;
@@ -753,7 +770,7 @@ PM_INLINE void trans_step(const R (&A)[N][N], const R (&b)[N], const R (&C)[Dim<
 // Pass-2 step from the low-rank record of V_{i-1} (R-P2REC, C_i = U U^T):
 //   w = A_i x_i + b_i + U (U^T v_{i-1}),  x_{i-1} = w - U G^-1 (S U)^T w,  G = I + U^T (S U),
 // which is (I + C_i S_{i-1})^-1 (A_i x_i + b_i + C_i v_{i-1}) by the Woodbury identity.
-template <typename R, int N, int NW>
+template <typename R, int N, int NW, uint32_t AM = ~0u, uint32_t UM = ~0u>
 PM_INLINE void trans_step_rec(const R (&A)[N][N], const R (&b)[N], const R (&U)[N][NW], const R (&SU)[N][NW],
                               const R (&u)[NW], R (&x)[N], bool& ok) {
   R w[N];
@@ -761,13 +778,15 @@ PM_INLINE void trans_step_rec(const R (&A)[N][N], const R (&b)[N], const R (&U)[
   for (int i = 0; i < N; ++i) {
     R s = b[i];
 #pragma unroll
-    for (int k = 0; k < N; ++k) s = fma(A[i][k], x[k], s);
+    for (int k = 0; k < N; ++k)
+      if (mask_nz(AM, i * N + k)) s = fma(A[i][k], x[k], s);
 #pragma unroll
-    for (int a = 0; a < NW; ++a) s = fma(U[i][a], u[a], s);
+    for (int a = 0; a < NW; ++a)
+      if (mask_nz(UM, i * NW + a)) s = fma(U[i][a], u[a], s);
     w[i] = s;
   }
   R Lg[NW][NW], dinv[NW], q[NW];
-  ldl_gram<R, N, NW>(U, SU, Lg, dinv, ok);
+  ldl_gram<R, N, NW, UM>(U, SU, Lg, dinv, ok);
 #pragma unroll
   for (int a = 0; a < NW; ++a) {
     R s = R(0);
@@ -780,7 +799,8 @@ PM_INLINE void trans_step_rec(const R (&A)[N][N], const R (&b)[N], const R (&U)[
   for (int i = 0; i < N; ++i) {
     R s = w[i];
 #pragma unroll
-    for (int a = 0; a < NW; ++a) s = fma(-U[i][a], q[a], s);
+    for (int a = 0; a < NW; ++a)
+      if (mask_nz(UM, i * NW + a)) s = fma(-U[i][a], q[a], s);
     x[i] = s;
   }
 }

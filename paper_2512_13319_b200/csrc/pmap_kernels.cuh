@@ -353,7 +353,7 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     } else {
       src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       if constexpr (Src::LOWRANK > 0)
-        vapply_lowrank<R, N, Src::LOWRANK>(e, src.U, cur, cur, ok, REC ? svt + m * NT + r : nullptr,
+        vapply_lowrank<R, N, Src::LOWRANK, Src::AMASK, Src::UMASK>(e, src.U, cur, cur, ok, REC ? svt + m * NT + r : nullptr,
                                            (int64_t)K * NT, src.zero_b != 0);
       else
         vapply<R, N, false>(e, cur, cur, nullptr, ok);
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
             for (int a = 0; a < NW; ++a) SU[i][a] = rc[i * NW + a];
 #pragma unroll
           for (int a = 0; a < NW; ++a) u[a] = rc[N * NW + a];
-          trans_step_rec<R, N, NW>(At, bt, src.U, SU, u, x, ok);
+          trans_step_rec<R, N, NW, Src::AMASK, Src::UMASK>(At, bt, src.U, SU, u, x, ok);
         }
       }
       __syncthreads();

@@ -30,6 +30,12 @@ constexpr int kNT = 64;  // runs (threads) per tile
 // large problems, 8 (512-node tiles) when that leaves too few tiles to fill the GPU
 constexpr int kKBig = 32;
 constexpr int kKSmall = 8;
+// Structural-zero masks compiled in (R-MASK): the Wiener-velocity model of P:519-548,
+// A = I - dt F with F = [[0, I], [0, 0]] (bits (i, j) -> 4 i + j) and U = sqrt(dt) L chol(W)
+// with L = [0; I] (bits (i, a) -> 2 i + a).  Any (nx, ny, nw) = (4, 2, 2) model whose
+// zeros include these zeros uses the specialised kernels.
+constexpr uint32_t kWienerAMask = (1u << 0) | (1u << 2) | (1u << 5) | (1u << 7) | (1u << 10) | (1u << 15);
+constexpr uint32_t kWienerUMask = (1u << 4) | (1u << 7);
 
 enum class Kind { LTI, TV, NL };
 
@@ -721,7 +727,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare(PlanState& p) {
 // ---------------------------------------------------------- instantiation
 // Factories are declared here and explicitly instantiated, one (dtype, shape,
 // model kind) per translation unit, in inst.cu (see pmap_make.cuh).
-template <typename R, int N, int NY, int KR, int NWC>
+template <typename R, int N, int NY, int KR, int NWC, uint32_t AM, uint32_t UM>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
                  const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
                  const double* Cm, const double* U);

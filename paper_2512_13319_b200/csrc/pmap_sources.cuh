@@ -18,11 +18,15 @@ namespace pmap {
 // y-dependent eta is precomputed on the host at plan time.
 // NWC > 0: the diffusion has low rank, C = dt Q = U U^T with U (N x NWC), and the
 // per-node value-function update uses the Woodbury form (vapply_lowrank, R-LOWRANK).
-template <typename R, int N, int NY, int NWC = 0>
+template <typename R, int N, int NY, int NWC = 0, uint32_t AM = ~0u, uint32_t UM = ~0u>
 struct SrcLTI {
   static constexpr int NS = Dim<N>::NS;
   static constexpr bool IS_LTI_SRC = true;
   static constexpr int LOWRANK = NWC;
+  // structural-zero masks of A (N x N) and U (N x NWC) this instantiation is specialised
+  // for (R-MASK); the plan picks it only when the model's zeros cover the mask's zeros
+  static constexpr uint32_t AMASK = AM;
+  static constexpr uint32_t UMASK = UM;
   static constexpr int NXB = N;  // row width of the nominal trajectory (unused)
   static constexpr bool NEEDS_XBAR = false;
   static constexpr int NYROW = NY;         // doubles of y per node

@@ -204,3 +204,19 @@ def test_euler_blocks_errors(torch_cuda):
     with pytest.raises(pm.MapError):  # only n = 10 is compiled
         pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
                 P0=spec.P0, substeps=7)
+
+
+@pytest.mark.parametrize("T", [5000, 300_001])
+def test_structural_zero_masks_bit_identical(torch_cuda, T, monkeypatch):
+    """R-MASK: the Wiener-velocity kernels specialised on the structural zeros of A and U
+    skip only terms whose factor is exactly 0, so they match the dense kernels bit for
+    bit (and the oracle to 1e-9)."""
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    _, y = wl.simulate_linear(spec, T, seed=77)
+    yd = to_dev(torch, y[None])
+    x_mask = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    monkeypatch.setenv("PMAP_NO_MASK", "1")
+    x_dense = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    assert np.array_equal(x_mask, x_dense)
+    assert rel(x_mask[0], oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)) < TOL64
