@@ -187,10 +187,14 @@ __global__ void __launch_bounds__(NT2) k_p1_tiles(const Geom g, const R* __restr
 
 // ----------------------------------------------------------------- pass 1c
 // Value-function carry entering every group: carry_g = GroupExcl_g (.) carry_in,
-// carry_in = the trajectory's incoming value function ((0,0) on rank 0).
+// carry_in = the trajectory's incoming value function ((0,0) on rank 0).  Time shards
+// (gathered != nullptr): thread 0 first folds the gathered chunk
+// aggregates of the ranks before this one, carry_in = Agg_{r-1} (x) ... (x) Agg_0 (.) (0, 0),
+// and stores it to carry_out (read by k_p2_down at the rank's first node).
 template <typename R, int N>
 __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __restrict__ group_agg,
-                                                   const R* __restrict__ carry_in, R* __restrict__ group_carry,
+                                                   const R* __restrict__ gathered, int rank,
+                                                   R* __restrict__ carry_out, R* __restrict__ group_carry,
                                                    R* __restrict__ total_agg, unsigned long long* flag) {
   using E = Elem<R, N>;
   using V = VF<R, N>;
@@ -224,12 +228,23 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
     __syncthreads();
   }
   store(acc, sh + t, NT3);
+  __shared__ R shc[V::SZ];
+  if (t == 0) {
+    V c0;
+    set_zero(c0);
+    if (gathered) {
+      for (int q = 0; q < rank; ++q) {
+        E a;
+        load(a, gathered + ((int64_t)q * g.batch + b) * E::SZ, 1);
+        vapply<R, N, false>(a, c0, c0, nullptr, ok);
+      }
+      store(c0, carry_out + b * V::SZ, 1);
+    }
+    store(c0, shc, 1);
+  }
   __syncthreads();
   V cin;
-  if (carry_in)
-    load(cin, carry_in + b * V::SZ, 1);
-  else
-    set_zero(cin);
+  load(cin, shc, 1);
   if (t == nact - 1 && total_agg) store(acc, total_agg + b * E::SZ, 1);
   V cur = cin;
   if (t > 0) {
@@ -447,11 +462,15 @@ __global__ void __launch_bounds__(NT2) k_p2_tiles(const Geom g, const R* __restr
 
 // x* at the last node of every tile group (exclusive suffix over group aggregates,
 // seeded with x_end = S_T^-1 v_T on the rank holding node T, or the shard carry).
+// Time shards: payload != nullptr (phase 2) -> thread 0 writes
+// this rank's chunk affine aggregate (+ x*_T = S_T^-1 v_T on the last rank) to payload;
+// gathered != nullptr (phase 3) -> x at the rank's last node is
+// Agg_{r+1} o ... o Agg_{G-1} (x*_T) from the gathered payloads.
 template <typename R, int N, int NT, int K>
 __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __restrict__ svl,
-                                                   const R* __restrict__ group_agg2, const R* __restrict__ xend_in,
-                                                   R* __restrict__ group_carry, R* __restrict__ total_agg2,
-                                                   unsigned long long* flag) {
+                                                   const R* __restrict__ group_agg2, const R* __restrict__ gathered,
+                                                   int rank, int world, R* __restrict__ group_carry,
+                                                   R* __restrict__ payload, unsigned long long* flag) {
   using A = Aff<R, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sh = reinterpret_cast<R*>(smem_raw);  // [A::SZ][NT4] + N
@@ -461,9 +480,15 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
   bool ok = true;
   if (t == 0) {
     R x[N];
-    if (xend_in) {
+    if (gathered) {
+      const int64_t PS = A::SZ + N;
 #pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = xend_in[b * N + i];
+      for (int i = 0; i < N; ++i) x[i] = gathered[((int64_t)(world - 1) * g.batch + b) * PS + A::SZ + i];
+      for (int q = world - 1; q > rank; --q) {
+        A a;
+        load(a, gathered + ((int64_t)q * g.batch + b) * PS, 1);
+        apply(a, x);
+      }
     } else {
       VF<R, N> V;
       load(V, svl + b * VF<R, N>::SZ, 1);
@@ -495,7 +520,14 @@ __global__ void __launch_bounds__(NT4) k_p2_groups(const Geom g, const R* __rest
   }
   store(acc, sh + t, NT4);
   __syncthreads();
-  if (t == 0 && total_agg2) store(acc, total_agg2 + b * A::SZ, 1);
+  if (t == 0 && payload) {
+    R* pp = payload + b * (A::SZ + N);
+    store(acc, pp, 1);
+    if (rank == world - 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) pp[A::SZ + i] = shx[i];
+    }
+  }
   R x[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) x[i] = shx[i];

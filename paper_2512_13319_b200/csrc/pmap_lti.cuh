@@ -43,10 +43,12 @@ struct LtiTables {
   R E1[N * N + 2 * N + 2 * NS];
   // the same, field-major: SF[f][l-1] (f over A, C, J) so lane r reads column r coalesced
   R SF[N * N + 2 * NS][NT];
-  // warp-synchronous Kogge-Stone, lane-indexed (coalesced) coefficient sets:
-  //   UW[lg][u][i][k][lane]: round d = 2^lg (< 32), own span d, partner span min(lane-d+1, d)
-  //   UX[u][i][k][lane]:     cross-warp step, own span lane+1 (in warp 1), partner span 32
-  R UW[5][4][N][N][32];
+  // warp-synchronous Kogge-Stone coefficient sets (compact, so they stay L1-resident):
+  //   UWc: round d = 2^lg (< 32) at offset (d - 1) * 4 N^2, layout [u][i][k][slot], slot =
+  //        partner span - 1 in 0..d-1 (own span d); lane l >= d reads slot min(l - d, d - 1),
+  //        so the d - 1 partial lanes read consecutive doubles and the rest one broadcast slot
+  //   UX[u][i][k][lane]: cross-warp step, own span lane+1 (in warp 1), partner span 32
+  R UWc[31 * 4 * N * N];
   R UX[4][N][N][32];
   // Kogge-Stone round d (1, 2, 4, ..), partner span l2 in 1..d: index d + l2 - 2
   R U1[NT - 1][N][N];
@@ -325,7 +327,7 @@ __global__ void k_lti_setup(const LtiNode<R, N, NY> src, LtiTables<R, N, NT, K>*
     }
   }
   // lane-indexed copies for the warp-synchronous scan
-  auto coeff = [&](int l1, int l2, int lane, R (*dst)[N][N][32]) {
+  auto coeff = [&](int l1, int l2, int slot, R* dst, int stride) {
     // own span l1 (left), partner span l2 (right): U1 = A2 M, U2 = A2 M C1, U3 = A1^T M^T, U4 = A1^T M^T J2
     R C1[Dim<N>::NS], J2[Dim<N>::NS], A1[N][N], A2[N][N], C1m[N][N], J2m[N][N], M[N][N], A2M[N][N], T[N][N];
     for (int k = 0; k < Dim<N>::NS; ++k) {
@@ -352,27 +354,26 @@ __global__ void k_lti_setup(const LtiNode<R, N, NY> src, LtiTables<R, N, NT, K>*
     matmul<R, N>(AtMt, J2m, U4);
     for (int i = 0; i < N; ++i)
       for (int j = 0; j < N; ++j) {
-        dst[0][i][j][lane] = A2M[i][j];
-        dst[1][i][j][lane] = T[i][j];
-        dst[2][i][j][lane] = AtMt[i][j];
-        dst[3][i][j][lane] = U4[i][j];
+        dst[((0 * N + i) * N + j) * stride + slot] = A2M[i][j];
+        dst[((1 * N + i) * N + j) * stride + slot] = T[i][j];
+        dst[((2 * N + i) * N + j) * stride + slot] = AtMt[i][j];
+        dst[((3 * N + i) * N + j) * stride + slot] = U4[i][j];
       }
   };
   for (int lg = 0; lg < 5; ++lg) {
     const int d = 1 << lg;
-    for (int lane = 0; lane < 32; ++lane) {
-      if (lane < d || d > NT / 2) {
-        for (int u = 0; u < 4; ++u)
-          for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) tab->UW[lg][u][i][j][lane] = R(0);
+    R* base = tab->UWc + (d - 1) * 4 * N * N;
+    for (int slot = 0; slot < d; ++slot) {
+      if (d > NT / 2) {
+        for (int q = 0; q < 4 * N * N; ++q) base[q * d + slot] = R(0);
         continue;
       }
-      coeff(d, min(lane - d + 1, d), lane, tab->UW[lg]);
+      coeff(d, slot + 1, slot, base, d);
     }
   }
   for (int lane = 0; lane < 32; ++lane) {
     if (NT > 32)
-      coeff(lane + 1, 32, lane, tab->UX);
+      coeff(lane + 1, 32, lane, &tab->UX[0][0][0][0], 32);
     else
       for (int u = 0; u < 4; ++u)
         for (int i = 0; i < N; ++i)
@@ -396,8 +397,11 @@ PM_INLINE void matvec_acc(const R* __restrict__ M, const R (&x)[N], R (&y)[N]) {
 // REV: reversed node order (two-filter pass B over mirrored elements).
 // The tile's y block is staged through shared memory (coalesced global reads, a
 // padded row per run so the per-run reads are bank-conflict free).
+#ifndef PM_REDUCE_MINB
+#define PM_REDUCE_MINB 8
+#endif
 template <typename R, int N, int NY, int NT, int K, bool REV>
-__global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__ LtiFoldParams<R, N, NY, K, Log2<NT>::value> fp,
+__global__ void __launch_bounds__(NT, PM_REDUCE_MINB) k_p1_reduce_lti(const __grid_constant__ LtiFoldParams<R, N, NY, K, Log2<NT>::value> fp,
                                                       const Geom g, int64_t j_lo, int64_t n_int,
                                                       const R* __restrict__ y,
                                                       const LtiTables<R, N, NT, K>* __restrict__ tab,
@@ -489,8 +493,8 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
   static_assert(NT == 32 || NT == 64, "tile of one or two warps");
   const int lane = r & 31;
   const unsigned FULL = 0xffffffffu;
-  auto step = [&](const R* __restrict__ U, const R (&b2)[N], const R (&h2)[N]) {
-    // U = [4][N][N][32] (lane-indexed): b = U1 b1 + U2 eta2 + b2 ; eta = U3 eta2 - U4 b1 + eta1
+  auto step = [&](const R* __restrict__ U, int stride, int slot, const R (&b2)[N], const R (&h2)[N]) {
+    // U = [4][N][N][stride] (slot-indexed): b = U1 b1 + U2 eta2 + b2 ; eta = U3 eta2 - U4 b1 + eta1
     R nb[N], nh[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -498,10 +502,10 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
       R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        sb = fma(__ldg(U + ((0 * N + i) * N + k) * 32 + lane), bb[k], sb);
-        sb2 = fma(__ldg(U + ((1 * N + i) * N + k) * 32 + lane), h2[k], sb2);
-        sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * 32 + lane), h2[k], sh_);
-        sh2 = fma(-__ldg(U + ((3 * N + i) * N + k) * 32 + lane), bb[k], sh2);
+        sb = fma(__ldg(U + ((0 * N + i) * N + k) * stride + slot), bb[k], sb);
+        sb2 = fma(__ldg(U + ((1 * N + i) * N + k) * stride + slot), h2[k], sb2);
+        sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * stride + slot), h2[k], sh_);
+        sh2 = fma(-__ldg(U + ((3 * N + i) * N + k) * stride + slot), bb[k], sh2);
       }
       nb[i] = sb + sb2;
       nh[i] = sh_ + sh2;
@@ -521,7 +525,7 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
       b2[i] = __shfl_up_sync(FULL, bb[i], d);
       h2[i] = __shfl_up_sync(FULL, hh[i], d);
     }
-    if (lane >= d) step(&tab->UW[lg][0][0][0][0], b2, h2);
+    if (lane >= d) step(tab->UWc + (d - 1) * 4 * N * N, d, min(lane - d, d - 1), b2, h2);
   }
   if (NT == 64) {
     __shared__ R tot[2 * N];
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(NT, 8) k_p1_reduce_lti(const __grid_constant__
         b2[i] = tot[i];
         h2[i] = tot[N + i];
       }
-      step(&tab->UX[0][0][0][0], b2, h2);
+      step(&tab->UX[0][0][0][0], 32, lane, b2, h2);
     }
   }
   // the inclusive prefix: data parts only -- its matrix parts (a span of r + 1 runs)

@@ -260,66 +260,6 @@ inline map_status cuda_fail(PlanState& p, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail((p), _e, #call);  \
   } while (0)
 
-// shard exchange helpers (host-side sequencing; the folds run in tiny kernels)
-template <typename R, int N>
-__global__ void k_shard_fold1(int world, int rank, int64_t batch, const R* __restrict__ gathered,
-                              R* __restrict__ carry_in, unsigned long long* flag) {
-  // gathered: [world][batch][E::SZ]; carry for `rank` = Agg_{rank-1} (x) ... (x) Agg_0 (.) (0,0)
-  using E = Elem<R, N>;
-  using V = VF<R, N>;
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  bool ok = true;
-  V cur;
-  set_zero(cur);
-  for (int q = 0; q < rank; ++q) {
-    E a;
-    load(a, gathered + ((int64_t)q * batch + b) * E::SZ, 1);
-    vapply<R, N, false>(a, cur, cur, nullptr, ok);
-  }
-  store(cur, carry_in + b * V::SZ, 1);
-  if (!ok) atomicMin(flag, 0ull);
-}
-
-template <typename R, int N>
-__global__ void k_shard_pack2(int64_t batch, bool last, const R* __restrict__ total2, const R* __restrict__ svl,
-                              R* __restrict__ payload, unsigned long long* flag) {
-  // payload per trajectory: [Aff total][x_T (last rank only)]
-  using A = Aff<R, N>;
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  for (int k = 0; k < A::SZ; ++k) payload[b * (A::SZ + N) + k] = total2[b * A::SZ + k];
-  if (last) {
-    VF<R, N> V;
-    load(V, svl + b * VF<R, N>::SZ, 1);
-    R x[N];
-    bool ok = true;
-    spd_solve<R, N>(V.S, V.v, x, ok);
-    for (int i = 0; i < N; ++i) payload[b * (A::SZ + N) + A::SZ + i] = x[i];
-    if (!ok) atomicMin(flag, 0ull);
-  }
-}
-
-template <typename R, int N>
-__global__ void k_shard_fold2(int world, int rank, int64_t batch, const R* __restrict__ gathered,
-                              R* __restrict__ xend) {
-  // x at this rank's last node = Agg_{rank+1} o ... o Agg_{world-1} (x_T)
-  using A = Aff<R, N>;
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  const int64_t PS = A::SZ + N;
-  R x[N];
-  for (int i = 0; i < N; ++i) x[i] = gathered[((int64_t)(world - 1) * batch + b) * PS + A::SZ + i];
-  for (int q = world - 1; q > rank; --q) {
-    A a;
-    load(a, gathered + ((int64_t)q * batch + b) * PS, 1);
-    apply(a, x);
-  }
-  for (int i = 0; i < N; ++i) xend[b * N + i] = x[i];
-}
-
-
-
 template <typename R, int N, int NY, class Src, int K>
 struct RunnerT : Runner {
   Src src;
@@ -416,6 +356,11 @@ struct RunnerT : Runner {
     cudaFuncSetAttribute(k_p2_groups<R, N, kNT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_p2groups());
     if constexpr (IS_LTI) {
+      // the LTI reduce is latency bound: let as many 17.5 KB CTAs reside as registers allow
+      cudaFuncSetAttribute(k_p1_reduce_lti<R, N, NY, kNT, K, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           100);
+      cudaFuncSetAttribute(k_p1_reduce_lti<R, N, NY, kNT, K, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           100);
       cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, K, Src, false>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reduce());
       cudaFuncSetAttribute(k_p1_reduce_lti_edge<R, N, NY, kNT, K, Mirror<Src>, true>,
@@ -460,7 +405,8 @@ struct RunnerT : Runner {
     if (payload)  // chunk aggregate only (group carries are recomputed in phase 2)
       PM_LAUNCH(p, s, K_P1_GROUPS,
                 (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                    g, W(L.group_agg1), nullptr, W(L.group_carry1), static_cast<R*>(payload), p.dflag)));
+                    g, W(L.group_agg1), nullptr, 0, nullptr, W(L.group_carry1), static_cast<R*>(payload),
+                    p.dflag)));
   }
 
   void phase2(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* payload) override {
@@ -472,16 +418,10 @@ struct RunnerT : Runner {
     const R* xbar = static_cast<const R*>(xbarv);
     const unsigned ntiles = (unsigned)(g.batch * g.tpt);
     cudaStream_t s = p.stream;
-    const R* carry_in = nullptr;
-    if (gathered) {
-      PM_LAUNCH(p, s, K_SHARD,
-                (k_shard_fold1<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
-                    p.d.world, p.d.rank, g.batch, static_cast<const R*>(gathered), W(L.carry_in), p.dflag)));
-      carry_in = W(L.carry_in);
-    }
     PM_LAUNCH(p, s, K_P1_GROUPS,
               (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                  g, W(L.group_agg1), carry_in, W(L.group_carry1), nullptr, p.dflag)));
+                  g, W(L.group_agg1), static_cast<const R*>(gathered), p.d.rank, W(L.carry_in),
+                  W(L.group_carry1), nullptr, p.dflag)));
     const R* span1 = (use_lti && tab) ? tab->E1 : nullptr;
     const R* sf = (use_lti && tab) ? &tab->SF[0][0] : nullptr;
     p.rec_done = false;
@@ -504,11 +444,8 @@ struct RunnerT : Runner {
     if (payload) {
       PM_LAUNCH(p, s, K_P2_GROUPS,
                 (k_p2_groups<R, N, kNT, K><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
-                    g, W(L.svl), W(L.group_agg2), nullptr, W(L.group_carry2), W(L.total2), p.dflag)));
-      PM_LAUNCH(p, s, K_SHARD,
-                (k_shard_pack2<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
-                    g.batch, p.d.rank == p.d.world - 1, W(L.total2), W(L.svl), static_cast<R*>(payload),
-                    p.dflag)));
+                    g, W(L.svl), W(L.group_agg2), nullptr, p.d.rank, p.d.world, W(L.group_carry2),
+                    static_cast<R*>(payload), p.dflag)));
     }
   }
 
@@ -523,16 +460,10 @@ struct RunnerT : Runner {
     R* x = static_cast<R*>(xv);
     const unsigned ntiles = (unsigned)(g.batch * g.tpt);
     cudaStream_t s = p.stream;
-    const R* xend_in = nullptr;
-    if (gathered) {
-      PM_LAUNCH(p, s, K_SHARD,
-                (k_shard_fold2<R, N><<<(unsigned)((g.batch + 63) / 64), 64, 0, s>>>(
-                    p.d.world, p.d.rank, g.batch, static_cast<const R*>(gathered), W(L.xend))));
-      xend_in = W(L.xend);
-    }
     PM_LAUNCH(p, s, K_P2_GROUPS,
               (k_p2_groups<R, N, kNT, K><<<(unsigned)g.batch, NT4, smem_p2groups(), s>>>(
-                  g, W(L.svl), W(L.group_agg2), xend_in, W(L.group_carry2), nullptr, p.dflag)));
+                  g, W(L.svl), W(L.group_agg2), static_cast<const R*>(gathered), p.d.rank, p.d.world,
+                  W(L.group_carry2), nullptr, p.dflag)));
     if ((fm || fP) && p.rec_done) {
       p.err = "filter outputs need full (S, v) storage: pass filt_m/filt_P at phase 2 as well";
       return;
@@ -607,7 +538,7 @@ struct RunnerT : Runner {
                     g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
       PM_LAUNCH(p, s, K_P1_GROUPS,
                 (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                    g, W(L.group_agg1), nullptr, W(L.group_carry1), nullptr, p.dflag)));
+                    g, W(L.group_agg1), nullptr, 0, nullptr, W(L.group_carry1), nullptr, p.dflag)));
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
@@ -621,7 +552,7 @@ struct RunnerT : Runner {
                     g, W(L.tf_tile), W(L.tf_tincl), W(L.tf_gagg), p.dflag)));
       PM_LAUNCH(p, s2, K_TF_GROUPS,
                 (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s2>>>(
-                    g, W(L.tf_gagg), nullptr, W(L.tf_gcarry), nullptr, p.dflag)));
+                    g, W(L.tf_gagg), nullptr, 0, nullptr, W(L.tf_gcarry), nullptr, p.dflag)));
       cudaEventRecord(p.ev_join, s);
       cudaStreamWaitEvent(s2, p.ev_join, 0);
       PM_LAUNCH(p, s2, K_TF_DOWN,
