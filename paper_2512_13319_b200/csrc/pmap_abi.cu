@@ -229,6 +229,69 @@ static map_status check_flag(PlanState& p) {
   return MAP_OK;
 }
 
+// Run `body` (which launches one solve on p.stream) through the plan's graph cache:
+// the first call with a key runs eagerly (it also sizes any lazily allocated scratch),
+// the second captures the launches (kernels, fork/join events, NCCL all-gathers) into a
+// CUDA graph on a private stream, later calls replay it on p.stream.  Profiling or
+// PMAP_NO_GRAPH=1 run eagerly; a failed capture falls back to eager launches for good.
+template <class Body>
+static map_status graph_run(PlanState& p, const void* const (&key)[6], Body body) {
+  const char* ng = getenv("PMAP_NO_GRAPH");
+  if (p.prof || (ng && ng[0] == '1')) {
+    body();
+    return MAP_OK;
+  }
+  PlanState::GraphEntry* e = nullptr;
+  for (auto& g : p.lgraphs)
+    if (memcmp(g.key, key, sizeof g.key) == 0) e = &g;
+  if (!e) {
+    if (p.lgraphs.size() >= 8) {  // bounded cache: drop the oldest entry
+      if (p.lgraphs.front().exec) cudaGraphExecDestroy(p.lgraphs.front().exec);
+      p.lgraphs.erase(p.lgraphs.begin());
+    }
+    PlanState::GraphEntry ne{};
+    memcpy(ne.key, key, sizeof ne.key);
+    p.lgraphs.push_back(ne);
+    body();
+    return MAP_OK;
+  }
+  if (e->no_graph) {
+    body();
+    return MAP_OK;
+  }
+  if (!e->exec) {
+    cudaStream_t cs;
+    PM_CK(p, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaStream_t saved = p.stream;
+    p.stream = cs;
+    const int64_t l0 = p.launches;
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      body();
+      ok = cudaStreamEndCapture(cs, &graph) == cudaSuccess && p.err.empty();
+    }
+    p.stream = saved;
+    cudaStreamDestroy(cs);
+    if (ok) ok = cudaGraphInstantiate(&e->exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {  // capture unsupported here: eager from now on
+      cudaGetLastError();
+      e->exec = nullptr;
+      e->no_graph = true;
+      p.err.clear();
+      p.launches = l0;
+      body();
+      return MAP_OK;
+    }
+    e->launches = p.launches - l0;
+    p.launches = l0;
+  }
+  PM_CK(p, cudaGraphLaunch(e->exec, p.stream));
+  p.launches += e->launches;
+  return MAP_OK;
+}
+
 static map_status ensure_stage(PlanState& p, void** buf, size_t* have, size_t need) {
   if (*have >= need) return MAP_OK;
   if (*buf) cudaFree(*buf);
@@ -545,6 +608,8 @@ void map_plan_destroy(map_plan_t p) {
   if (!p) return;
   cudaStreamSynchronize(p->stream);
   if (p->graph) cudaGraphExecDestroy(p->graph);
+  for (auto& g : p->lgraphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   cudaFree(p->ws);
   cudaFree(p->dflag);
   cudaFree(p->xbuf[0]);
@@ -653,7 +718,11 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
     p->err = "time-sharded plan without an NCCL communicator: drive the exchange with map_shard_phase";
     return MAP_E_NCCL;
   }
-  p->runner->rts(*p, yd, nullptr, xd, md, Pd);
+  {
+    const void* key[6] = {yd, xd, md, Pd, nullptr, "rts"};
+    map_status gs = graph_run(*p, key, [&] { p->runner->rts(*p, yd, nullptr, xd, md, Pd); });
+    if (gs) return gs;
+  }
   std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
   outs.push_back({x_map, {xd, xb}});
   if (filt_m) outs.push_back({filt_m, {md, mb}});
@@ -684,7 +753,11 @@ map_status map_two_filter(map_plan_t p, const void* y, void* x_map, void* smooth
   if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
   if (!st) st = stage_out_buf(*p, smooth_P, Pb, &p->stage_aux, &p->stage_aux_bytes, &Pd, &blocking);
   if (st) return st;
-  p->runner->two_filter(*p, yd, xd, Pd);
+  {
+    const void* key[6] = {yd, xd, Pd, nullptr, nullptr, "tf"};
+    map_status gs = graph_run(*p, key, [&] { p->runner->two_filter(*p, yd, xd, Pd); });
+    if (gs) return gs;
+  }
   std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
   outs.push_back({x_map, {xd, xb}});
   if (smooth_P) outs.push_back({smooth_P, {Pd, Pb}});

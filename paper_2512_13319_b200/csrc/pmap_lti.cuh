@@ -410,7 +410,11 @@ __global__ void __launch_bounds__(NT, PM_REDUCE_MINB) k_p1_reduce_lti(const __gr
   // The tile's y block is staged in two halves (KH nodes of every run at a time) to keep
   // shared memory small (more CTAs per SM and room in L1 for the scan tables).
   // Padded run rows: 16-byte aligned, consecutive runs 4 banks apart.
-  constexpr int KH = K / 2;
+#ifndef PM_REDUCE_SPLIT
+#define PM_REDUCE_SPLIT 2
+#endif
+  constexpr int NSPLIT = (K / PM_REDUCE_SPLIT) % 2 == 0 ? PM_REDUCE_SPLIT : 2;
+  constexpr int KH = K / NSPLIT;
   static_assert(K % 4 == 0, "run length");
   constexpr int ROW = ((KH * NY * (int)sizeof(R) + 15) / 16 * 16 + 16) / (int)sizeof(R);
   __shared__ __align__(16) R ys[NT * ROW];
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(NT, PM_REDUCE_MINB) k_p1_reduce_lti(const __gr
     acc1[i] = R(0);
   }
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NSPLIT; ++h) {
     // one cp.async (LDGSTS) per node row, all in flight at once
 #pragma unroll 4
     for (int q = r; q < NT * KH; q += NT) {
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(NT, PM_REDUCE_MINB) k_p1_reduce_lti(const __gr
           acc1[i] = fma(fp.GK[m + 1][i][k], y1[k], acc1[i]);
         }
     }
-    if (h == 0) __syncthreads();  // the buffer is refilled by the second half
+    if (h + 1 < NSPLIT) __syncthreads();  // the buffer is refilled by the next part
   }
   R bb[N], hh[N];
 #pragma unroll

@@ -177,6 +177,15 @@ struct PlanState {
   std::string err;
   int64_t launches = 0;
   NcclApi nccl;
+  // linear-solve graph cache (map_solve_linear / map_two_filter on device buffers): a key
+  // seen once runs eagerly, the second time it is captured, then replayed
+  struct GraphEntry {
+    const void* key[6];
+    cudaGraphExec_t exec;
+    int64_t launches;
+    bool no_graph;
+  };
+  std::vector<GraphEntry> lgraphs;
   // nonlinear graph cache
   cudaGraphExec_t graph = nullptr;
   const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -220,3 +220,50 @@ def test_structural_zero_masks_bit_identical(torch_cuda, T, monkeypatch):
     x_dense = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
     assert np.array_equal(x_mask, x_dense)
     assert rel(x_mask[0], oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)) < TOL64
+
+
+@pytest.mark.parametrize("method", ["rts", "tf", "shard_nccl"])
+def test_graph_replay_matches_eager(torch_cuda, method, monkeypatch):
+    """Repeated solves on the same device buffers are captured into a CUDA graph (second
+    call) and replayed (third call on); every call must equal the eager launches exactly."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 70_001
+    _, y = wl.simulate_linear(spec, T, seed=5)
+    yd = to_dev(torch, y[None])
+    comm = None
+    created = False
+    if method == "shard_nccl":
+        import os
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+            created = True
+        comm = dist.group.WORLD._get_backend(torch.device("cuda", 0))._comm_ptr()
+        monkeypatch.setenv("PMAP_FORCE_SHARD", "1")
+    try:
+        _graph_replay_body(torch, pm, spec, T, y, yd, comm, method)
+    finally:
+        if created:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def _graph_replay_body(torch, pm, spec, T, y, yd, comm, method):
+    plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                   P0=spec.P0, nccl_comm=comm)
+    x = torch.empty((1, T + 1, 4), dtype=torch.float64, device="cuda")
+    run = (lambda: plan.two_filter(yd, x)) if method == "tf" else (lambda: plan.solve_linear(yd, x))
+    outs = []
+    for _ in range(4):
+        x.zero_()
+        run()
+        plan.sync()
+        outs.append(x.cpu().numpy().copy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    assert rel(outs[-1][0], xo) < TOL64
