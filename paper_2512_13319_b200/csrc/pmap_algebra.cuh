@@ -535,6 +535,125 @@ PM_INLINE void combine(const Elem<R, N>& e1, const Elem<R, N>& e2, Elem<R, N>& o
   out = o;
 }
 
+// Right operand of combine_g read in place from a field-major (SoA) element, e.g. a
+// partner's slot in shared memory: field f at p[f * s].  Keeps the partner out of
+// registers (the register-resident combine of two elements spills at 255 registers).
+template <typename R, int N>
+struct ElemRef {
+  const R* p;
+  int64_t s;
+  PM_INLINE R A(int i, int j) const { return p[(i * N + j) * s]; }
+  PM_INLINE R b(int i) const { return p[(N * N + i) * s]; }
+  PM_INLINE R C(int k) const { return p[(N * N + N + k) * s]; }
+  PM_INLINE R h(int i) const { return p[(N * N + N + Dim<N>::NS + i) * s]; }
+  PM_INLINE R J(int k) const { return p[(N * N + 2 * N + Dim<N>::NS + k) * s]; }
+};
+
+template <typename R, int N, class E2>
+PM_INLINE void combine_g(const Elem<R, N>& e1, const E2& e2, Elem<R, N>& out, bool& ok) {
+  LUF<R, N> f;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = (i == j) ? R(1) : R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.C[sidx(i, k, N)], e2.J(sidx(k, j, N)), s);
+      f.a[i][j] = s;
+    }
+  lu_factor(f, ok);
+  R X1[N][N], X3[N][N], x2[N], z[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    R t[N], u[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) { t[i] = e1.A[i][c]; u[i] = e1.C[sidx(i, c, N)]; }
+    lu_solve(f, t);
+    lu_solve(f, u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) { X1[i][c] = t[i]; X3[i][c] = u[i]; }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = e1.b[i], w = e2.h(i);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      s = fma(e1.C[sidx(i, k, N)], e2.h(k), s);
+      w = fma(-e2.J(sidx(i, k, N)), e1.b[k], w);
+    }
+    x2[i] = s;
+    z[i] = w;
+  }
+  lu_solve(f, x2);
+  lu_solve_t(f, z);
+  Elem<R, N> o;
+  // A, b
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e2.A(i, k), X1[k][j], s);
+      o.A[i][j] = s;
+    }
+    R s = e2.b(i);
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(e2.A(i, k), x2[k], s);
+    o.b[i] = s;
+  }
+  // C = (A2 X3) A2^T + C2 (upper triangle)
+  {
+    R T1[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        R s = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(e2.A(i, k), X3[k][j], s);
+        T1[i][j] = s;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R s = e2.C(sidx(i, j, N));
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(T1[i][k], e2.A(j, k), s);
+        o.C[sidx(i, j, N)] = s;
+      }
+  }
+  // J = A1^T (J2 X1) + J1 (upper triangle); eta = A1^T z + eta1
+  {
+    R Y[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        R s = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(e2.J(sidx(i, k, N)), X1[k][j], s);
+        Y[i][j] = s;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i; j < N; ++j) {
+        R s = e1.J[sidx(i, j, N)];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], Y[k][j], s);
+        o.J[sidx(i, j, N)] = s;
+      }
+      R s = e1.h[i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(e1.A[k][i], z[k], s);
+      o.h[i] = s;
+    }
+  }
+  out = o;
+}
+
 // e1 (x) (0, 0, 0, v, S): the value function of P:333-336 one interval earlier.
 //   S' = A1^T S (I + C1 S)^-1 A1 + J1,  v' = A1^T (I + S C1)^-1 (v - S b1) + eta1.
 // Also returns the pass-2 transition of the same interval (P:163-198 discretised,

@@ -683,11 +683,7 @@ __global__ void __launch_bounds__(NT) k_p1_reduce_lti_edge(const __grid_constant
   for (int d = 1; d < NT; d <<= 1) {
     store(acc, sh + r, NT);
     __syncthreads();
-    if (r >= d) {
-      E p;
-      load(p, sh + r - d, NT);
-      combine(acc, p, acc, ok);
-    }
+    if (r >= d) combine_g(acc, ElemRef<R, N>{sh + r - d, NT}, acc, ok);
     __syncthreads();
   }
   store(acc, run_incl + tile * (int64_t)E::SZ * NT + r, NT);
