@@ -18,6 +18,7 @@
 #include "pmap_tf.cuh"
 #include "pmap_lti.cuh"
 #include "pmap_seq.cuh"
+#include "pmap_lti_scan.cuh"
 #include <cstdlib>
 #include <type_traits>
 
@@ -280,6 +281,8 @@ struct RunnerT : Runner {
   static constexpr bool kRec = Src::LOWRANK > 0 && Src::LOWRANK * (N + 1) < VF<R, N>::SZ;
   using Tab = LtiTables<R, N, kNT, K>;
   Tab* tab = nullptr;    // pass-1 tables (LTI only)
+  LtiScanTables<R, N>* scan_tab = nullptr;    // data-only tile / group scans (LTI only)
+  LtiScanTables<R, N>* scan_tab_m = nullptr;  // the same for the mirrored elements (two-filter pass B)
   Tab* tab_m = nullptr;  // mirrored-element tables (two-filter pass B)
   LtiNode<R, N, NY> lnode{}, lnode_m{};
   LtiFoldParams<R, N, NY, K, Log2<kNT>::value> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
@@ -288,6 +291,8 @@ struct RunnerT : Runner {
   ~RunnerT() override {
     cudaFree(tab);
     cudaFree(tab_m);
+    cudaFree(scan_tab);
+    cudaFree(scan_tab_m);
   }
 
   bool prepare(PlanState& p) override;
@@ -340,6 +345,40 @@ struct RunnerT : Runner {
     }
   }
 
+  // Scans of tile aggregates within groups and of group aggregates (carries): the
+  // data-only LTI kernels (pmap_lti_scan.cuh) when the plan has their tables and the
+  // trajectory has at most kScanB groups, else the general kernels.
+  bool lti_scan(const PlanState& p, bool rev) const {
+    const char* e = getenv("PMAP_NO_LTI_SCAN");
+    return use_lti && (rev ? scan_tab_m : scan_tab) && p.g.gpt <= kScanB && smem_scan() <= 180 * 1024 &&
+           !(e && e[0] == '1');
+  }
+  void tiles1(PlanState& p, cudaStream_t s, int kid, bool rev, R* tile_agg, R* tile_incl, R* group_agg) {
+    const Geom& g = p.g;
+    if (lti_scan(p, rev))
+      PM_LAUNCH(p, s, kid,
+                (k_p1_tiles_lti<R, N><<<(unsigned)(g.batch * g.gpt), kScanB, smem_scan(), s>>>(
+                    g, tile_agg, tile_incl, group_agg, rev ? scan_tab_m : scan_tab, lti_jlo(g, rev), lti_jhi(g),
+                    p.dflag)));
+    else
+      PM_LAUNCH(p, s, kid,
+                (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(g, tile_agg, tile_incl,
+                                                                                         group_agg, p.dflag)));
+  }
+  void groups1(PlanState& p, cudaStream_t s, int kid, bool rev, R* group_agg, const R* gathered, R* carry_out,
+               R* group_carry, R* total) {
+    const Geom& g = p.g;
+    if (lti_scan(p, rev))
+      PM_LAUNCH(p, s, kid,
+                (k_p1_groups_lti<R, N><<<(unsigned)g.batch, kScanB, smem_scan(), s>>>(
+                    g, group_agg, gathered, p.d.rank, carry_out, group_carry, total, rev ? scan_tab_m : scan_tab,
+                    lti_jlo(g, rev), lti_jhi(g), p.dflag)));
+    else
+      PM_LAUNCH(p, s, kid,
+                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
+                    g, group_agg, gathered, p.d.rank, carry_out, group_carry, total, p.dflag)));
+  }
+
   size_t ws_bytes(const Geom& g, bool tf) const override {
     WsLayout<R, N, K> L;
     L.plan(g, tf);
@@ -348,6 +387,7 @@ struct RunnerT : Runner {
   int sizeof_real() const override { return (int)sizeof(R); }
 
   static size_t smem_reduce() { return sizeof(R) * E::SZ * kNT; }
+  static size_t smem_scan() { return sizeof(R) * E::SZ * kScanB; }
   static size_t smem_tiles() { return sizeof(R) * E::SZ * NT2; }
   static size_t smem_groups() { return sizeof(R) * E::SZ * NT3; }
   static size_t smem_down() { return sizeof(R) * (A::SZ * kNT > V::SZ ? A::SZ * kNT : V::SZ); }
@@ -365,6 +405,10 @@ struct RunnerT : Runner {
     cudaFuncSetAttribute(k_p2_groups<R, N, kNT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_p2groups());
     if constexpr (IS_LTI) {
+      if (smem_scan() <= 180 * 1024) {
+        cudaFuncSetAttribute(k_p1_tiles_lti<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_scan());
+        cudaFuncSetAttribute(k_p1_groups_lti<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_scan());
+      }
       // the LTI reduce is latency bound: let as many 17.5 KB CTAs reside as registers allow
       cudaFuncSetAttribute(k_p1_reduce_lti<R, N, NY, kNT, K, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            100);
@@ -408,14 +452,10 @@ struct RunnerT : Runner {
     const R* xbar = static_cast<const R*>(xbarv);
     cudaStream_t s = p.stream;
     reduce1<false>(p, s, K_P1_REDUCE, src, fold, tab, y, xbar, W(L.run_incl), W(L.tile_agg1));
-    PM_LAUNCH(p, s, K_P1_TILES,
-              (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
-                  g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
+    tiles1(p, s, K_P1_TILES, false, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1));
     if (payload)  // chunk aggregate only (group carries are recomputed in phase 2)
-      PM_LAUNCH(p, s, K_P1_GROUPS,
-                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                    g, W(L.group_agg1), nullptr, 0, nullptr, W(L.group_carry1), static_cast<R*>(payload),
-                    p.dflag)));
+      groups1(p, s, K_P1_GROUPS, false, W(L.group_agg1), nullptr, nullptr, W(L.group_carry1),
+              static_cast<R*>(payload));
   }
 
   void phase2(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* payload) override {
@@ -427,10 +467,8 @@ struct RunnerT : Runner {
     const R* xbar = static_cast<const R*>(xbarv);
     const unsigned ntiles = (unsigned)(g.batch * g.tpt);
     cudaStream_t s = p.stream;
-    PM_LAUNCH(p, s, K_P1_GROUPS,
-              (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                  g, W(L.group_agg1), static_cast<const R*>(gathered), p.d.rank, W(L.carry_in),
-                  W(L.group_carry1), nullptr, p.dflag)));
+    groups1(p, s, K_P1_GROUPS, false, W(L.group_agg1), static_cast<const R*>(gathered), W(L.carry_in),
+            W(L.group_carry1), nullptr);
     const R* span1 = (use_lti && tab) ? tab->E1 : nullptr;
     const R* sf = (use_lti && tab) ? &tab->SF[0][0] : nullptr;
     p.rec_done = false;
@@ -542,12 +580,8 @@ struct RunnerT : Runner {
       cudaStreamWaitEvent(s2, p.ev_fork, 0);
       // pass A: forward filter (S_i, v_i)
       reduce1<false>(p, s, K_P1_REDUCE, src, fold, tab, y, nullptr, W(L.run_incl), W(L.tile_agg1));
-      PM_LAUNCH(p, s, K_P1_TILES,
-                (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s>>>(
-                    g, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1), p.dflag)));
-      PM_LAUNCH(p, s, K_P1_GROUPS,
-                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s>>>(
-                    g, W(L.group_agg1), nullptr, 0, nullptr, W(L.group_carry1), nullptr, p.dflag)));
+      tiles1(p, s, K_P1_TILES, false, W(L.tile_agg1), W(L.tile_incl1), W(L.group_agg1));
+      groups1(p, s, K_P1_GROUPS, false, W(L.group_agg1), nullptr, nullptr, W(L.group_carry1), nullptr);
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
@@ -556,12 +590,8 @@ struct RunnerT : Runner {
       // pass B: backward information filter over mirrored elements (reverse node order)
       Mirror<Src> mir{src, g.node0 + g.Nn - 1};
       reduce1<true>(p, s2, K_TF_REDUCE, mir, fold_m, tab_m, y, nullptr, W(L.tf_run), W(L.tf_tile));
-      PM_LAUNCH(p, s2, K_TF_TILES,
-                (k_p1_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_tiles(), s2>>>(
-                    g, W(L.tf_tile), W(L.tf_tincl), W(L.tf_gagg), p.dflag)));
-      PM_LAUNCH(p, s2, K_TF_GROUPS,
-                (k_p1_groups<R, N><<<(unsigned)g.batch, NT3, smem_groups(), s2>>>(
-                    g, W(L.tf_gagg), nullptr, 0, nullptr, W(L.tf_gcarry), nullptr, p.dflag)));
+      tiles1(p, s2, K_TF_TILES, true, W(L.tf_tile), W(L.tf_tincl), W(L.tf_gagg));
+      groups1(p, s2, K_TF_GROUPS, true, W(L.tf_gagg), nullptr, nullptr, W(L.tf_gcarry), nullptr);
       cudaEventRecord(p.ev_join, s);
       cudaStreamWaitEvent(s2, p.ev_join, 0);
       PM_LAUNCH(p, s2, K_TF_DOWN,
@@ -632,6 +662,25 @@ bool RunnerT<R, N, NY, Src, K>::prepare(PlanState& p) {
       return false;
     k_lti_setup<R, N, NY, kNT, K><<<1, 1>>>(lnode, tab, dok);
     k_lti_setup<R, N, NY, kNT, K><<<1, 1>>>(lnode_m, tab_m, dok + 1);
+    int* dok2 = nullptr;
+    if (cudaMalloc(&scan_tab, sizeof(LtiScanTables<R, N>)) == cudaSuccess &&
+        cudaMalloc(&scan_tab_m, sizeof(LtiScanTables<R, N>)) == cudaSuccess &&
+        cudaMalloc(&dok2, 2 * sizeof(int)) == cudaSuccess) {
+      k_lti_scan_setup<R, N, kNT, K><<<1, 1>>>(tab, scan_tab, dok2);
+      k_lti_scan_setup<R, N, kNT, K><<<1, 1>>>(tab_m, scan_tab_m, dok2 + 1);
+      int ok2[2] = {0, 0};
+      if (cudaMemcpy(ok2, dok2, sizeof ok2, cudaMemcpyDeviceToHost) != cudaSuccess || !ok2[0] || !ok2[1]) {
+        cudaGetLastError();
+        cudaFree(scan_tab);
+        cudaFree(scan_tab_m);
+        scan_tab = scan_tab_m = nullptr;  // general scans
+      }
+    } else {
+      cudaGetLastError();
+      cudaFree(scan_tab);
+      scan_tab = scan_tab_m = nullptr;
+    }
+    cudaFree(dok2);
     int ok[2] = {0, 0};
     cudaError_t e = cudaMemcpy(ok, dok, sizeof ok, cudaMemcpyDeviceToHost);
     cudaFree(dok);

@@ -267,3 +267,26 @@ def _graph_replay_body(torch, pm, spec, T, y, yd, comm, method):
         assert np.array_equal(o, outs[0])
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     assert rel(outs[-1][0], xo) < TOL64
+
+
+@pytest.mark.parametrize("case,T,B", [("rts", 300_001, 1), ("rts", 10_000_000, 1), ("tf", 40_000, 3),
+                                       ("rts_k8", 9_000, 2), ("rts", 2_048 * 128 * 3, 1), ("rts", 2_048 * 3 - 1, 1)])
+def test_lti_data_only_scans_match_general(torch_cuda, case, T, B, monkeypatch):
+    """The data-only LTI tile / group scans (pmap_lti_scan.cuh) agree with the general
+    combine-based scans to rounding (<= 1e-12 relative) and with the oracle (1e-9)."""
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    if case == "rts_k8":
+        monkeypatch.setenv("PMAP_K", "8")
+    _, y = wl.simulate_linear(spec, T, seed=T % 1000, batch=B)
+    y = y.reshape(B, T + 1, 2)
+    yd = to_dev(torch, y)
+    run = (lambda pl: pl.two_filter(yd)) if case == "tf" else (lambda pl: pl.solve_linear(yd))
+    x_scan = run(gpu_plan(spec, T, batch=B)).cpu().numpy()
+    monkeypatch.setenv("PMAP_NO_LTI_SCAN", "1")
+    x_gen = run(gpu_plan(spec, T, batch=B)).cpu().numpy()
+    for b in range(B):
+        assert rel(x_scan[b], x_gen[b]) < 1e-12
+        if T <= 400_000:
+            assert rel(x_scan[b], oracle.kf_rts(ora_model(spec), y[b], T, spec.t0, spec.tf)) < TOL64

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_next_rows_gpu.py -q -x -k "data_only" > gpurun_out/p31_scan.log 2>&1; echo "rc=$?" >> gpurun_out/p31_scan.log
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/p31_all.log 2>&1; echo "rc=$?" >> gpurun_out/p31_all.log
+for c in C3 C2 C5; do timeout 600 python bench.py --config $c --steps 100 --no-cpu-baseline --no-e2e --no-seq > gpurun_out/b31_$c.log 2>&1; done
+for G in 8; do timeout 300 python tools/shard_probe.py $G >> gpurun_out/p31_probe.log 2>&1; done
