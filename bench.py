@@ -60,6 +60,7 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
     d = 8
     reduce_fl = 2 * N * ny if lti else combine  # LTI: impulse-response fold (y_m -> (b, eta))
     vsz2 = vsz  # per-node values pass 1 stores for pass 2
+    vapply_dense = vapply
     if nw > 0:  # R-LOWRANK node update (vapply_lowrank), R-P2REC records when smaller than (S, v)
         r = nw
         am = np.ones((N, N), bool) if amask is None else np.asarray(amask, bool)
@@ -72,6 +73,10 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         # when b == 0), q = G^-1 U^T w, w - S U q, B A, A^T (B A) + J, A^T w + eta
         vapply = (N * nU + chol + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
                   + nU + r * r + N * r + N * nA + ata + nA)
+        gram_d = sum((a + 1) * N for a in range(r))
+        chol_d = gram_d + r * (r - 1) // 2 * (r + 1) + r
+        vapply_dense = (N * N * r + chol_d + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
+                        + N * r + r * r + N * r + N * N * N + ns * N + N * N)
         if r * (N + 1) < vsz:
             vsz2 = r * (N + 1)
             vapply += nU  # U^T v
@@ -86,8 +91,16 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
             "solve": (2 * (combine + 2 * build + vapply + vapply_tr / K + trans + build // 2),
                       d * (3 * ny_row + 2 * vsz + nx)),
         }
+    # two-filter pass B epilogue (k_tf_down): mirrored node update (the mirrored diffusion
+    # factor is dense) + LDL^T solve of (S + Lam - J^m) x = v + xi - eta^m; reads y, the
+    # stored (S, v) and the run prefix, writes x
+    ldl = N ** 3 // 6 + N * N + 2 * N * N
+    vap_m = vapply_dense if nw > 0 else vapply
+    tf_down = (2 * (vap_m + ldl + 2 * N + ns), d * (ny + esz / K + vsz + nx))
     return {
         "k_p1_reduce": (2 * reduce_fl, d * (ny + esz / K)),
+        "k_tf_reduce": (2 * reduce_fl, d * (ny + esz / K)),
+        "k_tf_down": tf_down,
         "k_p1_down": (2 * (vapply + vapply_tr / K), d * (ny + esz / K + vsz2 + asz / K)),
         "k_p2_down": (2 * trans, d * (vsz2 + nx + asz / K)),
         "solve": (2 * (reduce_fl + vapply + vapply_tr / K + trans), d * (ny + 2 * vsz + nx)),
