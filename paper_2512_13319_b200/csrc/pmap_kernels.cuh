@@ -82,6 +82,72 @@ PM_INLINE void load_prefix(Elem<R, N>& p, const R* __restrict__ row, const R* __
   }
 }
 
+// Inclusive scan over the NT runs of a tile, data parts (b, eta) only (R-LTI): warp-
+// synchronous Kogge-Stone with shuffles and the compact coefficient tables (UWc: lanes
+// d..2d-2 read consecutive slots, the rest one broadcast slot), then one cross-warp step
+// with warp 0's total (UX).  Thread r holds its run's aggregate on entry, the inclusive
+// prefix of runs 0..r on exit.
+template <typename R, int N, int NT>
+PM_INLINE void lti_run_scan(const R* __restrict__ UWc, const R* __restrict__ UX, int r, R (&bb)[N], R (&hh)[N]) {
+  static_assert(NT == 32 || NT == 64, "tile of one or two warps");
+  const int lane = r & 31;
+  const unsigned FULL = 0xffffffffu;
+  auto step = [&](const R* __restrict__ U, int stride, int slot, const R (&b2)[N], const R (&h2)[N]) {
+    // U = [4][N][N][stride] (slot-indexed): b = U1 b1 + U2 eta2 + b2 ; eta = U3 eta2 - U4 b1 + eta1
+    R nb[N], nh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      // two independent accumulators per output (halves the dependent FMA chain)
+      R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sb = fma(__ldg(U + ((0 * N + i) * N + k) * stride + slot), bb[k], sb);
+        sb2 = fma(__ldg(U + ((1 * N + i) * N + k) * stride + slot), h2[k], sb2);
+        sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * stride + slot), h2[k], sh_);
+        sh2 = fma(-__ldg(U + ((3 * N + i) * N + k) * stride + slot), bb[k], sh2);
+      }
+      nb[i] = sb + sb2;
+      nh[i] = sh_ + sh2;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = nb[i];
+      hh[i] = nh[i];
+    }
+  };
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {
+    const int d = 1 << lg;
+    R b2[N], h2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b2[i] = __shfl_up_sync(FULL, bb[i], d);
+      h2[i] = __shfl_up_sync(FULL, hh[i], d);
+    }
+    if (lane >= d) step(UWc + (d - 1) * 4 * N * N, d, min(lane - d, d - 1), b2, h2);
+  }
+  if (NT == 64) {
+    __shared__ R tot[2 * N];
+    if (r == 31) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        tot[i] = bb[i];
+        tot[N + i] = hh[i];
+      }
+    }
+    __syncthreads();
+    if (r >= 32) {
+      R b2[N], h2[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        b2[i] = tot[i];
+        h2[i] = tot[N + i];
+      }
+      step(UX, 32, lane, b2, h2);
+    }
+  }
+}
+
 // ----------------------------------------------------------------- pass 1a
 // nsel > 0: only the listed tiles {jsel0, jsel1} of each trajectory (the boundary
 // tiles left over by the LTI-specialised reduce), else every tile.
@@ -263,6 +329,80 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
   if (!ok) flag_node(flag, g.node0);
 }
 
+// Value function entering run r of a tile: cur (the tile carry) advanced over runs
+// 0..r-1.  LTI interior tiles (uwc != nullptr): the exclusive run prefix is scanned here
+// from the stored run aggregates, data parts only (lti_run_scan; matrix parts from the
+// plan table sf); otherwise the reduce stored the inclusive prefixes (load_prefix).
+template <typename R, int N, int NT>
+PM_INLINE void run_carry(const R* __restrict__ run_incl, const Geom& g, int64_t tile, int r, bool interior,
+                         const R* __restrict__ sf, const R* __restrict__ uwc, const R* __restrict__ ux,
+                         VF<R, N>& cur, bool& ok) {
+  using E = Elem<R, N>;
+#ifdef PM_REDUCE_TREE
+  if (interior && uwc) {  // block-uniform
+    const R* pa = run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r;  // run aggregates
+    R bb[N], hh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = pa[(N * N + i) * NT];
+      hh[i] = pa[(N * N + N + Dim<N>::NS + i) * NT];
+    }
+    lti_run_scan<R, N, NT>(uwc, ux, r, bb, hh);
+    // exclusive prefix of run r = inclusive prefix of run r - 1
+    __shared__ R x31[2 * N];
+    if (r == 31) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        x31[i] = bb[i];
+        x31[N + i] = hh[i];
+      }
+    }
+    R pb[N], ph[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      pb[i] = __shfl_up_sync(0xffffffffu, bb[i], 1);
+      ph[i] = __shfl_up_sync(0xffffffffu, hh[i], 1);
+    }
+    __syncthreads();
+    if (r == 32) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        pb[i] = x31[i];
+        ph[i] = x31[N + i];
+      }
+    }
+    if (r > 0) {
+      E p;
+      const R* sfr = sf + (r - 1);
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) p.A[i][j] = __ldg(sfr + (f++) * NT);
+#pragma unroll
+      for (int k = 0; k < Dim<N>::NS; ++k) p.C[k] = __ldg(sfr + (f++) * NT);
+#pragma unroll
+      for (int k = 0; k < Dim<N>::NS; ++k) p.J[k] = __ldg(sfr + (f++) * NT);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        p.b[i] = pb[i];
+        p.h[i] = ph[i];
+      }
+      vapply<R, N, false>(p, cur, cur, nullptr, ok);
+    }
+    return;
+  }
+#else
+  (void)uwc;
+  (void)ux;
+#endif
+  if (r > 0) {
+    E p;
+    load_prefix<R, N, NT>(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), interior ? sf + (r - 1) : nullptr);
+    vapply<R, N, false>(p, cur, cur, nullptr, ok);
+  }
+}
+
 // ----------------------------------------------------------------- pass 1d
 // 6 resident 64-thread CTAs per SM for nx <= 4 (<= 168 registers: measured 10 %
 // faster than the unconstrained 186-register build at nx = 4); nx = 5 unconstrained.
@@ -282,7 +422,8 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
                                                 R* __restrict__ run_suf, R* __restrict__ tile_agg2,
                                                 unsigned long long* flag, const R* __restrict__ span1,
                                                 const R* __restrict__ sf, int64_t j_lo, int64_t j_hi,
-                                                R* __restrict__ svl) {
+                                                R* __restrict__ svl, const R* __restrict__ uwc = nullptr,
+                                                const R* __restrict__ ux = nullptr) {
   static_assert(!REC || Src::LOWRANK > 0, "pass-2 records need a low-rank source");
   using E = Elem<R, N>;
   using V = VF<R, N>;
@@ -313,11 +454,7 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
   load(cur, sh, 1);
   __syncthreads();
   const bool interior = sf && j >= j_lo && j < j_hi;
-  if (r > 0) {
-    E p;
-    load_prefix<R, N, NT>(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), interior ? sf + (r - 1) : nullptr);
-    vapply<R, N, false>(p, cur, cur, nullptr, ok);
-  }
+  run_carry<R, N, NT>(run_incl, g, tile, r, interior, sf, uwc, ux, cur, ok);
   // Pass-2 aggregate of the run (maps x*_e -> x*_{s-1}), R-RUNAGG: by dynamic
   // programming it is the argmin of V_{s-1}(x) + R(x_e; x) over x for the run's own
   // aggregate element R, i.e. the transition of vapply(R, V_{s-1}) -- one solve per

@@ -393,6 +393,68 @@ PM_INLINE void matvec_acc(const R* __restrict__ M, const R (&x)[N], R (&y)[N]) {
   }
 }
 
+// Total of the NT run aggregates of a tile (data parts): a binary tree over aligned,
+// equal spans, so every combine uses the full-span coefficient set of its level
+// (fp.Uf, constant-bank operands; no table loads).  Thread NT-1 ends with the total.
+template <typename R, int N, int NY, int NT, int K>
+PM_INLINE void lti_run_reduce(const LtiFoldParams<R, N, NY, K, Log2<NT>::value>& fp, int r, R (&bb)[N],
+                              R (&hh)[N]) {
+  const int lane = r & 31;
+  const unsigned FULL = 0xffffffffu;
+  auto step = [&](int lg, const R (&b2)[N], const R (&h2)[N]) {
+    R nb[N], nh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sb = fma(fp.Uf[lg][0][i][k], bb[k], sb);
+        sb2 = fma(fp.Uf[lg][1][i][k], h2[k], sb2);
+        sh_ = fma(fp.Uf[lg][2][i][k], h2[k], sh_);
+        sh2 = fma(-fp.Uf[lg][3][i][k], bb[k], sh2);
+      }
+      nb[i] = sb + sb2;
+      nh[i] = sh_ + sh2;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = nb[i];
+      hh[i] = nh[i];
+    }
+  };
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {
+    const int d = 1 << lg;
+    R b2[N], h2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b2[i] = __shfl_up_sync(FULL, bb[i], d);
+      h2[i] = __shfl_up_sync(FULL, hh[i], d);
+    }
+    if (((lane + 1) & (2 * d - 1)) == 0) step(lg, b2, h2);  // lane ends an aligned span of 2d runs
+  }
+  if (NT == 64) {
+    __shared__ R tot[2 * N];
+    if (r == 31) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        tot[i] = bb[i];
+        tot[N + i] = hh[i];
+      }
+    }
+    __syncthreads();
+    if (r == 63) {
+      R b2[N], h2[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        b2[i] = tot[i];
+        h2[i] = tot[N + i];
+      }
+      step(5, b2, h2);
+    }
+  }
+}
+
 // Interior tiles only: blockIdx.x -> (trajectory b, tile j = j_lo + blockIdx.x % n_int).
 // REV: reversed node order (two-filter pass B over mirrored elements).
 // The tile's y block is staged through shared memory (coalesced global reads, a
@@ -491,74 +553,22 @@ __global__ void __launch_bounds__(NT, PM_REDUCE_MINB) k_p1_reduce_lti(const __gr
       oa[(N * N + N + Dim<N>::NS + i) * NT] = hh[i];
     }
   }
-  // Scan over the runs, data parts only: warp-synchronous Kogge-Stone with shuffles
-  // (lane-indexed coefficient tables -> coalesced loads, no divergence), then one
-  // cross-warp step with warp 0's total.
-  static_assert(NT == 32 || NT == 64, "tile of one or two warps");
-  const int lane = r & 31;
-  const unsigned FULL = 0xffffffffu;
-  auto step = [&](const R* __restrict__ U, int stride, int slot, const R (&b2)[N], const R (&h2)[N]) {
-    // U = [4][N][N][stride] (slot-indexed): b = U1 b1 + U2 eta2 + b2 ; eta = U3 eta2 - U4 b1 + eta1
-    R nb[N], nh[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      // two independent accumulators per output (halves the dependent FMA chain)
-      R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        sb = fma(__ldg(U + ((0 * N + i) * N + k) * stride + slot), bb[k], sb);
-        sb2 = fma(__ldg(U + ((1 * N + i) * N + k) * stride + slot), h2[k], sb2);
-        sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * stride + slot), h2[k], sh_);
-        sh2 = fma(-__ldg(U + ((3 * N + i) * N + k) * stride + slot), bb[k], sh2);
-      }
-      nb[i] = sb + sb2;
-      nh[i] = sh_ + sh2;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      bb[i] = nb[i];
-      hh[i] = nh[i];
-    }
-  };
-#pragma unroll
-  for (int lg = 0; lg < 5; ++lg) {
-    const int d = 1 << lg;
-    R b2[N], h2[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      b2[i] = __shfl_up_sync(FULL, bb[i], d);
-      h2[i] = __shfl_up_sync(FULL, hh[i], d);
-    }
-    if (lane >= d) step(tab->UWc + (d - 1) * 4 * N * N, d, min(lane - d, d - 1), b2, h2);
-  }
-  if (NT == 64) {
-    __shared__ R tot[2 * N];
-    if (r == 31) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        tot[i] = bb[i];
-        tot[N + i] = hh[i];
-      }
-    }
-    __syncthreads();
-    if (r >= 32) {
-      R b2[N], h2[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        b2[i] = tot[i];
-        h2[i] = tot[N + i];
-      }
-      step(&tab->UX[0][0][0][0], 32, lane, b2, h2);
-    }
-  }
-  // the inclusive prefix: data parts only -- its matrix parts (a span of r + 1 runs)
-  // are the plan table SF[.][r], which the consumers (load_prefix) read instead
+#ifndef PM_REDUCE_TREE
+  // inclusive run prefixes here (the down-sweeps then read them)
+  lti_run_scan<R, N, NT>(tab->UWc, &tab->UX[0][0][0][0], r, bb, hh);
   R* out = run_incl + tile * (int64_t)E::SZ * NT + r;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     out[(N * N + i) * NT] = bb[i];
     out[(N * N + N + Dim<N>::NS + i) * NT] = hh[i];
   }
+#else
+  // PM_REDUCE_TREE (measured slower at C3: the scan moved into the occupancy-limited
+  // down-sweep costs more than it saves here): only the tile aggregate, a tree over
+  // aligned equal spans with uniform (constant-bank) coefficients; the down-sweeps scan
+  // the stored run aggregates themselves (run_carry)
+  lti_run_reduce<R, N, NY, NT, K>(fp, r, bb, hh);
+#endif
   if (r == NT - 1) {
     E e;
 #pragma unroll

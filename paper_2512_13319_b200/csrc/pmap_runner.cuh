@@ -345,6 +345,20 @@ struct RunnerT : Runner {
     }
   }
 
+  // in-tile run-scan tables for the down-sweeps (reduce stores run aggregates only, R-LTI)
+  const R* uwc(bool rev) const {
+#ifndef PM_REDUCE_TREE
+    (void)rev;
+    return nullptr;
+#else
+    const Tab* t = rev ? tab_m : tab;
+    return (use_lti && t) ? t->UWc : nullptr;
+#endif
+  }
+  const R* ux(bool rev) const {
+    const Tab* t = rev ? tab_m : tab;
+    return (use_lti && t) ? &t->UX[0][0][0][0] : nullptr;
+  }
   // Scans of tile aggregates within groups and of group aggregates (carries): the
   // data-only LTI kernels (pmap_lti_scan.cuh) when the plan has their tables and the
   // trajectory has at most kScanB groups, else the general kernels.
@@ -478,12 +492,12 @@ struct RunnerT : Runner {
         PM_LAUNCH(p, s, K_P1_DOWN,
                   (k_p1_down<R, N, NY, kNT, K, Src, true, true><<<ntiles, kNT, smem_down(), s>>>(
                       src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
-                      W(L.tile_agg2), p.dflag, span1, sf, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
+                      W(L.tile_agg2), p.dflag, span1, sf, lti_jlo(g, false), lti_jhi(g), W(L.svl), uwc(false), ux(false))));
     } else {
       PM_LAUNCH(p, s, K_P1_DOWN,
                 (k_p1_down<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, xbar, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), W(L.run_suf),
-                    W(L.tile_agg2), p.dflag, span1, sf, lti_jlo(g, false), lti_jhi(g), W(L.svl))));
+                    W(L.tile_agg2), p.dflag, span1, sf, lti_jlo(g, false), lti_jhi(g), W(L.svl), uwc(false), ux(false))));
     }
     PM_LAUNCH(p, s, K_P2_TILES,
               (k_p2_tiles<R, N><<<(unsigned)(g.batch * g.gpt), NT2, smem_p2tiles(), s>>>(
@@ -586,7 +600,7 @@ struct RunnerT : Runner {
                 (k_p1_down<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, smem_down(), s>>>(
                     src, g, y, nullptr, W(L.run_incl), W(L.tile_incl1), W(L.group_carry1), W(L.sv), nullptr,
                     nullptr, p.dflag, nullptr, (use_lti && tab) ? &tab->SF[0][0] : nullptr, lti_jlo(g, false),
-                    lti_jhi(g), nullptr)));
+                    lti_jhi(g), nullptr, uwc(false), ux(false))));
       // pass B: backward information filter over mirrored elements (reverse node order)
       Mirror<Src> mir{src, g.node0 + g.Nn - 1};
       reduce1<true>(p, s2, K_TF_REDUCE, mir, fold_m, tab_m, y, nullptr, W(L.tf_run), W(L.tf_tile));
@@ -597,7 +611,8 @@ struct RunnerT : Runner {
       PM_LAUNCH(p, s2, K_TF_DOWN,
                 (k_tf_down<R, N, NY, kNT, K, Src><<<ntiles, kNT, smem_down(), s2>>>(
                     mir, g, y, W(L.tf_run), W(L.tf_tincl), W(L.tf_gcarry), W(L.sv), x, static_cast<R*>(Psv), p.dflag,
-                    (use_lti && tab_m) ? &tab_m->SF[0][0] : nullptr, lti_jlo(g, true), lti_jhi(g))));
+                    (use_lti && tab_m) ? &tab_m->SF[0][0] : nullptr, lti_jlo(g, true), lti_jhi(g), uwc(true),
+                    ux(true))));
       cudaEventRecord(p.ev_fork, s2);
       cudaStreamWaitEvent(s, p.ev_fork, 0);
     } else {

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
                                                 const R* __restrict__ tile_incl, const R* __restrict__ group_carry,
                                                 const R* __restrict__ sv, R* __restrict__ x_out,
                                                 R* __restrict__ Ps_out, unsigned long long* flag, const R* __restrict__ sf, int64_t j_lo,
-                                                int64_t j_hi) {
+                                                int64_t j_hi, const R* __restrict__ uwc = nullptr,
+                                                const R* __restrict__ ux = nullptr) {
   using E = Elem<R, N>;
   using V = VF<R, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -66,12 +67,7 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
   __syncthreads();
   V cur;
   load(cur, sh, 1);
-  if (r > 0) {
-    E p;
-    const bool interior = sf && j >= j_lo && j < j_hi;
-    load_prefix<R, N, NT>(p, run_incl + tile * (int64_t)E::SZ * NT + (r - 1), interior ? sf + (r - 1) : nullptr);
-    vapply<R, N, false>(p, cur, cur, nullptr, ok);
-  }
+  run_carry<R, N, NT>(run_incl, g, tile, r, sf && j >= j_lo && j < j_hi, sf, uwc, ux, cur, ok);
   // x is staged in shared memory in chunks of KC nodes and stored as contiguous segments
   constexpr int KC = 8;
   static_assert(K % KC == 0, "chunking");
