@@ -490,20 +490,42 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     store(agg, sh + r, NT);  // parked in shared memory across the node loop
   }
   R* svt = sv + tile * (int64_t)V::SZ * K * NT;
+  // measurements prefetched two nodes ahead into registers: consecutive threads own runs
+  // K nodes apart, so a y row is one half-used sector per thread and mostly misses L1
+  constexpr bool kPF = NY <= 4;
+  R ya[kPF ? NY : 1], yn[kPF ? NY : 1];
+  if constexpr (kPF) {
+#pragma unroll
+    for (int k = 0; k < NY; ++k) {
+      ya[k] = (l0 < g.Nn) ? yb[l0 * NY + k] : R(0);
+      yn[k] = (l0 + 1 < g.Nn) ? yb[(l0 + 1) * NY + k] : R(0);
+    }
+  }
 #pragma unroll kDownUnroll
   for (int m = 0; m < K; ++m) {
     const int64_t l = l0 + m;
     if (l >= g.Nn) break;
     const int64_t gi = g.node0 + l;
+    R yc[kPF ? NY : 1];
+    const R* yrow = yb + l * NY;
+    if constexpr (kPF) {
+#pragma unroll
+      for (int k = 0; k < NY; ++k) {
+        yc[k] = ya[k];
+        ya[k] = yn[k];
+        yn[k] = (m + 2 < K && l + 2 < g.Nn) ? yb[(l + 2) * NY + k] : R(0);
+      }
+      yrow = yc;
+    }
     E e;
     if (gi == 0) {
-      src.node(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
+      src.node(gi, yrow, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
 #pragma unroll
       for (int k = 0; k < Dim<N>::NS; ++k) cur.S[k] = e.J[k];
 #pragma unroll
       for (int i = 0; i < N; ++i) cur.v[i] = e.h[i];
     } else {
-      src.node_interior(gi, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
+      src.node_interior(gi, yrow, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
       if constexpr (Src::LOWRANK > 0)
         vapply_lowrank<R, N, Src::LOWRANK, Src::AMASK, Src::UMASK>(e, src.U, cur, cur, ok, REC ? svt + m * NT + r : nullptr,
                                            (int64_t)K * NT, src.zero_b != 0);
