@@ -490,32 +490,34 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     store(agg, sh + r, NT);  // parked in shared memory across the node loop
   }
   R* svt = sv + tile * (int64_t)V::SZ * K * NT;
-  // measurements prefetched two nodes ahead into registers: consecutive threads own runs
-  // K nodes apart, so a y row is one half-used sector per thread and mostly misses L1
-  constexpr bool kPF = NY <= 4;
-  R ya[kPF ? NY : 1], yn[kPF ? NY : 1];
-  if constexpr (kPF) {
-#pragma unroll
-    for (int k = 0; k < NY; ++k) {
-      ya[k] = (l0 < g.Nn) ? yb[l0 * NY + k] : R(0);
-      yn[k] = (l0 + 1 < g.Nn) ? yb[(l0 + 1) * NY + k] : R(0);
+  // measurements prefetched two nodes ahead with cp.async (LDGSTS) into a per-thread
+  // ring in shared memory: consecutive threads own runs K nodes apart, so a y row is one
+  // half-used sector per thread and mostly misses L1; an asynchronous copy keeps the
+  // latency off the recursion without a register dependency
+  constexpr int YB = NY * (int)sizeof(R);
+  constexpr bool kPF = (YB == 4 || YB == 8 || YB == 16);
+  __shared__ __align__(16) R yring[kPF ? NT : 1][4][kPF ? NY : 1];
+  auto ypf = [&](int m) {  // issue the copy of node l0 + m into slot m & 3 (one commit group)
+    if constexpr (kPF) {
+      if (m < K && l0 + m < g.Nn) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&yring[r][m & 3][0]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(yb + (l0 + m) * NY), "n"(YB));
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-  }
+  };
+  ypf(0);
+  ypf(1);
 #pragma unroll kDownUnroll
   for (int m = 0; m < K; ++m) {
     const int64_t l = l0 + m;
     if (l >= g.Nn) break;
     const int64_t gi = g.node0 + l;
-    R yc[kPF ? NY : 1];
     const R* yrow = yb + l * NY;
     if constexpr (kPF) {
-#pragma unroll
-      for (int k = 0; k < NY; ++k) {
-        yc[k] = ya[k];
-        ya[k] = yn[k];
-        yn[k] = (m + 2 < K && l + 2 < g.Nn) ? yb[(l + 2) * NY + k] : R(0);
-      }
-      yrow = yc;
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // node m's copy has landed
+      yrow = &yring[r][m & 3][0];
+      ypf(m + 2);
     }
     E e;
     if (gi == 0) {
@@ -535,6 +537,7 @@ __global__ void PM_DOWN_LB(NT) k_p1_down(const __grid_constant__ Src src, const 
     if (!REC) store(cur, svt + m * NT + r, (int64_t)K * NT);
     if (l == g.Nn - 1 && svl) store(cur, svl + b * V::SZ, 1);
   }
+  if constexpr (kPF) asm volatile("cp.async.wait_all;\n" ::: "memory");
   if (!finite_vf(cur)) ok = false;
   if (!P2) {
     if (!ok) flag_node(flag, g.node0 + l0);
