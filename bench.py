@@ -77,10 +77,15 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         chol_d = gram_d + r * (r - 1) // 2 * (r + 1) + r
         vapply_dense = (N * N * r + chol_d + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
                         + N * r + r * r + N * r + N * N * N + ns * N + N * N)
+        compact = (N == 4 and r == 2 and umask is not None and np.array_equal(
+            um, np.array([[0, 0], [0, 0], [1, 0], [0, 1]], bool)))  # CompactRec (pmap_algebra.cuh)
         if r * (N + 1) < vsz:
             vsz2 = r * (N + 1)
             vapply += nU  # U^T v
-            trans = nA + nU + chol + r * N + r * r + nU
+        if compact:  # the record holds S[:, 2:4] (7 values) and v[2:4]; pass 2 forms S U, U^T v
+            vsz2 = 9
+            vapply -= nU
+            trans = nA + nU + chol + r * N + r * r + nU + ((N * r + r) // 2 if compact else 0)
     if euler_n > 0:
         ny_row = euler_n * ny
         build = 2 * N * ny_row

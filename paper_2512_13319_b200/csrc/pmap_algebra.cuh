@@ -22,6 +22,18 @@ namespace pmap {
 
 #define PM_INLINE __device__ __forceinline__
 
+// Compact pass-2 record (R-P2REC with R-MASK): when every column a of U has exactly one
+// structural non-zero, at row ka (the Wiener-velocity factor U = c [0; I]: rows 2, 3),
+// S U = S[:, ka] U[ka][a] and U^T v = U[ka][a] v[ka], so the record stores the columns
+// S[:, ka] (symmetric duplicates once) and v[ka] instead of the products: 9 values instead
+// of 10 at nx = 4, bit-identical after the pass-2 reconstruction (the products are
+// single roundings either way).
+template <int N, int NW, uint32_t UM>
+struct CompactRec {
+  static constexpr bool value = (N == 4 && NW == 2 && UM == ((1u << 4) | (1u << 7)));
+  static constexpr int SIZE = 9;
+};
+
 // Structural-zero masks (DESIGN.md R-MASK): bit (i * cols + j) set = entry (i, j) may be
 // non-zero.  Inside fully unrolled loops the test folds at compile time, so the terms
 // of entries that are structurally zero are never issued -- bit-identical results
@@ -755,7 +767,18 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
         }
       SU[i][a] = s;
     }
-  if (rec) {
+  if (rec && CompactRec<N, NW, UM>::value) {
+    // columns 2 and 3 of S (S23 once) and v2, v3 -- see CompactRec
+    rec[0 * rstride] = V.S[sidx(0, 2, N)];
+    rec[1 * rstride] = V.S[sidx(1, 2, N)];
+    rec[2 * rstride] = V.S[sidx(2, 2, N)];
+    rec[3 * rstride] = V.S[sidx(0, 3, N)];
+    rec[4 * rstride] = V.S[sidx(1, 3, N)];
+    rec[5 * rstride] = V.S[sidx(2, 3, N)];
+    rec[6 * rstride] = V.S[sidx(3, 3, N)];
+    rec[7 * rstride] = V.v[N > 2 ? 2 : 0];
+    rec[8 * rstride] = V.v[N > 3 ? 3 : 0];
+  } else if (rec) {
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll

@@ -746,7 +746,8 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
   if constexpr (REC) {
     // pass-2 records (R-P2REC): the record of step m sits in the run's own slot m
     constexpr int NW = Src::LOWRANK > 0 ? Src::LOWRANK : 1;
-    constexpr int RS = N * NW + NW;
+    constexpr bool CR = CompactRec<N, NW, Src::UMASK>::value;
+    constexpr int RS = CR ? CompactRec<N, NW, Src::UMASK>::SIZE : N * NW + NW;
     R rn[RS], rn2[RS];  // records of the next two steps (two nodes of loads in flight)
     auto fetch_rec = [&](int m, R (&rr)[RS]) {
 #pragma unroll
@@ -774,12 +775,24 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
         if (valid && gi != 0) {
           R At[N][N], bt[N], Ct[Dim<N>::NS], SU[N][NW], u[NW];
           src.trans(gi, nullptr, nullptr, At, bt, Ct);
+          if constexpr (CR) {  // columns 2, 3 of S and v2, v3 (CompactRec)
+            const R c0 = src.U[N > 2 ? 2 : 0][0], c1 = src.U[N > 3 ? 3 : 0][NW > 1 ? 1 : 0];
+            const R s2[4] = {rc[0], rc[1], rc[2], rc[5]}, s3[4] = {rc[3], rc[4], rc[5], rc[6]};
 #pragma unroll
-          for (int i = 0; i < N; ++i)
+            for (int i = 0; i < N; ++i) {
+              SU[i][0] = s2[i < 4 ? i : 0] * c0;
+              SU[i][NW > 1 ? 1 : 0] = s3[i < 4 ? i : 0] * c1;
+            }
+            u[0] = c0 * rc[7];
+            u[NW > 1 ? 1 : 0] = c1 * rc[8 < RS ? 8 : 0];
+          } else {
 #pragma unroll
-            for (int a = 0; a < NW; ++a) SU[i][a] = rc[i * NW + a];
+            for (int i = 0; i < N; ++i)
 #pragma unroll
-          for (int a = 0; a < NW; ++a) u[a] = rc[N * NW + a];
+              for (int a = 0; a < NW; ++a) SU[i][a] = rc[i * NW + a];
+#pragma unroll
+            for (int a = 0; a < NW; ++a) u[a] = rc[N * NW + a];
+          }
           trans_step_rec<R, N, NW, Src::AMASK, Src::UMASK>(At, bt, src.U, SU, u, x, ok);
         }
       }
