@@ -82,10 +82,11 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         if r * (N + 1) < vsz:
             vsz2 = r * (N + 1)
             vapply += nU  # U^T v
+            trans = nA + nU + chol + r * N + r * r + nU
         if compact:  # the record holds S[:, 2:4] (7 values) and v[2:4]; pass 2 forms S U, U^T v
             vsz2 = 9
             vapply -= nU
-            trans = nA + nU + chol + r * N + r * r + nU + ((N * r + r) // 2 if compact else 0)
+            trans += (N * r + r) // 2
     if euler_n > 0:
         ny_row = euler_n * ny
         build = 2 * N * ny_row
