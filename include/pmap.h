@@ -89,7 +89,8 @@ typedef struct {
                           P:416-427 (dA/ds sign corrected) with a measurement at
                           every substep, so y rows hold n*ny values ([batch][T+1][n][ny],
                           block i's substep k = fine time t_{i-1} + (k+1) dt/n; row 0 holds
-                          y(t_0) in its last sub-slot).  LTI linear models, world == 1, RTS
+                          y(t_0) in its last sub-slot).  LTI linear models only (a time-varying
+                          model with n > 1 -> MAP_E_UNSUPPORTED), world == 1, RTS
                           form (map_solve_linear / map_solve_sequential); compiled for n = 10
                           at (nx, ny) = (1, 1), (4, 2) (else MAP_E_UNSUPPORTED).  x_map is
                           returned at the block boundaries t_i. */
@@ -169,10 +170,15 @@ map_status map_solve_sequential(map_plan_t plan, int32_t method, const void* y, 
  * c_i = f(xbar_i) - F_i xbar_i, H_i = dh(xbar_i), r_i = h(xbar_i) - H_i xbar_i;
  * bearing residuals wrapped to (-pi, pi], R-WRAP) and runs the parallel RTS
  * solve.  x_init [batch][T+1][nx] nullable -> xbar^(0) = m0 at every node (R-INIT).
- * tol > 0: stop after the first pass whose max |x - xbar| < tol (checked on the
- * device; one host read per pass); tol == 0: run exactly `passes` passes with no
- * host synchronisation (captured as one CUDA graph).  passes_run (host, nullable)
- * receives the number of passes executed.  Nonlinear plans only. */
+ * tol > 0: stop after the first pass whose max |x - xbar| < tol.  The test runs on the
+ * device: the pass is the body of a CUDA-graph WHILE node whose condition a one-thread
+ * kernel sets from the device-side max |dx|, so the call synchronises the host once per
+ * solve (to report passes_run), not once per pass.  If `passes` passes run without
+ * reaching tol, x_map holds the last iterate and the call returns MAP_E_DIVERGED
+ * (map_last_error gives max |dx| and the pass count).  tol == 0: run exactly `passes`
+ * passes with no host synchronisation (captured as one CUDA graph).  passes_run (host,
+ * nullable) receives the number of passes executed.  A host x_init is read before the
+ * call returns.  Nonlinear plans only. */
 map_status map_solve_nonlinear(map_plan_t plan, const void* y, int32_t passes, double tol,
                                const void* x_init, void* x_map, int32_t* passes_run);
 

@@ -55,6 +55,7 @@ def _lib(long_double: bool = False):
         lib.ora_two_filter.argtypes = [ctypes.POINTER(OraModel), P, P]
         lib.ora_kf_rts_cov.argtypes = [ctypes.POINTER(OraModel), P, P, P]
         lib.ora_euler_rts.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P, ctypes.c_int]
+        lib.ora_euler_block.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P, P, P, P, P, ctypes.c_int]
         lib.ora_batch.argtypes = [ctypes.POINTER(OraModel), ctypes.c_long, P, P, ctypes.c_int]
         lib.ora_ieks.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long,
                                  ctypes.c_double, ctypes.c_double, P, P, P, P, P, P, ctypes.c_int, P, P, P]
@@ -164,6 +165,29 @@ def euler_rts(model: LinearModel, y_fine, T: int, nsub: int, t0: float, tf: floa
     if rc:
         raise FloatingPointError(f"oracle euler_rts failed rc={rc}")
     return x
+
+
+def euler_block(model: LinearModel, y_sub, nsub: int, length: float, g6_printed: bool = False, lib=None):
+    """One Euler block element alone (step 1 of euler_rts; P:416-427 from the boundary of
+    P:427): nsub explicit Euler substeps of length length/nsub, substep k reading y_sub[k].
+    Returns (A, b, C, eta, J).  `lib`: another build of oracle.c (mutation checks of the pins)."""
+    nx = model.nx
+    y = _f64(y_sub).reshape(nsub, model.ny)
+    A, C, J = (np.empty((nx, nx)) for _ in range(3))
+    b, eta = np.empty(nx), np.empty(nx)
+    s = model._struct(1, 0.0, length)
+    rc = (lib or _lib()).ora_euler_block(ctypes.byref(s), nsub, _ptr(y), _ptr(A), _ptr(b), _ptr(C), _ptr(eta),
+                                         _ptr(J), 1 if g6_printed else 0)
+    if rc:
+        raise FloatingPointError(f"oracle euler_block failed rc={rc}")
+    return A, b, C, eta, J
+
+
+def load_variant(path: str):
+    """ctypes handle of another build of oracle.c (pin mutation checks only)."""
+    lib = ctypes.CDLL(path)
+    lib.ora_euler_block.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int] + [ctypes.c_void_p] * 6 + [ctypes.c_int]
+    return lib
 
 
 def two_filter(model: LinearModel, y, T: int, t0: float, tf: float, long_double: bool = False):

@@ -549,6 +549,96 @@ int ora_ieks(int kind, const double* params, int nx, int ny, int nw, long T, dou
  * y_fine: [n T + 1][ny]; x_map: [T + 1][nx] at the block boundaries.  LTI models only. */
 static void mm_(int n, const REAL* X, const REAL* Y, REAL* Z) { mat_mul(n, n, n, X, Y, Z); }
 
+/* Step 1 of the Euler-block method: the element (A, b, C, eta, J) of one block of
+ * nsub explicit Euler substeps of length de of the backward ODEs P:416-427, from the
+ * boundary (I, 0, 0, 0, 0) of P:427; substep k reads y_sub[k] (fine time
+ * t_{i-1} + (k+1) de).  Ft = -F, ct = -c, HRi = H^T R^-1, HRH = H^T R^-1 H. */
+static void euler_block(int nx, int ny, int nsub, REAL de, const node_model* nm, const REAL* Ft, const REAL* ct,
+                        const REAL* HRi, const REAL* HRH, const double* y_sub, int g6_printed, REAL* A, REAL* b,
+                        REAL* C, REAL* eta, REAL* J) {
+  for (int a = 0; a < nx * nx; ++a) {
+    A[a] = (a % (nx + 1) == 0) ? 1 : 0;
+    C[a] = J[a] = 0;
+  }
+  for (int a = 0; a < nx; ++a) b[a] = eta[a] = 0;
+  for (int k = 0; k < nsub; ++k) {
+    const double* yk = y_sub + (long)k * ny;
+    REAL AQ[MAXN * MAXN], JQ[MAXN * MAXN], t1[MAXN * MAXN], t2[MAXN * MAXN], JT[MAXN * MAXN];
+    REAL dA[MAXN * MAXN], db[MAXN], dC[MAXN * MAXN], deta[MAXN], dJ[MAXN * MAXN], u[MAXN];
+    mm_(nx, A, nm->Q, AQ);
+    mm_(nx, J, nm->Q, JQ);
+    for (int a = 0; a < nx; ++a)
+      for (int c = 0; c < nx; ++c) JT[a * nx + c] = J[c * nx + a];
+    mm_(nx, AQ, g6_printed ? JT : J, t1);
+    mm_(nx, A, Ft, t2);
+    for (int a = 0; a < nx * nx; ++a) dA[a] = (g6_printed ? -t1[a] : t1[a]) - t2[a];   /* dA/ds */
+    mat_vec(nx, nx, AQ, eta, u);
+    mat_vec(nx, nx, A, ct, db);
+    for (int a = 0; a < nx; ++a) db[a] = -u[a] - db[a];                               /* db/ds */
+    mat_mul_bt(nx, nx, nx, AQ, A, dC);
+    for (int a = 0; a < nx * nx; ++a) dC[a] = -dC[a];                                 /* dC/ds */
+    for (int a = 0; a < nx; ++a) {                                                    /* deta/ds */
+      REAL s = 0;
+      for (int c = 0; c < nx; ++c) s += JQ[a * nx + c] * eta[c] - Ft[c * nx + a] * eta[c] + J[a * nx + c] * ct[c];
+      for (int q = 0; q < ny; ++q) s -= HRi[a * ny + q] * ((REAL)yk[q] - nm->r[q]);
+      deta[a] = s;
+    }
+    mm_(nx, JQ, J, t1);                                                               /* dJ/ds */
+    mm_(nx, J, Ft, t2);
+    for (int a = 0; a < nx; ++a)
+      for (int c = 0; c < nx; ++c) {
+        REAL s = t1[a * nx + c] - t2[a * nx + c] - HRH[a * nx + c];
+        for (int l = 0; l < nx; ++l) s -= Ft[l * nx + a] * J[l * nx + c];
+        dJ[a * nx + c] = s;
+      }
+    for (int a = 0; a < nx * nx; ++a) { A[a] -= de * dA[a]; C[a] -= de * dC[a]; J[a] -= de * dJ[a]; }
+    for (int a = 0; a < nx; ++a) { b[a] -= de * db[a]; eta[a] -= de * deta[a]; }
+  }
+  symmetrize(nx, C);
+  symmetrize(nx, J);
+}
+
+/* Model quantities of the Euler-block ODEs (LTI): F~ = -F, c~ = -c,
+ * H^T R^-1 and H^T R^-1 H. */
+static int euler_setup(const ora_model* md, node_model* nm, REAL* Ft, REAL* ct, REAL* HRi, REAL* HRH) {
+  int nx = md->nx, ny = md->ny;
+  REAL Ri[MAXN * MAXN];
+  model_at(md, 0, nm);
+  for (int a = 0; a < nx * nx; ++a) Ft[a] = -nm->F[a];
+  for (int a = 0; a < nx; ++a) ct[a] = -nm->c[a];
+  for (int a = 0; a < ny * ny; ++a) Ri[a] = (a % (ny + 1) == 0) ? 1 : 0;
+  { REAL Rc[MAXN * MAXN]; memcpy(Rc, nm->R, sizeof Rc); if (lu_solve(ny, ny, Rc, Ri)) return 1; }
+  for (int a = 0; a < nx; ++a)            /* H^T R^-1 (nx x ny) */
+    for (int q = 0; q < ny; ++q) {
+      REAL s = 0;
+      for (int l = 0; l < ny; ++l) s += nm->H[l * nx + a] * Ri[l * ny + q];
+      HRi[a * ny + q] = s;
+    }
+  mat_mul(nx, ny, nx, HRi, nm->H, HRH);
+  return 0;
+}
+
+/* The block element alone (pins, tests/test_oracle_pins.py): one block of length
+ * (tf - t0) / T split into nsub substeps, measurements y_sub [nsub][ny]; outputs
+ * A, C, J (nx x nx), b, eta (nx). */
+int ora_euler_block(const ora_model* md, int nsub, const double* y_sub, double* A, double* b, double* C,
+                    double* eta, double* J, int g6_printed) {
+  int nx = md->nx, ny = md->ny;
+  if (nx > MAXN || ny > MAXN || md->T < 1 || nsub < 1) return 2;
+  node_model nm;
+  REAL Ft[MAXN * MAXN], ct[MAXN], HRi[MAXN * MAXN], HRH[MAXN * MAXN];
+  if (euler_setup(md, &nm, Ft, ct, HRi, HRH)) return 1;
+  REAL de = ((REAL)md->tf - (REAL)md->t0) / (REAL)md->T / nsub;
+  REAL A_[MAXN * MAXN], b_[MAXN], C_[MAXN * MAXN], e_[MAXN], J_[MAXN * MAXN];
+  euler_block(nx, ny, nsub, de, &nm, Ft, ct, HRi, HRH, y_sub, g6_printed, A_, b_, C_, e_, J_);
+  store(nx * nx, A_, A);
+  store(nx, b_, b);
+  store(nx * nx, C_, C);
+  store(nx, e_, eta);
+  store(nx * nx, J_, J);
+  return 0;
+}
+
 int ora_euler_rts(const ora_model* md, int nsub, const double* y_fine, double* x_map, int g6_printed) {
   int nx = md->nx, ny = md->ny;
   long T = md->T, N = T + 1;
@@ -557,19 +647,8 @@ int ora_euler_rts(const ora_model* md, int nsub, const double* y_fine, double* x
     return 2;
   REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)T, de = dt / nsub;
   node_model nm;
-  model_at(md, 0, &nm);
-  REAL Ft[MAXN * MAXN], ct[MAXN], Ri[MAXN * MAXN], HRi[MAXN * MAXN], HRH[MAXN * MAXN];
-  for (int a = 0; a < nx * nx; ++a) Ft[a] = -nm.F[a];
-  for (int a = 0; a < nx; ++a) ct[a] = -nm.c[a];
-  for (int a = 0; a < ny * ny; ++a) Ri[a] = (a % (ny + 1) == 0) ? 1 : 0;
-  { REAL Rc[MAXN * MAXN]; memcpy(Rc, nm.R, sizeof Rc); if (lu_solve(ny, ny, Rc, Ri)) return 1; }
-  for (int a = 0; a < nx; ++a)            /* H^T R^-1 (nx x ny) */
-    for (int q = 0; q < ny; ++q) {
-      REAL s = 0;
-      for (int l = 0; l < ny; ++l) s += nm.H[l * nx + a] * Ri[l * ny + q];
-      HRi[a * ny + q] = s;
-    }
-  mat_mul(nx, ny, nx, HRi, nm.H, HRH);
+  REAL Ft[MAXN * MAXN], ct[MAXN], HRi[MAXN * MAXN], HRH[MAXN * MAXN];
+  if (euler_setup(md, &nm, Ft, ct, HRi, HRH)) return 1;
   REAL* EA = malloc(sizeof(REAL) * N * nx * nx);
   REAL* Eb = malloc(sizeof(REAL) * N * nx);
   REAL* EC = malloc(sizeof(REAL) * N * nx * nx);
@@ -596,43 +675,9 @@ int ora_euler_rts(const ora_model* md, int nsub, const double* y_fine, double* x
   }
   for (long i = 1; i <= T && !rc; ++i) {
     /* 1. block element by n Euler substeps of P:416-427 (backwards in s from the boundary) */
-    REAL A[MAXN * MAXN], b[MAXN] = {0}, C[MAXN * MAXN] = {0}, eta[MAXN] = {0}, J[MAXN * MAXN] = {0};
-    for (int a = 0; a < nx * nx; ++a) A[a] = (a % (nx + 1) == 0) ? 1 : 0;
-    for (int k = 0; k < nsub; ++k) {
-      const double* yk = y_fine + ((i - 1) * nsub + k + 1) * ny;
-      REAL AQ[MAXN * MAXN], JQ[MAXN * MAXN], t1[MAXN * MAXN], t2[MAXN * MAXN], JT[MAXN * MAXN];
-      REAL dA[MAXN * MAXN], db[MAXN], dC[MAXN * MAXN], deta[MAXN], dJ[MAXN * MAXN], u[MAXN];
-      mm_(nx, A, nm.Q, AQ);
-      mm_(nx, J, nm.Q, JQ);
-      for (int a = 0; a < nx; ++a)
-        for (int c = 0; c < nx; ++c) JT[a * nx + c] = J[c * nx + a];
-      mm_(nx, AQ, g6_printed ? JT : J, t1);
-      mm_(nx, A, Ft, t2);
-      for (int a = 0; a < nx * nx; ++a) dA[a] = (g6_printed ? -t1[a] : t1[a]) - t2[a];   /* dA/ds */
-      mat_vec(nx, nx, AQ, eta, u);
-      mat_vec(nx, nx, A, ct, db);
-      for (int a = 0; a < nx; ++a) db[a] = -u[a] - db[a];                               /* db/ds */
-      mat_mul_bt(nx, nx, nx, AQ, A, dC);
-      for (int a = 0; a < nx * nx; ++a) dC[a] = -dC[a];                                 /* dC/ds */
-      for (int a = 0; a < nx; ++a) {                                                    /* deta/ds */
-        REAL s = 0;
-        for (int c = 0; c < nx; ++c) s += JQ[a * nx + c] * eta[c] - Ft[c * nx + a] * eta[c] + J[a * nx + c] * ct[c];
-        for (int q = 0; q < ny; ++q) s -= HRi[a * ny + q] * ((REAL)yk[q] - nm.r[q]);
-        deta[a] = s;
-      }
-      mm_(nx, JQ, J, t1);                                                               /* dJ/ds */
-      mm_(nx, J, Ft, t2);
-      for (int a = 0; a < nx; ++a)
-        for (int c = 0; c < nx; ++c) {
-          REAL s = t1[a * nx + c] - t2[a * nx + c] - HRH[a * nx + c];
-          for (int l = 0; l < nx; ++l) s -= Ft[l * nx + a] * J[l * nx + c];
-          dJ[a * nx + c] = s;
-        }
-      for (int a = 0; a < nx * nx; ++a) { A[a] -= de * dA[a]; C[a] -= de * dC[a]; J[a] -= de * dJ[a]; }
-      for (int a = 0; a < nx; ++a) { b[a] -= de * db[a]; eta[a] -= de * deta[a]; }
-    }
-    symmetrize(nx, C);
-    symmetrize(nx, J);
+    REAL A[MAXN * MAXN], b[MAXN], C[MAXN * MAXN], eta[MAXN], J[MAXN * MAXN];
+    euler_block(nx, ny, nsub, de, &nm, Ft, ct, HRi, HRH, y_fine + ((i - 1) * nsub + 1) * ny, g6_printed, A, b, C,
+                eta, J);
     memcpy(EA + i * nx * nx, A, sizeof(REAL) * nx * nx);
     memcpy(Eb + i * nx, b, sizeof(REAL) * nx);
     memcpy(EC + i * nx * nx, C, sizeof(REAL) * nx * nx);

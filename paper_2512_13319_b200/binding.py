@@ -112,9 +112,34 @@ def _ptr(a) -> int | None:
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.flags.c_contiguous
+        if not a.flags.c_contiguous:
+            raise ValueError("NumPy buffers passed to the C ABI must be C-contiguous")
         return a.ctypes.data
     return a.data_ptr()  # torch.Tensor (device or host)
+
+
+def _check_buf(name: str, a, dtype: str, numel: int) -> None:
+    """The C ABI takes plain pointers and cannot check sizes: validate a caller buffer
+    (dtype == the plan dtype, contiguous, exactly `numel` elements, CUDA or host memory)."""
+    if a is None:
+        return
+    want = np.float64 if dtype == "f64" else np.float32
+    if isinstance(a, np.ndarray):
+        ok_dtype, contig, n, dev = a.dtype == want, a.flags.c_contiguous, a.size, "cpu"
+    else:
+        import torch
+        if not isinstance(a, torch.Tensor):
+            raise ValueError(f"{name}: expected a torch.Tensor or numpy.ndarray, got {type(a).__name__}")
+        ok_dtype = a.dtype == (torch.float64 if dtype == "f64" else torch.float32)
+        contig, n, dev = a.is_contiguous(), a.numel(), a.device.type
+    if not ok_dtype:
+        raise ValueError(f"{name}: dtype must match the plan dtype ({dtype})")
+    if not contig:
+        raise ValueError(f"{name}: buffer must be contiguous")
+    if n != numel:
+        raise ValueError(f"{name}: expected {numel} elements, got {n}")
+    if dev not in ("cuda", "cpu"):
+        raise ValueError(f"{name}: buffer must live in CUDA device memory or host memory")
 
 
 def shard_range(rank: int, world: int, T: int) -> tuple[int, int]:
@@ -231,8 +256,26 @@ class Plan:
         self.rank, self.world = rank, world
         self.node0, a1 = shard_range(rank, world, T)
         self.n_local = a1 - self.node0
+        self.ny_row = ny * max(1, substeps)
         lin = nl = None
+
+        def shape_ok(name, a, base):  # constant (base) or time-varying ((T+1,) + base)
+            a = np.asarray(a)
+            if a.shape != base and a.shape != (T + 1,) + base:
+                raise ValueError(f"{name}: shape {a.shape}, expected {base} or {(T + 1,) + base}")
+        for name, a, base in (("L", L, (nx, nw)), ("W", W, (nw, nw)), ("R", R, (ny, ny))):
+            shape_ok(name, a, base)
+        if m0.shape != (nx,) or P0.shape != (nx, nx):
+            raise ValueError(f"m0/P0: shapes {m0.shape}/{P0.shape}, expected ({nx},)/({nx}, {nx})")
         if nl_kind is None:
+            if F is None or H is None:
+                raise ValueError("linear plans need F and H")
+            shape_ok("F", F, (nx, nx))
+            shape_ok("H", H, (ny, nx))
+            if c is not None:
+                shape_ok("c", c, (nx,))
+            if r is not None:
+                shape_ok("r", r, (ny,))
             lin = LinearModel()
             arrs = dict(F=(F, 2), c=(c, 1), L=(L, 2), W=(W, 2), H=(H, 2), r=(r, 1), R=(R, 2))
             for k, (a, nd) in arrs.items():
@@ -271,10 +314,19 @@ class Plan:
         dev = like.device if hasattr(like, "device") else "cpu"
         return torch.empty(shape, dtype=self.torch_dtype, device=dev)
 
+    def _check_io(self, y=None, **outs):
+        nodes = self.batch * self.n_local
+        ns = self.nx * (self.nx + 1) // 2
+        _check_buf("y", y, self.dtype, nodes * self.ny_row)
+        rows = dict(x_map=self.nx, x_init=self.nx, filt_m=self.nx, filt_P=ns, smooth_P=ns)
+        for k, a in outs.items():
+            _check_buf(k, a, self.dtype, nodes * rows[k])
+
     def solve_linear(self, y, x_map=None, filt_m=None, filt_P=None):
         """Parallel RTS MAP (pass 1 + pass 2).  y: [batch][n_local][ny] (torch, device or host)."""
         if x_map is None:
             x_map = self._out(y, self.batch, self.n_local, self.nx)
+        self._check_io(y, x_map=x_map, filt_m=filt_m, filt_P=filt_P)
         map_solve_linear(self.handle, y, x_map, filt_m, filt_P)
         return x_map
 
@@ -283,6 +335,7 @@ class Plan:
         the smoother covariances."""
         if x_map is None:
             x_map = self._out(y, self.batch, self.n_local, self.nx)
+        self._check_io(y, x_map=x_map, smooth_P=smooth_P)
         map_two_filter(self.handle, y, x_map, smooth_P)
         return x_map
 
@@ -290,12 +343,14 @@ class Plan:
         """Sequential on-device baseline (map_solve_sequential): method 0 = RTS, 1 = two-filter."""
         if x_map is None:
             x_map = self._out(y, self.batch, self.n_local, self.nx)
+        self._check_io(y, x_map=x_map, smooth_P=smooth_P)
         map_solve_sequential(self.handle, method, y, passes, x_map, smooth_P)
         return x_map
 
     def solve_nonlinear(self, y, passes: int = 10, tol: float = 0.0, x_init=None, x_map=None):
         if x_map is None:
             x_map = self._out(y, self.batch, self.n_local, self.nx)
+        self._check_io(y, x_map=x_map, x_init=x_init)
         run = map_solve_nonlinear(self.handle, y, passes, tol, x_init, x_map)
         return x_map, run
 
@@ -307,6 +362,13 @@ class Plan:
         phase's payload tensor (phases 1, 2) or x_map (phase 3).  Filter outputs are
         written at phase 3 and must be passed at phase 2 too (full (S, v) storage)."""
         import torch
+        if phase in (1, 2):
+            self._check_io(y, filt_m=filt_m, filt_P=filt_P)
+        else:
+            self._check_io(None, x_map=x_map, filt_m=filt_m, filt_P=filt_P)
+        if gathered is not None:
+            per = {2: map_shard_payload_bytes(self.handle, 1), 3: map_shard_payload_bytes(self.handle, 2)}[phase]
+            _check_buf("gathered", gathered, self.dtype, self.world * per // (8 if self.dtype == "f64" else 4))
         if phase in (1, 2):
             n = map_shard_payload_bytes(self.handle, phase) // (8 if self.dtype == "f64" else 4)
             payload = torch.empty(n, dtype=self.torch_dtype, device="cuda")

@@ -27,6 +27,26 @@ using namespace pmap_rt;
 
 namespace {
 
+// One counting step of the device-side IEKS stop (map_solve_nonlinear, tol > 0):
+// f[1] = max |dx| of the pass just run (bit pattern), f[2] = passes run, f[3] = that
+// dmax; the WHILE condition (when h != 0) stays set while dmax >= tol and passes remain.
+__global__ void k_ieks_decide(unsigned long long* f, double tol, int passes, cudaGraphConditionalHandle h,
+                              int use_h) {
+  const unsigned long long bits = f[1];
+  double dmax;
+  memcpy(&dmax, &bits, sizeof dmax);
+  const unsigned long long run = f[2] + 1;
+  f[2] = run;
+  f[3] = bits;
+  f[1] = 0;
+  if (use_h) cudaGraphSetConditional(h, (dmax >= tol && run < (unsigned long long)passes) ? 1u : 0u);
+}
+
+static void launch_ieks_decide(cudaStream_t s, unsigned long long* f, double tol, int passes,
+                               cudaGraphConditionalHandle h, bool use_h) {
+  k_ieks_decide<<<1, 1, 0, s>>>(f, tol, passes, h, use_h ? 1 : 0);
+}
+
 // ------------------------------------------------------------- dispatch
 template <typename R>
 static Runner* dispatch_lti(int kr, int nx, int ny, int lowrank, const double* A, const double* b,
@@ -385,6 +405,11 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   if (lin) {
     if (!lin->F || !lin->L || !lin->W || !lin->H || !lin->R) return MAP_E_ARG;
     const bool tv = lin->sF || lin->sc || lin->sL || lin->sW || lin->sH || lin->sr || lin->sR;
+    if (tv && d.substeps > 1) {
+      // Euler blocks are built for time-invariant models only (R-EULER): the kernels would
+      // read y rows of substeps * ny values as [T+1][ny] and return wrong trajectories
+      return MAP_E_UNSUPPORTED;
+    }
     if (!tv && d.substeps > 1) {  // paper-faithful Euler blocks of d.substeps substeps
       p->kind = Kind::LTI;
       p->euler = true;
@@ -568,8 +593,8 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     p->err = "workspace allocation failed";
     return MAP_E_CUDA;
   }
-  if (cudaMalloc(&p->dflag, 2 * sizeof(unsigned long long)) != cudaSuccess) return MAP_E_CUDA;
-  const unsigned long long init[2] = {ULLONG_MAX, 0ull};
+  if (cudaMalloc(&p->dflag, 4 * sizeof(unsigned long long)) != cudaSuccess) return MAP_E_CUDA;
+  const unsigned long long init[4] = {ULLONG_MAX, 0ull, 0ull, 0ull};
   cudaMemcpy(p->dflag, init, sizeof init, cudaMemcpyHostToDevice);
   if (p->kind == Kind::NL) {
     const size_t xb = (size_t)g.batch * g.Nn * nx * p->elem_real;
@@ -605,30 +630,7 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
 }
 
 void map_plan_destroy(map_plan_t p) {
-  if (!p) return;
-  cudaStreamSynchronize(p->stream);
-  if (p->graph) cudaGraphExecDestroy(p->graph);
-  for (auto& g : p->lgraphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  cudaFree(p->ws);
-  cudaFree(p->dflag);
-  cudaFree(p->xbuf[0]);
-  cudaFree(p->xbuf[1]);
-  cudaFree(p->stage_y);
-  cudaFree(p->stage_x);
-  cudaFree(p->stage_aux);
-  cudaFree(p->dev_tv);
-  cudaFree(p->scratch);
-  cudaFree(p->m0_dev);
-  if (p->stream2) cudaStreamDestroy(p->stream2);
-  if (p->stream3) cudaStreamDestroy(p->stream3);
-  if (p->stream4) cudaStreamDestroy(p->stream4);
-  for (cudaEvent_t e : {p->ev_edge0, p->ev_edge1, p->ev_edge2, p->ev_edge3})
-    if (e) cudaEventDestroy(e);
-  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-  if (p->ev_join) cudaEventDestroy(p->ev_join);
-  delete[] p->m0_host;
-  delete p;
+  delete p;  // ~PlanState synchronises the stream and frees everything the plan owns
 }
 
 // Resolve y (input) and x (output) to device buffers, staging host memory.
@@ -825,43 +827,70 @@ map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, doub
   if (st) return st;
   // xbar^(0)
   if (x_init) {
-    if (is_device_ptr(x_init))
+    if (is_device_ptr(x_init)) {
       PM_CK(*p, cudaMemcpyAsync(p->xbuf[0], x_init, xb, cudaMemcpyDeviceToDevice, p->stream));
-    else
+    } else {
+      // host buffer: the caller may reuse it once we return, so wait for the copy
       PM_CK(*p, cudaMemcpyAsync(p->xbuf[0], x_init, xb, cudaMemcpyHostToDevice, p->stream));
+      blocking = true;
+    }
   } else {
     p->runner->fill_m0(*p, p->xbuf[0]);
   }
+  // graph capture (private stream; p->stream / p->prof restored on every exit)
+  struct CaptureScope {
+    PlanState& p;
+    cudaStream_t cs = nullptr, saved;
+    bool saved_prof;
+    explicit CaptureScope(PlanState& pp) : p(pp), saved(pp.stream), saved_prof(pp.prof) {}
+    cudaError_t begin() {
+      cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+      if (e == cudaSuccess) {
+        p.stream = cs;
+        p.prof = false;
+      }
+      return e;
+    }
+    ~CaptureScope() {
+      p.stream = saved;
+      p.prof = saved_prof;
+      if (cs) {
+        cudaStreamCaptureStatus cst;
+        if (cudaStreamIsCapturing(cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+          cudaGraph_t junk = nullptr;
+          cudaStreamEndCapture(cs, &junk);
+          if (junk) cudaGraphDestroy(junk);
+        }
+        cudaStreamDestroy(cs);
+      }
+    }
+  };
+  const bool capture = p->d.world == 1 && !p->force_shard && !p->prof;  // profiling: plain launches
   int run = 0;
   if (tol == 0.0) {
     // fixed number of passes, no host synchronisation: one CUDA graph
     const void* key[4] = {yd, xd, (const void*)(intptr_t)passes, nullptr};
-    const bool capture = p->d.world == 1 && !p->force_shard && !p->prof;  // profiling: plain launches
     if (capture && !(p->graph && memcmp(key, p->graph_key, sizeof key) == 0)) {
       if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
       }
-      cudaStream_t cs;
-      PM_CK(*p, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-      cudaStream_t saved = p->stream;
-      const bool saved_prof = p->prof;
-      p->prof = false;
-      p->stream = cs;
-      int64_t l0 = p->launches;
-      cudaGraph_t graph;
-      PM_CK(*p, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      CaptureScope sc(*p);
+      PM_CK(*p, sc.begin());
+      const int64_t l0 = p->launches;
+      PM_CK(*p, cudaStreamBeginCapture(sc.cs, cudaStreamCaptureModeThreadLocal));
       for (int k = 0; k < passes; ++k) {
         void* out = (k == passes - 1) ? xd : p->xbuf[(k + 1) & 1];
         p->runner->rts(*p, yd, p->xbuf[k & 1], out, nullptr, nullptr);
       }
-      cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-      p->stream = saved;
-      p->prof = saved_prof;
-      cudaStreamDestroy(cs);
-      if (ce != cudaSuccess) return cuda_fail(*p, ce, "graph capture");
-      PM_CK(*p, cudaGraphInstantiate(&p->graph, graph, 0));
+      cudaGraph_t graph = nullptr;
+      PM_CK(*p, cudaStreamEndCapture(sc.cs, &graph));
+      cudaError_t ie = cudaGraphInstantiate(&p->graph, graph, 0);
       cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        p->graph = nullptr;
+        return cuda_fail(*p, ie, "graph instantiate");
+      }
       memcpy(p->graph_key, key, sizeof key);
       p->graph_launches = p->launches - l0;
       p->launches = l0;
@@ -876,27 +905,101 @@ map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, doub
       }
     }
     run = passes;
-  } else {
-    for (int k = 0; k < passes; ++k) {
-      void* in = p->xbuf[k & 1];
-      void* out = p->xbuf[(k + 1) & 1];
-      p->runner->rts(*p, yd, in, out, nullptr, nullptr);
-      PM_CK(*p, cudaMemsetAsync(p->dflag + 1, 0, sizeof(unsigned long long), p->stream));
-      p->runner->maxdiff(*p, in, out, p->dflag + 1);
-      unsigned long long bits = 0;
-      PM_CK(*p, cudaMemcpyAsync(&bits, p->dflag + 1, sizeof bits, cudaMemcpyDeviceToHost, p->stream));
-      PM_CK(*p, cudaStreamSynchronize(p->stream));
-      double dmax;
-      memcpy(&dmax, &bits, sizeof dmax);
-      ++run;
-      if (dmax < tol || k == passes - 1) {
-        PM_CK(*p, cudaMemcpyAsync(xd, out, xb, cudaMemcpyDeviceToDevice, p->stream));
-        break;
+    if (passes_run) *passes_run = run;
+    return finish(*p, blocking, {{x_map, {xd, xb}}});
+  }
+  // tol > 0: device-side stop.  One pass = rts(xbuf0 -> xbuf1), then
+  // dflag[1] = max |xbuf1 - xbuf0| with xbuf0 <- xbuf1, then k_ieks_decide (one thread)
+  // counts the pass in dflag[2], keeps dmax in dflag[3] and sets the loop condition
+  // (dmax >= tol and passes left).  Captured as the body of a CUDA-graph WHILE node, so a
+  // solve costs one host synchronisation (to report passes_run / divergence) instead of
+  // one per pass; eager host loop when profiling or time-sharded.
+  PM_CK(*p, cudaMemsetAsync(p->dflag + 1, 0, 3 * sizeof(unsigned long long), p->stream));
+  const void* key[4] = {yd, (const void*)(intptr_t)passes, nullptr, nullptr};
+  bool use_graph = capture;
+  if (use_graph && !(p->wgraph && memcmp(key, p->wgraph_key, sizeof key) == 0 && p->wgraph_tol == tol)) {
+    if (p->wgraph) {
+      cudaGraphExecDestroy(p->wgraph);
+      p->wgraph = nullptr;
+    }
+    cudaGraph_t top = nullptr;
+    PM_CK(*p, cudaGraphCreate(&top, 0));
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&h, top, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&cn, top, nullptr, 0, &cp);
+    const int64_t l0 = p->launches;
+    if (e == cudaSuccess) {
+      CaptureScope sc(*p);
+      e = sc.begin();
+      if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(sc.cs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        p->runner->rts(*p, yd, p->xbuf[0], p->xbuf[1], nullptr, nullptr);
+        p->runner->maxdiff(*p, p->xbuf[0], p->xbuf[1], p->dflag + 1, true);
+        launch_ieks_decide(sc.cs, p->dflag, tol, passes, h, true);
+        p->launches++;
+        cudaGraph_t body = nullptr;
+        e = cudaStreamEndCapture(sc.cs, &body);
       }
     }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&p->wgraph, top, 0);
+    cudaGraphDestroy(top);
+    if (e != cudaSuccess || !p->err.empty()) {  // conditional nodes unavailable: host loop
+      cudaGetLastError();
+      p->wgraph = nullptr;
+      p->err.clear();
+      use_graph = false;
+    } else {
+      memcpy(p->wgraph_key, key, sizeof key);
+      p->wgraph_tol = tol;
+      p->wgraph_launches = p->launches - l0;
+    }
+    p->launches = l0;
+  } else if (use_graph && !p->wgraph) {
+    use_graph = false;
   }
+  unsigned long long cnt[2] = {0, 0};
+  if (use_graph) {
+    PM_CK(*p, cudaGraphLaunch(p->wgraph, p->stream));
+    p->launches += p->wgraph_launches;  // per pass
+    PM_CK(*p, cudaMemcpyAsync(xd, p->xbuf[1], xb, cudaMemcpyDeviceToDevice, p->stream));
+    PM_CK(*p, cudaMemcpyAsync(cnt, p->dflag + 2, sizeof cnt, cudaMemcpyDeviceToHost, p->stream));
+    PM_CK(*p, cudaStreamSynchronize(p->stream));
+  } else {
+    for (int k = 0; k < passes; ++k) {
+      p->runner->rts(*p, yd, p->xbuf[0], p->xbuf[1], nullptr, nullptr);
+      p->runner->maxdiff(*p, p->xbuf[0], p->xbuf[1], p->dflag + 1, true);
+      launch_ieks_decide(p->stream, p->dflag, tol, passes, 0, false);
+      p->launches++;
+      PM_CK(*p, cudaMemcpyAsync(cnt, p->dflag + 2, sizeof cnt, cudaMemcpyDeviceToHost, p->stream));
+      PM_CK(*p, cudaStreamSynchronize(p->stream));
+      double dm;
+      memcpy(&dm, &cnt[1], sizeof dm);
+      if (!(dm >= tol)) break;
+    }
+    PM_CK(*p, cudaMemcpyAsync(xd, p->xbuf[1], xb, cudaMemcpyDeviceToDevice, p->stream));
+  }
+  run = (int)cnt[0];
+  double dmax;
+  memcpy(&dmax, &cnt[1], sizeof dmax);
   if (passes_run) *passes_run = run;
-  return finish(*p, blocking, {{x_map, {xd, xb}}});
+  map_status fs = finish(*p, blocking, {{x_map, {xd, xb}}});
+  if (fs != MAP_OK) return fs;
+  if (!(dmax < tol)) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "iterated linearisation did not reach tol %.3g: max |dx| = %.3g after %d passes", tol,
+             dmax, run);
+    p->err = buf;
+    return MAP_E_DIVERGED;  // x_map holds the last iterate
+  }
+  return MAP_OK;
 }
 
 int64_t map_shard_payload_bytes(map_plan_t p, int32_t phase) {

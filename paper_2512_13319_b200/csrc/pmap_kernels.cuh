@@ -896,14 +896,17 @@ __global__ void k_fill_m0(int64_t count, const R* __restrict__ m0, R* __restrict
   if (idx < count) xbar[idx] = m0[idx % N];
 }
 
-// max |a - b| as the bit pattern of a non-negative double (order-preserving)
-template <typename R>
-__global__ void k_maxdiff(int64_t count, const R* __restrict__ a, const R* __restrict__ b,
-                          unsigned long long* out) {
+// max |a - b| as the bit pattern of a non-negative double (order-preserving).
+// COPY: also a <- b (the iterated-linearisation loop of a CUDA-graph while node keeps
+// xbar in one buffer: pass k reads a, writes b, then a takes b's values).
+template <typename R, bool COPY = false>
+__global__ void k_maxdiff(int64_t count, R* __restrict__ a, const R* __restrict__ b, unsigned long long* out) {
   double m = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-    double d = fabs((double)a[i] - (double)b[i]);
+    const R bv = b[i];
+    double d = fabs((double)a[i] - (double)bv);
     m = (d > m || d != d) ? d : m;
+    if (COPY) a[i] = bv;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));

@@ -138,7 +138,8 @@ struct Runner {
   // sequential on-device baseline: method 0 = RTS, 1 = two-filter
   virtual void sequential(PlanState& p, int method, const void* y, const void* xbar, void* x, void* Ps) = 0;
   virtual void fill_m0(PlanState& p, void* xbar) = 0;
-  virtual void maxdiff(PlanState& p, const void* a, const void* b, unsigned long long* out) = 0;
+  // out <- max |a - b| (atomicMax of the bit pattern); copy: also a <- b
+  virtual void maxdiff(PlanState& p, void* a, const void* b, unsigned long long* out, bool copy) = 0;
   virtual int sizeof_real() const = 0;
 };
 
@@ -192,6 +193,11 @@ struct PlanState {
   const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
   int graph_passes = -1;
   int64_t graph_launches = 0;
+  // tol > 0 nonlinear graph: one CUDA-graph WHILE node around one pass
+  cudaGraphExec_t wgraph = nullptr;
+  const void* wgraph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  double wgraph_tol = -1.0;
+  int64_t wgraph_launches = 0;
   size_t elem_real = 8;
   bool want_filter = false;  // filter outputs requested for the current solve (full (S, v) storage)
   bool rec_done = false;     // phase 2 stored low-rank pass-2 records (R-P2REC) instead of (S, v)
@@ -219,6 +225,23 @@ struct PlanState {
       if (cudaMalloc(&scratch, bytes) == cudaSuccess) scratch_bytes = bytes;
     }
     return scratch;
+  }
+  // frees everything the plan owns (map_plan_destroy and every map_plan error return)
+  ~PlanState() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (graph) cudaGraphExecDestroy(graph);
+    if (wgraph) cudaGraphExecDestroy(wgraph);
+    for (auto& ge : lgraphs)
+      if (ge.exec) cudaGraphExecDestroy(ge.exec);
+    runner.reset();
+    for (void* q : {(void*)ws, (void*)dflag, xbuf[0], xbuf[1], stage_y, stage_x, stage_aux, dev_tv, scratch, m0_dev})
+      if (q) cudaFree(q);
+    for (cudaStream_t s : {stream2, stream3, stream4})
+      if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : {ev_edge0, ev_edge1, ev_edge2, ev_edge3, ev_fork, ev_join})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    delete[] m0_host;
   }
   cudaEvent_t ev_get() {
     if (ev_used == ev_pool.size()) {
@@ -645,10 +668,14 @@ struct RunnerT : Runner {
               (k_fill_m0<R, N><<<(unsigned)((n + 255) / 256), 256, 0, p.stream>>>(
                   n, static_cast<const R*>(p.m0_dev), static_cast<R*>(xbar))));
   }
-  void maxdiff(PlanState& p, const void* a, const void* b, unsigned long long* out) override {
+  void maxdiff(PlanState& p, void* a, const void* b, unsigned long long* out, bool copy) override {
     const int64_t n = p.g.batch * p.g.Nn * N;
-    PM_LAUNCH(p, p.stream, K_NL_MISC,
-              (k_maxdiff<R><<<296, 256, 0, p.stream>>>(n, static_cast<const R*>(a), static_cast<const R*>(b), out)));
+    if (copy)
+      PM_LAUNCH(p, p.stream, K_NL_MISC,
+                (k_maxdiff<R, true><<<296, 256, 0, p.stream>>>(n, static_cast<R*>(a), static_cast<const R*>(b), out)));
+    else
+      PM_LAUNCH(p, p.stream, K_NL_MISC,
+                (k_maxdiff<R, false><<<296, 256, 0, p.stream>>>(n, static_cast<R*>(a), static_cast<const R*>(b), out)));
   }
 };
 

@@ -204,6 +204,54 @@ def test_euler_blocks_errors(torch_cuda):
     with pytest.raises(pm.MapError):  # only n = 10 is compiled
         pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
                 P0=spec.P0, substeps=7)
+    # Euler blocks are LTI-only: a time-varying model with substeps > 1 must be refused
+    # (it used to fall through to the time-varying path and read y wrongly)
+    Ftv = np.repeat(spec.F[None], T + 1, axis=0)
+    with pytest.raises(pm.MapError) as ei:
+        pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=Ftv, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                P0=spec.P0, substeps=10)
+    assert ei.value.status == 2  # MAP_E_UNSUPPORTED
+
+
+def test_binding_rejects_bad_buffers(torch_cuda):
+    """The C ABI cannot check sizes: the binding validates dtype, contiguity, element
+    count and model shapes before any pointer crosses it."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 1000
+    plan = gpu_plan(spec, T)
+    good = torch.zeros((1, T + 1, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):  # fp32 buffer on an f64 plan
+        plan.solve_linear(good.float())
+    with pytest.raises(ValueError):  # too short
+        plan.solve_linear(good[:, :T])
+    with pytest.raises(ValueError):  # non-contiguous view
+        plan.solve_linear(torch.zeros((1, T + 1, 4), dtype=torch.float64, device="cuda")[:, :, :2])
+    with pytest.raises(ValueError):  # x_map of the wrong size
+        plan.solve_linear(good, x_map=torch.empty((1, T + 1, 3), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):  # H of the wrong shape
+        pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H[:, :3], R=spec.R, m0=spec.m0,
+                P0=spec.P0)
+    plan.solve_linear(good)  # the valid call still works
+
+
+def test_nonlinear_diverged_status(torch_cuda):
+    """tol > 0 that is not reached within `passes` returns MAP_E_DIVERGED with the last
+    iterate in x_map; the device-side stop reports the pass count."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = wl.van_der_pol()
+    T = 2000
+    _, y = wl.simulate_nonlinear(s, T, seed=3)
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=2, params=s.params)
+    yd = to_dev(torch, y[None])
+    x = torch.empty((1, T + 1, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(pm.MapError) as ei:
+        plan.solve_nonlinear(yd, passes=1, tol=1e-300, x_map=x)
+    assert ei.value.status == 6  # MAP_E_DIVERGED
+    xo, _ = oracle.ieks(2, s.params, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=1)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64  # the last (only) iterate was returned
 
 
 @pytest.mark.parametrize("T", [5000, 300_001])

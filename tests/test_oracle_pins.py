@@ -467,3 +467,92 @@ def test_golden_model_parameters():
     assert np.array_equal(np.diag(s.R), g["R_diag"])
     assert np.array_equal(s.m0, g["m0"])
     assert np.array_equal(np.diag(s.P0), g["P0_diag"])
+
+
+# ---------------------------------------------------------------- P14: Euler blocks, nx > 1
+def _euler_block_reference(F, c, Q, H, R, r, ys, length):
+    """The block as the composition of n exact one-substep elements of the discrete
+    model (R-ELEM, length delta = length / n, measurement weight delta at each substep end),
+    later substeps on the left (R-FLIP), by the combination rule P:395-407
+    (test_method_numpy.combine).  Independent of the oracle's ODE integration."""
+    from test_method_numpy import combine
+    n = len(ys)
+    d = length / n
+    Ri = np.linalg.inv(R)
+    acc = None
+    for k in range(n):
+        e = (np.eye(F.shape[0]) - d * F, -d * c, d * Q, d * H.T @ Ri @ (ys[k] - r), d * H.T @ Ri @ H)
+        acc = e if acc is None else combine(e, acc)
+    return acc
+
+
+P14_MODELS = {
+    # Wiener velocity (P:531-548) with drift and measurement offsets c, r != 0
+    "wiener": lambda: (wl.wiener_velocity().F, np.array([0.3, -0.2, 0.1, 0.05]), wl.wiener_velocity().L,
+                       wl.wiener_velocity().W, wl.wiener_velocity().H, wl.wiener_velocity().R, np.array([0.1, -0.3])),
+    # a dense random nx = 4 model: no product in the ODEs commutes by structure
+    "dense": lambda: (lambda g: (g.normal(size=(4, 4)), g.normal(size=4), g.normal(size=(4, 4)), np.eye(4),
+                                 g.normal(size=(2, 4)), np.diag([0.5, 0.2]), g.normal(size=2)))(np.random.default_rng(5)),
+}
+
+
+def _p14_ratios(model, lib=None, ns=(64, 128, 256, 512), length=0.05):
+    """Per-field error of the oracle's Euler block element against the exact composition,
+    and the error ratios per doubling of n (first order: -> 2)."""
+    F, c, L, W, H, R, r = model
+    Q = L @ W @ L.T
+    md = oracle.LinearModel(F, L, W, H, R, np.zeros(4), np.eye(4), c=c, r=r)
+    errs = []
+    for n in ns:
+        t = length * np.arange(1, n + 1) / n
+        ys = np.stack([np.sin(3 * t) + 0.5, np.cos(2 * t) - 0.2], 1)  # smooth measurement signal
+        eu = oracle.euler_block(md, ys, n, length, lib=lib)
+        rf = _euler_block_reference(F, c, Q, H, R, r, ys, length)
+        errs.append([np.abs(a - b).max() / np.abs(b).max() for a, b in zip(eu, rf)])
+    errs = np.array(errs)
+    return errs, errs[:-1] / errs[1:]
+
+
+@pytest.mark.parametrize("name", sorted(P14_MODELS))
+def test_P14_euler_block_element_nx4(name):
+    """P14 -- the oracle's n-substep Euler block element (A, b, C,
+    eta, J) at nx = 4 converges at first order (error ratio in [1.9, 2.1] per doubling of
+    n, for every field) to the same limit as the exact composition of n one-substep
+    elements.  Unlike P13 (n = 1 and the scalar OU case) this exercises every
+    non-commuting product of the ODEs (A Q~ J, J Q~ eta, J Q~ J, F~^T J)."""
+    errs, ratios = _p14_ratios(P14_MODELS[name]())
+    assert np.all((ratios > 1.9) & (ratios < 2.1)), (errs, ratios)
+    assert errs[-1].max() < 1e-3
+
+
+MUTATIONS = {
+    # d(eta)/ds and dJ/ds with Q~ J instead of J Q~
+    "JQ->QJ": ("mm_(nx, J, nm->Q, JQ);", "mm_(nx, nm->Q, J, JQ);"),
+    # dA/ds with Q~ A J instead of A Q~ J
+    "AQJ->QAJ": ("mm_(nx, AQ, g6_printed ? JT : J, t1);",
+                 "{ REAL QA_[MAXN * MAXN]; mm_(nx, nm->Q, A, QA_); mm_(nx, QA_, g6_printed ? JT : J, t1); }"),
+    # dC/ds with A^T Q~ A
+    "AQAt->AtQA": ("mat_mul_bt(nx, nx, nx, AQ, A, dC);",
+                   "{ REAL At_[MAXN * MAXN], t3_[MAXN * MAXN]; for (int a = 0; a < nx; ++a) for (int q = 0; q < nx; ++q) "
+                   "At_[a * nx + q] = A[q * nx + a]; mm_(nx, At_, nm->Q, t3_); mm_(nx, t3_, A, dC); }"),
+}
+
+
+@pytest.mark.parametrize("mut", sorted(MUTATIONS))
+def test_P14_detects_mutations(mut, tmp_path):
+    """The P14 pin is sensitive: an oracle build with a transposed product in the ODEs
+    fails it (the mutated element converges to another limit, so the ratios fall to ~1)."""
+    import subprocess
+    src = open(os.path.join(os.path.dirname(oracle.__file__), "oracle.c")).read()
+    old, new = MUTATIONS[mut]
+    assert src.count(old) == 1
+    path = tmp_path / "oracle_mut.c"
+    path.write_text(src.replace(old, new))
+    so = tmp_path / "liboracle_mut.so"
+    subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", str(so), str(path), "-lm"])
+    lib = oracle.load_variant(str(so))
+    failed = False
+    for name in sorted(P14_MODELS):
+        errs, ratios = _p14_ratios(P14_MODELS[name](), lib=lib)
+        failed |= not (np.all((ratios > 1.9) & (ratios < 2.1)) and errs[-1].max() < 1e-3)
+    assert failed, f"mutation {mut} not detected by P14"
