@@ -29,8 +29,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# FP64 (DFMA) peak derived from unit counts and clock: 148 SM x 64 FP64 FMA/clk x 2 flop x 1.965 GHz.
+# FP64 (DFMA) peak derived from unit counts and clock: 148 SM x 64 FP64 FMA/clk x 2 flop x 1.965 GHz,
+# and the figure a DFMA microbenchmark measured on this pool (tools/fp64_peak.cu,
+# profiles/r01_fp64_peak_probe.log); the roofline uses the measured one.
 FP64_PEAK_TFLOPS_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+FP64_PEAK_TFLOPS_MEASURED = 34.2
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -61,6 +64,7 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
     reduce_fl = 2 * N * ny if lti else combine  # LTI: impulse-response fold (y_m -> (b, eta))
     vsz2 = vsz  # per-node values pass 1 stores for pass 2
     vapply_dense = vapply
+    vapply_node = vapply
     if nw > 0:  # R-LOWRANK node update (vapply_lowrank), R-P2REC records when smaller than (S, v)
         r = nw
         am = np.ones((N, N), bool) if amask is None else np.asarray(amask, bool)
@@ -73,6 +77,7 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         # when b == 0), q = G^-1 U^T w, w - S U q, B A, A^T (B A) + J, A^T w + eta
         vapply = (N * nU + chol + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
                   + nU + r * r + N * r + N * nA + ata + nA)
+        vapply_node = vapply  # the plain node update (no pass-2 record written)
         gram_d = sum((a + 1) * N for a in range(r))
         chol_d = gram_d + r * (r - 1) // 2 * (r + 1) + r
         vapply_dense = (N * N * r + chol_d + r * (r - 1) // 2 * N + r * N + ns * r + (0 if zero_b else N * N)
@@ -103,13 +108,40 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
     ldl = N ** 3 // 6 + N * N + 2 * N * N
     vap_m = vapply_dense if nw > 0 else vapply
     tf_down = (2 * (vap_m + ldl + 2 * N + ns), d * (ny + esz / K + vsz + nx))
+    L = 64 * K  # nodes per tile
+    # LTI data recurrence of the boundary-tile reduce (lti_fold_data): per node eta = K y + h0,
+    # b += Wb eta + cb, eta' = We eta + ... (2 N^2 + N ny FMA); it covers <= 2 tiles per trajectory
+    edge = (2 * (2 * N * N + N * ny), d * (ny + esz / K))
+    # look-back path (pmap_lb.cuh, R-FWD): pass 1 = the LTI fold (2 N ny FMA) + per run four
+    # N x N mat-vecs with the plan's run tables (S pb, Gp u, C_R v, Wr t); reads y and the run
+    # tables (Gp, Wr, Phi: 3 N^2 per run), writes v entering each run (N) and the run suffix
+    # maps (N^2 + N).  Pass 2 = per node the forward recovery of x (R-FWD: U^T (S x - v), U u,
+    # A^-1 z on the structural non-zeros) + the value-function update (the same Woodbury /
+    # general update as k_p1_down) + eta = K y; reads y, the run's S (plan table), v and
+    # suffix map, writes x.
+    if nw > 0:
+        xstep = nU * (N + 1) + nU + nA + (0 if zero_b else N)
+    else:
+        xstep = 3 * N * N + N
+    lb1 = (2 * (2 * N * ny + 4 * N * N / K), d * (ny + 3 * N * N / K + N / K + asz / K))
+    lb2 = (2 * (vapply_node + xstep + N * ny), d * (ny + nx + ns / K + N / K + asz / K))
     return {
-        "k_p1_reduce": (2 * reduce_fl, d * (ny + esz / K)),
+        "k_p1_reduce": (2 * combine, d * (ny + esz / K)),          # general models: one combine per node
+        "k_p1_reduce_lti": (2 * 2 * N * ny, d * (ny + esz / K)),   # LTI: impulse-response fold
+        "k_p1_reduce_lti_edge": edge + ("edge",),
         "k_tf_reduce": (2 * reduce_fl, d * (ny + esz / K)),
+        "k_tf_reduce_lti_edge": edge + ("edge",),
         "k_tf_down": tf_down,
         "k_p1_down": (2 * (vapply + vapply_tr / K), d * (ny + esz / K + vsz2 + asz / K)),
         "k_p2_down": (2 * trans, d * (vsz2 + nx + asz / K)),
+        # tile / group scans: one combine per tile (per group), amortised per node
+        "k_p1_tiles": (2 * combine / L, d * 2 * esz / L), "k_p1_groups": (2 * combine / (L * 128), d * esz / L),
+        "k_p2_tiles": (2 * N ** 3 / L, d * 2 * asz / L), "k_p2_groups": (2 * N ** 3 / (L * 128), d * asz / L),
+        "k_tf_tiles": (2 * combine / L, d * 2 * esz / L), "k_tf_groups": (2 * combine / (L * 128), d * esz / L),
+        "k_lb_pass1": lb1,
+        "k_lb_pass2": lb2,
         "solve": (2 * (reduce_fl + vapply + vapply_tr / K + trans), d * (ny + 2 * vsz + nx)),
+        "solve_lb": (lb1[0] + lb2[0], lb1[1] + lb2[1]),
     }
 
 
@@ -325,6 +357,26 @@ def sequential_gpu(plan, config, yd, xd, ms_parallel, torch, stream):
             "what": "map_solve_sequential: one GPU thread per trajectory, same element build and fp64 algebra"}
 
 
+# ---------------------------------------------------------------- launcher
+def self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run with
+    N ranks (one per GPU, rendezvous on 127.0.0.1); fails loudly if N GPUs are not present."""
+    import socket
+    if args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA devices are visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc != 0:
+        raise SystemExit(rc)
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -339,6 +391,8 @@ def main():
     ap.add_argument("--no-seq", action="store_true", help="skip the sequential on-device baseline (SURVEY f1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -348,6 +402,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: the N ranks were not formed")
     torch.cuda.set_device(local)
     comm = None
     if world > 1:
@@ -360,7 +416,10 @@ def main():
     from workloads.models import CONFIGS
     substeps = CONFIGS[args.config].get("substeps", 1)
     spec, y_host, T, B = build_inputs(args.config, rank, world)
+    torch.cuda.synchronize()
+    tp = time.perf_counter()
     plan = make_plan(pm, spec, T, B, rank, world, comm, substeps)
+    plan_ms = (time.perf_counter() - tp) * 1e3  # map_plan: model preprocessing, LTI / look-back tables, workspace
     solve = solve_fn(plan, args.config)
     dev = torch.device("cuda", local)
     yd = torch.from_numpy(y_host).to(dev)
@@ -437,22 +496,24 @@ def main():
     if substeps > 1:  # Euler blocks: general kernels, element build from n*ny measurements
         counts = alg_counts(plan.nx, plan.ny, lti=False, euler_n=substeps)
     else:
-        counts = alg_counts(plan.nx, plan.ny, lti=os.environ.get("PMAP_GENERAL") != "1", nw=lowrank, zero_b=zero_b,
-                            amask=amask, umask=umask)
+        kk = 32 if B * -(-plan.n_local // 2048) >= 4 * 148 else 8  # the library's run length (choose_run_length)
+        counts = alg_counts(plan.nx, plan.ny, K=kk, lti=isinstance(spec, wl.LinearSpec) and np.ndim(spec.F) == 2,
+                            nw=lowrank, zero_b=zero_b, amask=amask, umask=umask)
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl
-    step_ms_prof = sum(v[0] for v in prof.values()) / max(1, min(args.steps, 50))
-    nodes_per_launch = B * plan.n_local
-    fl, by = counts.get(dname, counts["solve"])
-    achieved_tflops = fl * nodes_per_launch / (per_launch_ms * 1e-3) / 1e12
-    achieved_gbs = by * nodes_per_launch / (per_launch_ms * 1e-3) / 1e9
+    rec = counts.get(dname)
+    tile_nodes = 64 * (32 if B * -(-plan.n_local // 2048) >= 4 * 148 else 8)
+    if rec is not None:
+        fl, by = rec[0], rec[1]
+        # units one launch processes: every node, or the <= 2 boundary tiles per trajectory
+        nodes_per_launch = B * plan.n_local if len(rec) < 3 else B * min(plan.n_local, 2 * tile_nodes)
     traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from a committed ncu capture
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        rec = tr.get("kernels", {}).get(dname)
-        if rec and tr.get("nodes") == B * plan.n_local:
-            traffic = rec["dram_bytes_per_launch"]
+        trk = tr.get("kernels", {}).get(dname)
+        if trk and tr.get("nodes") in (B * plan.n_local, B * (plan.n_local - 1)):
+            traffic = trk["dram_bytes_per_launch"]
     except Exception:
         traffic = None
     try:
@@ -461,31 +522,45 @@ def main():
         hbm_src = "measured"
     except Exception:
         hbm, hbm_src = FALLBACK_HBM_GBS, "fallback"
-    # the binding roof of the dominant kernel: FP64 ALU (DFMA pipe) or HBM, whichever
-    # fraction is larger; the other is reported alongside
-    alu_frac = achieved_tflops / FP64_PEAK_TFLOPS_DERIVED
-    hbm_frac = achieved_gbs / hbm
-    alu_src = ("derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (MEASURED_PEAKS.json has no FP64; "
-               "DFMA microbenchmark measured 34.2 TF/s, profiles/r01_fp64_peak_probe.log)")
+    fp64 = FP64_PEAK_TFLOPS_MEASURED
+    alu_src = ("measured: DFMA microbenchmark 34.2 TF/s on this pool (tools/fp64_peak.cu, "
+               "profiles/r01_fp64_peak_probe.log); MEASURED_PEAKS.json has no FP64 figure; derived 148 SM x 64 "
+               "DFMA/clk x 2 x 1.965 GHz = %.1f TF/s" % FP64_PEAK_TFLOPS_DERIVED)
     hbm_desc = f"{hbm_src}: MEASURED_PEAKS.json hbm_gbs" if hbm_src == "measured" else "fallback (B200_PROFILING.md)"
-    if hbm_frac >= alu_frac:
-        roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                    "frac": hbm_frac, "peak_source": hbm_desc,
-                    "other_roof": {"bound": "alu", "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
-                                   "unit": "TFLOP/s", "frac": alu_frac, "peak_source": alu_src}}
+    if rec is None:
+        roofline = {"bound": None, "kernel": dname, "achieved": None, "peak": None, "unit": None, "frac": None,
+                    "traffic": traffic, "why": f"no algorithmic count for {dname}"}
     else:
-        roofline = {"bound": "alu", "kernel": dname, "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS_DERIVED,
-                    "unit": "TFLOP/s", "frac": alu_frac, "peak_source": alu_src,
-                    "other_roof": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                                   "frac": hbm_frac, "peak_source": hbm_desc}}
-    roofline.update({"traffic": traffic,
-                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)" if traffic else None,
-                     "alg_flops_per_node": fl, "alg_bytes_per_node": by, "kernel_ms_per_launch": per_launch_ms,
-                     "kernel_share_of_step": dms / max(1e-9, sum(v[0] for v in prof.values()))})
-    sfl, sby = counts["solve"]
-    solve_hbm = {"alg_bytes_per_node": sby, "achieved_gbs": sby * B * T / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
+        achieved_tflops = fl * nodes_per_launch / (per_launch_ms * 1e-3) / 1e12
+        achieved_gbs = by * nodes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        # the binding roof of the dominant kernel: FP64 ALU (DFMA pipe) or HBM, whichever
+        # fraction is larger; the other is reported alongside
+        alu_frac = achieved_tflops / fp64
+        hbm_frac = achieved_gbs / hbm
+        if hbm_frac >= alu_frac:
+            roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                        "frac": hbm_frac, "peak_source": hbm_desc,
+                        "other_roof": {"bound": "alu", "achieved": achieved_tflops, "peak": fp64,
+                                       "unit": "TFLOP/s", "frac": alu_frac, "peak_source": alu_src}}
+        else:
+            roofline = {"bound": "alu", "kernel": dname, "achieved": achieved_tflops, "peak": fp64,
+                        "unit": "TFLOP/s", "frac": alu_frac, "peak_source": alu_src,
+                        "other_roof": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                                       "frac": hbm_frac, "peak_source": hbm_desc}}
+        roofline.update({"traffic": traffic,
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)" if traffic else None,
+                         "alg_flops_per_node": fl, "alg_bytes_per_node": by, "nodes_per_launch": nodes_per_launch,
+                         "kernel_ms_per_launch": per_launch_ms,
+                         "kernel_share_of_step": dms / max(1e-9, sum(v[0] for v in prof.values()))})
+    lb = "k_lb_pass2" in prof
+    sfl, sby = counts["solve_lb" if lb else "solve"]
+    cfl, cby = counts["solve"]
+    solve_hbm = {"schedule": "look-back (2 kernels, R-FWD)" if lb else "scan hierarchy",
+                 "alg_bytes_per_node": sby, "achieved_gbs": sby * B * T / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
                  "peak_source": hbm_src, "frac_of_hbm_roofline": sby * B * T / (ms * 1e-3) / 1e9 / hbm,
-                 "alg_tflops": sfl * B * T / (ms * 1e-3) / 1e12}
+                 "alg_tflops": sfl * B * T / (ms * 1e-3) / 1e12, "frac_of_fp64_peak": sfl * B * T / (ms * 1e-3) / 1e12 / fp64,
+                 "canonical_bytes_per_node": cby,
+                 "canonical_frac_of_hbm_roofline": cby * B * T / (ms * 1e-3) / 1e9 / hbm}
 
     seq = None
     if world == 1 and not args.no_seq:
@@ -512,6 +587,8 @@ def main():
         "sequential_gpu": seq,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
+        "launches_per_solve": launches_per_step,
+        "plan_ms": plan_ms,
         "clocks": clk,
     }
     print(json.dumps(out), flush=True)

@@ -226,6 +226,12 @@ map_status map_profile_enable(map_plan_t plan, int32_t enable);
  * on error.  Resets the accumulation. */
 int32_t map_profile_read(map_plan_t plan, const char** names, double* ms, int64_t* launches, int32_t nmax);
 
+/* Diagnostics (tools/lb_timing.py): plans created with PMAP_LB_TIMING=1 in the
+ * environment record per-tile %globaltimer stamps at the phase boundaries of the two
+ * look-back kernels ([2 passes][tiles][8] uint64, ns).  Copies min(n, total) stamps of
+ * the last solve to `out` (host) and returns the total, 0 if not recorded, -1 on error. */
+int64_t map_debug_lb_timing(map_plan_t plan, uint64_t* out, int64_t n);
+
 /* Library version string. */
 const char* map_version(void);
 

@@ -25,7 +25,7 @@ STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 
 EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter", "map_solve_nonlinear",
            "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
            "map_profile_enable", "map_profile_read", "map_shard_payload_bytes", "map_shard_phase",
-           "map_version", "map_solve_sequential"]
+           "map_version", "map_solve_sequential", "map_debug_lb_timing"]
 
 
 class MapError(RuntimeError):
@@ -96,6 +96,8 @@ def load_library():
         lib.map_shard_payload_bytes.restype = I64
         lib.map_shard_phase.argtypes = [P, I32, P, P, P, P, P, P]
         lib.map_shard_phase.restype = ctypes.c_int
+        lib.map_debug_lb_timing.argtypes = [P, P, I64]
+        lib.map_debug_lb_timing.restype = I64
         _lib = lib
     return _lib
 
@@ -393,6 +395,17 @@ class Plan:
         if k < 0:
             raise MapError(3, map_last_error(self.handle))
         return {names[i].decode(): (ms[i], cnt[i]) for i in range(k)}
+
+    def lb_timing(self):
+        """Per-tile %globaltimer stamps of the last look-back solve ([2][tiles][8] uint64 ns),
+        recorded only by plans created with PMAP_LB_TIMING=1 (diagnostics); None otherwise."""
+        lib = load_library()
+        n = int(lib.map_debug_lb_timing(self.handle, None, 0))
+        if n <= 0:
+            return None
+        out = np.zeros(n, dtype=np.uint64)
+        lib.map_debug_lb_timing(self.handle, out.ctypes.data, n)
+        return out.reshape(2, -1, 8)
 
     @property
     def launches(self) -> int:

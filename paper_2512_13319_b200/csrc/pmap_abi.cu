@@ -367,6 +367,10 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     p->force_shard = fs && fs[0] == '1' && d.nccl_comm;
     const char* nr = getenv("PMAP_NO_P2REC");
     p->no_rec = nr && nr[0] == '1';
+    const char* nlb = getenv("PMAP_NO_LB");
+    p->no_lb = nlb && nlb[0] == '1';
+    const char* lbs = getenv("PMAP_LB_STRESS");
+    p->lb_stress = (lbs && lbs[0] == '1') ? 1 : 0;
   }
   const int nx = d.nx, ny = d.ny, nw = d.nw;
   const int NS = nx * (nx + 1) / 2;
@@ -1078,8 +1082,15 @@ int32_t map_profile_read(map_plan_t p, const char** names, double* ms, int64_t* 
   return k;
 }
 
-int64_t map_workspace_bytes(map_plan_t p) { return p ? (int64_t)p->ws_bytes : 0; }
+int64_t map_workspace_bytes(map_plan_t p) { return p ? (int64_t)(p->ws_bytes + p->lb_bytes) : 0; }
 
 int64_t map_last_launch_count(map_plan_t p) { return p ? p->launches : 0; }
+
+int64_t map_debug_lb_timing(map_plan_t p, uint64_t* out, int64_t n) {
+  if (!p || !p->lb_tim) return 0;
+  const int64_t m = n < (int64_t)p->lb_tim_n ? n : (int64_t)p->lb_tim_n;
+  if (out && m > 0 && cudaMemcpy(out, p->lb_tim, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)p->lb_tim_n;
+}
 
 }  // extern "C"

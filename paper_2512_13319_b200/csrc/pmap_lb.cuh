@@ -1,0 +1,1327 @@
+// pmap_lb.cuh -- single-pass decoupled look-back solve for time-invariant (LTI) models.
+//
+// Two kernels per solve ("look-back path"):
+//
+//   k_lb_pass1  pass 1 (value functions, P:260-341 / P:382-409), one CTA of three warps
+//               per tile (NT = 64 runs x K interior nodes): warps 1-2 stage y and fold the
+//               node elements' data parts per run (LTI impulse responses, R-LTI) and
+//               reduce them to the tile aggregate; warp 0 then runs the decoupled
+//               look-back over the preceding tiles for the value function entering the
+//               tile while warps 1-2, in parallel, scan the runs and build every run's
+//               pass-2 map (R-RUNAGG) and its in-tile suffix composition as affine
+//               functions of that still unknown value function; once warp 0 has it, the
+//               maps are finished with one mat-vec per run and stored for pass 2, with
+//               the tile's and (last arriver) the group's pass-2 offsets.
+//   k_lb_pass2  pass 2 (trajectory), one CTA of two warps per tile, tiles in
+//               reverse order: the y tile into shared memory while warp 0 looks back over
+//               the following tiles for x* at the tile's last node -- every map is already
+//               in memory, so it never waits, only stops early at a published prefix --
+//               then per run x*_{s-1} from its suffix map and a FORWARD sweep over the
+//               run's nodes that recomputes (S_i, v_i) from the run's value function and y
+//               and recovers x*_i (R-FWD):
+//                   x*_i = A_i^-1 [ x*_{i-1} - b_i + C_i (S_{i-1} x*_{i-1} - v_{i-1}) ],
+//               the transition x*_{i-1} = (I + C_i S_{i-1})^-1 (A_i x*_i + b_i + C_i v_{i-1})
+//               of R-TRANS solved for x*_i.  Nothing per node is stored between the
+//               passes: the schedule moves y twice and x once (+ O(1/K) run data).
+//
+// Plan tables (R-LTI).  Node 0 (E_0 = prior + y_0) is the carry-in, so every tile holds
+// only interior nodes: tile j covers nodes [1 + jL, 1 + (j+1)L), L = NT K, and every
+// tile but a ragged last one has the same matrix parts.  The value function entering
+// tile j has a data-independent S_j and a v that is affine in the v entering tile j-1:
+// v_end(j) = Gt_j v_end(j-1) + g_j with Gt_j = A^T (I + S_j C)^-1 and g_j = eta_j -
+// Gt_j S_j b_j from the tile's data parts (b_j, eta_j).  Every S-dependent matrix (per
+// tile, per run, and the products of Gt and of the tiles' pass-2 matrices Phi over
+// look-back windows) is computed once in map_plan, so the per-solve work is data parts,
+// mat-vecs and the node recursion.
+//
+// Look-back (both kernels, two levels): a tile first looks at the tiles of its group of
+// kLbGroup tiles (one warp window), then at whole groups, whose aggregates the group's
+// last-arriving tile publishes, so even the first wave of CTAs resolves in two window
+// steps; each window is one mat-vec per lane with a plan-time product and a warp sum.
+// Status words: 0 = nothing, 1 = aggregate, 2 = inclusive prefix; written with
+// st.release after the payload, polled relaxed, one acquire fence before the payload is
+// read through L2.  Tiles run in ticket order (atomic counter), so a CTA only ever
+// waits on CTAs that started before it (no deadlock).  Flags are cleared by the other
+// kernel of the solve, counters by their last user, so repeated solves (and CUDA-graph
+// replays) need no memset.
+#pragma once
+#include "pmap_lti.cuh"
+
+namespace pmap {
+
+constexpr int kLbGroup = 32;  // tiles per look-back group (one warp window)
+#ifndef PM_LB2_MAXREG
+#define PM_LB2_MAXREG 168
+#endif
+
+struct LbGeom {
+  int64_t Nn;     // nodes per trajectory (this launch)
+  int64_t tpt;    // tiles per trajectory
+  int64_t gpt;    // groups per trajectory
+  int64_t batch;
+};
+
+// Plan-time, data-independent quantities of tile j (shared by every trajectory).
+template <typename R, int N>
+struct LbTileTab {
+  R S[Dim<N>::NS];  // S of the value function entering tile j (after node jL)
+  R Gt[N][N];       // A_L^T (I + S C_L)^-1 (full tiles)
+  R Hs[N][N];       // Gt S
+};
+
+// Plan-time, data-independent quantities of run r of tile j, stored field-major
+// [tpt][F][NT] (lane r reads field f of its run coalesced):
+//   GP  = A_p^T (I + S_in C_p)^-1   v-map of the exclusive prefix of r runs (span element
+//                                    (A_p, C_p, J_p) of SF, S_in = S entering the tile):
+//                                    v_{s-1} = GP (v_in - S_in pb) + ph
+//   WR  = (I + C_R S_{s-1})^-1      the run's transition solve (R-RUNAGG, run element R)
+//   PHI = WR A_R                    the run's pass-2 matrix
+//   QB  = sum_{k >= r} Phi_r..Phi_{k-1} WR_k C_Rk GP_k   the v_in-coefficient of the run's
+//                                    suffix offset (beta_k = WR_k (rb_k + C_Rk v_{s-1,k}))
+//   SP  = S_{s-1}                   S entering the run (pass 2 restarts the node recursion there)
+// Empty runs of a ragged last tile are identity maps (PHI = I, WR = QB... = 0).
+template <int N>
+struct LbRunTab {
+  static constexpr int GP = 0, WR = N * N, PHI = 2 * N * N, QB = 3 * N * N, SP = 4 * N * N,
+                       F = 4 * N * N + Dim<N>::NS;
+};
+
+// One thread per (tile, run): GP, WR, PHI, SP from the tile's S and the LTI span tables.
+template <typename R, int N, int NY, int NT, int K>
+__global__ void k_lb_setup_runs(const LtiTables<R, N, NT, K>* __restrict__ tab, const LbTileTab<R, N>* __restrict__ lt,
+                                int64_t tpt, int64_t Nn, R* __restrict__ lrt, int* okflag) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= tpt * NT) return;
+  const int64_t j = idx / NT;
+  const int r = (int)(idx % NT);
+  const int64_t n0 = 1 + j * (int64_t)NT * K;
+  const int q = (int)max((int64_t)0, min((int64_t)K, Nn - n0 - (int64_t)r * K));
+  R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+  bool ok = true;
+  VF<R, N> cur;
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) cur.S[k] = lt[j].S[k];
+#pragma unroll
+  for (int i = 0; i < N; ++i) cur.v[i] = R(0);
+  R Gp[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) Gp[i][c] = (i == c) ? R(1) : R(0);
+  if (r > 0 && q > 0) {
+    Elem<R, N> p;
+    int f = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) p.A[i][jj] = tab->SF[f++][r - 1];
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) p.C[k] = tab->SF[f++][r - 1];
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) p.J[k] = tab->SF[f++][r - 1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) p.b[i] = p.h[i] = R(0);
+    // GP^T = (I + C_p S_in)^-1 A_p  (= vapply's transition matrix X1)
+    Aff<R, N> tr;
+    VF<R, N> out;
+    vapply<R, N, true>(p, cur, out, &tr, ok);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) Gp[i][c] = tr.P[c][i];
+    cur = out;
+  }
+  R Wr[N][N], Phi[N][N];
+  if (q == 0) {  // empty run: identity map
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        Wr[i][c] = R(0);
+        Phi[i][c] = (i == c) ? R(1) : R(0);
+      }
+  } else {
+    // run element R: one full run, or the partial run of the ragged last tile
+    Elem<R, N> ra;
+    if (q == K) {
+      load(ra, tab->E1, 1);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) ra.A[i][jj] = tab->PA[q - 1][i][jj];
+#pragma unroll
+      for (int k = 0; k < Dim<N>::NS; ++k) {
+        ra.C[k] = tab->PC[q - 1][k];
+        ra.J[k] = tab->PJ[q - 1][k];
+      }
+    }
+    // Wr = (I + C_R S)^-1 column by column, Phi = Wr A_R
+    LUF<R, N> fct;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        R s = (i == c) ? R(1) : R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          s = fma(ra.C[i <= k ? sidx(i, k, N) : sidx(k, i, N)], cur.S[k <= c ? sidx(k, c, N) : sidx(c, k, N)], s);
+        fct.a[i][c] = s;
+      }
+    lu_factor(fct, ok);
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R t[N], u[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        t[i] = (i == c) ? R(1) : R(0);
+        u[i] = ra.A[i][c];
+      }
+      lu_solve(fct, t);
+      lu_solve(fct, u);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        Wr[i][c] = t[i];
+        Phi[i][c] = u[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      rt[(LbRunTab<N>::GP + i * N + c) * NT] = Gp[i][c];
+      rt[(LbRunTab<N>::WR + i * N + c) * NT] = Wr[i][c];
+      rt[(LbRunTab<N>::PHI + i * N + c) * NT] = Phi[i][c];
+    }
+#pragma unroll
+  for (int k = 0; k < Dim<N>::NS; ++k) rt[(LbRunTab<N>::SP + k) * NT] = cur.S[k];
+  if (!ok) atomicExch(okflag, 0);
+}
+
+// One thread per tile, serial over the runs: the suffix coefficients QB_r (backwards),
+// and the tile's pass-2 matrix Phi_tile = Phi_0 Phi_1 ... Phi_{NT-1} (x at the tile's
+// last node -> x at the node before it).
+template <typename R, int N, int NT, int K>
+__global__ void k_lb_setup_tiles(const LtiTables<R, N, NT, K>* __restrict__ tab, R* __restrict__ lrt, int64_t tpt,
+                                 int64_t Nn, R* __restrict__ phit) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= tpt) return;
+  const int64_t n0 = 1 + j * (int64_t)NT * K;
+  R Q[N][N], P[N][N];  // running QB (suffix) and Phi product (suffix: Phi_r ... Phi_{NT-1})
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      Q[i][c] = R(0);
+      P[i][c] = (i == c) ? R(1) : R(0);
+    }
+  for (int r = NT - 1; r >= 0; --r) {
+    R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+    const int q = (int)max((int64_t)0, min((int64_t)K, Nn - n0 - (int64_t)r * K));
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) rt[(LbRunTab<N>::QB + i * N + c) * NT] = R(0);
+      continue;
+    }
+    R CR[Dim<N>::NS];
+#pragma unroll
+    for (int k = 0; k < Dim<N>::NS; ++k) CR[k] = (q == K) ? tab->E1[N * N + N + k] : tab->PC[q - 1][k];
+    R Wr[N][N], Ph[N][N], Gp[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        Wr[i][c] = rt[(LbRunTab<N>::WR + i * N + c) * NT];
+        Ph[i][c] = rt[(LbRunTab<N>::PHI + i * N + c) * NT];
+        Gp[i][c] = rt[(LbRunTab<N>::GP + i * N + c) * NT];
+      }
+    // B = Wr C_R Gp ; QB_r = B + Phi_r QB_{r+1}
+    R WC[N][N], Nq[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        R a = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) a = fma(Wr[i][k], CR[k <= c ? sidx(k, c, N) : sidx(c, k, N)], a);
+        WC[i][c] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        R a = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          a = fma(WC[i][k], Gp[k][c], a);
+          a = fma(Ph[i][k], Q[k][c], a);
+        }
+        Nq[i][c] = a;
+      }
+    R Np[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        R a = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) a = fma(Ph[i][k], P[k][c], a);
+        Np[i][c] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        Q[i][c] = Nq[i][c];
+        P[i][c] = Np[i][c];
+        rt[(LbRunTab<N>::QB + i * N + c) * NT] = Q[i][c];
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) phit[(j * N + i) * N + c] = P[i][c];
+}
+
+// Workspace pointers of the look-back path.
+template <typename R>
+struct LbWs {
+  R* agg1;    // [tiles][N]              g_j (pass-1 tile aggregate, data part)
+  R* pub1;    // [tiles][N]              v_end(j)
+  R* gagg1;   // [groups][N]             group g
+  R* rcv;     // [tiles][N][NT]          v entering each run (pass 1 -> pass 2)
+  R* ri;      // [tiles][Aff::SZ][NT]    run suffix maps: x at the tile's last node -> x_{s-1}
+  R* agg2;    // [tiles][N]              tile pass-2 offsets beta_tile (Phi_tile: plan)
+  R* gagg2;   // [groups][N]             group pass-2 offsets
+  R* pub2;    // [tiles][N]              x at the last node of tile j - 1 (pass-2 prefix)
+  R* seed;    // [batch][N]              x*_T = S_T^-1 v_T
+  unsigned* flag1;   // [tiles]
+  unsigned* gflag1;  // [groups]
+  unsigned* gcnt1;   // [groups]
+  unsigned* gcnt2;   // [groups]
+  unsigned* flag2;   // [tiles]
+  unsigned* ctr;     // [2] tickets of pass 1 / pass 2
+  const R* Pa;       // [tpt][kLbGroup + 1][N][N] plan: Pa[j][l] = Gt_{j-1} Gt_{j-2} ... Gt_{j-l}
+  const R* Pb;       // triangular [gpt][G + 1][N][N]: Pb[G][l] = GtG_{G-1} ... GtG_{G-l}
+  const R* Qa;       // [tpt][kLbGroup + 1][N][N] plan: Qa[j][l] = Phi_{j+1} Phi_{j+2} ... Phi_{j+l}
+  const R* Qb;       // triangular [gpt][gpt - G][N][N]: Qb[G][l] = PhiG_{G+1} ... PhiG_{G+l}
+  unsigned long long* tim;  // [2][tiles][8] globaltimer stamps (PMAP_LB_TIMING=1 diagnostics), else null
+};
+
+PM_INLINE unsigned long long lb_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define LB_STAMP(PASS, K)                                                                 \
+  do {                                                                                   \
+    if (w.tim && threadIdx.x == 0) w.tim[((PASS) * g.batch * g.tpt + tile) * 8 + (K)] = lb_now(); \
+  } while (0)
+
+// Status words are polled with relaxed gpu-scope loads (LDG.STRONG.GPU, no L1
+// invalidation per poll: an ld.acquire would emit CCTL.IVALL on every iteration and
+// flush the SM's L1 under the other CTAs' feet); once the warp has seen what it needs,
+// one fence.acq_rel.gpu orders the payload loads (read through L2) after the polls.
+PM_INLINE unsigned lb_ld_status(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PM_INLINE void lb_fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Group arrival counter: acq_rel, so the payload this thread published is visible to the
+// last arriver, which reads every tile's payload of the group after its own arrival.
+PM_INLINE unsigned lb_arrive(unsigned* p) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+PM_INLINE void lb_st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <typename R>
+PM_INLINE R lb_ldcg(const R* p) {
+  return __ldcg(p);
+}
+
+// Optional delay injection for the look-back stress test (PMAP_LB_STRESS): a
+// pseudo-random pause of up to ~16 us before a publication.
+PM_INLINE void lb_stress(int stress, int64_t key, int salt) {
+  if (stress) {
+    unsigned h = (unsigned)(key * 2654435761ull) ^ (unsigned)(salt * 40503);
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    const unsigned ns = (h & 7u) * 2000u;
+    for (unsigned t = 0; t < ns; t += 1000u) __nanosleep(1000u);
+  }
+}
+
+// The tile's y rows (nodes [n0, n0 + nvalid)) into padded shared-memory run rows,
+// one cp.async (LDGSTS) per node row, consecutive threads on consecutive rows.
+template <typename R, int NY, int NT, int K>
+struct LbYStage {
+  static constexpr int BYTES = NY * (int)sizeof(R);
+  static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16 || BYTES % 16 == 0, "row size");
+  static constexpr int ROW = ((K * NY * (int)sizeof(R) + 15) / 16 * 16 + 16) / (int)sizeof(R);
+  static PM_INLINE void issue(R* ys, const R* src_y, int nvalid, int tid, int nthreads) {
+    for (int q = tid; q < nvalid; q += nthreads) {
+      const int run = q / K, mm = q - run * K;
+      R* dst = ys + run * ROW + mm * NY;
+      const R* srcp = src_y + (int64_t)q * NY;
+      const unsigned sdst = (unsigned)__cvta_generic_to_shared(dst);
+      if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 16; ++c)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + 16 * c),
+                       "l"(srcp + c * (16 / sizeof(R))));
+      } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sdst), "l"(srcp), "n"(BYTES));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  static PM_INLINE void wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+};
+
+
+// Barrier of warps 1-2 (the 64 run threads of k_lb_pass1); warp 0 never joins it.
+PM_INLINE void lb_bar_runs() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+
+// Tile total of the NT = 64 run aggregates' data parts (r = run index 0..63, called by
+// the 64 run threads only): a tree over aligned equal spans with the constant-bank
+// coefficient sets of lti_run_reduce; run 63 ends with the total.
+template <typename R, int N, int NY, int K>
+PM_INLINE void lb_run_reduce64(const LtiFoldParams<R, N, NY, K, 6>& fp, int r, R (&bb)[N], R (&hh)[N], R* s_tot) {
+  const int lane = r & 31;
+  const unsigned FULL = 0xffffffffu;
+  auto step = [&](int lg, const R (&b2)[N], const R (&h2)[N]) {
+    R nb[N], nh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sb = fma(fp.Uf[lg][0][i][k], bb[k], sb);
+        sb2 = fma(fp.Uf[lg][1][i][k], h2[k], sb2);
+        sh_ = fma(fp.Uf[lg][2][i][k], h2[k], sh_);
+        sh2 = fma(-fp.Uf[lg][3][i][k], bb[k], sh2);
+      }
+      nb[i] = sb + sb2;
+      nh[i] = sh_ + sh2;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = nb[i];
+      hh[i] = nh[i];
+    }
+  };
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {
+    const int d = 1 << lg;
+    R b2[N], h2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b2[i] = __shfl_up_sync(FULL, bb[i], d);
+      h2[i] = __shfl_up_sync(FULL, hh[i], d);
+    }
+    if (((lane + 1) & (2 * d - 1)) == 0) step(lg, b2, h2);  // lane ends an aligned span of 2d runs
+  }
+  if (r == 31) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      s_tot[i] = bb[i];
+      s_tot[N + i] = hh[i];
+    }
+  }
+  lb_bar_runs();
+  if (r == 63) {
+    R b2[N], h2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b2[i] = s_tot[i];
+      h2[i] = s_tot[N + i];
+    }
+    step(5, b2, h2);
+  }
+  lb_bar_runs();  // s_tot is reused
+}
+
+// Inclusive scan of the 64 run aggregates' data parts (run threads only; the warp-
+// synchronous Kogge-Stone of lti_run_scan with the compact coefficient tables, the
+// cross-warp step through s_tot and the run barrier).
+template <typename R, int N>
+PM_INLINE void lb_run_scan64(const R* __restrict__ UWc, const R* __restrict__ UX, int r, R (&bb)[N], R (&hh)[N],
+                             R* s_tot) {
+  const int lane = r & 31;
+  const unsigned FULL = 0xffffffffu;
+  auto step = [&](const R* __restrict__ U, int stride, int slot, const R (&b2)[N], const R (&h2)[N]) {
+    R nb[N], nh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R sb = b2[i], sb2 = R(0), sh_ = hh[i], sh2 = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sb = fma(__ldg(U + ((0 * N + i) * N + k) * stride + slot), bb[k], sb);
+        sb2 = fma(__ldg(U + ((1 * N + i) * N + k) * stride + slot), h2[k], sb2);
+        sh_ = fma(__ldg(U + ((2 * N + i) * N + k) * stride + slot), h2[k], sh_);
+        sh2 = fma(-__ldg(U + ((3 * N + i) * N + k) * stride + slot), bb[k], sh2);
+      }
+      nb[i] = sb + sb2;
+      nh[i] = sh_ + sh2;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = nb[i];
+      hh[i] = nh[i];
+    }
+  };
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {
+    const int d = 1 << lg;
+    R b2[N], h2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b2[i] = __shfl_up_sync(FULL, bb[i], d);
+      h2[i] = __shfl_up_sync(FULL, hh[i], d);
+    }
+    if (lane >= d) step(UWc + (d - 1) * 4 * N * N, d, min(lane - d, d - 1), b2, h2);
+  }
+  if (r == 31) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      s_tot[i] = bb[i];
+      s_tot[N + i] = hh[i];
+    }
+  }
+  lb_bar_runs();
+  if (r >= 32) {
+    R b2[N], h2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      b2[i] = s_tot[i];
+      h2[i] = s_tot[N + i];
+    }
+    step(UX, 32, lane, b2, h2);
+  }
+}
+
+template <typename R, int N>
+PM_INLINE void lb_matvec(const R* __restrict__ P, const R (&x)[N], R (&o)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R a = R(0);
+#pragma unroll
+    for (int c = 0; c < N; ++c) a = fma(__ldg(P + i * N + c), x[c], a);
+    o[i] = a;
+  }
+}
+
+template <typename R, int N>
+PM_INLINE void lb_warp_sum(R (&s)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+}
+
+// ------------------------------------------------------------------ pass 1
+template <typename R, int N, int NY, int NT, int K, class Src>
+__global__ void __launch_bounds__(NT + 32, 4)
+    k_lb_pass1(const __grid_constant__ LtiFoldParams<R, N, NY, K, Log2<NT>::value> fp, const __grid_constant__ Src src,
+               const LbGeom g, const R* __restrict__ y, const LtiTables<R, N, NT, K>* __restrict__ tab,
+               const LbTileTab<R, N>* __restrict__ lt, const R* __restrict__ lrt, const LbWs<R> w,
+               unsigned long long* flag, int stress) {
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  using A = Aff<R, N>;
+  using YS = LbYStage<R, NY, NT, K>;
+  constexpr int L = NT * K;
+  constexpr int NS = Dim<N>::NS;
+  static_assert(NT == 64, "64 run threads (warps 1-2) per tile");
+  __shared__ __align__(16) R ys[NT * YS::ROW];
+  __shared__ int s_ticket, s_glast;
+  __shared__ R s_tile[2 * N];  // tile aggregate data parts (b, eta)
+  __shared__ R s_vin[N];       // v entering the tile (warp 0's look-back)
+  __shared__ R s_tot[2 * N];   // cross-warp step of the run reduce / scan
+  __shared__ R s_a32[A::SZ];   // runs 32..63 suffix map (cross-warp)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = tid - 32;  // run of the run threads (warps 1-2)
+  const unsigned FULL = 0xffffffffu;
+  if (tid == 0) {
+    const unsigned total = (unsigned)(g.batch * g.tpt);
+    const unsigned t = atomicAdd(&w.ctr[0], 1u);
+    if (t == total - 1) atomicExch(&w.ctr[0], 0u);  // every ticket is taken: reset for the next solve
+    s_ticket = (int)t;
+  }
+  __syncthreads();
+  const int64_t t = s_ticket;
+  const int64_t b = t / g.tpt, j = t % g.tpt;
+  const int64_t tile = b * g.tpt + j;
+  const int64_t G = j / kLbGroup;
+  const bool last = (j == g.tpt - 1);
+  LB_STAMP(0, 0);
+  if (tid == 0) w.flag2[tile] = 0u;  // pass-2 prefix status of the previous solve (that kernel has finished)
+  const int64_t n0 = 1 + j * (int64_t)L;
+  const int nvalid = (int)min((int64_t)L, g.Nn - n0);
+  const R* yb = y + b * g.Nn * NY;
+  YS::issue(ys, yb + n0 * NY, nvalid, tid, NT + 32);
+  YS::wait();
+  __syncthreads();
+  LB_STAMP(0, 1);
+  bool ok = true;
+  int q = 0;
+  R rb[N], rh[N], bb[N], hh[N];
+  if (warp >= 1) {
+    // run fold: data parts of the run aggregate (impulse responses on full runs, R-LTI;
+    // the LTI data recurrence on the partial run of a ragged last tile)
+    q = max(0, min(K, nvalid - r * K));
+    const R* yr = ys + r * YS::ROW;
+    if (q == K) {
+      R acc0[2 * N], acc1[2 * N];
+#pragma unroll
+      for (int i = 0; i < 2 * N; ++i) {
+        acc0[i] = fp.crun[i];
+        acc1[i] = R(0);
+      }
+#pragma unroll
+      for (int m = 0; m < K; m += 2) {
+#pragma unroll
+        for (int i = 0; i < 2 * N; ++i)
+#pragma unroll
+          for (int k = 0; k < NY; ++k) {
+            acc0[i] = fma(fp.GK[m][i][k], yr[m * NY + k], acc0[i]);
+            acc1[i] = fma(fp.GK[m + 1][i][k], yr[(m + 1) * NY + k], acc1[i]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        rb[i] = acc0[i] + acc1[i];
+        rh[i] = acc0[N + i] + acc1[N + i];
+      }
+    } else if (q > 0) {
+      lti_fold_data<R, N, NY, NT, K>(fp.node, tab, q, [&](int m) { return yr + m * NY; }, rb, rh);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) rb[i] = rh[i] = R(0);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = rb[i];
+      hh[i] = rh[i];
+    }
+    if (!last) {  // every tile but the last is full: the tile total by the tree
+      lb_run_reduce64<R, N, NY, K>(fp, r, bb, hh, s_tot);
+      if (r == NT - 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          s_tile[i] = bb[i];
+          s_tile[N + i] = hh[i];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  LB_STAMP(0, 2);
+  if (warp == 0) {
+    // ---- publish g_j, the group aggregate (last arriver), look back for v entering the tile
+    const LbTileTab<R, N>* tj = lt + j;
+    const int cnt = (int)(j - G * kLbGroup);  // tiles before j in its group
+    // the plan products this warp will need, loaded before anything waits on them:
+    // Pa[j][lane] (window (a)), Pb[G][lane] (first window of (b)), Gt_j, Hs_j
+    R Pa_l[N][N], Pb_l[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        Pa_l[i][c] = __ldg(w.Pa + ((j * (kLbGroup + 1) + lane) * N + i) * N + c);
+        Pb_l[i][c] = (lane <= G) ? __ldg(w.Pb + ((G * (G + 1) / 2 + lane) * N + i) * N + c) : R(0);
+      }
+    R gj[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+      if (!last) {
+        s = s_tile[N + i];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(-__ldg(&tj->Hs[i][k]), s_tile[k], s);
+      }
+      gj[i] = s;
+    }
+    const bool full_group = (G + 1) * kLbGroup <= g.tpt - 1;  // every tile of the group precedes the last tile
+    if (!last) {
+      if (lane == 0) {
+        lb_stress(stress, tile, 1);
+#pragma unroll
+        for (int i = 0; i < N; ++i) w.agg1[tile * N + i] = gj[i];
+        lb_st_release(&w.flag1[tile], 1u);
+        s_glast = full_group && lb_arrive(&w.gcnt1[b * g.gpt + G]) == kLbGroup - 1;
+      }
+      __syncwarp();
+      if (s_glast) {  // last arriver: g_G = sum_l Pa[32G + 32][l] g_{32G + 31 - l}
+        const int64_t k = G * kLbGroup + kLbGroup - 1 - lane;
+        R x[N], sg[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = lb_ldcg(w.agg1 + (b * g.tpt + k) * N + i);
+        lb_matvec<R, N>(w.Pa + (((G + 1) * kLbGroup) * (kLbGroup + 1) + lane) * N * N, x, sg);
+        lb_warp_sum<R, N>(sg);
+        if (lane == 0) {
+          lb_stress(stress, tile, 2);
+#pragma unroll
+          for (int i = 0; i < N; ++i) w.gagg1[(b * g.gpt + G) * N + i] = sg[i];
+          lb_st_release(&w.gflag1[b * g.gpt + G], 1u);
+          atomicExch(&w.gcnt1[b * g.gpt + G], 0u);
+        }
+      }
+    }
+    LB_STAMP(0, 3);
+    R eta0[N];  // v of node 0: P0^-1 m0 + K y_0 - K r (E_0's data), the terminal of the look-back
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = src.h00[i];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], yb[k], s);
+      eta0[i] = s;
+    }
+    R vin[N];
+    if (j == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) vin[i] = eta0[i];
+    } else {
+      //   v_end(j-1) = sum_{l < l*} Pa[j][l] g_{j-1-l} + Pa[j][l*] v_end(j-1-l*)
+      // over (a) the tiles before j in its group, and, if none of them holds a prefix,
+      // Pa[j][cnt] v_end(32G - 1) with (b) v_end(32G - 1) = sum_{l < l*} Pb[G][l] g_{G-1-l}
+      // + Pb[G][l*] v_end(group G-1-l*) over whole groups (group -1 = node 0).  Both
+      // windows are polled together; one fence; one round of payload loads.
+      const int64_t ka = j - 1 - lane;
+      const int64_t Gp = G - 1 - lane;
+      const bool needa = lane < cnt, needb = Gp >= 0;
+      unsigned sta = 0, stb = (Gp == -1) ? 3u : 0u;
+      unsigned prea = 0, preb = 0;
+      for (;;) {
+        if (needa && sta == 0u) sta = lb_ld_status(&w.flag1[b * g.tpt + ka]);
+        if (needb && stb == 0u) {
+          if (lb_ld_status(&w.flag1[b * g.tpt + Gp * kLbGroup + kLbGroup - 1]) == 2u)
+            stb = 2u;
+          else if (lb_ld_status(&w.gflag1[b * g.gpt + Gp]) == 1u)
+            stb = 1u;
+        }
+        if (__ballot_sync(FULL, needa && sta == 0u) == 0u) {
+          prea = __ballot_sync(FULL, needa && sta == 2u);
+          if (prea) break;  // a prefix in the group: (b) is not needed
+          if (__ballot_sync(FULL, needb && stb == 0u) == 0u) break;
+        }
+        __nanosleep(20);
+      }
+      LB_STAMP(0, 6);
+      lb_fence_acquire();
+      preb = prea ? 0u : __ballot_sync(FULL, stb >= 2u);
+      const int la = prea ? __ffs(prea) - 1 : cnt;  // (a) terms l < la, prefix at la if prea
+      R sa[N], sb[N];
+      {
+        R x[N];
+        const bool use = lane < la || (lane == la && prea);
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+          x[i] = !use ? R(0)
+                      : (lane < la ? lb_ldcg(w.agg1 + (b * g.tpt + ka) * N + i) : lb_ldcg(w.pub1 + (b * g.tpt + ka) * N + i));
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R t2 = R(0);
+#pragma unroll
+          for (int c = 0; c < N; ++c) t2 = fma(Pa_l[i][c], x[c], t2);
+          sa[i] = t2;
+        }
+      }
+      if (!prea) {
+        const int lb = preb ? __ffs(preb) - 1 : 32;
+        {
+          R x[N];
+          const bool use = lane <= lb && Gp >= -1 && (lane < lb || preb);
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+            x[i] = !use ? R(0)
+                        : (stb == 3u ? eta0[i]
+                                     : (lane < lb ? lb_ldcg(w.gagg1 + (b * g.gpt + Gp) * N + i)
+                                                  : lb_ldcg(w.pub1 + (b * g.tpt + Gp * kLbGroup + kLbGroup - 1) * N + i)));
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            R t2 = R(0);
+#pragma unroll
+            for (int c = 0; c < N; ++c) t2 = fma(Pb_l[i][c], x[c], t2);
+            sb[i] = t2;
+          }
+        }
+        if (!preb) {
+          // no prefix within 32 groups (first wave of a long trajectory): further windows
+          const R* PbG = w.Pb + (G * (G + 1) / 2) * N * N;
+          for (int64_t l0 = 32;; l0 += 32) {
+            const int64_t l = l0 + lane;
+            const int64_t Gq = G - 1 - l;
+            unsigned st = 0;
+            if (Gq >= 0) {
+              const unsigned* ft = &w.flag1[b * g.tpt + Gq * kLbGroup + kLbGroup - 1];
+              const unsigned* fg = &w.gflag1[b * g.gpt + Gq];
+              for (;;) {
+                if (lb_ld_status(ft) == 2u) { st = 2u; break; }
+                if (lb_ld_status(fg) == 1u) { st = 1u; break; }
+                __nanosleep(20);
+              }
+            } else if (Gq == -1) {
+              st = 3u;
+            }
+            const unsigned pre = __ballot_sync(FULL, st >= 2u);
+            lb_fence_acquire();
+            const int lstar = pre ? __ffs(pre) - 1 : 32;
+            if (lane <= lstar && Gq >= -1) {
+              R x[N], o[N];
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                x[i] = st == 3u ? eta0[i]
+                                : (lane < lstar ? lb_ldcg(w.gagg1 + (b * g.gpt + Gq) * N + i)
+                                                : lb_ldcg(w.pub1 + (b * g.tpt + Gq * kLbGroup + kLbGroup - 1) * N + i));
+              lb_matvec<R, N>(PbG + l * N * N, x, o);
+#pragma unroll
+              for (int i = 0; i < N; ++i) sb[i] += o[i];
+            }
+            if (pre) break;
+          }
+        }
+        lb_warp_sum<R, N>(sb);
+        // + Pa[j][cnt] v_end(32G - 1): Pa[j][cnt] is lane cnt's Pa_l
+        R o[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R t2 = R(0);
+#pragma unroll
+          for (int c = 0; c < N; ++c) t2 = fma(__shfl_sync(FULL, Pa_l[i][c], cnt), sb[c], t2);
+          o[i] = t2;
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) sa[i] += o[i];
+        }
+      }
+      lb_warp_sum<R, N>(sa);
+#pragma unroll
+      for (int i = 0; i < N; ++i) vin[i] = sa[i];
+    }
+    LB_STAMP(0, 4);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) s_vin[i] = vin[i];
+      if (!last) {  // inclusive prefix: v leaving the tile
+        lb_stress(stress, tile, 3);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R s = gj[i];
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(__ldg(&tj->Gt[i][k]), vin[k], s);
+          w.pub1[tile * N + i] = s;
+        }
+        lb_st_release(&w.flag1[tile], 2u);
+      }
+    }
+  }
+  // ---- run threads (in parallel with warp 0's look-back): the run maps as affine
+  // functions of the unknown v_in:  v_{s-1} = GP v_in + c,  c = ph - GP S_in pb,
+  // beta = WR (rb + C_R v_{s-1}) = beta0 + WR C_R GP v_in,  beta0 = WR (rb + C_R c);
+  // the suffix composition of (PHI, beta0) gives Incl_r with v_in = 0, and QB carries the
+  // v_in-coefficient of its offset.
+  R cvec[N];
+  A agg;
+  set_identity(agg);
+  const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + (r < 0 ? 0 : r);  // field f of run r at rt[f * NT]
+  if (warp >= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {  // the tree reduce above consumed bb, hh
+      bb[i] = rb[i];
+      hh[i] = rh[i];
+    }
+    lb_run_scan64<R, N>(tab->UWc, &tab->UX[0][0][0][0], r, bb, hh, s_tot);  // inclusive prefixes
+    R pb[N], ph[N];  // exclusive prefix = inclusive prefix of run r - 1 (0 for run 0)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      pb[i] = __shfl_up_sync(FULL, bb[i], 1);
+      ph[i] = __shfl_up_sync(FULL, hh[i], 1);
+    }
+    lb_bar_runs();
+    if (r == 32) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        pb[i] = s_tot[i];
+        ph[i] = s_tot[N + i];
+      }
+    }
+    if (r == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) pb[i] = ph[i] = R(0);
+    }
+    {
+      R u[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R s = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(-__ldg(&lt[j].S[i <= k ? sidx(i, k, N) : sidx(k, i, N)]), pb[k], s);
+        u[i] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R s = ph[i];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::GP + i * N + k) * NT), u[k], s);
+        cvec[i] = s;
+      }
+    }
+    if (q > 0) {
+      R CR[NS];  // C of the run element: one full run (E1) or the partial run of q nodes
+#pragma unroll
+      for (int k = 0; k < NS; ++k) CR[k] = (q == K) ? __ldg(&tab->E1[N * N + N + k]) : __ldg(&tab->PC[q - 1][k]);
+      R t2[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R s = rb[i];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(CR[i <= k ? sidx(i, k, N) : sidx(k, i, N)], cvec[k], s);
+        t2[i] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R s = R(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::WR + i * N + k) * NT), t2[k], s);
+        agg.q[i] = s;
+#pragma unroll
+        for (int c = 0; c < N; ++c) agg.P[i][c] = __ldg(rt + (LbRunTab<N>::PHI + i * N + c) * NT);
+      }
+    }
+    // in-tile suffix composition: Incl_r = agg_r o ... o agg_{NT-1}
+#pragma unroll 1
+    for (int d = 1; d < 32; d <<= 1) {
+      A o;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) o.P[i][c] = __shfl_down_sync(FULL, agg.P[i][c], d);
+        o.q[i] = __shfl_down_sync(FULL, agg.q[i], d);
+      }
+      if (lane + d < 32) compose(agg, o, agg);
+    }
+    if (r == 32) store(agg, s_a32, 1);
+    lb_bar_runs();
+    if (r < 32) {
+      A o;
+      load(o, s_a32, 1);
+      compose(agg, o, agg);
+    }
+  }
+  __syncthreads();  // v_in from warp 0
+  LB_STAMP(0, 5);
+  if (warp >= 1) {
+    R vin[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) vin[i] = s_vin[i];
+    R vp[N], qb[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = cvec[i], s2 = agg.q[i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s = fma(__ldg(rt + (LbRunTab<N>::GP + i * N + k) * NT), vin[k], s);
+        s2 = fma(__ldg(rt + (LbRunTab<N>::QB + i * N + k) * NT), vin[k], s2);
+      }
+      vp[i] = s;
+      qb[i] = s2;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      agg.q[i] = qb[i];
+      w.rcv[(tile * N + i) * NT + r] = vp[i];
+    }
+    store(agg, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
+    if (last && q > 0 && n0 + (int64_t)r * K + q == g.Nn) {  // this run ends at node T: x*_T = S_T^-1 v_T
+      V cur, vend;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) cur.S[k] = __ldg(rt + (LbRunTab<N>::SP + k) * NT);
+#pragma unroll
+      for (int i = 0; i < N; ++i) cur.v[i] = vp[i];
+      E ra;
+      if (q == K) {
+        load(ra, tab->E1, 1);
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int jj = 0; jj < N; ++jj) ra.A[i][jj] = __ldg(&tab->PA[q - 1][i][jj]);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          ra.C[k] = __ldg(&tab->PC[q - 1][k]);
+          ra.J[k] = __ldg(&tab->PJ[q - 1][k]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        ra.b[i] = rb[i];
+        ra.h[i] = rh[i];
+      }
+      vapply<R, N, false>(ra, cur, vend, nullptr, ok);
+      R xT[N];
+      spd_solve<R, N>(vend.S, vend.v, xT, ok);
+#pragma unroll
+      for (int i = 0; i < N; ++i) w.seed[b * N + i] = xT[i];
+    }
+    // the tile's pass-2 offset (run 0's suffix map) and, by the group's last arriver, the
+    // group's: beta_G = sum_l Qa[32G - 1][l] beta_{32G + l} (groups G >= 1)
+    if (r == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) w.agg2[tile * N + i] = agg.q[i];
+      const int gcount = (int)min((int64_t)kLbGroup, g.tpt - G * kLbGroup);
+      s_glast = G >= 1 && lb_arrive(&w.gcnt2[b * g.gpt + G]) == (unsigned)(gcount - 1);
+    }
+    lb_bar_runs();
+    if (s_glast && warp == 1) {
+      const int gcount = (int)min((int64_t)kLbGroup, g.tpt - G * kLbGroup);
+      R s[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) s[i] = R(0);
+      if (lane < gcount) {
+        R x[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = lb_ldcg(w.agg2 + (b * g.tpt + G * kLbGroup + lane) * N + i);
+        lb_matvec<R, N>(w.Qa + ((G * kLbGroup - 1) * (kLbGroup + 1) + lane) * N * N, x, s);
+      }
+      lb_warp_sum<R, N>(s);
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) w.gagg2[(b * g.gpt + G) * N + i] = s[i];
+        atomicExch(&w.gcnt2[b * g.gpt + G], 0u);
+      }
+    }
+  }
+  if (!ok) atomicMin(flag, (unsigned long long)(n0 + (int64_t)max(r, 0) * K));
+}
+
+
+// One forward node step (R-FWD + the node update): x <- A^-1 [x - b + C (S x - v)] with
+// the value function V = V_{i-1} entering node i, then V <- E_i (x) V (Woodbury form
+// for a low-rank diffusion C = U U^T, R-LOWRANK; the general update otherwise).
+template <typename R, int N, class Src>
+PM_INLINE void lb_node_step(const Src& src, const Elem<R, N>& e, VF<R, N>& V, R (&x)[N], bool& ok) {
+  constexpr int NW = Src::LOWRANK > 0 ? Src::LOWRANK : 1;
+  R z[N];
+  if constexpr (Src::LOWRANK > 0) {
+    // u = U^T (S x - v)
+    R u[NW];
+#pragma unroll
+    for (int a = 0; a < NW; ++a) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(Src::UMASK, k * NW + a)) {
+          R t = -V.v[k];
+#pragma unroll
+          for (int l = 0; l < N; ++l) t = fma(V.S[sidx(k, l, N)], x[l], t);
+          s = fma(src.U[k][a], t, s);
+        }
+      u[a] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = src.zero_b ? x[i] : x[i] - src.b[i];
+#pragma unroll
+      for (int a = 0; a < NW; ++a)
+        if (mask_nz(Src::UMASK, i * NW + a)) s = fma(src.U[i][a], u[a], s);
+      z[i] = s;
+    }
+  } else {
+    R t[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      R s = -V.v[k];
+#pragma unroll
+      for (int l = 0; l < N; ++l) s = fma(V.S[sidx(k, l, N)], x[l], s);
+      t[k] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = x[i] - src.b[i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(src.C[sidx(i, k, N)], t[k], s);
+      z[i] = s;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      if (mask_nz(Src::AMASK, i * N + k)) s = fma(src.Am[i][k], z[k], s);  // A^-1 shares A's masked pattern
+    x[i] = s;
+  }
+  if constexpr (Src::LOWRANK > 0)
+    vapply_lowrank<R, N, Src::LOWRANK, Src::AMASK, Src::UMASK>(e, src.U, V, V, ok, nullptr, 0, src.zero_b != 0);
+  else
+    vapply<R, N, false>(e, V, V, nullptr, ok);
+}
+
+template <typename R, int N>
+PM_INLINE void lb_store_x(R* __restrict__ dst, const R (&x)[N]) {
+  if constexpr (N == 4 && sizeof(R) == 8) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(x[3])
+                 : "memory");
+  } else if constexpr (N == 4 && sizeof(R) == 4) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3])
+                 : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) dst[i] = x[i];
+  }
+}
+
+
+// ------------------------------------------------------------------ pass 2
+// FO: also write the filter outputs m_i = S_i^-1 v_i, P_i = S_i^-1.
+template <typename R, int N, int NY, int NT, int K, class Src, bool FO>
+__global__ void __maxnreg__(PM_LB2_MAXREG)
+    k_lb_pass2(const __grid_constant__ Src src, const LbGeom g, const R* __restrict__ y,
+               const R* __restrict__ lrt, const LbWs<R> w, R* __restrict__ x_out, R* __restrict__ fm,
+               R* __restrict__ fP, unsigned long long* flag, int stress) {
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  using A = Aff<R, N>;
+  using YS = LbYStage<R, NY, NT, K>;
+  constexpr int L = NT * K;
+  constexpr int NS = Dim<N>::NS;
+  static_assert(NT == 64, "two warps per tile");
+  __shared__ __align__(16) R ys[NT * YS::ROW];
+  __shared__ int s_ticket;
+  __shared__ R s_x[N];  // x at the tile's last node
+  const int r = threadIdx.x, lane = r & 31;
+  const unsigned FULL = 0xffffffffu;
+  if (r == 0) {
+    const unsigned total = (unsigned)(g.batch * g.tpt);
+    const unsigned t = atomicAdd(&w.ctr[1], 1u);
+    if (t == total - 1) atomicExch(&w.ctr[1], 0u);
+    s_ticket = (int)t;
+  }
+  __syncthreads();
+  const int64_t t = s_ticket;
+  const int64_t b = t / g.tpt, j = g.tpt - 1 - t % g.tpt;  // reverse order
+  const int64_t tile = b * g.tpt + j;
+  const int64_t G = j / kLbGroup;
+  const bool last = (j == g.tpt - 1);
+  const int64_t n0 = 1 + j * (int64_t)L;
+  const int nvalid = (int)min((int64_t)L, g.Nn - n0);
+  const R* yb = y + b * g.Nn * NY;
+  LB_STAMP(1, 0);
+  YS::issue(ys, yb + n0 * NY, nvalid, r, NT);  // lands while warp 0 looks back
+  if (r < 32) {
+    if (lane == 0) {  // pass-1 status of this solve (that kernel has finished): clear for the next one
+      w.flag1[tile] = 0u;
+      if (j % kLbGroup == 0) w.gflag1[b * g.gpt + G] = 0u;
+    }
+    // look-back for x at the tile's last node.  Every map already exists (pass 1 wrote
+    // the tiles' and groups' offsets beta; their matrices are the plan products Qa, Qb),
+    // so nothing is waited for: a published prefix only shortens the walk.
+    //   x_last(j) = sum_{l < l*} Qa[j][l] beta_{j+1+l} + Qa[j][l*] x_last(j + l*)
+    // over (a) the following tiles of the group (x_last(k - 1) = tile k's prefix, the last
+    // tile's successor = the seed x*_T), else + Qa[j][cnt] x_end(group G) with (b)
+    // x_end(G) = sum_{l < l*} Qb[G][l] beta_{G+1+l} + Qb[G][l*] x_end(group G + l*) over
+    // whole groups (past the last group: the seed).  Both windows' status words are read
+    // once, one fence, one round of payload loads.
+    R seed[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) seed[i] = w.seed[b * N + i];
+    R xl[N];
+    if (last) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) xl[i] = seed[i];
+    } else {
+      const int64_t gend = min((G + 1) * kLbGroup, g.tpt) - 1;
+      const int cnt = (int)(gend - j);  // following tiles in the group
+      const R* QbG = w.Qb + (G * g.gpt - G * (G - 1) / 2) * N * N;
+      R Qa_l[N][N], Qb_l[N][N];
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          Qa_l[i][c] = __ldg(w.Qa + ((j * (kLbGroup + 1) + lane) * N + i) * N + c);
+          Qb_l[i][c] = (lane < g.gpt - G) ? __ldg(QbG + (lane * N + i) * N + c) : R(0);
+        }
+      const int64_t ka = j + 1 + lane;
+      const int64_t Gp = G + 1 + lane;
+      const unsigned sta = lane < cnt ? lb_ld_status(&w.flag2[b * g.tpt + ka]) : 0u;
+      // (b) status: 2 = prefix of the group's first tile, 1 = the group's map, 3 = the seed
+      const unsigned stb =
+          Gp < g.gpt ? (lb_ld_status(&w.flag2[b * g.tpt + Gp * kLbGroup]) == 2u ? 2u : 1u) : (Gp == g.gpt ? 3u : 0u);
+      const unsigned prea = __ballot_sync(FULL, sta == 2u);
+      const bool terma = !prea && gend == g.tpt - 1;  // the window reaches the last tile: the seed follows it
+      const unsigned preb = (prea || terma) ? 0u : __ballot_sync(FULL, stb >= 2u);
+      if (prea || preb) lb_fence_acquire();
+      const int la = prea ? __ffs(prea) - 1 : cnt;
+      R sa[N];
+      {
+        R x[N];
+        const bool use = lane < la || (lane == la && (prea || terma));
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+          x[i] = !use ? R(0)
+                      : (lane < la ? lb_ldcg(w.agg2 + (b * g.tpt + ka) * N + i)
+                                   : (prea ? lb_ldcg(w.pub2 + (b * g.tpt + ka) * N + i) : seed[i]));
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R t2 = R(0);
+#pragma unroll
+          for (int c = 0; c < N; ++c) t2 = fma(Qa_l[i][c], x[c], t2);
+          sa[i] = t2;
+        }
+      }
+      if (!prea && !terma) {
+        R sb[N];
+        const int lb = preb ? __ffs(preb) - 1 : 32;
+        {
+          R x[N];
+          const bool use = lane < lb || (lane == lb && preb);
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+            x[i] = !use ? R(0)
+                        : (stb == 3u ? seed[i]
+                                     : (lane < lb ? lb_ldcg(w.gagg2 + (b * g.gpt + Gp) * N + i)
+                                                  : lb_ldcg(w.pub2 + (b * g.tpt + Gp * kLbGroup) * N + i)));
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            R t2 = R(0);
+#pragma unroll
+            for (int c = 0; c < N; ++c) t2 = fma(Qb_l[i][c], x[c], t2);
+            sb[i] = t2;
+          }
+        }
+        if (!preb) {  // more than 32 groups to the nearest prefix (or the seed)
+          for (int64_t l0 = 32;; l0 += 32) {
+            const int64_t l = l0 + lane;
+            const int64_t Gq = G + 1 + l;
+            unsigned st = 0;
+            if (Gq < g.gpt)
+              st = lb_ld_status(&w.flag2[b * g.tpt + Gq * kLbGroup]) == 2u ? 2u : 1u;
+            else if (Gq == g.gpt)
+              st = 3u;
+            const unsigned pre = __ballot_sync(FULL, st >= 2u);
+            if (pre) lb_fence_acquire();
+            const int lstar = pre ? __ffs(pre) - 1 : 32;
+            if (lane <= lstar && Gq <= g.gpt) {
+              R x[N], o[N];
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                x[i] = st == 3u ? seed[i]
+                                : (lane < lstar ? lb_ldcg(w.gagg2 + (b * g.gpt + Gq) * N + i)
+                                                : lb_ldcg(w.pub2 + (b * g.tpt + Gq * kLbGroup) * N + i));
+              lb_matvec<R, N>(QbG + l * N * N, x, o);
+#pragma unroll
+              for (int i = 0; i < N; ++i) sb[i] += o[i];
+            }
+            if (pre) break;
+          }
+        }
+        lb_warp_sum<R, N>(sb);
+        R o[N];  // + Qa[j][cnt] x_end(G): Qa[j][cnt] is lane cnt's Qa_l
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R t2 = R(0);
+#pragma unroll
+          for (int c = 0; c < N; ++c) t2 = fma(__shfl_sync(FULL, Qa_l[i][c], cnt), sb[c], t2);
+          o[i] = t2;
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) sa[i] += o[i];
+        }
+      }
+      lb_warp_sum<R, N>(sa);
+#pragma unroll
+      for (int i = 0; i < N; ++i) xl[i] = sa[i];
+    }
+    LB_STAMP(1, 1);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) s_x[i] = xl[i];
+      if (j > 0) {  // prefix: x at the last node of tile j - 1 = Phi_j x_last(j) + beta_j
+        lb_stress(stress, tile, 4);
+        R o[N];
+        lb_matvec<R, N>(w.Qa + ((j - 1) * (kLbGroup + 1) + 1) * N * N, xl, o);
+#pragma unroll
+        for (int i = 0; i < N; ++i) w.pub2[tile * N + i] = o[i] + w.agg2[tile * N + i];
+        lb_st_release(&w.flag2[tile], 2u);
+      }
+    }
+  }
+  YS::wait();
+  __syncthreads();
+  LB_STAMP(1, 2);
+  const int q = max(0, min(K, nvalid - r * K));
+  bool ok = true;
+  if (q > 0) {
+    // x_{s-1} of the run from its suffix map; the value function entering the run (S from
+    // the plan's run table, v from pass 1); then the forward sweep over the run's nodes
+    R x[N];
+    {
+      A inc;
+      load(inc, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = s_x[i];
+      apply(inc, x);
+    }
+    V cur;
+    {
+      const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) cur.S[k] = __ldg(rt + (LbRunTab<N>::SP + k) * NT);
+#pragma unroll
+      for (int i = 0; i < N; ++i) cur.v[i] = w.rcv[(tile * N + i) * NT + r];
+    }
+    R* xo = x_out + b * g.Nn * N;
+    const int64_t s0 = n0 + (int64_t)r * K;
+    if (s0 == 1) {  // node 0 (the carry-in of the first tile)
+      lb_store_x<R, N>(xo, x);
+      if constexpr (FO) {
+        R m[N];
+        spd_solve<R, N>(cur.S, cur.v, m, ok);
+        R P[NS];
+        spd_inverse<R, N>(cur.S, P, ok);
+#pragma unroll
+        for (int i = 0; i < N; ++i) fm[(b * g.Nn) * N + i] = m[i];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) fP[(b * g.Nn) * NS + k] = P[k];
+      }
+    }
+    const R* yr = ys + r * YS::ROW;
+#pragma unroll 1
+    for (int m = 0; m < q; ++m) {
+      E e;
+      src.node_interior(s0 + m, yr + m * NY, nullptr, e);
+      lb_node_step<R, N, Src>(src, e, cur, x, ok);
+      lb_store_x<R, N>(xo + (s0 + m) * N, x);
+      if constexpr (FO) {
+        R mm[N];
+        spd_solve<R, N>(cur.S, cur.v, mm, ok);
+        R P[NS];
+        spd_inverse<R, N>(cur.S, P, ok);
+        const int64_t idx = b * g.Nn + s0 + m;
+#pragma unroll
+        for (int i = 0; i < N; ++i) fm[idx * N + i] = mm[i];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) fP[idx * NS + k] = P[k];
+      }
+    }
+    R s = R(0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) s += x[i];
+    if (!(s - s == R(0))) ok = false;
+  }
+  if (!ok) atomicMin(flag, (unsigned long long)(n0 + (int64_t)r * K));
+  LB_STAMP(1, 3);
+}
+
+}  // namespace pmap

@@ -19,6 +19,7 @@
 #include "pmap_lti.cuh"
 #include "pmap_seq.cuh"
 #include "pmap_lti_scan.cuh"
+#include "pmap_lb.cuh"
 #include <cstdlib>
 #include <type_traits>
 
@@ -205,6 +206,11 @@ struct PlanState {
   bool euler = false;        // paper-faithful Euler blocks: y rows of ny_row = substeps * ny
   int ny_row = 0;            // doubles of y per node
   bool force_shard = false;  // PMAP_FORCE_SHARD=1 with a communicator: run the NCCL path at world == 1 (tests)
+  bool no_lb = false;        // PMAP_NO_LB=1: LTI plans use the multi-kernel scan hierarchy instead of look-back
+  int lb_stress = 0;         // PMAP_LB_STRESS=1: delay injection in the look-back kernels (tests)
+  size_t lb_bytes = 0;       // look-back workspace
+  unsigned long long* lb_tim = nullptr;  // PMAP_LB_TIMING=1: per-tile globaltimer stamps (diagnostics)
+  size_t lb_tim_n = 0;
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
   cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -234,7 +240,7 @@ struct PlanState {
     for (auto& ge : lgraphs)
       if (ge.exec) cudaGraphExecDestroy(ge.exec);
     runner.reset();
-    for (void* q : {(void*)ws, (void*)dflag, xbuf[0], xbuf[1], stage_y, stage_x, stage_aux, dev_tv, scratch, m0_dev})
+    for (void* q : {(void*)lb_tim, (void*)ws, (void*)dflag, xbuf[0], xbuf[1], stage_y, stage_x, stage_aux, dev_tv, scratch, m0_dev})
       if (q) cudaFree(q);
     for (cudaStream_t s : {stream2, stream3, stream4})
       if (s) cudaStreamDestroy(s);
@@ -256,12 +262,13 @@ struct PlanState {
 // kernel classes reported by map_profile_read
 enum KernelId { K_P1_REDUCE = 0, K_P1_REDUCE_EDGE, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_GROUPS,
                 K_P2_DOWN, K_FILTER_OUT, K_TF_REDUCE, K_TF_REDUCE_EDGE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD,
-                K_NL_MISC, K_SEQ, K_COUNT };
+                K_NL_MISC, K_SEQ, K_LB_P1, K_LB_P2, K_P1_REDUCE_LTI, K_COUNT };
 inline const char* kernel_name(int id) {
   static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_reduce_lti_edge", "k_p1_tiles", "k_p1_groups",
                                        "k_p1_down", "k_p2_tiles", "k_p2_groups", "k_p2_down", "k_filter_out",
                                        "k_tf_reduce", "k_tf_reduce_lti_edge", "k_tf_tiles", "k_tf_groups",
-                                       "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff", "k_seq_rts/k_seq_tf"};
+                                       "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff", "k_seq_rts/k_seq_tf",
+                                       "k_lb_pass1", "k_lb_pass2", "k_p1_reduce_lti"};
   return (id >= 0 && id < K_COUNT) ? names[id] : "?";
 }
 
@@ -310,15 +317,50 @@ struct RunnerT : Runner {
   LtiNode<R, N, NY> lnode{}, lnode_m{};
   LtiFoldParams<R, N, NY, K, Log2<kNT>::value> fold{}, fold_m{};  // kernel-parameter copies of the fold tables
   bool use_lti = false;
+  // single-pass decoupled look-back path (pmap_lb.cuh), LTI single-GPU plans
+  bool use_lb = false;
+  LbGeom lbg{};
+  LbTileTab<R, N>* lbtab = nullptr;  // [tpt] plan tables
+  R* lbprod = nullptr;               // look-back window products Pa [tpt][33][N][N], Pb (triangular)
+  R* lbrun = nullptr;                // [tpt][LbRunTab::F][NT] plan run tables
+  unsigned char* lbws = nullptr;     // workspace
+  LbWs<R> lbw{};
+  double lb_amp = 0.0;               // forward-recovery amplification bound over a run (R-FWD)
 
   ~RunnerT() override {
     cudaFree(tab);
     cudaFree(tab_m);
     cudaFree(scan_tab);
     cudaFree(scan_tab_m);
+    cudaFree(lbtab);
+    cudaFree(lbprod);
+    cudaFree(lbrun);
+    cudaFree(lbws);
   }
 
   bool prepare(PlanState& p) override;
+  bool prepare_lb(PlanState& p);
+
+  // one look-back solve: k_lb_pass1 + k_lb_pass2 (2 launches)
+  void lb_rts(PlanState& p, const void* yv, void* xv, void* fm, void* fP) {
+    if constexpr (IS_LTI) {
+      const R* y = static_cast<const R*>(yv);
+      R* x = static_cast<R*>(xv);
+      const unsigned ntiles = (unsigned)(lbg.batch * lbg.tpt);
+      cudaStream_t s = p.stream;
+      PM_LAUNCH(p, s, K_LB_P1,
+                (k_lb_pass1<R, N, NY, kNT, K, Src><<<ntiles, kNT + 32, 0, s>>>(fold, src, lbg, y, tab, lbtab, lbrun, lbw,
+                                                                             p.dflag, p.lb_stress)));
+      if (fm || fP)
+        PM_LAUNCH(p, s, K_LB_P2,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, 0, s>>>(
+                      src, lbg, y, lbrun, lbw, x, static_cast<R*>(fm), static_cast<R*>(fP), p.dflag, p.lb_stress)));
+      else
+        PM_LAUNCH(p, s, K_LB_P2,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr,
+                                                                                 nullptr, p.dflag, p.lb_stress)));
+    }
+  }
 
   // interior (LTI-specialised) tile range [j_lo, j_hi) of a trajectory
   static int64_t lti_jlo(const Geom& g, bool rev) { return (rev || g.node0 == 0) ? 1 : 0; }
@@ -358,7 +400,7 @@ struct RunnerT : Runner {
                                                                           run_incl, tile_agg, p.dflag)));
     }
     if (n_int > 0)
-      PM_LAUNCH(p, s, kid,
+      PM_LAUNCH(p, s, kid == K_P1_REDUCE ? (int)K_P1_REDUCE_LTI : kid,
                 (k_p1_reduce_lti<R, N, NY, kNT, K, REV><<<(unsigned)(g.batch * n_int), kNT, 0, s>>>(
                     fpar, g, j_lo, n_int, y, tb, run_incl, tile_agg)));
     if (nsel > 0) {
@@ -574,6 +616,10 @@ struct RunnerT : Runner {
 
   void rts(PlanState& p, const void* y, const void* xbar, void* x, void* fm, void* fP) override {
     p.want_filter = fm || fP;
+    if (use_lb && p.d.world == 1 && !p.force_shard && !p.no_lb) {
+      lb_rts(p, y, x, fm, fP);
+      return;
+    }
     if (p.d.world == 1 && !p.force_shard) {
       phase1(p, y, xbar, nullptr);
       phase2(p, y, xbar, nullptr, nullptr);
@@ -749,10 +795,281 @@ bool RunnerT<R, N, NY, Src, K>::prepare(PlanState& p) {
         return true;
       };
       if (!pull(fold, lnode, tab) || !pull(fold_m, lnode_m, tab_m)) return false;
+      if (!prepare_lb(p)) {
+        cudaGetLastError();
+        use_lb = false;
+      }
     }
   }
   (void)p;
   return true;
+}
+
+// Plan-time tables of the look-back path (pmap_lb.cuh), host fp64: S entering every tile
+// (the data-independent Riccati part of the value function, chained over the tile span
+// element (A_L, C_L, J_L) of k_lti_setup from S_0 = J_0), Gt_j = A_L^T (I + S_j C_L)^-1,
+// Hs_j = Gt_j S_j, the group products of Gt, and the forward-recovery amplification
+// bound max_j || A^-1 (I + C S_j) ||_2^K (R-FWD) that decides whether the path is used.
+template <typename R, int N, int NY, class Src, int K>
+bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
+  if constexpr (!IS_LTI) {
+    return false;
+  } else {
+    if (p.d.world != 1) return false;
+    constexpr int NS = Dim<N>::NS;
+    const int64_t L = (int64_t)kNT * K;
+    LbGeom g{};
+    g.Nn = p.g.Nn;
+    g.batch = p.g.batch;
+    const int64_t M = g.Nn - 1;  // interior nodes
+    if (M < 1) return false;
+    g.tpt = (M + L - 1) / L;
+    g.gpt = (g.tpt + kLbGroup - 1) / kLbGroup;
+    // tile span element (matrix parts of NT full runs)
+    R sa[N][N], sc[NS], sj[NS];
+    if (cudaMemcpy(sa, tab->SA[kNT - 1], sizeof sa, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(sc, tab->SC[kNT - 1], sizeof sc, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(sj, tab->SJ[kNT - 1], sizeof sj, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return false;
+    auto full = [&](const R* pk, double* m) {
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) m[i * N + j] = (double)pk[i <= j ? sidx(i, j, N) : sidx(j, i, N)];
+    };
+    double AL[N * N], CL[N * N], JL[N * N], S[N * N], Cn[N * N], Am[N * N];
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        AL[i * N + j] = (double)sa[i][j];
+        Am[i * N + j] = (double)src.Am[i][j];
+      }
+    full(sc, CL);
+    full(sj, JL);
+    full(src.J0, S);
+    full(src.C, Cn);
+    auto mm = [&](const double* X, const double* Y, double* Z) {
+      double T[N * N];
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          double a = 0;
+          for (int k = 0; k < N; ++k) a += X[i * N + k] * Y[k * N + j];
+          T[i * N + j] = a;
+        }
+      memcpy(Z, T, sizeof T);
+    };
+    std::vector<LbTileTab<R, N>> ht((size_t)g.tpt);
+    std::vector<double> gt((size_t)g.tpt * N * N);
+    double amp = 0.0;
+    for (int64_t j = 0; j < g.tpt; ++j) {
+      LbTileTab<R, N>& e = ht[(size_t)j];
+      for (int i = 0; i < N; ++i)
+        for (int c = i; c < N; ++c) e.S[sidx(i, c, N)] = (R)(0.5 * (S[i * N + c] + S[c * N + i]));
+      // Gt = A^T (I + S C)^-1, Hs = Gt S
+      double M1[N * N], Mi[N * N], G[N * N], H[N * N];
+      mm(S, CL, M1);
+      for (int i = 0; i < N; ++i) M1[i * N + i] += 1.0;
+      if (!h_inv(N, M1, Mi)) return false;
+      double At[N * N];
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) At[i * N + c] = AL[c * N + i];
+      mm(At, Mi, G);
+      mm(G, S, H);
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) {
+          e.Gt[i][c] = (R)G[i * N + c];
+          e.Hs[i][c] = (R)H[i * N + c];
+          gt[(size_t)j * N * N + i * N + c] = G[i * N + c];
+        }
+      // forward-recovery step map A^-1 (I + C S) at this S: spectral norm by power iteration
+      {
+        double CS[N * N], Mf[N * N];
+        mm(Cn, S, CS);
+        for (int i = 0; i < N; ++i) CS[i * N + i] += 1.0;
+        mm(Am, CS, Mf);
+        double v[N], w2[N], nrm = 0;
+        for (int i = 0; i < N; ++i) v[i] = 0.5;  // unit vector (N <= 4) or close to it; renormalised below
+        {
+          double s0 = 0;
+          for (int i = 0; i < N; ++i) s0 += v[i] * v[i];
+          for (int i = 0; i < N; ++i) v[i] /= std::sqrt(s0);
+        }
+        for (int it = 0; it < 60; ++it) {  // v <- M^T M v / |M^T M v|;  |M|_2^2 = |M^T M v| at convergence
+          double u[N];
+          for (int i = 0; i < N; ++i) {
+            u[i] = 0;
+            for (int k = 0; k < N; ++k) u[i] += Mf[i * N + k] * v[k];
+          }
+          double s2 = 0;
+          for (int i = 0; i < N; ++i) {
+            w2[i] = 0;
+            for (int k = 0; k < N; ++k) w2[i] += Mf[k * N + i] * u[k];
+            s2 += w2[i] * w2[i];
+          }
+          s2 = std::sqrt(s2);
+          if (!(s2 > 0)) break;
+          nrm = std::sqrt(s2);
+          for (int i = 0; i < N; ++i) v[i] = w2[i] / s2;
+        }
+        amp = std::max(amp, std::pow(nrm, (double)K));
+      }
+      // S_{j+1} = J_L + A_L^T S (I + C_L S)^-1 A_L
+      double M2[N * N], M2i[N * N], X[N * N], Y[N * N], Sn[N * N];
+      mm(CL, S, M2);
+      for (int i = 0; i < N; ++i) M2[i * N + i] += 1.0;
+      if (!h_inv(N, M2, M2i)) return false;
+      mm(M2i, AL, X);
+      mm(S, X, Y);
+      mm(At, Y, Sn);
+      for (int i = 0; i < N * N; ++i) Sn[i] += JL[i];
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) S[i * N + c] = 0.5 * (Sn[i * N + c] + Sn[c * N + i]);
+      if (!h_is_finite(S, N * N)) return false;
+    }
+    lb_amp = amp;
+    const char* ma = getenv("PMAP_LB_MAX_AMP");
+    const double max_amp = ma ? atof(ma) : 1e6;
+    if (!(amp <= max_amp)) return false;  // forward recovery would amplify rounding: keep the scan hierarchy
+    // look-back window products: Pa[j][l] = Gt_{j-1} ... Gt_{j-l} (l = 0..kLbGroup), the
+    // group maps GtG_G = Pa[32G + 32][32], and Pb[G][l] = GtG_{G-1} ... GtG_{G-l} (l = 0..G)
+    constexpr int W1 = kLbGroup + 1;
+    const size_t npa = (size_t)g.tpt * W1 * N * N, npb = (size_t)(g.gpt * (g.gpt + 1) / 2) * N * N;
+    std::vector<double> pa(npa, 0.0), pb(npb, 0.0), gtg((size_t)g.gpt * N * N, 0.0);
+    for (int64_t j = 0; j < g.tpt; ++j) {
+      double P[N * N];
+      for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
+      for (int l = 0; l < W1; ++l) {
+        memcpy(&pa[((size_t)j * W1 + l) * N * N], P, sizeof P);
+        if (j - 1 - l < 0) break;
+        mm(P, &gt[(size_t)(j - 1 - l) * N * N], P);
+      }
+    }
+    for (int64_t G = 0; G + 1 < g.gpt; ++G)  // full groups (every group before the last)
+      memcpy(&gtg[(size_t)G * N * N], &pa[((size_t)(G + 1) * kLbGroup * W1 + kLbGroup) * N * N], sizeof(double) * N * N);
+    for (int64_t G = 0; G < g.gpt; ++G) {
+      double P[N * N];
+      for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
+      const size_t base = (size_t)(G * (G + 1) / 2);
+      for (int64_t l = 0; l <= G; ++l) {
+        memcpy(&pb[(base + l) * N * N], P, sizeof P);
+        if (l < G) mm(P, &gtg[(size_t)(G - 1 - l) * N * N], P);
+      }
+    }
+    if (cudaMalloc(&lbtab, sizeof(LbTileTab<R, N>) * g.tpt) != cudaSuccess) return false;
+    cudaMemcpy(lbtab, ht.data(), sizeof(LbTileTab<R, N>) * g.tpt, cudaMemcpyHostToDevice);
+    {  // per-run tables, one device thread per (tile, run)
+      const size_t rb = sizeof(R) * LbRunTab<N>::F * kNT * (size_t)g.tpt;
+      int* dok = nullptr;
+      if (cudaMalloc(&lbrun, rb) != cudaSuccess || cudaMalloc(&dok, sizeof(int)) != cudaSuccess) return false;
+      const int one = 1;
+      cudaMemcpy(dok, &one, sizeof one, cudaMemcpyHostToDevice);
+      const int64_t nthr = g.tpt * kNT;
+      k_lb_setup_runs<R, N, NY, kNT, K><<<(unsigned)((nthr + 127) / 128), 128>>>(tab, lbtab, g.tpt, g.Nn, lbrun, dok);
+      int okh = 0;
+      const cudaError_t e = cudaMemcpy(&okh, dok, sizeof okh, cudaMemcpyDeviceToHost);
+      cudaFree(dok);
+      if (e != cudaSuccess || !okh) return false;
+      p.lb_bytes += rb;
+    }
+    // QB per run and the pass-2 tile matrices Phi_tile(j) (device, one thread per tile),
+    // then the window products Qa[j][l] = Phi_{j+1} ... Phi_{j+l} (l = 0..kLbGroup), the
+    // group matrices PhiG_G = Qa[32G - 1][group size] (G >= 1, the last group included)
+    // and Qb[G][l] = PhiG_{G+1} ... PhiG_{G+l} (l = 0..gpt-1-G; the last one multiplies x*_T)
+    std::vector<double> phit((size_t)g.tpt * N * N);
+    {
+      R* dphi = nullptr;
+      if (cudaMalloc(&dphi, sizeof(R) * N * N * g.tpt) != cudaSuccess) return false;
+      k_lb_setup_tiles<R, N, kNT, K><<<(unsigned)((g.tpt + 127) / 128), 128>>>(tab, lbrun, g.tpt, g.Nn, dphi);
+      std::vector<R> hphi((size_t)g.tpt * N * N);
+      const cudaError_t e = cudaMemcpy(hphi.data(), dphi, sizeof(R) * N * N * g.tpt, cudaMemcpyDeviceToHost);
+      cudaFree(dphi);
+      if (e != cudaSuccess) return false;
+      for (size_t i = 0; i < hphi.size(); ++i) phit[i] = (double)hphi[i];
+    }
+    const size_t nqa = (size_t)g.tpt * W1 * N * N, nqb = (size_t)(g.gpt * (g.gpt + 1) / 2) * N * N;
+    std::vector<double> qa(nqa, 0.0), qb(nqb, 0.0), phig((size_t)g.gpt * N * N, 0.0);
+    for (int64_t j = 0; j < g.tpt; ++j) {
+      double P[N * N];
+      for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
+      for (int l = 0; l < W1; ++l) {
+        memcpy(&qa[((size_t)j * W1 + l) * N * N], P, sizeof P);
+        if (j + 1 + l >= g.tpt) break;
+        mm(P, &phit[(size_t)(j + 1 + l) * N * N], P);
+      }
+    }
+    for (int64_t G = 1; G < g.gpt; ++G) {
+      const int64_t cntG = std::min<int64_t>(kLbGroup, g.tpt - G * kLbGroup);
+      memcpy(&phig[(size_t)G * N * N], &qa[((size_t)(G * kLbGroup - 1) * W1 + cntG) * N * N], sizeof(double) * N * N);
+    }
+    for (int64_t G = 0; G < g.gpt; ++G) {
+      double P[N * N];
+      for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
+      const size_t base = (size_t)(G * g.gpt - G * (G - 1) / 2);
+      for (int64_t l = 0; l < g.gpt - G; ++l) {
+        memcpy(&qb[(base + l) * N * N], P, sizeof P);
+        if (G + 1 + l < g.gpt) mm(P, &phig[(size_t)(G + 1 + l) * N * N], P);
+      }
+    }
+    if (cudaMalloc(&lbprod, sizeof(R) * (npa + npb + nqa + nqb)) != cudaSuccess) return false;
+    {
+      std::vector<R> prod(npa + npb + nqa + nqb);
+      size_t o = 0;
+      for (const std::vector<double>* v : {&pa, &pb, &qa, &qb})
+        for (double d : *v) prod[o++] = (R)d;
+      cudaMemcpy(lbprod, prod.data(), sizeof(R) * prod.size(), cudaMemcpyHostToDevice);
+      p.lb_bytes += sizeof(R) * prod.size();
+    }
+    // workspace
+    const size_t tiles = (size_t)(g.batch * g.tpt), groups = (size_t)(g.batch * g.gpt);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = off;
+      off += (bytes + 255) / 256 * 256;
+      return o;
+    };
+    const size_t o_a1 = take(tiles * N * sizeof(R)), o_p1 = take(tiles * N * sizeof(R)),
+                 o_g1 = take(groups * N * sizeof(R)), o_rc = take(tiles * N * kNT * sizeof(R)),
+                 o_ri = take(tiles * Aff<R, N>::SZ * kNT * sizeof(R)), o_a2 = take(tiles * N * sizeof(R)),
+                 o_g2 = take(groups * N * sizeof(R)), o_p2 = take(tiles * N * sizeof(R)),
+                 o_sd = take((size_t)g.batch * N * sizeof(R));
+    const size_t f0 = off;
+    const size_t o_f1 = take(tiles * 4), o_gf1 = take(groups * 4), o_gc1 = take(groups * 4), o_gc2 = take(groups * 4),
+                 o_f2 = take(tiles * 4), o_ct = take(8);
+    if (cudaMalloc(&lbws, off) != cudaSuccess) return false;
+    if (cudaMemset(lbws + f0, 0, off - f0) != cudaSuccess) return false;
+    auto RP = [&](size_t o) { return reinterpret_cast<R*>(lbws + o); };
+    auto UP = [&](size_t o) { return reinterpret_cast<unsigned*>(lbws + o); };
+    lbw.agg1 = RP(o_a1);
+    lbw.pub1 = RP(o_p1);
+    lbw.gagg1 = RP(o_g1);
+    lbw.rcv = RP(o_rc);
+    lbw.ri = RP(o_ri);
+    lbw.agg2 = RP(o_a2);
+    lbw.gagg2 = RP(o_g2);
+    lbw.pub2 = RP(o_p2);
+    lbw.seed = RP(o_sd);
+    lbw.flag1 = UP(o_f1);
+    lbw.gflag1 = UP(o_gf1);
+    lbw.gcnt1 = UP(o_gc1);
+    lbw.gcnt2 = UP(o_gc2);
+    lbw.flag2 = UP(o_f2);
+    lbw.ctr = UP(o_ct);
+    lbw.Pa = lbprod;
+    lbw.Pb = lbprod + npa;
+    lbw.Qa = lbprod + npa + npb;
+    lbw.tim = nullptr;
+    {
+      const char* tm = getenv("PMAP_LB_TIMING");
+      if (tm && tm[0] == '1') {
+        if (cudaMalloc(&lbw.tim, sizeof(unsigned long long) * 16 * tiles) != cudaSuccess) return false;
+        cudaMemset(lbw.tim, 0, sizeof(unsigned long long) * 16 * tiles);
+        p.lb_tim = lbw.tim;
+        p.lb_tim_n = 16 * tiles;
+      }
+    }
+    lbw.Qb = lbprod + npa + npb + nqa;
+    lbg = g;
+    p.lb_bytes += off;
+    use_lb = true;
+    return true;
+  }
 }
 
 // ---------------------------------------------------------- instantiation

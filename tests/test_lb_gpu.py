@@ -1,0 +1,136 @@
+"""GPU parity of the single-pass decoupled look-back path (pmap_lb.cuh).
+
+LTI single-GPU solves run k_lb_pass1 + k_lb_pass2 (two launches).  These tests cover
+it against the CPU oracle (<= 1e-9 relative in fp64, G23, plus the per-component
+scaled error) and against the multi-kernel scan hierarchy (PMAP_NO_LB=1, <= 1e-12),
+at sizes that span one tile, several tiles, several look-back groups (32 tiles) and
+several warp windows of groups, with ragged tails; batches; filter outputs; both run
+lengths; fp32; and a stress mode that injects pseudo-random delays before every
+look-back publication (PMAP_LB_STRESS=1) so that the look-back walks through
+aggregates, group aggregates and prefixes in every combination.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+from test_parity_gpu import TOL32, TOL64, gpu_plan, ora_model, random_lti, rel, rel_comp, to_dev, torch_cuda  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+TILE = 64 * 32  # nodes per tile at K = 32 (group = 32 tiles = 65536 nodes)
+
+
+def _wiener_offsets():
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    spec.r = np.array([0.5, -0.25])
+    return spec
+
+
+@pytest.mark.parametrize("T", [1, 2, 33, TILE, TILE + 1, 3 * TILE + 17, 32 * TILE, 32 * TILE + 1, 33 * TILE + 5,
+                               40 * 32 * TILE + 999])
+def test_lb_matches_oracle(torch_cuda, T):
+    torch = torch_cuda
+    spec = _wiener_offsets()
+    _, y = wl.simulate_linear(spec, T, seed=T % 997)
+    plan = gpu_plan(spec, T)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    plan.sync()
+    if T >= TILE:  # dt <= 2.4e-3: the forward-recovery bound admits the look-back path (R-FWD)
+        assert plan.launches == 2  # k_lb_pass1 + k_lb_pass2
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    xg = x[0].cpu().numpy()
+    assert rel(xg, xo) < TOL64
+    assert rel_comp(xg, xo) < 1e-8
+
+
+@pytest.mark.parametrize("T,B", [(9_001, 3), (200_003, 2), (1_000, 64)])
+def test_lb_batch_and_hierarchy(torch_cuda, T, B, monkeypatch):
+    """Batches (tickets run trajectory-major across the whole grid) against the oracle and
+    against the multi-kernel scan hierarchy of round 1 (PMAP_NO_LB=1)."""
+    torch = torch_cuda
+    spec = _wiener_offsets()
+    _, y = wl.simulate_linear(spec, T, seed=T % 1000, batch=B)
+    y = y.reshape(B, T + 1, 2)
+    yd = to_dev(torch, y)
+    x_lb = gpu_plan(spec, T, batch=B).solve_linear(yd).cpu().numpy()
+    monkeypatch.setenv("PMAP_NO_LB", "1")
+    plan_h = gpu_plan(spec, T, batch=B)
+    x_h = plan_h.solve_linear(yd).cpu().numpy()
+    assert plan_h.launches > 2
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
+    for b in range(B):
+        assert rel(x_lb[b], x_h[b]) < 1e-12
+        assert rel(x_lb[b], xo[b]) < TOL64
+
+
+@pytest.mark.parametrize("T", [5_000, 70 * TILE + 3])
+def test_lb_stress_delays(torch_cuda, T, monkeypatch):
+    """Look-back under injected delays (up to ~16 us before each publication): results
+    stay within rounding of the undisturbed run and of the oracle, and repeated solves
+    (flags and tickets recycled without a memset) stay correct."""
+    torch = torch_cuda
+    spec = _wiener_offsets()
+    _, y = wl.simulate_linear(spec, T, seed=4)
+    yd = to_dev(torch, y[None])
+    x0 = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    monkeypatch.setenv("PMAP_LB_STRESS", "1")
+    plan = gpu_plan(spec, T)
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    for _ in range(3):
+        x = plan.solve_linear(yd)
+        plan.sync()
+        xs = x.cpu().numpy()
+        assert rel(xs[0], x0[0]) < 1e-12
+        assert rel(xs[0], xo) < TOL64
+
+
+def test_lb_filter_outputs(torch_cuda):
+    torch = torch_cuda
+    spec = _wiener_offsets()
+    T = 3 * TILE + 11
+    _, y = wl.simulate_linear(spec, T, seed=3)
+    xo, fm, fP = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf, want_filter=True)
+    plan = gpu_plan(spec, T)
+    nx = spec.nx
+    m = torch.empty((1, T + 1, nx), dtype=torch.float64, device="cuda")
+    P = torch.empty((1, T + 1, nx * (nx + 1) // 2), dtype=torch.float64, device="cuda")
+    x = plan.solve_linear(to_dev(torch, y[None]), filt_m=m, filt_P=P)
+    plan.sync()
+    assert plan.launches == 2
+    iu = np.triu_indices(nx)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    assert rel(m[0].cpu().numpy(), fm) < TOL64
+    assert rel(P[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
+
+
+@pytest.mark.parametrize("K", ["8", "32"])
+@pytest.mark.parametrize("shape", [(1, 1), (2, 1), (3, 2), (4, 2), (5, 2)])
+def test_lb_random_lti_shapes(torch_cuda, K, shape, monkeypatch):
+    """Every compiled LTI shape (full-rank and low-rank diffusion, c, r != 0) at both run
+    lengths, multi-tile with a ragged tail."""
+    torch = torch_cuda
+    monkeypatch.setenv("PMAP_K", K)
+    nx, ny = shape
+    spec = random_lti(nx, ny, seed=nx * 10 + ny)
+    T = 60_001
+    y = np.random.default_rng(nx + ny).standard_normal((T + 1, ny))
+    plan = gpu_plan(spec, T)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    plan.sync()
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+def test_lb_fp32(torch_cuda):
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 200_000
+    _, y = wl.simulate_linear(spec, T, seed=8)
+    plan = gpu_plan(spec, T, dtype="f32")
+    x = plan.solve_linear(to_dev(torch, y[None], dtype=torch.float32))
+    plan.sync()
+    assert plan.launches == 2
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    assert rel(x[0].cpu().numpy(), xo) < TOL32

@@ -323,6 +323,7 @@ def test_lti_data_only_scans_match_general(torch_cuda, case, T, B, monkeypatch):
     """The data-only LTI tile / group scans (pmap_lti_scan.cuh) agree with the general
     combine-based scans to rounding (<= 1e-12 relative) and with the oracle (1e-9)."""
     torch = torch_cuda
+    monkeypatch.setenv("PMAP_NO_LB", "1")  # the scan hierarchy (the look-back path has its own tests)
     spec = wl.wiener_velocity()
     spec.c = np.array([0.3, -0.2, 0.1, 0.05])
     if case == "rts_k8":

@@ -22,6 +22,18 @@ def rel(a, b):
     return np.abs(a - b).max() / np.abs(b).max()
 
 
+def rel_comp(a, b):
+    """Per-component scaled error (G23's second measure): for every state component k,
+    max_i |a[i, k] - b[i, k]| / max_i |b[i, k]|; the worst component.  Small components
+    (a turn rate next to positions, packed covariance entries) are held to their own
+    scale instead of the largest component's."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    a2, b2 = a.reshape(-1, a.shape[-1]), b.reshape(-1, b.shape[-1])
+    scale = np.abs(b2).max(axis=0)
+    scale = np.where(scale > 0, scale, np.abs(b2).max())
+    return float((np.abs(a2 - b2).max(axis=0) / scale).max())
+
+
 @pytest.fixture(scope="module")
 def torch_cuda():
     import torch
