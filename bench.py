@@ -124,6 +124,9 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
     else:
         xstep = 3 * N * N + N
     lb1 = (2 * (2 * N * ny + 4 * N * N / K), d * (ny + 3 * N * N / K + N / K + asz / K))
+    # pass 1b: per run v_{s-1} = GP v_in + c and the map offset q += QB v_in (reads GP, QB, c, q;
+    # writes c, q): 2 N^2 FMA and 2 N^2 + 4 N values per run
+    lb1b = (2 * (2 * N * N / K), d * ((2 * N * N + 4 * N) / K))
     lb2 = (2 * (vapply_node + xstep + N * ny), d * (ny + nx + ns / K + N / K + asz / K))
     return {
         "k_p1_reduce": (2 * combine, d * (ny + esz / K)),          # general models: one combine per node
@@ -138,10 +141,11 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         "k_p1_tiles": (2 * combine / L, d * 2 * esz / L), "k_p1_groups": (2 * combine / (L * 128), d * esz / L),
         "k_p2_tiles": (2 * N ** 3 / L, d * 2 * asz / L), "k_p2_groups": (2 * N ** 3 / (L * 128), d * asz / L),
         "k_tf_tiles": (2 * combine / L, d * 2 * esz / L), "k_tf_groups": (2 * combine / (L * 128), d * esz / L),
-        "k_lb_pass1": lb1,
+        "k_lb_pass1a": lb1,
+        "k_lb_pass1b": lb1b,
         "k_lb_pass2": lb2,
         "solve": (2 * (reduce_fl + vapply + vapply_tr / K + trans), d * (ny + 2 * vsz + nx)),
-        "solve_lb": (lb1[0] + lb2[0], lb1[1] + lb2[1]),
+        "solve_lb": (lb1[0] + lb1b[0] + lb2[0], lb1[1] + lb1b[1] + lb2[1]),
     }
 
 
@@ -555,7 +559,7 @@ def main():
     lb = "k_lb_pass2" in prof
     sfl, sby = counts["solve_lb" if lb else "solve"]
     cfl, cby = counts["solve"]
-    solve_hbm = {"schedule": "look-back (2 kernels, R-FWD)" if lb else "scan hierarchy",
+    solve_hbm = {"schedule": "look-back (3 kernels, R-FWD)" if lb else "scan hierarchy",
                  "alg_bytes_per_node": sby, "achieved_gbs": sby * B * T / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
                  "peak_source": hbm_src, "frac_of_hbm_roofline": sby * B * T / (ms * 1e-3) / 1e9 / hbm,
                  "alg_tflops": sfl * B * T / (ms * 1e-3) / 1e12, "frac_of_fp64_peak": sfl * B * T / (ms * 1e-3) / 1e12 / fp64,

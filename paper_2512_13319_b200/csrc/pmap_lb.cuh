@@ -1,21 +1,22 @@
 // pmap_lb.cuh -- single-pass decoupled look-back solve for time-invariant (LTI) models.
 //
-// Two kernels per solve ("look-back path"):
+// Three kernels per solve ("look-back path"):
 //
-//   k_lb_pass1  pass 1 (value functions, P:260-341 / P:382-409), one CTA of three warps
-//               per tile (NT = 64 runs x K interior nodes): warps 1-2 stage y and fold the
-//               node elements' data parts per run (LTI impulse responses, R-LTI) and
-//               reduce them to the tile aggregate; warp 0 then runs the decoupled
-//               look-back over the preceding tiles for the value function entering the
-//               tile while warps 1-2, in parallel, scan the runs and build every run's
-//               pass-2 map (R-RUNAGG) and its in-tile suffix composition as affine
-//               functions of that still unknown value function; once warp 0 has it, the
-//               maps are finished with one mat-vec per run and stored for pass 2, with
-//               the tile's and (last arriver) the group's pass-2 offsets.
+//   k_lb_pass1a pass 1 (value functions, P:260-341 / P:382-409), one CTA per tile (NT = 64
+//               runs x K interior nodes), no waiting: the y tile into shared memory, the run
+//               folds of the node elements' data parts (LTI impulse responses, R-LTI), the
+//               tile aggregate (and, by each group's last arriver, the group aggregate), the
+//               in-tile run scan and every run's pass-2 map (R-RUNAGG) with its in-tile
+//               suffix composition -- as affine functions of the still unknown value
+//               function entering the tile.
+//   k_lb_pass1b one warp per tile: the decoupled look-back over the tile aggregates for
+//               the value function entering the tile (all aggregates are in memory, so it
+//               never waits; a published prefix only shortens the walk), then the run
+//               values and maps are finished with one mat-vec per run, and the tiles' and
+//               groups' pass-2 offsets and x*_T are written for pass 2.
 //   k_lb_pass2  pass 2 (trajectory), one CTA of two warps per tile, tiles in
 //               reverse order: the y tile into shared memory while warp 0 looks back over
-//               the following tiles for x* at the tile's last node -- every map is already
-//               in memory, so it never waits, only stops early at a published prefix --
+//               the following tiles for x* at the tile's last node (again never waiting),
 //               then per run x*_{s-1} from its suffix map and a FORWARD sweep over the
 //               run's nodes that recomputes (S_i, v_i) from the run's value function and y
 //               and recovers x*_i (R-FWD):
@@ -34,15 +35,16 @@
 // look-back windows) is computed once in map_plan, so the per-solve work is data parts,
 // mat-vecs and the node recursion.
 //
-// Look-back (both kernels, two levels): a tile first looks at the tiles of its group of
-// kLbGroup tiles (one warp window), then at whole groups, whose aggregates the group's
-// last-arriving tile publishes, so even the first wave of CTAs resolves in two window
-// steps; each window is one mat-vec per lane with a plan-time product and a warp sum.
-// Status words: 0 = nothing, 1 = aggregate, 2 = inclusive prefix; written with
-// st.release after the payload, polled relaxed, one acquire fence before the payload is
-// read through L2.  Tiles run in ticket order (atomic counter), so a CTA only ever
-// waits on CTAs that started before it (no deadlock).  Flags are cleared by the other
-// kernel of the solve, counters by their last user, so repeated solves (and CUDA-graph
+// Look-back (passes 1b and 2, two levels): a tile first looks at the tiles of its group
+// of kLbGroup tiles (one warp window), then at whole groups, whose aggregates the
+// previous kernel wrote, so a walk is at most a few windows even for the first wave;
+// each window is one mat-vec per lane with a plan-time product and a warp sum.  Every
+// aggregate exists before the look-back runs, so nothing ever waits: prefix status
+// words (0 = none, 2 = inclusive prefix; written with st.release after the payload,
+// read relaxed, one acquire fence before a prefix payload is read through L2) only cut
+// a walk short.  Tiles run in ticket order (atomic counter), so the tiles a look-back
+// reaches first are the ones most likely done.  Flags are cleared by the other kernel
+// of the solve, counters by their last user, so repeated solves (and CUDA-graph
 // replays) need no memset.
 #pragma once
 #include "pmap_lti.cuh"
@@ -59,7 +61,20 @@ struct LbGeom {
   int64_t tpt;    // tiles per trajectory
   int64_t gpt;    // groups per trajectory
   int64_t batch;
+  int64_t S1, S2;  // ticket strides of pass 1b (warps) and pass 2 (CTAs): the resident counts
 };
+
+// Strided ticket order of the look-back kernels: ticket t -> tile (t mod S) C + t div S,
+// C = ceil(total / S), a bijection of [0, S C).  With S = the number of CTAs (warps)
+// resident at once, a tile's neighbour in the scan direction was taken one full wave
+// earlier, so its prefix is usually published by the time the tile looks back: the
+// look-back is then one status read and one payload read.  Tickets past `total` map to
+// tiles >= total and their CTAs (warps) exit at once.
+__host__ __device__ inline int64_t lb_stride_map(int64_t t, int64_t total, int64_t S) {
+  const int64_t C = (total + S - 1) / S;
+  return (t % S) * C + t / S;
+}
+__host__ __device__ inline int64_t lb_ticket_count(int64_t total, int64_t S) { return ((total + S - 1) / S) * S; }
 
 // Plan-time, data-independent quantities of tile j (shared by every trajectory).
 template <typename R, int N>
@@ -298,6 +313,7 @@ struct LbWs {
   R* gagg2;   // [groups][N]             group pass-2 offsets
   R* pub2;    // [tiles][N]              x at the last node of tile j - 1 (pass-2 prefix)
   R* seed;    // [batch][N]              x*_T = S_T^-1 v_T
+  R* seedrb;  // [batch][2N]             data parts of the run ending at node T (pass 1a -> 1b)
   unsigned* flag1;   // [tiles]
   unsigned* gflag1;  // [groups]
   unsigned* gcnt1;   // [groups]
@@ -337,6 +353,12 @@ PM_INLINE unsigned lb_arrive(unsigned* p) {
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
   return old;
+}
+// Bulk L2 prefetch (cp.async.bulk.prefetch, UBLKPF): pulls a contiguous block (16-B
+// aligned, size a multiple of 16) into L2 without registers or shared memory, so the
+// plan-table rows a tile reads later are L2 hits instead of DRAM round trips.
+PM_INLINE void lb_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 PM_INLINE void lb_st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -527,57 +549,47 @@ PM_INLINE void lb_warp_sum(R (&s)[N]) {
     for (int i = 0; i < N; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
 }
 
-// ------------------------------------------------------------------ pass 1
+// ------------------------------------------------------------------ pass 1a
+// Per tile, no waiting: the run folds of the node elements' data parts (LTI impulse
+// responses, R-LTI), the tile aggregate g_j (tree over the runs) and, by the group's last
+// arriver, the group aggregate g_G; then the in-tile run scan and every run's pass-2 map
+// as an affine function of the still unknown v entering the tile:
+//   v_{s-1} = GP v_in + c,   c = ph - GP S_in pb,
+//   beta = WR (rb + C_R v_{s-1}) = beta0 + WR C_R GP v_in,   beta0 = WR (rb + C_R c);
+// the suffix composition of (PHI, beta0) is each run's map with v_in = 0 (its offset's
+// v_in-coefficient QB is a plan table).  Stored: c (rcv), the maps (ri), g_j.
 template <typename R, int N, int NY, int NT, int K, class Src>
-__global__ void __launch_bounds__(NT + 32, 4)
-    k_lb_pass1(const __grid_constant__ LtiFoldParams<R, N, NY, K, Log2<NT>::value> fp, const __grid_constant__ Src src,
-               const LbGeom g, const R* __restrict__ y, const LtiTables<R, N, NT, K>* __restrict__ tab,
-               const LbTileTab<R, N>* __restrict__ lt, const R* __restrict__ lrt, const LbWs<R> w,
-               unsigned long long* flag, int stress) {
-  using E = Elem<R, N>;
-  using V = VF<R, N>;
+__global__ void __launch_bounds__(NT, 6)
+    k_lb_pass1a(const __grid_constant__ LtiFoldParams<R, N, NY, K, Log2<NT>::value> fp, const LbGeom g,
+                const R* __restrict__ y, const LtiTables<R, N, NT, K>* __restrict__ tab,
+                const LbTileTab<R, N>* __restrict__ lt, const R* __restrict__ lrt, const LbWs<R> w) {
   using A = Aff<R, N>;
   using YS = LbYStage<R, NY, NT, K>;
   constexpr int L = NT * K;
   constexpr int NS = Dim<N>::NS;
-  static_assert(NT == 64, "64 run threads (warps 1-2) per tile");
+  static_assert(NT == 64, "64 run threads per tile");
   __shared__ __align__(16) R ys[NT * YS::ROW];
-  __shared__ int s_ticket, s_glast;
-  __shared__ R s_tile[2 * N];  // tile aggregate data parts (b, eta)
-  __shared__ R s_vin[N];       // v entering the tile (warp 0's look-back)
-  __shared__ R s_tot[2 * N];   // cross-warp step of the run reduce / scan
-  __shared__ R s_a32[A::SZ];   // runs 32..63 suffix map (cross-warp)
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r = tid - 32;  // run of the run threads (warps 1-2)
+  __shared__ R s_tot[2 * N];  // cross-warp step of the run reduce / scan
+  __shared__ R s_a32[A::SZ];  // runs 32..63 suffix map (cross-warp)
+  const int r = threadIdx.x, lane = r & 31;
   const unsigned FULL = 0xffffffffu;
-  if (tid == 0) {
-    const unsigned total = (unsigned)(g.batch * g.tpt);
-    const unsigned t = atomicAdd(&w.ctr[0], 1u);
-    if (t == total - 1) atomicExch(&w.ctr[0], 0u);  // every ticket is taken: reset for the next solve
-    s_ticket = (int)t;
-  }
-  __syncthreads();
-  const int64_t t = s_ticket;
-  const int64_t b = t / g.tpt, j = t % g.tpt;
-  const int64_t tile = b * g.tpt + j;
+  const int64_t tile = blockIdx.x;
+  const int64_t b = tile / g.tpt, j = tile % g.tpt;
   const int64_t G = j / kLbGroup;
   const bool last = (j == g.tpt - 1);
   LB_STAMP(0, 0);
-  if (tid == 0) w.flag2[tile] = 0u;  // pass-2 prefix status of the previous solve (that kernel has finished)
   const int64_t n0 = 1 + j * (int64_t)L;
   const int nvalid = (int)min((int64_t)L, g.Nn - n0);
   const R* yb = y + b * g.Nn * NY;
-  YS::issue(ys, yb + n0 * NY, nvalid, tid, NT + 32);
+  if (r == 0)  // this tile's run tables GP, WR, PHI (read after the scan) into L2 now
+    lb_prefetch_l2(lrt + j * (int64_t)LbRunTab<N>::F * NT, (unsigned)(sizeof(R) * 3 * N * N * NT));
+  YS::issue(ys, yb + n0 * NY, nvalid, r, NT);
   YS::wait();
   __syncthreads();
   LB_STAMP(0, 1);
-  bool ok = true;
-  int q = 0;
+  const int q = max(0, min(K, nvalid - r * K));
   R rb[N], rh[N], bb[N], hh[N];
-  if (warp >= 1) {
-    // run fold: data parts of the run aggregate (impulse responses on full runs, R-LTI;
-    // the LTI data recurrence on the partial run of a ragged last tile)
-    q = max(0, min(K, nvalid - r * K));
+  {
     const R* yr = ys + r * YS::ROW;
     if (q == K) {
       R acc0[2 * N], acc1[2 * N];
@@ -607,30 +619,230 @@ __global__ void __launch_bounds__(NT + 32, 4)
 #pragma unroll
       for (int i = 0; i < N; ++i) rb[i] = rh[i] = R(0);
     }
+  }
+  if (!last) {  // every tile but the last is full: g_j from the tile total (tree over the runs)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       bb[i] = rb[i];
       hh[i] = rh[i];
     }
-    if (!last) {  // every tile but the last is full: the tile total by the tree
-      lb_run_reduce64<R, N, NY, K>(fp, r, bb, hh, s_tot);
-      if (r == NT - 1) {
+    lb_run_reduce64<R, N, NY, K>(fp, r, bb, hh, s_tot);
+    if (r == NT - 1) {
+      R gj[N];
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          s_tile[i] = bb[i];
-          s_tile[N + i] = hh[i];
-        }
+      for (int i = 0; i < N; ++i) {
+        R s = hh[i];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s = fma(-__ldg(&lt[j].Hs[i][k]), bb[k], s);
+        gj[i] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) w.agg1[tile * N + i] = gj[i];
+    }
+  }
+  const bool full_group = (G + 1) * kLbGroup <= g.tpt - 1;  // every tile of the group precedes the last tile
+  LB_STAMP(0, 2);
+  // in-tile inclusive scan; exclusive prefix (pb, ph) of run r (0 for run 0)
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    bb[i] = rb[i];
+    hh[i] = rh[i];
+  }
+  lb_run_scan64<R, N>(tab->UWc, &tab->UX[0][0][0][0], r, bb, hh, s_tot);
+  R pb[N], ph[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    pb[i] = __shfl_up_sync(FULL, bb[i], 1);
+    ph[i] = __shfl_up_sync(FULL, hh[i], 1);
+  }
+  __syncthreads();
+  if (r == 32) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      pb[i] = s_tot[i];
+      ph[i] = s_tot[N + i];
+    }
+  }
+  if (r == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) pb[i] = ph[i] = R(0);
+  }
+  const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;  // field f of run r at rt[f * NT]
+  R cvec[N];
+  {
+    R u[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(-__ldg(&lt[j].S[i <= k ? sidx(i, k, N) : sidx(k, i, N)]), pb[k], s);
+      u[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = ph[i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::GP + i * N + k) * NT), u[k], s);
+      cvec[i] = s;
+    }
+  }
+  A agg;
+  set_identity(agg);
+  if (q > 0) {
+    R CR[NS];  // C of the run element: one full run (E1) or the partial run of q nodes
+#pragma unroll
+    for (int k = 0; k < NS; ++k) CR[k] = (q == K) ? __ldg(&tab->E1[N * N + N + k]) : __ldg(&tab->PC[q - 1][k]);
+    R t2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = rb[i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(CR[i <= k ? sidx(i, k, N) : sidx(k, i, N)], cvec[k], s);
+      t2[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::WR + i * N + k) * NT), t2[k], s);
+      agg.q[i] = s;
+#pragma unroll
+      for (int c = 0; c < N; ++c) agg.P[i][c] = __ldg(rt + (LbRunTab<N>::PHI + i * N + c) * NT);
+    }
+  }
+  // in-tile suffix composition: Incl_r = agg_r o ... o agg_{NT-1}
+#pragma unroll 1
+  for (int d = 1; d < 32; d <<= 1) {
+    A o;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int c = 0; c < N; ++c) o.P[i][c] = __shfl_down_sync(FULL, agg.P[i][c], d);
+      o.q[i] = __shfl_down_sync(FULL, agg.q[i], d);
+    }
+    if (lane + d < 32) compose(agg, o, agg);
+  }
+  if (r == 32) store(agg, s_a32, 1);
+  __syncthreads();
+  if (r < 32) {
+    A o;
+    load(o, s_a32, 1);
+    compose(agg, o, agg);
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) w.rcv[(tile * N + i) * NT + r] = cvec[i];
+  store(agg, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
+  if (last && q > 0 && n0 + (int64_t)r * K + q == g.Nn) {  // the run ending at node T: keep its data parts
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      w.seedrb[b * 2 * N + i] = rb[i];
+      w.seedrb[b * 2 * N + N + i] = rh[i];
+    }
+  }
+  // the group aggregate, by the group's last arriver (after everything else of the tile,
+  // so the atomic's round trip is off the tile's critical path):
+  //   g_G = sum_l Pa[32G + 32][l] g_{32G + 31 - l}
+  if (full_group && r >= 32) {
+    unsigned gl = 0;
+    if (r == NT - 1) gl = lb_arrive(&w.gcnt1[b * g.gpt + G]) == kLbGroup - 1;
+    gl = __shfl_sync(FULL, gl, 31);
+    if (gl) {
+      R x[N], sg[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = lb_ldcg(w.agg1 + (b * g.tpt + G * kLbGroup + kLbGroup - 1 - lane) * N + i);
+      lb_matvec<R, N>(w.Pa + (((G + 1) * kLbGroup) * (kLbGroup + 1) + lane) * N * N, x, sg);
+      lb_warp_sum<R, N>(sg);
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) w.gagg1[(b * g.gpt + G) * N + i] = sg[i];
+        atomicExch(&w.gcnt1[b * g.gpt + G], 0u);
       }
     }
   }
-  __syncthreads();
-  LB_STAMP(0, 2);
-  if (warp == 0) {
-    // ---- publish g_j, the group aggregate (last arriver), look back for v entering the tile
-    const LbTileTab<R, N>* tj = lt + j;
-    const int cnt = (int)(j - G * kLbGroup);  // tiles before j in its group
-    // the plan products this warp will need, loaded before anything waits on them:
-    // Pa[j][lane] (window (a)), Pb[G][lane] (first window of (b)), Gt_j, Hs_j
+  LB_STAMP(0, 3);
+}
+
+// ------------------------------------------------------------------ pass 1b
+// One warp per tile: the decoupled look-back for v entering the tile over the tile
+// aggregates g (pass 1a wrote every g and group g_G, so nothing is waited for; a
+// published prefix only shortens the walk):
+//   v_end(j-1) = sum_{l < l*} Pa[j][l] g_{j-1-l} + Pa[j][l*] v_end(j-1-l*)
+// over the tiles of j's group, else + Pa[j][cnt] v_end(32G - 1) with
+//   v_end(32G - 1) = sum_{l < l*} Pb[G][l] g_{G-1-l} + Pb[G][l*] v_end(group G-1-l*)
+// over whole groups (group -1 = node 0); then the finished run values for pass 2:
+// v_{s-1} = GP v_in + c (rcv), the maps' offsets q += QB v_in (ri), the tile's pass-2
+// offset beta_tile (agg2), the group's (last arriver, agg2 -> gagg2), and x*_T.
+template <typename R, int N, int NY, int NT, int K, class Src>
+__global__ void __launch_bounds__(128)
+    k_lb_pass1b(const __grid_constant__ Src src, const LbGeom g, const R* __restrict__ y,
+                const LtiTables<R, N, NT, K>* __restrict__ tab, const LbTileTab<R, N>* __restrict__ lt,
+                const R* __restrict__ lrt, const LbWs<R> w, unsigned long long* flag, int stress) {
+  using E = Elem<R, N>;
+  using V = VF<R, N>;
+  using A = Aff<R, N>;
+  constexpr int NS = Dim<N>::NS;
+  constexpr int L = NT * K;
+  static_assert(NT == 64, "two runs per lane");
+  __shared__ int s_ticket[4];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  const int64_t total = g.batch * g.tpt;
+  const int64_t nticket = lb_ticket_count(total, g.S1);
+  if ((int64_t)blockIdx.x * 4 + wid >= nticket) return;  // no ticket for the grid's spare warps
+  if (lane == 0) {
+    const unsigned t = atomicAdd(&w.ctr[0], 1u);
+    if (t == nticket - 1) atomicExch(&w.ctr[0], 0u);  // every ticket is taken: reset for the next solve
+    s_ticket[wid] = (int)t;
+  }
+  __syncwarp();
+  const int64_t t = s_ticket[wid];
+  if (t >= nticket) return;
+  const int64_t u = lb_stride_map(t, total, g.S1);
+  if (u >= total) return;
+  const int64_t b = u / g.tpt, j = u % g.tpt;
+  const int64_t tile = b * g.tpt + j;
+  const int64_t G = j / kLbGroup;
+  const bool last = (j == g.tpt - 1);
+  const int64_t n0 = 1 + j * (int64_t)L;
+  if (lane == 0) {
+    w.flag2[tile] = 0u;  // pass-2 prefix status of the previous solve
+    if (w.tim) w.tim[tile * 8 + 4] = lb_now();
+    // what the run values need after the look-back, into L2 now: GP, QB, c, the maps' offsets
+    const R* rt0 = lrt + j * (int64_t)LbRunTab<N>::F * NT;
+    lb_prefetch_l2(rt0 + LbRunTab<N>::GP * NT, (unsigned)(sizeof(R) * N * N * NT));
+    lb_prefetch_l2(rt0 + LbRunTab<N>::QB * NT, (unsigned)(sizeof(R) * N * N * NT));
+    lb_prefetch_l2(w.rcv + tile * (int64_t)N * NT, (unsigned)(sizeof(R) * N * NT));
+    lb_prefetch_l2(w.ri + tile * (int64_t)A::SZ * NT + N * N * NT, (unsigned)(sizeof(R) * N * NT));
+  }
+  const R* yb = y + b * g.Nn * NY;
+  R eta0[N];  // v of node 0: P0^-1 m0 + K y_0 - K r (E_0's data)
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R s = src.h00[i];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], __ldg(yb + k), s);
+    eta0[i] = s;
+  }
+  R vin[N];
+  bool quick = false;
+  if (j > 0) {  // the usual case (strided tickets): the previous tile's prefix is v_in
+    unsigned s0 = 0;
+    if (lane == 0) s0 = lb_ld_status(&w.flag1[b * g.tpt + j - 1]);
+    s0 = __shfl_sync(FULL, s0, 0);
+    if (s0 == 2u) {
+      lb_fence_acquire();
+#pragma unroll
+      for (int i = 0; i < N; ++i) vin[i] = lb_ldcg(w.pub1 + (b * g.tpt + j - 1) * N + i);
+      quick = true;
+    }
+  }
+  if (j == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) vin[i] = eta0[i];
+  } else if (!quick) {
+    const int cnt = (int)(j - G * kLbGroup);
+    const int64_t ka = j - 1 - lane;
+    const int64_t Gp = G - 1 - lane;
     R Pa_l[N][N], Pb_l[N][N];
 #pragma unroll
     for (int i = 0; i < N; ++i)
@@ -639,310 +851,139 @@ __global__ void __launch_bounds__(NT + 32, 4)
         Pa_l[i][c] = __ldg(w.Pa + ((j * (kLbGroup + 1) + lane) * N + i) * N + c);
         Pb_l[i][c] = (lane <= G) ? __ldg(w.Pb + ((G * (G + 1) / 2 + lane) * N + i) * N + c) : R(0);
       }
-    R gj[N];
+    // (b) status of group Gp: 2 = its last tile's prefix, 1 = its aggregate (written by
+    // pass 1a), 3 = node 0
+    auto group_status = [&](int64_t Gx) -> unsigned {
+      if (Gx < -1) return 0u;
+      if (Gx == -1) return 3u;
+      return lb_ld_status(&w.flag1[b * g.tpt + Gx * kLbGroup + kLbGroup - 1]) == 2u ? 2u : 1u;
+    };
+    const unsigned sta = lane < cnt ? lb_ld_status(&w.flag1[b * g.tpt + ka]) : 0u;
+    const unsigned prea = __ballot_sync(FULL, sta == 2u);
+    const unsigned stb = prea ? 0u : group_status(Gp);
+    const unsigned preb = prea ? 0u : __ballot_sync(FULL, stb >= 2u);
+    if (prea || preb) lb_fence_acquire();
+    const int la = prea ? __ffs(prea) - 1 : cnt;
+    R sa[N];
+    {
+      R x[N];
+      const bool use = lane < la || (lane == la && prea);
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      R s = R(0);
-      if (!last) {
-        s = s_tile[N + i];
+      for (int i = 0; i < N; ++i)
+        x[i] = !use ? R(0)
+                    : (lane < la ? w.agg1[(b * g.tpt + ka) * N + i] : lb_ldcg(w.pub1 + (b * g.tpt + ka) * N + i));
 #pragma unroll
-        for (int k = 0; k < N; ++k) s = fma(-__ldg(&tj->Hs[i][k]), s_tile[k], s);
-      }
-      gj[i] = s;
-    }
-    const bool full_group = (G + 1) * kLbGroup <= g.tpt - 1;  // every tile of the group precedes the last tile
-    if (!last) {
-      if (lane == 0) {
-        lb_stress(stress, tile, 1);
+      for (int i = 0; i < N; ++i) {
+        R t2 = R(0);
 #pragma unroll
-        for (int i = 0; i < N; ++i) w.agg1[tile * N + i] = gj[i];
-        lb_st_release(&w.flag1[tile], 1u);
-        s_glast = full_group && lb_arrive(&w.gcnt1[b * g.gpt + G]) == kLbGroup - 1;
-      }
-      __syncwarp();
-      if (s_glast) {  // last arriver: g_G = sum_l Pa[32G + 32][l] g_{32G + 31 - l}
-        const int64_t k = G * kLbGroup + kLbGroup - 1 - lane;
-        R x[N], sg[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) x[i] = lb_ldcg(w.agg1 + (b * g.tpt + k) * N + i);
-        lb_matvec<R, N>(w.Pa + (((G + 1) * kLbGroup) * (kLbGroup + 1) + lane) * N * N, x, sg);
-        lb_warp_sum<R, N>(sg);
-        if (lane == 0) {
-          lb_stress(stress, tile, 2);
-#pragma unroll
-          for (int i = 0; i < N; ++i) w.gagg1[(b * g.gpt + G) * N + i] = sg[i];
-          lb_st_release(&w.gflag1[b * g.gpt + G], 1u);
-          atomicExch(&w.gcnt1[b * g.gpt + G], 0u);
-        }
+        for (int c = 0; c < N; ++c) t2 = fma(Pa_l[i][c], x[c], t2);
+        sa[i] = t2;
       }
     }
-    LB_STAMP(0, 3);
-    R eta0[N];  // v of node 0: P0^-1 m0 + K y_0 - K r (E_0's data), the terminal of the look-back
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      R s = src.h00[i];
-#pragma unroll
-      for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], yb[k], s);
-      eta0[i] = s;
-    }
-    R vin[N];
-    if (j == 0) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) vin[i] = eta0[i];
-    } else {
-      //   v_end(j-1) = sum_{l < l*} Pa[j][l] g_{j-1-l} + Pa[j][l*] v_end(j-1-l*)
-      // over (a) the tiles before j in its group, and, if none of them holds a prefix,
-      // Pa[j][cnt] v_end(32G - 1) with (b) v_end(32G - 1) = sum_{l < l*} Pb[G][l] g_{G-1-l}
-      // + Pb[G][l*] v_end(group G-1-l*) over whole groups (group -1 = node 0).  Both
-      // windows are polled together; one fence; one round of payload loads.
-      const int64_t ka = j - 1 - lane;
-      const int64_t Gp = G - 1 - lane;
-      const bool needa = lane < cnt, needb = Gp >= 0;
-      unsigned sta = 0, stb = (Gp == -1) ? 3u : 0u;
-      unsigned prea = 0, preb = 0;
-      for (;;) {
-        if (needa && sta == 0u) sta = lb_ld_status(&w.flag1[b * g.tpt + ka]);
-        if (needb && stb == 0u) {
-          if (lb_ld_status(&w.flag1[b * g.tpt + Gp * kLbGroup + kLbGroup - 1]) == 2u)
-            stb = 2u;
-          else if (lb_ld_status(&w.gflag1[b * g.gpt + Gp]) == 1u)
-            stb = 1u;
-        }
-        if (__ballot_sync(FULL, needa && sta == 0u) == 0u) {
-          prea = __ballot_sync(FULL, needa && sta == 2u);
-          if (prea) break;  // a prefix in the group: (b) is not needed
-          if (__ballot_sync(FULL, needb && stb == 0u) == 0u) break;
-        }
-        __nanosleep(20);
-      }
-      LB_STAMP(0, 6);
-      lb_fence_acquire();
-      preb = prea ? 0u : __ballot_sync(FULL, stb >= 2u);
-      const int la = prea ? __ffs(prea) - 1 : cnt;  // (a) terms l < la, prefix at la if prea
-      R sa[N], sb[N];
+    if (!prea) {
+      R sb[N];
+      const int lb = preb ? __ffs(preb) - 1 : 32;
       {
         R x[N];
-        const bool use = lane < la || (lane == la && prea);
+        const bool use = lane < lb || (lane == lb && preb);
 #pragma unroll
         for (int i = 0; i < N; ++i)
           x[i] = !use ? R(0)
-                      : (lane < la ? lb_ldcg(w.agg1 + (b * g.tpt + ka) * N + i) : lb_ldcg(w.pub1 + (b * g.tpt + ka) * N + i));
+                      : (stb == 3u ? eta0[i]
+                                   : (lane < lb ? w.gagg1[(b * g.gpt + Gp) * N + i]
+                                                : lb_ldcg(w.pub1 + (b * g.tpt + Gp * kLbGroup + kLbGroup - 1) * N + i)));
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           R t2 = R(0);
 #pragma unroll
-          for (int c = 0; c < N; ++c) t2 = fma(Pa_l[i][c], x[c], t2);
-          sa[i] = t2;
+          for (int c = 0; c < N; ++c) t2 = fma(Pb_l[i][c], x[c], t2);
+          sb[i] = t2;
         }
       }
-      if (!prea) {
-        const int lb = preb ? __ffs(preb) - 1 : 32;
-        {
-          R x[N];
-          const bool use = lane <= lb && Gp >= -1 && (lane < lb || preb);
+      if (!preb) {  // more than 32 groups to the nearest prefix (or node 0)
+        const R* PbG = w.Pb + (G * (G + 1) / 2) * N * N;
+        for (int64_t l0 = 32;; l0 += 32) {
+          const int64_t l = l0 + lane;
+          const int64_t Gq = G - 1 - l;
+          const unsigned st = group_status(Gq);
+          const unsigned pre = __ballot_sync(FULL, st >= 2u);
+          if (pre) lb_fence_acquire();
+          const int lstar = pre ? __ffs(pre) - 1 : 32;
+          if (lane <= lstar && Gq >= -1) {
+            R x[N], o[N];
 #pragma unroll
-          for (int i = 0; i < N; ++i)
-            x[i] = !use ? R(0)
-                        : (stb == 3u ? eta0[i]
-                                     : (lane < lb ? lb_ldcg(w.gagg1 + (b * g.gpt + Gp) * N + i)
-                                                  : lb_ldcg(w.pub1 + (b * g.tpt + Gp * kLbGroup + kLbGroup - 1) * N + i)));
+            for (int i = 0; i < N; ++i)
+              x[i] = st == 3u ? eta0[i]
+                              : (lane < lstar ? w.gagg1[(b * g.gpt + Gq) * N + i]
+                                              : lb_ldcg(w.pub1 + (b * g.tpt + Gq * kLbGroup + kLbGroup - 1) * N + i));
+            lb_matvec<R, N>(PbG + l * N * N, x, o);
 #pragma unroll
-          for (int i = 0; i < N; ++i) {
-            R t2 = R(0);
-#pragma unroll
-            for (int c = 0; c < N; ++c) t2 = fma(Pb_l[i][c], x[c], t2);
-            sb[i] = t2;
+            for (int i = 0; i < N; ++i) sb[i] += o[i];
           }
-        }
-        if (!preb) {
-          // no prefix within 32 groups (first wave of a long trajectory): further windows
-          const R* PbG = w.Pb + (G * (G + 1) / 2) * N * N;
-          for (int64_t l0 = 32;; l0 += 32) {
-            const int64_t l = l0 + lane;
-            const int64_t Gq = G - 1 - l;
-            unsigned st = 0;
-            if (Gq >= 0) {
-              const unsigned* ft = &w.flag1[b * g.tpt + Gq * kLbGroup + kLbGroup - 1];
-              const unsigned* fg = &w.gflag1[b * g.gpt + Gq];
-              for (;;) {
-                if (lb_ld_status(ft) == 2u) { st = 2u; break; }
-                if (lb_ld_status(fg) == 1u) { st = 1u; break; }
-                __nanosleep(20);
-              }
-            } else if (Gq == -1) {
-              st = 3u;
-            }
-            const unsigned pre = __ballot_sync(FULL, st >= 2u);
-            lb_fence_acquire();
-            const int lstar = pre ? __ffs(pre) - 1 : 32;
-            if (lane <= lstar && Gq >= -1) {
-              R x[N], o[N];
-#pragma unroll
-              for (int i = 0; i < N; ++i)
-                x[i] = st == 3u ? eta0[i]
-                                : (lane < lstar ? lb_ldcg(w.gagg1 + (b * g.gpt + Gq) * N + i)
-                                                : lb_ldcg(w.pub1 + (b * g.tpt + Gq * kLbGroup + kLbGroup - 1) * N + i));
-              lb_matvec<R, N>(PbG + l * N * N, x, o);
-#pragma unroll
-              for (int i = 0; i < N; ++i) sb[i] += o[i];
-            }
-            if (pre) break;
-          }
-        }
-        lb_warp_sum<R, N>(sb);
-        // + Pa[j][cnt] v_end(32G - 1): Pa[j][cnt] is lane cnt's Pa_l
-        R o[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          R t2 = R(0);
-#pragma unroll
-          for (int c = 0; c < N; ++c) t2 = fma(__shfl_sync(FULL, Pa_l[i][c], cnt), sb[c], t2);
-          o[i] = t2;
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int i = 0; i < N; ++i) sa[i] += o[i];
+          if (pre) break;
         }
       }
-      lb_warp_sum<R, N>(sa);
+      lb_warp_sum<R, N>(sb);
+      R o[N];  // + Pa[j][cnt] v_end(32G - 1): Pa[j][cnt] is lane cnt's Pa_l
 #pragma unroll
-      for (int i = 0; i < N; ++i) vin[i] = sa[i];
-    }
-    LB_STAMP(0, 4);
-    if (lane == 0) {
+      for (int i = 0; i < N; ++i) {
+        R t2 = R(0);
 #pragma unroll
-      for (int i = 0; i < N; ++i) s_vin[i] = vin[i];
-      if (!last) {  // inclusive prefix: v leaving the tile
-        lb_stress(stress, tile, 3);
+        for (int c = 0; c < N; ++c) t2 = fma(__shfl_sync(FULL, Pa_l[i][c], cnt), sb[c], t2);
+        o[i] = t2;
+      }
+      if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          R s = gj[i];
-#pragma unroll
-          for (int k = 0; k < N; ++k) s = fma(__ldg(&tj->Gt[i][k]), vin[k], s);
-          w.pub1[tile * N + i] = s;
-        }
-        lb_st_release(&w.flag1[tile], 2u);
+        for (int i = 0; i < N; ++i) sa[i] += o[i];
       }
     }
+    lb_warp_sum<R, N>(sa);
+#pragma unroll
+    for (int i = 0; i < N; ++i) vin[i] = sa[i];
   }
-  // ---- run threads (in parallel with warp 0's look-back): the run maps as affine
-  // functions of the unknown v_in:  v_{s-1} = GP v_in + c,  c = ph - GP S_in pb,
-  // beta = WR (rb + C_R v_{s-1}) = beta0 + WR C_R GP v_in,  beta0 = WR (rb + C_R c);
-  // the suffix composition of (PHI, beta0) gives Incl_r with v_in = 0, and QB carries the
-  // v_in-coefficient of its offset.
-  R cvec[N];
-  A agg;
-  set_identity(agg);
-  const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + (r < 0 ? 0 : r);  // field f of run r at rt[f * NT]
-  if (warp >= 1) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) {  // the tree reduce above consumed bb, hh
-      bb[i] = rb[i];
-      hh[i] = rh[i];
-    }
-    lb_run_scan64<R, N>(tab->UWc, &tab->UX[0][0][0][0], r, bb, hh, s_tot);  // inclusive prefixes
-    R pb[N], ph[N];  // exclusive prefix = inclusive prefix of run r - 1 (0 for run 0)
+  if (lane == 0 && w.tim) w.tim[tile * 8 + 5] = lb_now();
+  if (lane == 0 && !last) {  // inclusive prefix: v leaving the tile
+    lb_stress(stress, tile, 3);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      pb[i] = __shfl_up_sync(FULL, bb[i], 1);
-      ph[i] = __shfl_up_sync(FULL, hh[i], 1);
+      R s = w.agg1[tile * N + i];
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(__ldg(&lt[j].Gt[i][k]), vin[k], s);
+      w.pub1[tile * N + i] = s;
     }
-    lb_bar_runs();
-    if (r == 32) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        pb[i] = s_tot[i];
-        ph[i] = s_tot[N + i];
-      }
-    }
-    if (r == 0) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) pb[i] = ph[i] = R(0);
-    }
-    {
-      R u[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        R s = R(0);
-#pragma unroll
-        for (int k = 0; k < N; ++k) s = fma(-__ldg(&lt[j].S[i <= k ? sidx(i, k, N) : sidx(k, i, N)]), pb[k], s);
-        u[i] = s;
-      }
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        R s = ph[i];
-#pragma unroll
-        for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::GP + i * N + k) * NT), u[k], s);
-        cvec[i] = s;
-      }
-    }
-    if (q > 0) {
-      R CR[NS];  // C of the run element: one full run (E1) or the partial run of q nodes
-#pragma unroll
-      for (int k = 0; k < NS; ++k) CR[k] = (q == K) ? __ldg(&tab->E1[N * N + N + k]) : __ldg(&tab->PC[q - 1][k]);
-      R t2[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        R s = rb[i];
-#pragma unroll
-        for (int k = 0; k < N; ++k) s = fma(CR[i <= k ? sidx(i, k, N) : sidx(k, i, N)], cvec[k], s);
-        t2[i] = s;
-      }
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        R s = R(0);
-#pragma unroll
-        for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::WR + i * N + k) * NT), t2[k], s);
-        agg.q[i] = s;
-#pragma unroll
-        for (int c = 0; c < N; ++c) agg.P[i][c] = __ldg(rt + (LbRunTab<N>::PHI + i * N + c) * NT);
-      }
-    }
-    // in-tile suffix composition: Incl_r = agg_r o ... o agg_{NT-1}
-#pragma unroll 1
-    for (int d = 1; d < 32; d <<= 1) {
-      A o;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-#pragma unroll
-        for (int c = 0; c < N; ++c) o.P[i][c] = __shfl_down_sync(FULL, agg.P[i][c], d);
-        o.q[i] = __shfl_down_sync(FULL, agg.q[i], d);
-      }
-      if (lane + d < 32) compose(agg, o, agg);
-    }
-    if (r == 32) store(agg, s_a32, 1);
-    lb_bar_runs();
-    if (r < 32) {
-      A o;
-      load(o, s_a32, 1);
-      compose(agg, o, agg);
-    }
+    lb_st_release(&w.flag1[tile], 2u);
   }
-  __syncthreads();  // v_in from warp 0
-  LB_STAMP(0, 5);
-  if (warp >= 1) {
-    R vin[N];
+  // finish the run values: two runs per lane
+  bool ok = true;
 #pragma unroll
-    for (int i = 0; i < N; ++i) vin[i] = s_vin[i];
-    R vp[N], qb[N];
+  for (int h = 0; h < 2; ++h) {
+    const int r = lane + 32 * h;
+    const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+    R* cv = w.rcv + tile * (int64_t)N * NT + r;
+    R* qv = w.ri + tile * (int64_t)A::SZ * NT + N * N * NT + r;  // the offset fields of the run's map
+    R vp[N], qn[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      R s = cvec[i], s2 = agg.q[i];
+      R s = cv[i * NT], s2 = qv[i * NT];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         s = fma(__ldg(rt + (LbRunTab<N>::GP + i * N + k) * NT), vin[k], s);
         s2 = fma(__ldg(rt + (LbRunTab<N>::QB + i * N + k) * NT), vin[k], s2);
       }
       vp[i] = s;
-      qb[i] = s2;
+      qn[i] = s2;
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      agg.q[i] = qb[i];
-      w.rcv[(tile * N + i) * NT + r] = vp[i];
+      cv[i * NT] = vp[i];
+      qv[i * NT] = qn[i];
     }
-    store(agg, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
-    if (last && q > 0 && n0 + (int64_t)r * K + q == g.Nn) {  // this run ends at node T: x*_T = S_T^-1 v_T
+    if (r == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) w.agg2[tile * N + i] = qn[i];  // run 0's map = the tile's pass-2 map
+    }
+    const int q = (int)max((int64_t)0, min((int64_t)K, g.Nn - n0 - (int64_t)r * K));
+    if (last && q > 0 && n0 + (int64_t)r * K + q == g.Nn) {  // the run ending at node T: x*_T = S_T^-1 v_T
       V cur, vend;
 #pragma unroll
       for (int k = 0; k < NS; ++k) cur.S[k] = __ldg(rt + (LbRunTab<N>::SP + k) * NT);
@@ -964,8 +1005,8 @@ __global__ void __launch_bounds__(NT + 32, 4)
       }
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        ra.b[i] = rb[i];
-        ra.h[i] = rh[i];
+        ra.b[i] = w.seedrb[b * 2 * N + i];
+        ra.h[i] = w.seedrb[b * 2 * N + N + i];
       }
       vapply<R, N, false>(ra, cur, vend, nullptr, ok);
       R xT[N];
@@ -973,17 +1014,14 @@ __global__ void __launch_bounds__(NT + 32, 4)
 #pragma unroll
       for (int i = 0; i < N; ++i) w.seed[b * N + i] = xT[i];
     }
-    // the tile's pass-2 offset (run 0's suffix map) and, by the group's last arriver, the
-    // group's: beta_G = sum_l Qa[32G - 1][l] beta_{32G + l} (groups G >= 1)
-    if (r == 0) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) w.agg2[tile * N + i] = agg.q[i];
-      const int gcount = (int)min((int64_t)kLbGroup, g.tpt - G * kLbGroup);
-      s_glast = G >= 1 && lb_arrive(&w.gcnt2[b * g.gpt + G]) == (unsigned)(gcount - 1);
-    }
-    lb_bar_runs();
-    if (s_glast && warp == 1) {
-      const int gcount = (int)min((int64_t)kLbGroup, g.tpt - G * kLbGroup);
+  }
+  // the group's pass-2 offset, by its last arriver: beta_G = sum_l Qa[32G - 1][l] beta_{32G + l}
+  if (G >= 1) {
+    const int gcount = (int)min((int64_t)kLbGroup, g.tpt - G * kLbGroup);
+    unsigned gl = 0;
+    if (lane == 0) gl = lb_arrive(&w.gcnt2[b * g.gpt + G]) == (unsigned)(gcount - 1);
+    gl = __shfl_sync(FULL, gl, 0);
+    if (gl) {
       R s[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) s[i] = R(0);
@@ -1001,9 +1039,9 @@ __global__ void __launch_bounds__(NT + 32, 4)
       }
     }
   }
-  if (!ok) atomicMin(flag, (unsigned long long)(n0 + (int64_t)max(r, 0) * K));
+  if (lane == 0 && w.tim) w.tim[tile * 8 + 6] = lb_now();
+  if (!ok) atomicMin(flag, (unsigned long long)(g.Nn - 1));
 }
-
 
 // One forward node step (R-FWD + the node update): x <- A^-1 [x - b + C (S x - v)] with
 // the value function V = V_{i-1} entering node i, then V <- E_i (x) V (Woodbury form
@@ -1101,15 +1139,18 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
   __shared__ R s_x[N];  // x at the tile's last node
   const int r = threadIdx.x, lane = r & 31;
   const unsigned FULL = 0xffffffffu;
+  const int64_t total = g.batch * g.tpt;
+  const int64_t nticket = lb_ticket_count(total, g.S2);
   if (r == 0) {
-    const unsigned total = (unsigned)(g.batch * g.tpt);
     const unsigned t = atomicAdd(&w.ctr[1], 1u);
-    if (t == total - 1) atomicExch(&w.ctr[1], 0u);
+    if (t == nticket - 1) atomicExch(&w.ctr[1], 0u);
     s_ticket = (int)t;
   }
   __syncthreads();
-  const int64_t t = s_ticket;
-  const int64_t b = t / g.tpt, j = g.tpt - 1 - t % g.tpt;  // reverse order
+  const int64_t u = lb_stride_map(s_ticket, total, g.S2);
+  if (u >= total) return;
+  const int64_t ur = total - 1 - u;  // reverse order
+  const int64_t b = ur / g.tpt, j = ur % g.tpt;
   const int64_t tile = b * g.tpt + j;
   const int64_t G = j / kLbGroup;
   const bool last = (j == g.tpt - 1);
@@ -1117,6 +1158,11 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
   const int nvalid = (int)min((int64_t)L, g.Nn - n0);
   const R* yb = y + b * g.Nn * NY;
   LB_STAMP(1, 0);
+  if (r == 0) {  // what the runs read after the look-back, into L2 now: S, the maps, v
+    lb_prefetch_l2(lrt + j * (int64_t)LbRunTab<N>::F * NT + LbRunTab<N>::SP * NT, (unsigned)(sizeof(R) * NS * NT));
+    lb_prefetch_l2(w.ri + tile * (int64_t)A::SZ * NT, (unsigned)(sizeof(R) * A::SZ * NT));
+    lb_prefetch_l2(w.rcv + tile * (int64_t)N * NT, (unsigned)(sizeof(R) * N * NT));
+  }
   YS::issue(ys, yb + n0 * NY, nvalid, r, NT);  // lands while warp 0 looks back
   if (r < 32) {
     if (lane == 0) {  // pass-1 status of this solve (that kernel has finished): clear for the next one
@@ -1132,9 +1178,14 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
     // x_end(G) = sum_{l < l*} Qb[G][l] beta_{G+1+l} + Qb[G][l*] x_end(group G + l*) over
     // whole groups (past the last group: the seed).  Both windows' status words are read
     // once, one fence, one round of payload loads.
-    R seed[N];
+    R seed[N], Phj[N][N], bej[N];  // x*_T; this tile's map (Phi_j = Qa[j-1][1], beta_j) for its prefix
 #pragma unroll
-    for (int i = 0; i < N; ++i) seed[i] = w.seed[b * N + i];
+    for (int i = 0; i < N; ++i) {
+      seed[i] = w.seed[b * N + i];
+      bej[i] = j > 0 ? w.agg2[tile * N + i] : R(0);
+#pragma unroll
+      for (int c = 0; c < N; ++c) Phj[i][c] = j > 0 ? __ldg(w.Qa + (((j - 1) * (kLbGroup + 1) + 1) * N + i) * N + c) : R(0);
+    }
     R xl[N];
     if (last) {
 #pragma unroll
@@ -1143,6 +1194,19 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
       const int64_t gend = min((G + 1) * kLbGroup, g.tpt) - 1;
       const int cnt = (int)(gend - j);  // following tiles in the group
       const R* QbG = w.Qb + (G * g.gpt - G * (G - 1) / 2) * N * N;
+      bool quick = false;
+      if (cnt > 0) {  // the usual case (strided tickets): the next tile's prefix is x_last(j)
+        unsigned s0 = 0;
+        if (lane == 0) s0 = lb_ld_status(&w.flag2[b * g.tpt + j + 1]);
+        s0 = __shfl_sync(FULL, s0, 0);
+        if (s0 == 2u) {
+          lb_fence_acquire();
+#pragma unroll
+          for (int i = 0; i < N; ++i) xl[i] = lb_ldcg(w.pub2 + (b * g.tpt + j + 1) * N + i);
+          quick = true;
+        }
+      }
+      if (!quick) {
       R Qa_l[N][N], Qb_l[N][N];
 #pragma unroll
       for (int i = 0; i < N; ++i)
@@ -1242,6 +1306,7 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
       lb_warp_sum<R, N>(sa);
 #pragma unroll
       for (int i = 0; i < N; ++i) xl[i] = sa[i];
+      }
     }
     LB_STAMP(1, 1);
     if (lane == 0) {
@@ -1249,10 +1314,13 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
       for (int i = 0; i < N; ++i) s_x[i] = xl[i];
       if (j > 0) {  // prefix: x at the last node of tile j - 1 = Phi_j x_last(j) + beta_j
         lb_stress(stress, tile, 4);
-        R o[N];
-        lb_matvec<R, N>(w.Qa + ((j - 1) * (kLbGroup + 1) + 1) * N * N, xl, o);
 #pragma unroll
-        for (int i = 0; i < N; ++i) w.pub2[tile * N + i] = o[i] + w.agg2[tile * N + i];
+        for (int i = 0; i < N; ++i) {
+          R a = bej[i];
+#pragma unroll
+          for (int c = 0; c < N; ++c) a = fma(Phj[i][c], xl[c], a);
+          w.pub2[tile * N + i] = a;
+        }
         lb_st_release(&w.flag2[tile], 2u);
       }
     }

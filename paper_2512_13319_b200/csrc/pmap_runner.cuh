@@ -262,13 +262,13 @@ struct PlanState {
 // kernel classes reported by map_profile_read
 enum KernelId { K_P1_REDUCE = 0, K_P1_REDUCE_EDGE, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_GROUPS,
                 K_P2_DOWN, K_FILTER_OUT, K_TF_REDUCE, K_TF_REDUCE_EDGE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD,
-                K_NL_MISC, K_SEQ, K_LB_P1, K_LB_P2, K_P1_REDUCE_LTI, K_COUNT };
+                K_NL_MISC, K_SEQ, K_LB_P1, K_LB_P2, K_P1_REDUCE_LTI, K_LB_P1B, K_COUNT };
 inline const char* kernel_name(int id) {
   static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_reduce_lti_edge", "k_p1_tiles", "k_p1_groups",
                                        "k_p1_down", "k_p2_tiles", "k_p2_groups", "k_p2_down", "k_filter_out",
                                        "k_tf_reduce", "k_tf_reduce_lti_edge", "k_tf_tiles", "k_tf_groups",
                                        "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff", "k_seq_rts/k_seq_tf",
-                                       "k_lb_pass1", "k_lb_pass2", "k_p1_reduce_lti"};
+                                       "k_lb_pass1a", "k_lb_pass2", "k_p1_reduce_lti", "k_lb_pass1b"};
   return (id >= 0 && id < K_COUNT) ? names[id] : "?";
 }
 
@@ -341,7 +341,7 @@ struct RunnerT : Runner {
   bool prepare(PlanState& p) override;
   bool prepare_lb(PlanState& p);
 
-  // one look-back solve: k_lb_pass1 + k_lb_pass2 (2 launches)
+  // one look-back solve: k_lb_pass1a + k_lb_pass1b + k_lb_pass2 (3 launches)
   void lb_rts(PlanState& p, const void* yv, void* xv, void* fm, void* fP) {
     if constexpr (IS_LTI) {
       const R* y = static_cast<const R*>(yv);
@@ -349,15 +349,19 @@ struct RunnerT : Runner {
       const unsigned ntiles = (unsigned)(lbg.batch * lbg.tpt);
       cudaStream_t s = p.stream;
       PM_LAUNCH(p, s, K_LB_P1,
-                (k_lb_pass1<R, N, NY, kNT, K, Src><<<ntiles, kNT + 32, 0, s>>>(fold, src, lbg, y, tab, lbtab, lbrun, lbw,
-                                                                             p.dflag, p.lb_stress)));
+                (k_lb_pass1a<R, N, NY, kNT, K, Src><<<ntiles, kNT, 0, s>>>(fold, lbg, y, tab, lbtab, lbrun, lbw)));
+      const unsigned n1b = (unsigned)((lb_ticket_count(ntiles, lbg.S1) + 3) / 4);
+      const unsigned n2 = (unsigned)lb_ticket_count(ntiles, lbg.S2);
+      PM_LAUNCH(p, s, K_LB_P1B,
+                (k_lb_pass1b<R, N, NY, kNT, K, Src><<<n1b, 128, 0, s>>>(src, lbg, y, tab, lbtab, lbrun, lbw, p.dflag,
+                                                                      p.lb_stress)));
       if (fm || fP)
         PM_LAUNCH(p, s, K_LB_P2,
-                  (k_lb_pass2<R, N, NY, kNT, K, Src, true><<<ntiles, kNT, 0, s>>>(
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, true><<<n2, kNT, 0, s>>>(
                       src, lbg, y, lbrun, lbw, x, static_cast<R*>(fm), static_cast<R*>(fP), p.dflag, p.lb_stress)));
       else
         PM_LAUNCH(p, s, K_LB_P2,
-                  (k_lb_pass2<R, N, NY, kNT, K, Src, false><<<ntiles, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, false><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr,
                                                                                  nullptr, p.dflag, p.lb_stress)));
     }
   }
@@ -1028,7 +1032,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
                  o_g1 = take(groups * N * sizeof(R)), o_rc = take(tiles * N * kNT * sizeof(R)),
                  o_ri = take(tiles * Aff<R, N>::SZ * kNT * sizeof(R)), o_a2 = take(tiles * N * sizeof(R)),
                  o_g2 = take(groups * N * sizeof(R)), o_p2 = take(tiles * N * sizeof(R)),
-                 o_sd = take((size_t)g.batch * N * sizeof(R));
+                 o_sd = take((size_t)g.batch * N * sizeof(R)), o_sr = take((size_t)g.batch * 2 * N * sizeof(R));
     const size_t f0 = off;
     const size_t o_f1 = take(tiles * 4), o_gf1 = take(groups * 4), o_gc1 = take(groups * 4), o_gc2 = take(groups * 4),
                  o_f2 = take(tiles * 4), o_ct = take(8);
@@ -1045,6 +1049,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     lbw.gagg2 = RP(o_g2);
     lbw.pub2 = RP(o_p2);
     lbw.seed = RP(o_sd);
+    lbw.seedrb = RP(o_sr);
     lbw.flag1 = UP(o_f1);
     lbw.gflag1 = UP(o_gf1);
     lbw.gcnt1 = UP(o_gc1);
@@ -1065,6 +1070,19 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       }
     }
     lbw.Qb = lbprod + npa + npb + nqa;
+    // ticket strides = resident CTAs (warps) of the look-back kernels on this device
+    {
+      int dev = 0, nsm = 148, b1 = 0, b2 = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_lb_pass1b<R, N, NY, kNT, K, Src>, 128, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_lb_pass2<R, N, NY, kNT, K, Src, false>, kNT, 0);
+      const char* sd = getenv("PMAP_LB_STRIDE");  // "0": plain (unstrided) ticket order (A/B checks)
+      const bool plain = sd && sd[0] == '0';
+      g.S1 = plain ? (int64_t)1 << 40 : std::max<int64_t>(1, (int64_t)b1 * 4 * nsm);
+      g.S2 = plain ? (int64_t)1 << 40 : std::max<int64_t>(1, (int64_t)b2 * nsm);
+      if (plain) g.S1 = g.S2 = std::max<int64_t>(1, g.batch * g.tpt);
+    }
     lbg = g;
     p.lb_bytes += off;
     use_lb = true;

@@ -1,6 +1,6 @@
 """GPU parity of the single-pass decoupled look-back path (pmap_lb.cuh).
 
-LTI single-GPU solves run k_lb_pass1 + k_lb_pass2 (two launches).  These tests cover
+LTI single-GPU solves run k_lb_pass1a + k_lb_pass1b + k_lb_pass2 (three launches).  These tests cover
 it against the CPU oracle (<= 1e-9 relative in fp64, G23, plus the per-component
 scaled error) and against the multi-kernel scan hierarchy (PMAP_NO_LB=1, <= 1e-12),
 at sizes that span one tile, several tiles, several look-back groups (32 tiles) and
@@ -19,6 +19,7 @@ from test_parity_gpu import TOL32, TOL64, gpu_plan, ora_model, random_lti, rel, 
 pytestmark = pytest.mark.gpu
 
 TILE = 64 * 32  # nodes per tile at K = 32 (group = 32 tiles = 65536 nodes)
+LB_LAUNCHES = 3  # k_lb_pass1a, k_lb_pass1b, k_lb_pass2
 
 
 def _wiener_offsets():
@@ -38,7 +39,7 @@ def test_lb_matches_oracle(torch_cuda, T):
     x = plan.solve_linear(to_dev(torch, y[None]))
     plan.sync()
     if T >= TILE:  # dt <= 2.4e-3: the forward-recovery bound admits the look-back path (R-FWD)
-        assert plan.launches == 2  # k_lb_pass1 + k_lb_pass2
+        assert plan.launches == LB_LAUNCHES
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     xg = x[0].cpu().numpy()
     assert rel(xg, xo) < TOL64
@@ -58,7 +59,7 @@ def test_lb_batch_and_hierarchy(torch_cuda, T, B, monkeypatch):
     monkeypatch.setenv("PMAP_NO_LB", "1")
     plan_h = gpu_plan(spec, T, batch=B)
     x_h = plan_h.solve_linear(yd).cpu().numpy()
-    assert plan_h.launches > 2
+    assert plan_h.launches > LB_LAUNCHES
     xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=0)
     for b in range(B):
         assert rel(x_lb[b], x_h[b]) < 1e-12
@@ -98,7 +99,7 @@ def test_lb_filter_outputs(torch_cuda):
     P = torch.empty((1, T + 1, nx * (nx + 1) // 2), dtype=torch.float64, device="cuda")
     x = plan.solve_linear(to_dev(torch, y[None]), filt_m=m, filt_P=P)
     plan.sync()
-    assert plan.launches == 2
+    assert plan.launches == LB_LAUNCHES
     iu = np.triu_indices(nx)
     assert rel(x[0].cpu().numpy(), xo) < TOL64
     assert rel(m[0].cpu().numpy(), fm) < TOL64
@@ -131,6 +132,6 @@ def test_lb_fp32(torch_cuda):
     plan = gpu_plan(spec, T, dtype="f32")
     x = plan.solve_linear(to_dev(torch, y[None], dtype=torch.float32))
     plan.sync()
-    assert plan.launches == 2
+    assert plan.launches == LB_LAUNCHES
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     assert rel(x[0].cpu().numpy(), xo) < TOL32

@@ -263,11 +263,19 @@ def test_structural_zero_masks_bit_identical(torch_cuda, T, monkeypatch):
     spec = wl.wiener_velocity()
     _, y = wl.simulate_linear(spec, T, seed=77)
     yd = to_dev(torch, y[None])
+    x_lb_mask = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    monkeypatch.setenv("PMAP_NO_LB", "1")  # the scan hierarchy is deterministic: bit for bit
     x_mask = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
     monkeypatch.setenv("PMAP_NO_MASK", "1")
     x_dense = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
     assert np.array_equal(x_mask, x_dense)
     assert rel(x_mask[0], oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)) < TOL64
+    # the look-back path (masked node step and forward recovery) agrees to rounding: its
+    # look-back depth, hence the association of a few sums, varies run to run
+    monkeypatch.delenv("PMAP_NO_LB")
+    x_lb_dense = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    assert rel(x_lb_mask[0], x_lb_dense[0]) < 1e-13
+    assert rel(x_lb_mask[0], x_mask[0]) < 1e-12
 
 
 @pytest.mark.parametrize("method", ["rts", "tf", "shard_nccl"])
@@ -312,7 +320,10 @@ def _graph_replay_body(torch, pm, spec, T, y, yd, comm, method):
         plan.sync()
         outs.append(x.cpu().numpy().copy())
     for o in outs[1:]:
-        assert np.array_equal(o, outs[0])
+        if method == "rts":  # look-back path: reproducible to rounding (look-back depth varies)
+            assert rel(o[0], outs[0][0]) < 1e-13
+        else:
+            assert np.array_equal(o, outs[0])
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     assert rel(outs[-1][0], xo) < TOL64
 

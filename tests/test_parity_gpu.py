@@ -258,11 +258,15 @@ def test_fp32_variant(torch_cuda, cfg):
     assert rel(x[0].cpu().numpy(), xo) < TOL32
 
 
-def test_host_buffers_and_determinism(torch_cuda):
-    """Host (NumPy) buffers go through the C ABI's staging path; results are bitwise
-    reproducible run to run (fixed scan tree)."""
+@pytest.mark.parametrize("path", ["lookback", "hierarchy"])
+def test_host_buffers_and_determinism(torch_cuda, path, monkeypatch):
+    """Host (NumPy) buffers go through the C ABI's staging path.  The scan hierarchy
+    (fixed scan tree) is bitwise reproducible run to run; the look-back path to rounding
+    (its look-back depth, hence the association of a few sums, depends on timing)."""
     import paper_2512_13319_b200 as pm
     torch = torch_cuda
+    if path == "hierarchy":
+        monkeypatch.setenv("PMAP_NO_LB", "1")
     spec = wl.wiener_velocity()
     T = 10_000
     _, y = wl.simulate_linear(spec, T, seed=5)
@@ -271,7 +275,10 @@ def test_host_buffers_and_determinism(torch_cuda):
     pm.map_solve_linear(plan.handle, np.ascontiguousarray(y[None]), xh)
     xd = plan.solve_linear(to_dev(torch, y[None])).cpu().numpy()
     xd2 = plan.solve_linear(to_dev(torch, y[None])).cpu().numpy()
-    assert np.array_equal(xh, xd) and np.array_equal(xd, xd2)
+    if path == "hierarchy":
+        assert np.array_equal(xh, xd) and np.array_equal(xd, xd2)
+    else:
+        assert rel(xh[0], xd[0]) < 1e-13 and rel(xd[0], xd2[0]) < 1e-13
     assert rel(xh[0], oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)) < TOL64
 
 

@@ -15,8 +15,8 @@ os.environ["PMAP_LB_TIMING"] = "1"
 
 # stamp slots in the order they are taken (pmap_lb.cuh LB_STAMP)
 PHASES = {
-    0: [(0, 1, "ticket, y staged"), (1, 2, "fold + tile reduce"), (2, 3, "publish g, group agg"),
-        (3, 6, "look-back polls"), (6, 4, "look-back sums"), (4, 5, "join run threads")],
+    0: [(0, 1, "1a: y staged"), (1, 2, "1a: fold + tile reduce"), (2, 3, "1a: scan + run maps"),
+        (4, 5, "1b: look-back"), (5, 6, "1b: run values, offsets")],
     1: [(0, 1, "look-back"), (1, 2, "y staged"), (2, 3, "node loop")],
 }
 
@@ -49,10 +49,13 @@ def main():
             if len(d):
                 print(f"  {nm:22s} median {np.median(d):7.2f} us  p90 {np.percentile(d, 90):7.2f}  max {d.max():7.2f}"
                       f"  (n={ok.sum()})")
-        end = tt[:, last]
-        ok = end > 0
-        life = (end[ok] - tt[ok, 0]) / 1e3
-        print(f"  tile lifetime median {np.median(life):.2f} us, p90 {np.percentile(life, 90):.2f} us")
+        for s0, s1 in ((0, 3), (4, 6)) if ps == 0 else ((0, 3),):
+            ok = (tt[:, s0] > 0) & (tt[:, s1] > 0)
+            if ok.any():
+                life = (tt[ok, s1] - tt[ok, s0]) / 1e3
+                span = (tt[ok, s1].max() - tt[ok, s0].min()) / 1e3
+                print(f"  stamps {s0}..{s1}: lifetime median {np.median(life):.2f} us, p90 {np.percentile(life, 90):.2f};"
+                      f" span {span:.1f} us")
 
 
 if __name__ == "__main__":
