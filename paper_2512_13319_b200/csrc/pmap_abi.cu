@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -583,7 +584,20 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   if (!rn) return MAP_E_UNSUPPORTED;
   p->runner.reset(rn);
   p->elem_real = rn->sizeof_real();
+  const bool ptime = getenv("PMAP_PLAN_TIMING") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = tnow();
+  auto tlog = [&](const char* what) {
+    if (ptime) {
+      cudaDeviceSynchronize();
+      fprintf(stderr, "[pmap plan] %-28s %8.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(tnow() - t0).count());
+      t0 = tnow();
+    }
+  };
+  tlog("model preprocessing");
   rn->set_attrs();
+  tlog("set_attrs");
   if (!rn->prepare(*p)) {
     cudaGetLastError();
     p->err = "plan preparation (LTI tables) failed";
@@ -591,6 +605,7 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   }
   // workspace
   p->ws_tf = (p->kind != Kind::NL) && d.world == 1;
+  tlog("prepare (LTI + look-back tables)");
   p->ws_bytes = rn->ws_bytes(g, p->ws_tf);
   if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) {
     cudaGetLastError();
@@ -629,6 +644,7 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     p->err = cudaGetErrorString(e);
     return MAP_E_CUDA;
   }
+  tlog("workspace, streams, events");
   *out = p.release();
   return MAP_OK;
 }

@@ -301,6 +301,48 @@ __global__ void k_lb_setup_tiles(const LtiTables<R, N, NT, K>* __restrict__ tab,
     for (int c = 0; c < N; ++c) phit[(j * N + i) * N + c] = P[i][c];
 }
 
+// One thread per tile: the look-back window products (fp64 accumulation)
+//   Pa[j][l] = Gt_{j-1} Gt_{j-2} ... Gt_{j-l},   Qa[j][l] = Phi_{j+1} ... Phi_{j+l},
+// l = 0..kLbGroup (entries reaching past the trajectory stay as the caller zeroed them).
+template <typename R, int N>
+__global__ void k_lb_setup_window(const LbTileTab<R, N>* __restrict__ lt, const R* __restrict__ phit, int64_t tpt,
+                                  R* __restrict__ Pa, R* __restrict__ Qa) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= tpt) return;
+  constexpr int W1 = kLbGroup + 1;
+  for (int which = 0; which < 2; ++which) {
+    double P[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) P[i][c] = (i == c) ? 1.0 : 0.0;
+    R* out = (which == 0 ? Pa : Qa) + j * W1 * N * N;
+    for (int l = 0; l < W1; ++l) {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) out[(l * N + i) * N + c] = (R)P[i][c];
+      const int64_t k = which == 0 ? j - 1 - l : j + 1 + l;
+      if (k < 0 || k >= tpt) break;
+      double T[N][N];
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          double a = 0.0;
+#pragma unroll
+          for (int m = 0; m < N; ++m)
+            a = fma(P[i][m], (double)(which == 0 ? lt[k].Gt[m][c] : phit[(k * N + m) * N + c]), a);
+          T[i][c] = a;
+        }
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) P[i][c] = T[i][c];
+    }
+  }
+}
+
 // Workspace pointers of the look-back path.
 template <typename R>
 struct LbWs {

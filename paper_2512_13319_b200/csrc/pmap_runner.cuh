@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -799,6 +800,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare(PlanState& p) {
         return true;
       };
       if (!pull(fold, lnode, tab) || !pull(fold_m, lnode_m, tab_m)) return false;
+      if (getenv("PMAP_PLAN_TIMING")) fprintf(stderr, "[pmap plan]   LTI setup kernels + table pulls done\n");
       if (!prepare_lb(p)) {
         cudaGetLastError();
         use_lb = false;
@@ -820,6 +822,17 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     return false;
   } else {
     if (p.d.world != 1) return false;
+    const bool ptime = getenv("PMAP_PLAN_TIMING") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = tnow();
+    auto tlog = [&](const char* what) {
+      if (ptime) {
+        cudaDeviceSynchronize();
+        fprintf(stderr, "[pmap plan]   lb: %-22s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(tnow() - t0).count());
+        t0 = tnow();
+      }
+    };
     constexpr int NS = Dim<N>::NS;
     const int64_t L = (int64_t)kNT * K;
     LbGeom g{};
@@ -928,25 +941,21 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       if (!h_is_finite(S, N * N)) return false;
     }
     lb_amp = amp;
+    tlog("S chain (host)");
     const char* ma = getenv("PMAP_LB_MAX_AMP");
     const double max_amp = ma ? atof(ma) : 1e6;
     if (!(amp <= max_amp)) return false;  // forward recovery would amplify rounding: keep the scan hierarchy
-    // look-back window products: Pa[j][l] = Gt_{j-1} ... Gt_{j-l} (l = 0..kLbGroup), the
-    // group maps GtG_G = Pa[32G + 32][32], and Pb[G][l] = GtG_{G-1} ... GtG_{G-l} (l = 0..G)
+    // group maps GtG_G = Gt_{32G+31} ... Gt_{32G} (host) and Pb[G][l] = GtG_{G-1} ... GtG_{G-l}
+    // (l = 0..G); the per-tile window products Pa, Qa are built on the device below
     constexpr int W1 = kLbGroup + 1;
     const size_t npa = (size_t)g.tpt * W1 * N * N, npb = (size_t)(g.gpt * (g.gpt + 1) / 2) * N * N;
-    std::vector<double> pa(npa, 0.0), pb(npb, 0.0), gtg((size_t)g.gpt * N * N, 0.0);
-    for (int64_t j = 0; j < g.tpt; ++j) {
+    std::vector<double> pb(npb, 0.0), gtg((size_t)g.gpt * N * N, 0.0);
+    for (int64_t G = 0; G + 1 < g.gpt; ++G) {  // full groups (every group before the last)
       double P[N * N];
       for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
-      for (int l = 0; l < W1; ++l) {
-        memcpy(&pa[((size_t)j * W1 + l) * N * N], P, sizeof P);
-        if (j - 1 - l < 0) break;
-        mm(P, &gt[(size_t)(j - 1 - l) * N * N], P);
-      }
+      for (int64_t k = G * kLbGroup; k < (G + 1) * kLbGroup; ++k) mm(&gt[(size_t)k * N * N], P, P);
+      memcpy(&gtg[(size_t)G * N * N], P, sizeof P);
     }
-    for (int64_t G = 0; G + 1 < g.gpt; ++G)  // full groups (every group before the last)
-      memcpy(&gtg[(size_t)G * N * N], &pa[((size_t)(G + 1) * kLbGroup * W1 + kLbGroup) * N * N], sizeof(double) * N * N);
     for (int64_t G = 0; G < g.gpt; ++G) {
       double P[N * N];
       for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
@@ -956,6 +965,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
         if (l < G) mm(P, &gtg[(size_t)(G - 1 - l) * N * N], P);
       }
     }
+    tlog("Pa, Pb (host)");
     if (cudaMalloc(&lbtab, sizeof(LbTileTab<R, N>) * g.tpt) != cudaSuccess) return false;
     cudaMemcpy(lbtab, ht.data(), sizeof(LbTileTab<R, N>) * g.tpt, cudaMemcpyHostToDevice);
     {  // per-run tables, one device thread per (tile, run)
@@ -972,6 +982,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       if (e != cudaSuccess || !okh) return false;
       p.lb_bytes += rb;
     }
+    tlog("run tables (device)");
     // QB per run and the pass-2 tile matrices Phi_tile(j) (device, one thread per tile),
     // then the window products Qa[j][l] = Phi_{j+1} ... Phi_{j+l} (l = 0..kLbGroup), the
     // group matrices PhiG_G = Qa[32G - 1][group size] (G >= 1, the last group included)
@@ -988,19 +999,13 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       for (size_t i = 0; i < hphi.size(); ++i) phit[i] = (double)hphi[i];
     }
     const size_t nqa = (size_t)g.tpt * W1 * N * N, nqb = (size_t)(g.gpt * (g.gpt + 1) / 2) * N * N;
-    std::vector<double> qa(nqa, 0.0), qb(nqb, 0.0), phig((size_t)g.gpt * N * N, 0.0);
-    for (int64_t j = 0; j < g.tpt; ++j) {
+    std::vector<double> qb(nqb, 0.0), phig((size_t)g.gpt * N * N, 0.0);
+    for (int64_t G = 1; G < g.gpt; ++G) {  // PhiG_G = Phi_{32G} ... Phi_{32G + n_G - 1} (the last group included)
+      const int64_t cntG = std::min<int64_t>(kLbGroup, g.tpt - G * kLbGroup);
       double P[N * N];
       for (int i = 0; i < N * N; ++i) P[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
-      for (int l = 0; l < W1; ++l) {
-        memcpy(&qa[((size_t)j * W1 + l) * N * N], P, sizeof P);
-        if (j + 1 + l >= g.tpt) break;
-        mm(P, &phit[(size_t)(j + 1 + l) * N * N], P);
-      }
-    }
-    for (int64_t G = 1; G < g.gpt; ++G) {
-      const int64_t cntG = std::min<int64_t>(kLbGroup, g.tpt - G * kLbGroup);
-      memcpy(&phig[(size_t)G * N * N], &qa[((size_t)(G * kLbGroup - 1) * W1 + cntG) * N * N], sizeof(double) * N * N);
+      for (int64_t k = G * kLbGroup; k < G * kLbGroup + cntG; ++k) mm(P, &phit[(size_t)k * N * N], P);
+      memcpy(&phig[(size_t)G * N * N], P, sizeof P);
     }
     for (int64_t G = 0; G < g.gpt; ++G) {
       double P[N * N];
@@ -1011,15 +1016,27 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
         if (G + 1 + l < g.gpt) mm(P, &phig[(size_t)(G + 1 + l) * N * N], P);
       }
     }
+    tlog("Phi_tile, Pb, Qb (host)");
     if (cudaMalloc(&lbprod, sizeof(R) * (npa + npb + nqa + nqb)) != cudaSuccess) return false;
     {
-      std::vector<R> prod(npa + npb + nqa + nqb);
-      size_t o = 0;
-      for (const std::vector<double>* v : {&pa, &pb, &qa, &qb})
-        for (double d : *v) prod[o++] = (R)d;
-      cudaMemcpy(lbprod, prod.data(), sizeof(R) * prod.size(), cudaMemcpyHostToDevice);
-      p.lb_bytes += sizeof(R) * prod.size();
+      std::vector<R> small(npb + nqb);
+      for (size_t i = 0; i < npb; ++i) small[i] = (R)pb[i];
+      for (size_t i = 0; i < nqb; ++i) small[npb + i] = (R)qb[i];
+      cudaMemset(lbprod, 0, sizeof(R) * (npa + nqa));
+      cudaMemcpy(lbprod + npa, small.data(), sizeof(R) * npb, cudaMemcpyHostToDevice);
+      cudaMemcpy(lbprod + npa + npb + nqa, small.data() + npb, sizeof(R) * nqb, cudaMemcpyHostToDevice);
+      R* dphi = nullptr;  // Phi_tile again (device) for the window products
+      std::vector<R> hphi(phit.size());
+      for (size_t i = 0; i < phit.size(); ++i) hphi[i] = (R)phit[i];
+      if (cudaMalloc(&dphi, sizeof(R) * hphi.size()) != cudaSuccess) return false;
+      cudaMemcpy(dphi, hphi.data(), sizeof(R) * hphi.size(), cudaMemcpyHostToDevice);
+      k_lb_setup_window<R, N><<<(unsigned)((g.tpt + 127) / 128), 128>>>(lbtab, dphi, g.tpt, lbprod, lbprod + npa + npb);
+      const cudaError_t e = cudaDeviceSynchronize();
+      cudaFree(dphi);
+      if (e != cudaSuccess) return false;
+      p.lb_bytes += sizeof(R) * (npa + npb + nqa + nqb);
     }
+    tlog("upload products");
     // workspace
     const size_t tiles = (size_t)(g.batch * g.tpt), groups = (size_t)(g.batch * g.gpt);
     size_t off = 0;
@@ -1085,6 +1102,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     }
     lbg = g;
     p.lb_bytes += off;
+    tlog("workspace");
     use_lb = true;
     return true;
   }

@@ -180,7 +180,9 @@ def test_c3_full_size(torch_cuda):
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     plan = gpu_plan(spec, T)
     x = plan.solve_linear(to_dev(torch, y[None]))
-    assert rel(x[0].cpu().numpy(), xo) < TOL64
+    xg = x[0].cpu().numpy()
+    assert rel(xg, xo) < TOL64
+    assert rel_comp(xg, xo) < 1e-8  # each state component on its own scale (G23)
 
 
 def test_c5_two_filter_batch(torch_cuda):
@@ -205,6 +207,7 @@ def test_nonlinear_ct(torch_cuda, T):
     x, run = plan.solve_nonlinear(to_dev(torch, y[None]), passes=10)
     assert run == 10
     assert rel(x[0].cpu().numpy(), xo) < TOL64
+    assert rel_comp(x[0].cpu().numpy(), xo) < 1e-8  # the turn rate on its own scale (G23)
     # per-iterate parity: 3 passes
     xo3, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=3)
     x3, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=3)
@@ -494,3 +497,43 @@ def test_lowrank_node_update(torch_cuda, lowrank, monkeypatch):
     xt = plan.two_filter(to_dev(torch, y[None]))
     assert rel(x[0].cpu().numpy(), xo) < TOL64
     assert rel(xt[0].cpu().numpy(), xo) < TOL64
+
+
+def test_ct_bearing_crosses_pi(torch_cuda):
+    """Coordinated turn whose target passes the negative x-axis: the bearing h_2 =
+    atan2(zeta, xi) wraps from +pi to -pi mid-trajectory.  The residual wrap (R-WRAP,
+    G13) must make GPU and oracle agree per iterate (normwise and per component)."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    s = wl.coordinated_turn()
+    s.m0 = np.array([-5.0, 0.8, 0.0, -1.0, 0.1])  # heading down across the negative x-axis
+    s.P0 = np.diag([0.01, 0.01, 0.01, 0.01, 0.01])
+    T = 20_000
+    xs, y = wl.simulate_nonlinear(s, T, seed=31)
+    bearing = np.arctan2(xs[:, 1], xs[:, 0])
+    assert np.any(np.abs(np.diff(bearing)) > np.pi)  # the true bearing wraps
+    assert np.any(np.abs(np.diff(y[:, 1])) > np.pi)  # and so do the measurements
+    plan = pm.Plan(T=T, t0=s.t0, tf=s.tf, L=s.L, W=s.W, R=s.R, m0=s.m0, P0=s.P0, nl_kind=1)
+    for passes in (1, 4, 10):
+        xo, _ = oracle.ieks(1, None, s.L, s.W, s.R, s.m0, s.P0, y, T, s.t0, s.tf, passes=passes)
+        x, _ = plan.solve_nonlinear(to_dev(torch, y[None]), passes=passes)
+        xg = x[0].cpu().numpy()
+        assert rel(xg, xo) < TOL64
+        assert rel_comp(xg, xo) < 1e-8
+    # the MAP track is continuous through the wrap (no jump from a 2 pi bearing residual):
+    # consecutive positions differ by about speed x dt ~ 2.5e-4
+    assert np.abs(np.diff(xg[:, :2], axis=0)).max() < 0.01
+
+
+def test_fp32_c3_full_size(torch_cuda):
+    """fp32 variant at BASELINE config 3 (T = 1e7, dt = 5e-7): relative error against the
+    fp64 oracle within the north_star's 1e-3 (measured value in DESIGN.md)."""
+    torch = torch_cuda
+    spec, y, T, _ = wl.make_workload("C3")
+    plan = gpu_plan(spec, T, dtype="f32")
+    x = plan.solve_linear(to_dev(torch, y[None], dtype=torch.float32))
+    plan.sync()
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    e = rel(x[0].cpu().numpy(), xo)
+    print(f"fp32 C3 relative error {e:.3e}")
+    assert e < TOL32

@@ -1,5 +1,5 @@
-# Quick GPU check: all GPU tests, C3/C2/C5 bench lines without baselines, the 8-way shard probe.
+# Quick GPU check: all GPU tests, the default bench line and the other configs (no baselines).
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/p33_all.log 2>&1; echo "rc=$?" >> gpurun_out/p33_all.log
-for c in C3 C2 C5; do timeout 600 python bench.py --config $c --steps 100 --no-cpu-baseline --no-e2e --no-seq > gpurun_out/b33_$c.log 2>&1; done
-for G in 8; do timeout 300 python tools/shard_probe.py $G >> gpurun_out/p33_probe.log 2>&1; done
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/chk_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/chk_pytest.log
+timeout 600 python bench.py > gpurun_out/chk_bench.log 2>&1; echo "rc=$?" >> gpurun_out/chk_bench.log
+for c in C1 C2 C4 C5 C2E; do timeout 600 python bench.py --config $c --steps 50 --no-cpu-baseline --no-e2e --no-seq > gpurun_out/chk_bench_$c.log 2>&1; done
