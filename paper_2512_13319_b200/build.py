@@ -27,6 +27,7 @@ EULER_SHAPES = [(1, 1), (4, 2)]  # OU (C1) and Wiener velocity
 EULER_NSUB = 10                  # substeps per block
 
 RUN_LENGTHS = (32, 8)  # nodes per run (tile = 64 runs): large / small problems
+NL_TINY_K = 4          # nonlinear plans on modest grids (general combines: shorter chains)
 
 
 def units(f64_only: bool = False):
@@ -44,6 +45,10 @@ def units(f64_only: bool = False):
             for nx, ny in EULER_SHAPES:  # paper-faithful Euler blocks
                 out.append((f"inst_{tag}_K{K}_eu{nx}{ny}", base + [f"-DPM_NX={nx}", f"-DPM_NY={ny}", "-DPM_KIND=4",
                                                                    f"-DPM_NSUB={EULER_NSUB}"], "inst.cu"))
+        # nonlinear models also get the tiny run length (pmap_abi.cu choose_run_length)
+        tb = ["-DPM_R=" + R, f"-DPM_K={NL_TINY_K}"]
+        out.append((f"inst_{tag}_K{NL_TINY_K}_ct", tb + ["-DPM_NX=5", "-DPM_NY=2", "-DPM_KIND=2"], "inst.cu"))
+        out.append((f"inst_{tag}_K{NL_TINY_K}_vdp", tb + ["-DPM_NX=2", "-DPM_NY=1", "-DPM_KIND=3"], "inst.cu"))
     out.append(("pmap_abi", [], "pmap_abi.cu"))
     return out
 

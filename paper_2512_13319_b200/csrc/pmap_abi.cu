@@ -205,21 +205,28 @@ template <typename R>
 static Runner* dispatch_nl(int kr, int kind, double dt, double mu, double dv, const double* C, const double* Ri,
                            const double* P0i, const double* P0im0) {
   if (kind == MAP_NL_COORD_TURN)
-    return kr == kKBig ? make_nl<R, 5, 2, 1, kKBig>(dt, mu, dv, C, Ri, P0i, P0im0)
-                       : make_nl<R, 5, 2, 1, kKSmall>(dt, mu, dv, C, Ri, P0i, P0im0);
+    return kr == kKBig     ? make_nl<R, 5, 2, 1, kKBig>(dt, mu, dv, C, Ri, P0i, P0im0)
+           : kr == kKTiny ? make_nl<R, 5, 2, 1, kKTiny>(dt, mu, dv, C, Ri, P0i, P0im0)
+                          : make_nl<R, 5, 2, 1, kKSmall>(dt, mu, dv, C, Ri, P0i, P0im0);
   if (kind == MAP_NL_VAN_DER_POL)
-    return kr == kKBig ? make_nl<R, 2, 1, 2, kKBig>(dt, mu, dv, C, Ri, P0i, P0im0)
-                       : make_nl<R, 2, 1, 2, kKSmall>(dt, mu, dv, C, Ri, P0i, P0im0);
+    return kr == kKBig     ? make_nl<R, 2, 1, 2, kKBig>(dt, mu, dv, C, Ri, P0i, P0im0)
+           : kr == kKTiny ? make_nl<R, 2, 1, 2, kKTiny>(dt, mu, dv, C, Ri, P0i, P0im0)
+                          : make_nl<R, 2, 1, 2, kKSmall>(dt, mu, dv, C, Ri, P0i, P0im0);
   return nullptr;
 }
 
 // Run length: 2048-node tiles when they give >= 4 tiles per SM-slot-row of the GPU
 // (148 SMs), else 512-node tiles so small problems still fill the machine.
-static int choose_run_length(int64_t Nn, int64_t batch) {
+static int choose_run_length(int64_t Nn, int64_t batch, bool nonlinear) {
   const char* e = getenv("PMAP_K");
   if (e && atoi(e) == kKSmall) return kKSmall;
   if (e && atoi(e) == kKBig) return kKBig;
+  if (e && atoi(e) == kKTiny && nonlinear) return kKTiny;
   const int64_t tiles_big = batch * ((Nn + (int64_t)kNT * kKBig - 1) / ((int64_t)kNT * kKBig));
+  if (nonlinear) {  // general combines: the chain length decides; tiny runs until the GPU is full
+    const int64_t tiles_tiny = batch * ((Nn + (int64_t)kNT * kKTiny - 1) / ((int64_t)kNT * kKTiny));
+    return tiles_tiny <= 16 * 148 ? kKTiny : (tiles_big >= 4 * 148 ? kKBig : kKSmall);
+  }
   return tiles_big >= 4 * 148 ? kKBig : kKSmall;
 }
 
@@ -385,7 +392,7 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
   g.Nn = a1 - a0;
   g.node0 = a0;
   g.batch = d.batch;
-  const int kr = choose_run_length(g.Nn, g.batch);
+  const int kr = choose_run_length(g.Nn, g.batch, nl != nullptr);
   const int64_t L = (int64_t)kNT * kr;
   g.tpt = (g.Nn + L - 1) / L;
   g.gpt = (g.tpt + NT2 - 1) / NT2;

@@ -184,10 +184,16 @@ __global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src sr
     const int64_t l = REV ? g.Nn - 1 - lr : lr;  // REV: suffix scan (two-filter pass B)
     E e;
     src.node(g.node0 + l, yb + l * NY, Src::NEEDS_XBAR ? xb + l * N : nullptr, e);
-    if (m == 0)
+    if (m == 0) {
       acc = e;
-    else
+    } else if constexpr (N >= 5) {
+      // acc = E_l (x) acc (R-FLIP) with the right operand read in place from this thread's
+      // shared-memory slot: two register-resident nx = 5 elements spill at 255 registers
+      store(acc, sh + r, NT);
+      combine_g(e, ElemRef<R, N>{sh + r, NT}, acc, ok);
+    } else {
       combine(e, acc, acc, ok);  // acc = E_l (x) acc   (R-FLIP)
+    }
     if (has_node0 && m >= 1) {
       if (m == 1)
         acc_x0 = e;
@@ -198,15 +204,13 @@ __global__ void __launch_bounds__(NT) k_p1_reduce(const __grid_constant__ Src sr
   // the run's own aggregate (pass 2 derives its transition from it, R-RUNAGG)
   store(has_node0 ? acc_x0 : acc, run_incl + (g.batch * g.tpt + tile) * (int64_t)E::SZ * NT + r, NT);
   // inclusive Kogge-Stone scan over the runs of the tile: In_r = In_r (x) In_{r-d}
+  // (the partner read in place from its shared-memory slot, combine_g)
+  __syncthreads();
 #pragma unroll 1
   for (int d = 1; d < NT; d <<= 1) {
     store(acc, sh + r, NT);
     __syncthreads();
-    if (r >= d) {
-      E p;
-      load(p, sh + r - d, NT);
-      combine(acc, p, acc, ok);
-    }
+    if (r >= d) combine_g(acc, ElemRef<R, N>{sh + r - d, NT}, acc, ok);
     __syncthreads();
   }
   store(acc, run_incl + tile * (int64_t)E::SZ * NT + r, NT);
@@ -239,11 +243,7 @@ __global__ void __launch_bounds__(NT2) k_p1_tiles(const Geom g, const R* __restr
   for (int d = 1; d < cnt; d <<= 1) {
     store(acc, sh + t, NT2);
     __syncthreads();
-    if (t >= d) {
-      E p;
-      load(p, sh + t - d, NT2);
-      combine(acc, p, acc, ok);
-    }
+    if (t >= d) combine_g(acc, ElemRef<R, N>{sh + t - d, NT2}, acc, ok);  // partner read in place
     __syncthreads();
   }
   if (valid) store(acc, tile_incl + (b * g.tpt + jt) * E::SZ, 1);
@@ -286,11 +286,7 @@ __global__ void __launch_bounds__(NT3) k_p1_groups(const Geom g, const R* __rest
   for (int d = 1; d < nact; d <<= 1) {
     store(acc, sh + t, NT3);
     __syncthreads();
-    if (t >= d) {
-      E p;
-      load(p, sh + t - d, NT3);
-      combine(acc, p, acc, ok);
-    }
+    if (t >= d) combine_g(acc, ElemRef<R, N>{sh + t - d, NT3}, acc, ok);  // partner read in place
     __syncthreads();
   }
   store(acc, sh + t, NT3);
@@ -721,7 +717,7 @@ __global__ void __launch_bounds__(NT) k_p2_down(const __grid_constant__ Src src,
                                                 R* __restrict__ x_out, unsigned long long* flag) {
   using V = VF<R, N>;
   using A = Aff<R, N>;
-  constexpr int KC = 8;  // nodes per staged chunk
+  constexpr int KC = K < 8 ? K : 8;  // nodes per staged chunk
   static_assert(K % KC == 0, "chunking");
   __shared__ R xs[NT][KC * N + 1];
   const int64_t tile = blockIdx.x;

@@ -33,6 +33,9 @@ constexpr int kNT = 64;  // runs (threads) per tile
 // large problems, 8 (512-node tiles) when that leaves too few tiles to fill the GPU
 constexpr int kKBig = 32;
 constexpr int kKSmall = 8;
+// nonlinear plans: the general pass-1 reduce runs a serial chain of K general combines
+// per thread plus the in-tile scan, so short runs (more threads, shorter chains) pay
+constexpr int kKTiny = 4;
 // Structural-zero masks compiled in (R-MASK): the Wiener-velocity model of P:519-548,
 // A = I - dt F with F = [[0, I], [0, 0]] (bits (i, j) -> 4 i + j) and U = sqrt(dt) L chol(W)
 // with L = [0; I] (bits (i, a) -> 2 i + a).  Any (nx, ny, nw) = (4, 2, 2) model whose

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(NT) k_tf_down(const __grid_constant__ Mirror<S
   load(cur, sh, 1);
   run_carry<R, N, NT>(run_incl, g, tile, r, sf && j >= j_lo && j < j_hi, sf, uwc, ux, cur, ok);
   // x is staged in shared memory in chunks of KC nodes and stored as contiguous segments
-  constexpr int KC = 8;
+  constexpr int KC = K < 8 ? K : 8;
   static_assert(K % KC == 0, "chunking");
   __shared__ R xs[NT][KC * N + 1];
 #pragma unroll 1
