@@ -215,12 +215,12 @@ def build_inputs(config: str, rank: int, world: int):
     return spec, np.ascontiguousarray(y[:, a0:a1]), T, B
 
 
-def make_plan(pm, spec, T, B, rank, world, comm, substeps=1):
+def make_plan(pm, spec, T, B, rank, world, comm, substeps=1, mixed=False):
     import workloads as wl
     if isinstance(spec, wl.LinearSpec):
         return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H,
                        r=spec.r, R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, rank=rank, world=world,
-                       nccl_comm=comm, substeps=substeps)
+                       nccl_comm=comm, substeps=substeps, mixed=mixed)
     return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, L=spec.L, W=spec.W, R=spec.R, m0=spec.m0, P0=spec.P0,
                    nl_kind=spec.kind, params=spec.params, batch=B, rank=rank, world=world, nccl_comm=comm)
 
@@ -393,6 +393,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-seq", action="store_true", help="skip the sequential on-device baseline (SURVEY f1)")
+    ap.add_argument("--mixed", action="store_true",
+                    help="MAP_FLAG_MIXED: fp32 node recursion in pass 2 from fp64 carries (SURVEY f4; not the headline)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -422,7 +424,7 @@ def main():
     spec, y_host, T, B = build_inputs(args.config, rank, world)
     torch.cuda.synchronize()
     tp = time.perf_counter()
-    plan = make_plan(pm, spec, T, B, rank, world, comm, substeps)
+    plan = make_plan(pm, spec, T, B, rank, world, comm, substeps, mixed=args.mixed)
     plan_ms = (time.perf_counter() - tp) * 1e3  # map_plan: model preprocessing, LTI / look-back tables, workspace
     solve = solve_fn(plan, args.config)
     dev = torch.device("cuda", local)
@@ -578,7 +580,8 @@ def main():
     out = {
         "metric": "smoothed time steps/s (fp64 parallel MAP scan)",
         "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 (pass-2 node recursion f32, MAP_FLAG_MIXED)" if args.mixed else "f64",
         "data": "synthetic (seeded Euler-Maruyama simulation of the paper's SDE, NumPy PCG64 seed 0)",
         "config": {"workload": workload_name(args.config, T, B), "T": T, "batch": B, "nx": plan.nx, "ny": plan.ny,
                    "parallelism": f"time-shard x{world}" if world > 1 else "single GPU",

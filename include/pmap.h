@@ -76,6 +76,14 @@ typedef enum {
 
 typedef struct map_plan_s* map_plan_t;
 
+/* map_plan_desc.flags.  MAP_FLAG_MIXED: mixed-precision pass 2 -- on the
+ * look-back path of an fp64 LTI plan, the per-node recursion of pass 2 (the value-function
+ * update and the forward recovery of x*, R-FWD) runs in fp32 from fp64 run carries, while
+ * pass 1, every scan / look-back, the plan tables and all I/O stay fp64.  Rounding then
+ * does not accumulate across runs (each restarts from fp64 values): about 1e-6 relative
+ * instead of 1e-15.  Ignored on other paths. */
+#define MAP_FLAG_MIXED 1
+
 typedef struct {
   int32_t nx, ny, nw;  /* state, measurement, diffusion dims */
   int32_t dtype;       /* map_dtype: compute precision and dtype of y / x buffers */
@@ -94,7 +102,7 @@ typedef struct {
                           form (map_solve_linear / map_solve_sequential); compiled for n = 10
                           at (nx, ny) = (1, 1), (4, 2) (else MAP_E_UNSUPPORTED).  x_map is
                           returned at the block boundaries t_i. */
-  int32_t reserved1;
+  int32_t flags;       /* MAP_FLAG_* (0 = none) */
   void* nccl_comm;     /* ncclComm_t borrowed from the caller (e.g. torch's
                           ProcessGroupNCCL._comm_ptr()); NULL when world == 1, or
                           when the caller drives the exchange (map_shard_phase) */
@@ -138,6 +146,17 @@ void map_plan_destroy(map_plan_t plan);
  * [batch][T+1][nx*(nx+1)/2] (upper triangle, row-major) = S_i^-1, the
  * Kalman--Bucy filter mean / covariance.  Linear plans only. */
 map_status map_solve_linear(map_plan_t plan, const void* y, void* x_map, void* filt_m, void* filt_P);
+
+/* Linear MAP by the parallel RTS form with the smoother covariances (SURVEY f4, P:509,
+ * DESIGN.md R-SCOV): x_map as map_solve_linear, smooth_P [batch][T+1][nx*(nx+1)/2]
+ * (upper triangle, row-major) = Cov(x_i | y_0..y_T), the RTS covariance recursion
+ * P^s_{i-1} = Phi_i P^s_i Phi_i^T + Sigma_i (Phi_i = (I + C_i S_{i-1})^-1 A_i,
+ * Sigma_i = (I + C_i S_{i-1})^-1 C_i, P^s_T = S_T^-1).  Its maps P -> Phi P Phi^T + Sigma
+ * compose associatively; for a time-invariant model they are data-independent, so the
+ * plan scans them over the tiles once (first call) and pass 2 runs the recursion forward
+ * inside each run (R-FWD).  Single-GPU LTI plans on the look-back path; otherwise
+ * MAP_E_UNSUPPORTED (map_two_filter gives smoother covariances for every linear plan). */
+map_status map_solve_linear_cov(map_plan_t plan, const void* y, void* x_map, void* smooth_P);
 
 /* Linear MAP by the parallel two-filter form (information-form
  * backward filter, DESIGN.md R-TF): the backward-information suffix scan runs

@@ -17,6 +17,7 @@ import numpy as np
 LIB_PATH = os.environ.get("PMAP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpmap.so")
 
 MAP_F64, MAP_F32 = 0, 1
+MAP_FLAG_MIXED = 1  # mixed-precision pass 2 (include/pmap.h)
 MAP_NL_COORD_TURN, MAP_NL_VAN_DER_POL = 1, 2
 STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 4: "MAP_E_NCCL",
           5: "MAP_E_NUMERIC", 6: "MAP_E_DIVERGED"}
@@ -25,7 +26,7 @@ STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 
 EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter", "map_solve_nonlinear",
            "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
            "map_profile_enable", "map_profile_read", "map_shard_payload_bytes", "map_shard_phase",
-           "map_version", "map_solve_sequential", "map_debug_lb_timing"]
+           "map_version", "map_solve_sequential", "map_debug_lb_timing", "map_solve_linear_cov"]
 
 
 class MapError(RuntimeError):
@@ -38,7 +39,7 @@ class PlanDesc(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nw", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("T", ctypes.c_int64), ("batch", ctypes.c_int64), ("t0", ctypes.c_double), ("tf", ctypes.c_double),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("substeps", ctypes.c_int32),
-                ("reserved1", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+                ("flags", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
 class LinearModel(ctypes.Structure):
@@ -71,6 +72,8 @@ def load_library():
         lib.map_solve_linear.argtypes = [P, P, P, P, P]
         lib.map_solve_linear.restype = ctypes.c_int
         lib.map_two_filter.argtypes = [P, P, P, P]
+        lib.map_solve_linear_cov.argtypes = [P, P, P, P]
+        lib.map_solve_linear_cov.restype = ctypes.c_int
         lib.map_two_filter.restype = ctypes.c_int
         lib.map_solve_sequential.argtypes = [P, I32, P, I32, P, P]
         lib.map_solve_sequential.restype = ctypes.c_int
@@ -168,6 +171,10 @@ def map_solve_linear(plan: int, y, x_map, filt_m=None, filt_P=None) -> None:
     _check(load_library().map_solve_linear(plan, _ptr(y), _ptr(x_map), _ptr(filt_m), _ptr(filt_P)), plan)
 
 
+def map_solve_linear_cov(plan: int, y, x_map, smooth_P) -> None:
+    _check(load_library().map_solve_linear_cov(plan, _ptr(y), _ptr(x_map), _ptr(smooth_P)), plan)
+
+
 def map_two_filter(plan: int, y, x_map, smooth_P=None) -> None:
     _check(load_library().map_two_filter(plan, _ptr(y), _ptr(x_map), _ptr(smooth_P)), plan)
 
@@ -235,7 +242,7 @@ class Plan:
     def __init__(self, *, T: int, t0: float, tf: float, m0, P0, L, W, R, F=None, H=None, c=None, r=None,
                  batch: int = 1, dtype: str = "f64", nl_kind: int | None = None, params=None,
                  rank: int = 0, world: int = 1, nccl_comm: int | None = None, stream: int | None = None,
-                 substeps: int = 1):
+                 substeps: int = 1, mixed: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2512_13319_b200 needs a CUDA device (no CPU fallback)")
@@ -251,6 +258,7 @@ class Plan:
         d.T, d.batch, d.t0, d.tf = T, batch, t0, tf
         d.rank, d.world = rank, world
         d.substeps = substeps
+        d.flags = MAP_FLAG_MIXED if mixed else 0
         self.substeps = substeps
         d.nccl_comm = nccl_comm
         self.stream = torch.cuda.current_stream().cuda_stream if stream is None else stream
@@ -331,6 +339,17 @@ class Plan:
         self._check_io(y, x_map=x_map, filt_m=filt_m, filt_P=filt_P)
         map_solve_linear(self.handle, y, x_map, filt_m, filt_P)
         return x_map
+
+    def solve_linear_cov(self, y, x_map=None, smooth_P=None):
+        """Parallel RTS MAP and the smoother covariances (map_solve_linear_cov); returns
+        (x_map, smooth_P [batch][n_local][nx(nx+1)/2])."""
+        if x_map is None:
+            x_map = self._out(y, self.batch, self.n_local, self.nx)
+        if smooth_P is None:
+            smooth_P = self._out(y, self.batch, self.n_local, self.nx * (self.nx + 1) // 2)
+        self._check_io(y, x_map=x_map, smooth_P=smooth_P)
+        map_solve_linear_cov(self.handle, y, x_map, smooth_P)
+        return x_map, smooth_P
 
     def two_filter(self, y, x_map=None, smooth_P=None):
         """Parallel two-filter MAP; smooth_P (optional, [batch][T+1][nx(nx+1)/2]) receives

@@ -377,6 +377,7 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
     p->no_rec = nr && nr[0] == '1';
     const char* nlb = getenv("PMAP_NO_LB");
     p->no_lb = nlb && nlb[0] == '1';
+    p->mixed = (d.flags & MAP_FLAG_MIXED) != 0 && d.dtype == MAP_F64;
     const char* lbs = getenv("PMAP_LB_STRESS");
     p->lb_stress = (lbs && lbs[0] == '1') ? 1 : 0;
   }
@@ -756,6 +757,38 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
   outs.push_back({x_map, {xd, xb}});
   if (filt_m) outs.push_back({filt_m, {md, mb}});
   if (filt_P) outs.push_back({filt_P, {Pd, Pb}});
+  return finish(*p, blocking, outs);
+}
+
+map_status map_solve_linear_cov(map_plan_t p, const void* y, void* x_map, void* smooth_P) {
+  if (!p || !y || !x_map || !smooth_P) return MAP_E_ARG;
+  if (p->kind == Kind::NL || p->euler) {
+    p->err = "map_solve_linear_cov needs a linear plan without Euler blocks";
+    return MAP_E_ARG;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  const size_t Pb = (size_t)g.batch * g.Nn * (p->d.nx * (p->d.nx + 1) / 2) * es;
+  bool blocking = false;
+  const void* yd;
+  void *xd, *Pd = nullptr;
+  map_status st = stage_in(*p, y, yb, &yd, &blocking);
+  if (!st) st = stage_out_buf(*p, x_map, xb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (!st) st = stage_out_buf(*p, smooth_P, Pb, &p->stage_aux, &p->stage_aux_bytes, &Pd, &blocking);
+  if (st) return st;
+  bool ok = true;
+  {
+    const void* key[6] = {yd, xd, Pd, nullptr, nullptr, "cov"};
+    map_status gs = graph_run(*p, key, [&] { ok = p->runner->rts_cov(*p, yd, xd, Pd); });
+    if (gs) return gs;
+  }
+  if (!ok) return MAP_E_UNSUPPORTED;
+  std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
+  outs.push_back({x_map, {xd, xb}});
+  outs.push_back({smooth_P, {Pd, Pb}});
   return finish(*p, blocking, outs);
 }
 

@@ -47,6 +47,8 @@
 // of the solve, counters by their last user, so repeated solves (and CUDA-graph
 // replays) need no memset.
 #pragma once
+#include <type_traits>
+
 #include "pmap_lti.cuh"
 
 namespace pmap {
@@ -1162,13 +1164,212 @@ PM_INLINE void lb_store_x(R* __restrict__ dst, const R (&x)[N]) {
 }
 
 
+// Smoother covariance, forward inside a run (R-FWD applied to the RTS covariance
+// recursion P^s_{i-1} = Phi_i P^s_i Phi_i^T + Sigma_i, Phi_i = M^-1 A_i, Sigma_i = M^-1 C_i,
+// M = I + C_i S_{i-1}, R-SCOV):  P^s_i = A_i^-1 (M P^s_{i-1} M^T - C_i M^T) A_i^-T,
+// C M^T = C + C S C (symmetric).  S = S_{i-1}; the upper triangle only.
+template <typename R, int N, class Src>
+PM_INLINE void lb_cov_step(const Src& src, const R (&S)[Dim<N>::NS], R (&P)[Dim<N>::NS]) {
+  R Cf[N][N], Sf[N][N], Pf[N][N], M[N][N], CS[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      Cf[i][c] = src.C[i <= c ? sidx(i, c, N) : sidx(c, i, N)];
+      Sf[i][c] = S[i <= c ? sidx(i, c, N) : sidx(c, i, N)];
+      Pf[i][c] = P[i <= c ? sidx(i, c, N) : sidx(c, i, N)];
+    }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R a = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) a = fma(Cf[i][k], Sf[k][c], a);
+      CS[i][c] = a;
+      M[i][c] = a + (i == c ? R(1) : R(0));
+    }
+  R MP[N][N], Tm[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R a = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) a = fma(M[i][k], Pf[k][c], a);
+      MP[i][c] = a;
+    }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R a = -Cf[i][c];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        a = fma(MP[i][k], M[c][k], a);
+        a = fma(-CS[i][k], Cf[k][c], a);
+      }
+      Tm[i][c] = a;
+    }
+  R AT[N][N];  // A^-1 Tm
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      R a = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(Src::AMASK, i * N + k)) a = fma(src.Am[i][k], Tm[k][c], a);
+      AT[i][c] = a;
+    }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = i; c < N; ++c) {
+      R a = R(0);
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(Src::AMASK, c * N + k)) a = fma(AT[i][k], src.Am[c][k], a);
+      P[sidx(i, c, N)] = a;
+    }
+}
+
+// Plan time, one thread per tile: the run maps of the covariance recursion, Phi_r and
+// Sigma_r = WR_r C_R, composed over the tile (run 0 outermost): Sigma_tile (Phi_tile is
+// k_lb_setup_tiles').  (Phi_a, Sigma_a) o (Phi_b, Sigma_b) = (Phi_a Phi_b, Phi_a Sigma_b Phi_a^T + Sigma_a).
+template <typename R, int N, int NT, int K>
+__global__ void k_lb_cov_tiles(const LtiTables<R, N, NT, K>* __restrict__ tab, const R* __restrict__ lrt, int64_t tpt,
+                               int64_t Nn, double* __restrict__ sig_tile) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= tpt) return;
+  const int64_t n0 = 1 + j * (int64_t)NT * K;
+  double Sg[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) Sg[i][c] = 0.0;
+  for (int r = NT - 1; r >= 0; --r) {
+    const int q = (int)max((int64_t)0, min((int64_t)K, Nn - n0 - (int64_t)r * K));
+    if (q == 0) continue;
+    const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+    double Ph[N][N], Wr[N][N], Cr[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        Ph[i][c] = (double)rt[(LbRunTab<N>::PHI + i * N + c) * NT];
+        Wr[i][c] = (double)rt[(LbRunTab<N>::WR + i * N + c) * NT];
+        const int kk = i <= c ? sidx(i, c, N) : sidx(c, i, N);
+        Cr[i][c] = (double)((q == K) ? tab->E1[N * N + N + kk] : tab->PC[q - 1][kk]);
+      }
+    double T[N][N], U[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) a = fma(Ph[i][k], Sg[k][c], a);
+        T[i][c] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          a = fma(T[i][k], Ph[c][k], a);
+          a = fma(Wr[i][k], Cr[k][c], a);
+        }
+        U[i][c] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < N; ++c) Sg[i][c] = 0.5 * (U[i][c] + U[c][i]);
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) sig_tile[(j * N + i) * N + c] = Sg[i][c];
+}
+
+// Plan time, one thread per tile: from P^s at the tile's last node, backwards over the
+// runs, P^s at the node before each run (the start value of the forward recursion).
+template <typename R, int N, int NT, int K>
+__global__ void k_lb_cov_runs(const LtiTables<R, N, NT, K>* __restrict__ tab, const R* __restrict__ lrt, int64_t tpt,
+                              int64_t Nn, const double* __restrict__ pend, R* __restrict__ lcov) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= tpt) return;
+  const int64_t n0 = 1 + j * (int64_t)NT * K;
+  double P[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < N; ++c) P[i][c] = pend[(j * N + i) * N + c];
+  for (int r = NT - 1; r >= 0; --r) {
+    const int q = (int)max((int64_t)0, min((int64_t)K, Nn - n0 - (int64_t)r * K));
+    if (q > 0) {
+      const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+      double Ph[N][N], Wr[N][N], Cr[N][N], T[N][N], U[N][N];
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          Ph[i][c] = (double)rt[(LbRunTab<N>::PHI + i * N + c) * NT];
+          Wr[i][c] = (double)rt[(LbRunTab<N>::WR + i * N + c) * NT];
+          const int kk = i <= c ? sidx(i, c, N) : sidx(c, i, N);
+          Cr[i][c] = (double)((q == K) ? tab->E1[N * N + N + kk] : tab->PC[q - 1][kk]);
+        }
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          double a = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) a = fma(Ph[i][k], P[k][c], a);
+          T[i][c] = a;
+        }
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          double a = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            a = fma(T[i][k], Ph[c][k], a);
+            a = fma(Wr[i][k], Cr[k][c], a);
+          }
+          U[i][c] = a;
+        }
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) P[i][c] = 0.5 * (U[i][c] + U[c][i]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = i; c < N; ++c) lcov[(j * Dim<N>::NS + sidx(i, c, N)) * NT + r] = (R)P[i][c];
+  }
+}
+
 // ------------------------------------------------------------------ pass 2
-// FO: also write the filter outputs m_i = S_i^-1 v_i, P_i = S_i^-1.
-template <typename R, int N, int NY, int NT, int K, class Src, bool FO>
+// OUT = 1: also write the filter outputs m_i = S_i^-1 v_i, P_i = S_i^-1 to
+// (fm, fP); OUT = 2: the smoother covariances P^s_i (R-SCOV) to fP, forward inside each run
+// from the plan's P^s at the node before the run (lcov).
+// RC: precision of the per-node recursion (R, or float from an fp64 plan: MAP_FLAG_MIXED,
+// where every run restarts from fp64 carries and x leaves as fp64).
+template <typename R, int N, int NY, int NT, int K, class Src, int OUT, typename RC = R>
 __global__ void __maxnreg__(PM_LB2_MAXREG)
-    k_lb_pass2(const __grid_constant__ Src src, const LbGeom g, const R* __restrict__ y,
+    k_lb_pass2(const __grid_constant__ typename Src::template rebind<RC> src, const LbGeom g, const R* __restrict__ y,
                const R* __restrict__ lrt, const LbWs<R> w, R* __restrict__ x_out, R* __restrict__ fm,
-               R* __restrict__ fP, unsigned long long* flag, int stress) {
+               R* __restrict__ fP, const R* __restrict__ lcov, unsigned long long* flag, int stress) {
+  constexpr bool FO = OUT == 1;
+  constexpr bool MIXED = !std::is_same<R, RC>::value;
+  static_assert(!MIXED || OUT == 0, "mixed precision: trajectory only");
+  using SrcC = typename Src::template rebind<RC>;
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
@@ -1375,26 +1576,48 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
   if (q > 0) {
     // x_{s-1} of the run from its suffix map; the value function entering the run (S from
     // the plan's run table, v from pass 1); then the forward sweep over the run's nodes
-    R x[N];
+    RC x[N];
     {
       A inc;
       load(inc, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
+      R xr[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = s_x[i];
-      apply(inc, x);
+      for (int i = 0; i < N; ++i) xr[i] = s_x[i];
+      apply(inc, xr);
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = (RC)xr[i];
     }
-    V cur;
+    VF<RC, N> cur;
     {
       const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
 #pragma unroll
-      for (int k = 0; k < NS; ++k) cur.S[k] = __ldg(rt + (LbRunTab<N>::SP + k) * NT);
+      for (int k = 0; k < NS; ++k) cur.S[k] = (RC)__ldg(rt + (LbRunTab<N>::SP + k) * NT);
 #pragma unroll
-      for (int i = 0; i < N; ++i) cur.v[i] = w.rcv[(tile * N + i) * NT + r];
+      for (int i = 0; i < N; ++i) cur.v[i] = (RC)w.rcv[(tile * N + i) * NT + r];
     }
     R* xo = x_out + b * g.Nn * N;
     const int64_t s0 = n0 + (int64_t)r * K;
+    R Ps[OUT == 2 ? NS : 1];  // smoother covariance at the current node
+    if constexpr (OUT == 2) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k) Ps[k] = __ldg(lcov + (j * NS + k) * NT + r);
+    }
+    auto store_x = [&](R* dst) {
+      if constexpr (MIXED) {
+        R xr[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) xr[i] = (R)x[i];
+        lb_store_x<R, N>(dst, xr);
+      } else {
+        lb_store_x<R, N>(dst, x);
+      }
+    };
     if (s0 == 1) {  // node 0 (the carry-in of the first tile)
-      lb_store_x<R, N>(xo, x);
+      store_x(xo);
+      if constexpr (OUT == 2) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) fP[(b * g.Nn) * NS + k] = Ps[k];
+      }
       if constexpr (FO) {
         R m[N];
         spd_solve<R, N>(cur.S, cur.v, m, ok);
@@ -1409,10 +1632,22 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
     const R* yr = ys + r * YS::ROW;
 #pragma unroll 1
     for (int m = 0; m < q; ++m) {
-      E e;
-      src.node_interior(s0 + m, yr + m * NY, nullptr, e);
-      lb_node_step<R, N, Src>(src, e, cur, x, ok);
-      lb_store_x<R, N>(xo + (s0 + m) * N, x);
+      Elem<RC, N> e;
+      if constexpr (MIXED) {
+        RC yc[NY];
+#pragma unroll
+        for (int k = 0; k < NY; ++k) yc[k] = (RC)yr[m * NY + k];
+        src.node_interior(s0 + m, yc, nullptr, e);
+      } else {
+        src.node_interior(s0 + m, yr + m * NY, nullptr, e);
+      }
+      if constexpr (OUT == 2) {
+        lb_cov_step<R, N, SrcC>(src, cur.S, Ps);  // with S_{i-1}, before the node update
+#pragma unroll
+        for (int k = 0; k < NS; ++k) fP[(b * g.Nn + s0 + m) * NS + k] = Ps[k];
+      }
+      lb_node_step<RC, N, SrcC>(src, e, cur, x, ok);
+      store_x(xo + (s0 + m) * N);
       if constexpr (FO) {
         R mm[N];
         spd_solve<R, N>(cur.S, cur.v, mm, ok);
@@ -1425,10 +1660,10 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
         for (int k = 0; k < NS; ++k) fP[idx * NS + k] = P[k];
       }
     }
-    R s = R(0);
+    RC s = RC(0);
 #pragma unroll
     for (int i = 0; i < N; ++i) s += x[i];
-    if (!(s - s == R(0))) ok = false;
+    if (!(s - s == RC(0))) ok = false;
   }
   if (!ok) atomicMin(flag, (unsigned long long)(n0 + (int64_t)r * K));
   LB_STAMP(1, 3);

@@ -140,6 +140,8 @@ struct Runner {
   virtual void phase3(PlanState& p, const void* y, const void* xbar, const void* gathered, void* x, void* fm,
                       void* fP) = 0;
   virtual void two_filter(PlanState& p, const void* y, void* x, void* Ps) = 0;
+  // parallel RTS with smoother covariances (false + p.err when the plan cannot)
+  virtual bool rts_cov(PlanState& p, const void* y, void* x, void* Ps) = 0;
   // sequential on-device baseline: method 0 = RTS, 1 = two-filter
   virtual void sequential(PlanState& p, int method, const void* y, const void* xbar, void* x, void* Ps) = 0;
   virtual void fill_m0(PlanState& p, void* xbar) = 0;
@@ -212,6 +214,7 @@ struct PlanState {
   bool force_shard = false;  // PMAP_FORCE_SHARD=1 with a communicator: run the NCCL path at world == 1 (tests)
   bool no_lb = false;        // PMAP_NO_LB=1: LTI plans use the multi-kernel scan hierarchy instead of look-back
   int lb_stress = 0;         // PMAP_LB_STRESS=1: delay injection in the look-back kernels (tests)
+  bool mixed = false;        // MAP_FLAG_MIXED: fp32 node recursion in pass 2 (look-back path, fp64 plans)
   size_t lb_bytes = 0;       // look-back workspace
   unsigned long long* lb_tim = nullptr;  // PMAP_LB_TIMING=1: per-tile globaltimer stamps (diagnostics)
   size_t lb_tim_n = 0;
@@ -304,6 +307,16 @@ inline map_status cuda_fail(PlanState& p, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail((p), _e, #call);  \
   } while (0)
 
+// fp32 copy of an LTI source (mixed-precision pass 2); other sources have none
+template <class Src, class = void>
+struct LbSrcF {
+  using type = Src;
+};
+template <class Src>
+struct LbSrcF<Src, std::void_t<typename Src::template rebind<float>>> {
+  using type = typename Src::template rebind<float>;
+};
+
 template <typename R, int N, int NY, class Src, int K>
 struct RunnerT : Runner {
   Src src;
@@ -327,6 +340,10 @@ struct RunnerT : Runner {
   LbTileTab<R, N>* lbtab = nullptr;  // [tpt] plan tables
   R* lbprod = nullptr;               // look-back window products Pa [tpt][33][N][N], Pb (triangular)
   R* lbrun = nullptr;                // [tpt][LbRunTab::F][NT] plan run tables
+  R* lbcov = nullptr;                // [tpt][NS][NT] smoother covariance before each run (built on first use)
+  // the model in fp32 for the mixed-precision pass 2 (MAP_FLAG_MIXED)
+  std::conditional_t<IS_LTI, typename LbSrcF<Src>::type, Src> srcf{};
+  std::vector<double> lb_phit;       // pass-2 tile matrices (host copy, for the covariance chain)
   unsigned char* lbws = nullptr;     // workspace
   LbWs<R> lbw{};
   double lb_amp = 0.0;               // forward-recovery amplification bound over a run (R-FWD)
@@ -339,14 +356,16 @@ struct RunnerT : Runner {
     cudaFree(lbtab);
     cudaFree(lbprod);
     cudaFree(lbrun);
+    cudaFree(lbcov);
     cudaFree(lbws);
   }
 
   bool prepare(PlanState& p) override;
   bool prepare_lb(PlanState& p);
 
-  // one look-back solve: k_lb_pass1a + k_lb_pass1b + k_lb_pass2 (3 launches)
-  void lb_rts(PlanState& p, const void* yv, void* xv, void* fm, void* fP) {
+  // one look-back solve: k_lb_pass1a + k_lb_pass1b + k_lb_pass2 (3 launches); Ps != null:
+  // smoother covariances (pass 2 with OUT = 2, plan tables built on first use)
+  void lb_rts(PlanState& p, const void* yv, void* xv, void* fm, void* fP, void* Ps = nullptr) {
     if constexpr (IS_LTI) {
       const R* y = static_cast<const R*>(yv);
       R* x = static_cast<R*>(xv);
@@ -359,16 +378,42 @@ struct RunnerT : Runner {
       PM_LAUNCH(p, s, K_LB_P1B,
                 (k_lb_pass1b<R, N, NY, kNT, K, Src><<<n1b, 128, 0, s>>>(src, lbg, y, tab, lbtab, lbrun, lbw, p.dflag,
                                                                       p.lb_stress)));
-      if (fm || fP)
+      if (Ps)
         PM_LAUNCH(p, s, K_LB_P2,
-                  (k_lb_pass2<R, N, NY, kNT, K, Src, true><<<n2, kNT, 0, s>>>(
-                      src, lbg, y, lbrun, lbw, x, static_cast<R*>(fm), static_cast<R*>(fP), p.dflag, p.lb_stress)));
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, 2><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr,
+                                                                         static_cast<R*>(Ps), lbcov, p.dflag,
+                                                                         p.lb_stress)));
+      else if (fm || fP)
+        PM_LAUNCH(p, s, K_LB_P2,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, 1><<<n2, kNT, 0, s>>>(
+                      src, lbg, y, lbrun, lbw, x, static_cast<R*>(fm), static_cast<R*>(fP), nullptr, p.dflag,
+                      p.lb_stress)));
+      else if (p.mixed && std::is_same<R, double>::value)  // MAP_FLAG_MIXED: fp32 node recursion
+        PM_LAUNCH(p, s, K_LB_P2,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, 0, float><<<n2, kNT, 0, s>>>(
+                      srcf, lbg, y, lbrun, lbw, x, nullptr, nullptr, nullptr, p.dflag, p.lb_stress)));
       else
         PM_LAUNCH(p, s, K_LB_P2,
-                  (k_lb_pass2<R, N, NY, kNT, K, Src, false><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr,
-                                                                                 nullptr, p.dflag, p.lb_stress)));
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, 0><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr, nullptr,
+                                                                         nullptr, p.dflag, p.lb_stress)));
     }
   }
+
+  // Parallel RTS with smoother covariances (map_solve_linear_cov): look-back plans only.
+  bool rts_cov(PlanState& p, const void* y, void* x, void* Ps) override {
+    if (!(use_lb && p.d.world == 1 && !p.force_shard && !p.no_lb)) {
+      p.err = "smoother covariances of the parallel RTS need a single-GPU LTI look-back plan (map_two_filter gives them "
+              "for every linear plan)";
+      return false;
+    }
+    if (!lbcov && !prepare_lb_cov(p)) {
+      p.err = "plan tables of the smoother covariance failed";
+      return false;
+    }
+    lb_rts(p, y, x, nullptr, nullptr, Ps);
+    return true;
+  }
+  bool prepare_lb_cov(PlanState& p);
 
   // interior (LTI-specialised) tile range [j_lo, j_hi) of a trajectory
   static int64_t lti_jlo(const Geom& g, bool rev) { return (rev || g.node0 == 0) ? 1 : 0; }
@@ -1001,6 +1046,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       if (e != cudaSuccess) return false;
       for (size_t i = 0; i < hphi.size(); ++i) phit[i] = (double)hphi[i];
     }
+    lb_phit = phit;
     const size_t nqa = (size_t)g.tpt * W1 * N * N, nqb = (size_t)(g.gpt * (g.gpt + 1) / 2) * N * N;
     std::vector<double> qb(nqb, 0.0), phig((size_t)g.gpt * N * N, 0.0);
     for (int64_t G = 1; G < g.gpt; ++G) {  // PhiG_G = Phi_{32G} ... Phi_{32G + n_G - 1} (the last group included)
@@ -1096,7 +1142,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_lb_pass1b<R, N, NY, kNT, K, Src>, 128, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_lb_pass2<R, N, NY, kNT, K, Src, false>, kNT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_lb_pass2<R, N, NY, kNT, K, Src, 0>, kNT, 0);
       const char* sd = getenv("PMAP_LB_STRIDE");  // "0": plain (unstrided) ticket order (A/B checks)
       const bool plain = sd && sd[0] == '0';
       g.S1 = plain ? (int64_t)1 << 40 : std::max<int64_t>(1, (int64_t)b1 * 4 * nsm);
@@ -1105,9 +1151,116 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     }
     lbg = g;
     p.lb_bytes += off;
+    srcf = src.template cast<float>();
     tlog("workspace");
     use_lb = true;
     return true;
+  }
+}
+
+// Plan tables of the smoother covariance (R-SCOV, look-back path), on first use: the
+// covariance maps of the tiles (k_lb_cov_tiles), P^s_T = S_T^-1 (S_T from the last run's
+// S and its element), the backward chain P^s at every tile end (host fp64:
+// P_end(j-1) = Phi_j P_end(j) Phi_j^T + Sigma_j), then P^s before every run (k_lb_cov_runs).
+template <typename R, int N, int NY, class Src, int K>
+bool RunnerT<R, N, NY, Src, K>::prepare_lb_cov(PlanState& p) {
+  if constexpr (!IS_LTI) {
+    return false;
+  } else {
+    (void)p;
+    const LbGeom& g = lbg;
+    const int64_t tpt = g.tpt;
+    double* dsig = nullptr;
+    double* dpend = nullptr;
+    if (cudaMalloc(&dsig, sizeof(double) * N * N * tpt) != cudaSuccess) return false;
+    k_lb_cov_tiles<R, N, kNT, K><<<(unsigned)((tpt + 127) / 128), 128>>>(tab, lbrun, tpt, g.Nn, dsig);
+    std::vector<double> sig((size_t)tpt * N * N);
+    if (cudaMemcpy(sig.data(), dsig, sizeof(double) * sig.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaFree(dsig);
+      return false;
+    }
+    cudaFree(dsig);
+    // S_T: the last run's S and its element (one full run or the partial run of q nodes)
+    const int64_t L = (int64_t)kNT * K, n0 = 1 + (tpt - 1) * L, nvalid = g.Nn - n0;
+    const int rT = (int)((nvalid - 1) / K), q = (int)(nvalid - (int64_t)rT * K);
+    constexpr int NS = Dim<N>::NS;
+    R sp[NS], ea[N][N], ec[NS], ej[NS];
+    for (int k = 0; k < NS; ++k)
+      if (cudaMemcpy(&sp[k], lbrun + ((tpt - 1) * (int64_t)LbRunTab<N>::F + LbRunTab<N>::SP + k) * kNT + rT, sizeof(R),
+                     cudaMemcpyDeviceToHost) != cudaSuccess)
+        return false;
+    if (q == K) {
+      R e1[N * N + 2 * N + 2 * NS];
+      if (cudaMemcpy(e1, tab->E1, sizeof e1, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) ea[i][c] = e1[i * N + c];
+      for (int k = 0; k < NS; ++k) {
+        ec[k] = e1[N * N + N + k];
+        ej[k] = e1[N * N + 2 * N + NS + k];
+      }
+    } else if (cudaMemcpy(ea, tab->PA[q - 1], sizeof ea, cudaMemcpyDeviceToHost) != cudaSuccess ||
+               cudaMemcpy(ec, tab->PC[q - 1], sizeof ec, cudaMemcpyDeviceToHost) != cudaSuccess ||
+               cudaMemcpy(ej, tab->PJ[q - 1], sizeof ej, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      return false;
+    }
+    auto full = [&](const R* pk, double* m) {
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) m[i * N + c] = (double)pk[i <= c ? sidx(i, c, N) : sidx(c, i, N)];
+    };
+    auto mm = [&](const double* X, const double* Y, double* Z) {
+      double T[N * N];
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) {
+          double a = 0;
+          for (int k = 0; k < N; ++k) a += X[i * N + k] * Y[k * N + c];
+          T[i * N + c] = a;
+        }
+      memcpy(Z, T, sizeof T);
+    };
+    double S[N * N], C[N * N], J[N * N], A[N * N], At[N * N], M1[N * N], M1i[N * N], X[N * N], ST[N * N], PT[N * N];
+    full(sp, S);
+    full(ec, C);
+    full(ej, J);
+    for (int i = 0; i < N; ++i)
+      for (int c = 0; c < N; ++c) {
+        A[i * N + c] = (double)ea[i][c];
+        At[c * N + i] = (double)ea[i][c];
+      }
+    mm(C, S, M1);  // S_T = A^T S (I + C S)^-1 A + J
+    for (int i = 0; i < N; ++i) M1[i * N + i] += 1.0;
+    if (!h_inv(N, M1, M1i)) return false;
+    mm(M1i, A, X);
+    mm(S, X, X);
+    mm(At, X, ST);
+    for (int i = 0; i < N * N; ++i) ST[i] += J[i];
+    if (!h_inv(N, ST, PT)) return false;
+    std::vector<double> pend((size_t)tpt * N * N);
+    for (int i = 0; i < N; ++i)
+      for (int c = 0; c < N; ++c) pend[((size_t)(tpt - 1) * N + i) * N + c] = 0.5 * (PT[i * N + c] + PT[c * N + i]);
+    for (int64_t j = tpt - 1; j >= 1; --j) {
+      const double* Ph = &lb_phit[(size_t)j * N * N];
+      double T1[N * N], T2[N * N], Pht[N * N];
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) Pht[c * N + i] = Ph[i * N + c];
+      mm(Ph, &pend[(size_t)j * N * N], T1);
+      mm(T1, Pht, T2);
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) {
+          const double v = T2[i * N + c] + sig[((size_t)j * N + i) * N + c];
+          const double w = T2[c * N + i] + sig[((size_t)j * N + c) * N + i];
+          pend[((size_t)(j - 1) * N + i) * N + c] = 0.5 * (v + w);
+        }
+    }
+    if (cudaMalloc(&dpend, sizeof(double) * pend.size()) != cudaSuccess ||
+        cudaMalloc(&lbcov, sizeof(R) * NS * kNT * tpt) != cudaSuccess) {
+      cudaFree(dpend);
+      return false;
+    }
+    cudaMemcpy(dpend, pend.data(), sizeof(double) * pend.size(), cudaMemcpyHostToDevice);
+    k_lb_cov_runs<R, N, kNT, K><<<(unsigned)((tpt + 127) / 128), 128>>>(tab, lbrun, tpt, g.Nn, dpend, lbcov);
+    const cudaError_t e = cudaDeviceSynchronize();
+    cudaFree(dpend);
+    return e == cudaSuccess;
   }
 }
 

@@ -47,6 +47,38 @@ struct SrcLTI {
   int zero_b = 0, zero_bm = 0;  // b == 0 / bm == 0 (c == 0): the node updates skip S b
   static constexpr bool HAS_MIRROR = true;
 
+  // the same model in another precision (mixed-precision pass 2, MAP_FLAG_MIXED)
+  template <typename R2>
+  using rebind = SrcLTI<R2, N, NY, NWC, AM, UM>;
+  template <typename R2>
+  __host__ rebind<R2> cast() const {
+    rebind<R2> o;
+    for (int i = 0; i < N; ++i) {
+      for (int j = 0; j < N; ++j) {
+        o.A[i][j] = (R2)A[i][j];
+        o.Am[i][j] = (R2)Am[i][j];
+      }
+      o.b[i] = (R2)b[i];
+      o.bm[i] = (R2)bm[i];
+      o.h0[i] = (R2)h0[i];
+      o.h00[i] = (R2)h00[i];
+      for (int k = 0; k < NY; ++k) o.K[i][k] = (R2)K[i][k];
+      for (int a = 0; a < (NWC > 0 ? NWC : 1); ++a) {
+        o.U[i][a] = (R2)U[i][a];
+        o.Um[i][a] = (R2)Um[i][a];
+      }
+    }
+    for (int k = 0; k < NS; ++k) {
+      o.C[k] = (R2)C[k];
+      o.J[k] = (R2)J[k];
+      o.J0[k] = (R2)J0[k];
+      o.Cm[k] = (R2)Cm[k];
+    }
+    o.zero_b = zero_b;
+    o.zero_bm = zero_bm;
+    return o;
+  }
+
   // Mirrored element M_i of node gi (R-TF); the terminal node Tg has no transition.
   PM_INLINE void mirror(int64_t gi, int64_t Tg, const R* yrow, Elem<R, N>& e) const {
     R yv[NY];

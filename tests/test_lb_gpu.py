@@ -135,3 +135,59 @@ def test_lb_fp32(torch_cuda):
     assert plan.launches == LB_LAUNCHES
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     assert rel(x[0].cpu().numpy(), xo) < TOL32
+
+
+@pytest.mark.parametrize("T,B", [(3 * TILE + 11, 1), (40 * 32 * TILE + 999, 1), (9_001, 3)])
+def test_lb_smoother_covariance(torch_cuda, T, B):
+    """Parallel RTS smoother covariances (map_solve_linear_cov): the plan's
+    covariance chain over the tiles plus the forward recursion inside each run, against
+    the oracle's textbook RTS covariance recursion (P1-cov pins it to dense conditioning)."""
+    torch = torch_cuda
+    spec = _wiener_offsets()
+    _, y = wl.simulate_linear(spec, T, seed=T % 101, batch=B)
+    y = y.reshape(B, T + 1, 2)
+    plan = gpu_plan(spec, T, batch=B)
+    x, P = plan.solve_linear_cov(to_dev(torch, y))
+    plan.sync()
+    assert plan.launches == LB_LAUNCHES
+    iu = np.triu_indices(spec.nx)
+    for b in range(B):
+        xo, Po = oracle.kf_rts_cov(ora_model(spec), y[b], T, spec.t0, spec.tf)
+        assert rel(x[b].cpu().numpy(), xo) < TOL64
+        Pp = Po[:, iu[0], iu[1]]
+        assert rel(P[b].cpu().numpy(), Pp) < TOL64
+        assert rel_comp(P[b].cpu().numpy(), Pp) < 1e-8
+
+
+def test_lb_smoother_covariance_unsupported(torch_cuda, monkeypatch):
+    """Plans off the look-back path refuse map_solve_linear_cov with MAP_E_UNSUPPORTED."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    monkeypatch.setenv("PMAP_NO_LB", "1")
+    spec = wl.wiener_velocity()
+    T = 5_000
+    _, y = wl.simulate_linear(spec, T, seed=1)
+    with pytest.raises(pm.MapError) as ei:
+        gpu_plan(spec, T).solve_linear_cov(to_dev(torch, y[None]))
+    assert ei.value.status == 2
+
+
+@pytest.mark.parametrize("T", [100_000, 10_000_000])
+def test_lb_mixed_precision(torch_cuda, T):
+    """Mixed-precision pass 2 (MAP_FLAG_MIXED): the per-node recursion in fp32
+    from fp64 run carries; pass 1, the look-backs, the plan tables and all I/O fp64.
+    Rounding does not accumulate across runs, so the error stays near fp32 epsilon times
+    the run length (measured value in DESIGN.md), far below the fp32 variant's."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    _, y = wl.simulate_linear(spec, T, seed=2)
+    plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                   P0=spec.P0, mixed=True)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    plan.sync()
+    assert plan.launches == LB_LAUNCHES
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    e = rel(x[0].cpu().numpy(), xo)
+    print(f"mixed precision T={T}: relative error {e:.3e}")
+    assert e < 1e-5
