@@ -18,6 +18,10 @@ template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2, ~0u, ~0u>(const double*, 
 template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2, pmap_rt::kWienerAMask, pmap_rt::kWienerUMask>(
     const double*, const double*, const double*, const double*, const double*, const double*, const double*,
     const double*, const double*, const double*, const double*, const double*);
+template Runner* make_lti<PM_R, PM_NX, PM_NY, PM_K, 2, pmap_rt::kWienerAMask, pmap_rt::kWienerUMask,
+                          pmap_rt::kWienerSMask>(const double*, const double*, const double*, const double*,
+                                                 const double*, const double*, const double*, const double*,
+                                                 const double*, const double*, const double*, const double*);
 #endif
 #elif PM_KIND == 1
 template Runner* make_tv<PM_R, PM_NX, PM_NY, PM_K>(const PM_R*, const PM_R*, const PM_R*, const PM_R*, const PM_R*,

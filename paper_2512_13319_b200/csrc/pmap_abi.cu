@@ -59,8 +59,17 @@ static Runner* dispatch_lti(int kr, int nx, int ny, int lowrank, const double* A
     uint32_t am = 0, um = 0;
     for (int i = 0; i < 16; ++i) am |= (A[i] != 0.0 ? 1u : 0u) << i;
     for (int i = 0; i < 8; ++i) um |= (U[i] != 0.0 ? 1u : 0u) << i;
+    uint32_t sm = 0;  // packed entries where J or J0 is non-zero (R-SMASK)
+    for (int k = 0; k < 10; ++k) sm |= ((J[k] != 0.0 || J0[k] != 0.0) ? 1u : 0u) << k;
     const char* nm = getenv("PMAP_NO_MASK");
-    if (!(nm && nm[0] == '1') && (am & ~kWienerAMask) == 0 && (um & ~kWienerUMask) == 0)
+    const char* nsm = getenv("PMAP_NO_SMASK");
+    const bool masked = !(nm && nm[0] == '1') && (am & ~kWienerAMask) == 0 && (um & ~kWienerUMask) == 0;
+    if (masked && !(nsm && nsm[0] == '1') && (sm & ~kWienerSMask) == 0)
+      return kr == kKBig ? make_lti<R, 4, 2, kKBig, 2, kWienerAMask, kWienerUMask, kWienerSMask>(
+                               A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U)
+                         : make_lti<R, 4, 2, kKSmall, 2, kWienerAMask, kWienerUMask, kWienerSMask>(
+                               A, b, C, J, K, h0, J0, h00, Am, bm, Cm, U);
+    if (masked)
       return kr == kKBig ? make_lti<R, 4, 2, kKBig, 2, kWienerAMask, kWienerUMask>(A, b, C, J, K, h0, J0, h00, Am,
                                                                                    bm, Cm, U)
                          : make_lti<R, 4, 2, kKSmall, 2, kWienerAMask, kWienerUMask>(A, b, C, J, K, h0, J0, h00,

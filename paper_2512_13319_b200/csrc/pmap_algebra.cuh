@@ -50,6 +50,83 @@ __host__ __device__ constexpr int sidx(int i, int j, int N) {
   return i <= j ? i * N - (i * (i - 1)) / 2 + (j - i) : j * N - (j * (j - 1)) / 2 + (i - j);
 }
 
+// Structural zeros of the value function's S (R-SMASK): SM is a mask over the packed
+// upper triangle.  Given the zeros of S, U and A, these are the entries of S U, of
+// G = I + U^T S U, of its LDL^T factor L, of Y = L^-1 (S U)^T and of B A (B = S - S U
+// G^-1 U^T S) that can be non-zero; closed(): the low-rank node update maps an S with
+// zeros outside SM to one with zeros outside SM whenever J has them (checked at plan
+// time), so the pass-2 node recursion never computes those entries.
+__host__ __device__ constexpr bool sm_nz(uint32_t sm, int i, int j, int N) { return mask_nz(sm, sidx(i, j, N)); }
+__host__ __device__ constexpr uint32_t lr_su_mask(int N, int NW, uint32_t UM, uint32_t SM) {
+  uint32_t m = 0;
+  for (int i = 0; i < N; ++i)
+    for (int a = 0; a < NW; ++a)
+      for (int k = 0; k < N; ++k)
+        if (sm_nz(SM, i, k, N) && mask_nz(UM, k * NW + a)) m |= 1u << (i * NW + a);
+  return m;
+}
+__host__ __device__ constexpr uint32_t lr_g_mask(int N, int NW, uint32_t UM, uint32_t SU) {
+  uint32_t m = 0;
+  for (int a = 0; a < NW; ++a)
+    for (int c = 0; c <= a; ++c) {
+      bool nz = a == c;
+      for (int k = 0; k < N; ++k)
+        if (mask_nz(UM, k * NW + a) && mask_nz(SU, k * NW + c)) nz = true;
+      if (nz) m |= 1u << (a * NW + c);
+    }
+  return m;
+}
+__host__ __device__ constexpr uint32_t lr_l_mask(int NW, uint32_t G) {
+  uint32_t m = 0;
+  for (int c = 0; c < NW; ++c)
+    for (int a = c + 1; a < NW; ++a) {
+      bool nz = mask_nz(G, a * NW + c);
+      for (int k = 0; k < c; ++k)
+        if (mask_nz(m, a * NW + k) && mask_nz(m, c * NW + k)) nz = true;
+      if (nz) m |= 1u << (a * NW + c);
+    }
+  return m;
+}
+__host__ __device__ constexpr uint32_t lr_y_mask(int N, int NW, uint32_t SU, uint32_t L) {
+  uint32_t m = 0;
+  for (int a = 0; a < NW; ++a)
+    for (int j = 0; j < N; ++j) {
+      bool nz = mask_nz(SU, j * NW + a);
+      for (int c = 0; c < a; ++c)
+        if (mask_nz(L, a * NW + c) && mask_nz(m, c * N + j)) nz = true;
+      if (nz) m |= 1u << (a * N + j);
+    }
+  return m;
+}
+__host__ __device__ constexpr uint32_t lr_ba_mask(int N, uint32_t AM, uint32_t SM) {
+  uint32_t m = 0;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j)
+      for (int k = 0; k < N; ++k)
+        if (sm_nz(SM, i, k, N) && mask_nz(AM, k * N + j)) m |= 1u << (i * N + j);
+  return m;
+}
+__host__ __device__ constexpr bool lr_closed(int N, int NW, uint32_t AM, uint32_t SM, uint32_t Y, uint32_t BA) {
+  for (int i = 0; i < N; ++i)
+    for (int j = i; j < N; ++j) {
+      if (sm_nz(SM, i, j, N)) continue;
+      for (int a = 0; a < NW; ++a)  // B = S - Ys^T Y
+        if (mask_nz(Y, a * N + i) && mask_nz(Y, a * N + j)) return false;
+      for (int k = 0; k < N; ++k)  // S' = A^T (B A) + J
+        if (mask_nz(AM, k * N + i) && mask_nz(BA, k * N + j)) return false;
+    }
+  return true;
+}
+template <int N, int NW, uint32_t AM, uint32_t UM, uint32_t SM>
+struct LrMasks {
+  static constexpr uint32_t SU = lr_su_mask(N, NW, UM, SM);
+  static constexpr uint32_t G = lr_g_mask(N, NW, UM, SU);
+  static constexpr uint32_t L = lr_l_mask(NW, G);
+  static constexpr uint32_t Y = lr_y_mask(N, NW, SU, L);
+  static constexpr uint32_t BA = lr_ba_mask(N, AM, SM);
+  static constexpr bool closed = lr_closed(N, NW, AM, SM, Y, BA);
+};
+
 template <typename R, int N>
 struct Elem {
   static constexpr int NS = Dim<N>::NS;
@@ -213,8 +290,9 @@ PM_INLINE float pm_rcp_ge1(float x) { return __frcp_rn(x); }
 
 // G = L D L^T of the small SPD matrix G = I + U^T (S U) (NW x NW, pivots >= 1),
 // sqrt-free.  In: SU = S U.  Out: unit lower L (strict part), Dinv = D^-1.
-template <typename R, int N, int NW, uint32_t UM = ~0u>
-PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW], R (&Dinv)[NW], bool& ok) {
+// ldl_gram with the structural zeros of S U (SUM) and of L (LM) skipped (R-SMASK).
+template <typename R, int N, int NW, uint32_t UM, uint32_t SUM, uint32_t LM>
+PM_INLINE void ldl_gram_m(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW], R (&Dinv)[NW], bool& ok) {
   R G[NW][NW];
 #pragma unroll
   for (int a = 0; a < NW; ++a)
@@ -223,7 +301,7 @@ PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW
       R s = (a == c) ? R(1) : R(0);
 #pragma unroll
       for (int k = 0; k < N; ++k)
-        if (mask_nz(UM, k * NW + a)) s = fma(U[k][a], SU[k][c], s);
+        if (mask_nz(UM, k * NW + a) && mask_nz(SUM, k * NW + c)) s = fma(U[k][a], SU[k][c], s);
       G[a][c] = s;
     }
   R D[NW];
@@ -231,18 +309,29 @@ PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW
   for (int c = 0; c < NW; ++c) {
     R d = G[c][c];
 #pragma unroll
-    for (int k = 0; k < c; ++k) d = fma(-L[c][k] * D[k], L[c][k], d);
+    for (int k = 0; k < c; ++k)
+      if (mask_nz(LM, c * NW + k)) d = fma(-L[c][k] * D[k], L[c][k], d);
     ok = ok && (d > R(0));
     D[c] = d;
     Dinv[c] = pm_rcp_ge1(d);
 #pragma unroll
     for (int a = c + 1; a < NW; ++a) {
+      if (!mask_nz(LM, a * NW + c)) {
+        L[a][c] = R(0);
+        continue;
+      }
       R t = G[a][c];
 #pragma unroll
-      for (int k = 0; k < c; ++k) t = fma(-L[a][k] * D[k], L[c][k], t);
+      for (int k = 0; k < c; ++k)
+        if (mask_nz(LM, a * NW + k) && mask_nz(LM, c * NW + k)) t = fma(-L[a][k] * D[k], L[c][k], t);
       L[a][c] = t * Dinv[c];
     }
   }
+}
+
+template <typename R, int N, int NW, uint32_t UM = ~0u>
+PM_INLINE void ldl_gram(const R (&U)[N][NW], const R (&SU)[N][NW], R (&L)[NW][NW], R (&Dinv)[NW], bool& ok) {
+  ldl_gram_m<R, N, NW, UM, ~0u, ~0u>(U, SU, L, Dinv, ok);
 }
 
 // q <- G^-1 q with G = L D L^T from ldl_gram.
@@ -749,9 +838,11 @@ PM_INLINE void vapply(const Elem<R, N>& e1, const VF<R, N>& V, VF<R, N>& out, Af
 // Same value function as vapply (up to rounding); the N x N pivoted LU becomes an
 // NW x NW sqrt-free LDL^T.  zero_b: b == 0 (skips S b).  rec (nullable): pass-2
 // record [S U | U^T v] of the input value function (R-P2REC), field stride rstride.
-template <typename R, int N, int NW, uint32_t AM = ~0u, uint32_t UM = ~0u>
+template <typename R, int N, int NW, uint32_t AM = ~0u, uint32_t UM = ~0u, uint32_t SM = ~0u>
 PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const VF<R, N>& V, VF<R, N>& out,
                               bool& ok, R* rec = nullptr, int64_t rstride = 0, bool zero_b = false) {
+  using MK = LrMasks<N, NW, AM, UM, SM>;
+  static_assert(SM == ~0u || MK::closed, "S mask not closed under the low-rank node update");
   R SU[N][NW];
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -761,7 +852,7 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       bool first = true;
 #pragma unroll
       for (int k = 0; k < N; ++k)
-        if (mask_nz(UM, k * NW + a)) {
+        if (mask_nz(UM, k * NW + a) && sm_nz(SM, i, k, N)) {
           s = first ? V.S[sidx(i, k, N)] * U[k][a] : fma(V.S[sidx(i, k, N)], U[k][a], s);
           first = false;
         }
@@ -793,16 +884,21 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     }
   }
   R Lg[NW][NW], dinv[NW];
-  ldl_gram<R, N, NW, UM>(U, SU, Lg, dinv, ok);
+  ldl_gram_m<R, N, NW, UM, MK::SU, MK::L>(U, SU, Lg, dinv, ok);
   // Y = L^-1 (S U)^T, Ys = D^-1 Y:  S U G^-1 (S U)^T = Ys^T Y
   R Y[NW][N], Ys[NW][N];
 #pragma unroll
   for (int j = 0; j < N; ++j)
 #pragma unroll
     for (int a = 0; a < NW; ++a) {
+      if (!mask_nz(MK::Y, a * N + j)) {
+        Y[a][j] = Ys[a][j] = R(0);
+        continue;
+      }
       R s = SU[j][a];
 #pragma unroll
-      for (int c = 0; c < a; ++c) s = fma(-Lg[a][c], Y[c][j], s);
+      for (int c = 0; c < a; ++c)
+        if (mask_nz(MK::L, a * NW + c) && mask_nz(MK::Y, c * N + j)) s = fma(-Lg[a][c], Y[c][j], s);
       Y[a][j] = s;
       Ys[a][j] = s * dinv[a];
     }
@@ -812,9 +908,14 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
   for (int i = 0; i < N; ++i)
 #pragma unroll
     for (int j = i; j < N; ++j) {
+      if (!sm_nz(SM, i, j, N)) {  // closed mask: B has S's zeros
+        B[i][j] = B[j][i] = R(0);
+        continue;
+      }
       R s = V.S[sidx(i, j, N)];
 #pragma unroll
-      for (int a = 0; a < NW; ++a) s = fma(-Ys[a][i], Y[a][j], s);
+      for (int a = 0; a < NW; ++a)
+        if (mask_nz(MK::Y, a * N + i) && mask_nz(MK::Y, a * N + j)) s = fma(-Ys[a][i], Y[a][j], s);
       B[i][j] = s;
       B[j][i] = s;
     }
@@ -825,7 +926,8 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
     R s = V.v[i];
     if (!zero_b) {
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(-V.S[sidx(i, k, N)], e1.b[k], s);
+      for (int k = 0; k < N; ++k)
+        if (sm_nz(SM, i, k, N)) s = fma(-V.S[sidx(i, k, N)], e1.b[k], s);
     }
     w[i] = s;
   }
@@ -842,7 +944,8 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
   for (int i = 0; i < N; ++i) {
     R s = w[i];
 #pragma unroll
-    for (int a = 0; a < NW; ++a) s = fma(-SU[i][a], q[a], s);
+    for (int a = 0; a < NW; ++a)
+      if (mask_nz(MK::SU, i * NW + a)) s = fma(-SU[i][a], q[a], s);
     w[i] = s;
   }
   // BA = B A ; S' = A^T (B A) + J (upper triangle) ; v' = A^T w2 + eta
@@ -854,7 +957,7 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
       R s = R(0);
 #pragma unroll
       for (int k = 0; k < N; ++k)
-        if (mask_nz(AM, k * N + j)) s = fma(B[i][k], e1.A[k][j], s);
+        if (mask_nz(AM, k * N + j) && sm_nz(SM, i, k, N)) s = fma(B[i][k], e1.A[k][j], s);
       BA[i][j] = s;
     }
   VF<R, N> o;
@@ -862,10 +965,14 @@ PM_INLINE void vapply_lowrank(const Elem<R, N>& e1, const R (&U)[N][NW], const V
   for (int i = 0; i < N; ++i) {
 #pragma unroll
     for (int j = i; j < N; ++j) {
+      if (!sm_nz(SM, i, j, N)) {  // closed mask (J's zeros checked at plan time)
+        o.S[sidx(i, j, N)] = R(0);
+        continue;
+      }
       R s = e1.J[sidx(i, j, N)];
 #pragma unroll
       for (int k = 0; k < N; ++k)
-        if (mask_nz(AM, k * N + i)) s = fma(e1.A[k][i], BA[k][j], s);
+        if (mask_nz(AM, k * N + i) && mask_nz(MK::BA, k * N + j)) s = fma(e1.A[k][i], BA[k][j], s);
       o.S[sidx(i, j, N)] = s;
     }
     R s = e1.h[i];

@@ -1087,6 +1087,21 @@ __global__ void __launch_bounds__(128)
   if (!ok) atomicMin(flag, (unsigned long long)(g.Nn - 1));
 }
 
+// The structural-zero mask of S a source's pass-2 node recursion may rely on (R-SMASK;
+// SrcLTI::SMASK, ~0u = dense for every other source).
+template <class Src, class = void>
+struct SrcSMask {
+  static constexpr uint32_t value = ~0u;
+};
+template <class Src>
+struct SrcSMask<Src, std::void_t<decltype(Src::SMASK)>> {
+  static constexpr uint32_t value = Src::SMASK;
+};
+template <class Src>
+__host__ __device__ constexpr uint32_t src_smask() {
+  return SrcSMask<Src>::value;
+}
+
 // One forward node step (R-FWD + the node update): x <- A^-1 [x - b + C (S x - v)] with
 // the value function V = V_{i-1} entering node i, then V <- E_i (x) V (Woodbury form
 // for a low-rank diffusion C = U U^T, R-LOWRANK; the general update otherwise).
@@ -1105,7 +1120,8 @@ PM_INLINE void lb_node_step(const Src& src, const Elem<R, N>& e, VF<R, N>& V, R 
         if (mask_nz(Src::UMASK, k * NW + a)) {
           R t = -V.v[k];
 #pragma unroll
-          for (int l = 0; l < N; ++l) t = fma(V.S[sidx(k, l, N)], x[l], t);
+          for (int l = 0; l < N; ++l)
+            if (sm_nz(src_smask<Src>(), k, l, N)) t = fma(V.S[sidx(k, l, N)], x[l], t);
           s = fma(src.U[k][a], t, s);
         }
       u[a] = s;
@@ -1144,7 +1160,8 @@ PM_INLINE void lb_node_step(const Src& src, const Elem<R, N>& e, VF<R, N>& V, R 
     x[i] = s;
   }
   if constexpr (Src::LOWRANK > 0)
-    vapply_lowrank<R, N, Src::LOWRANK, Src::AMASK, Src::UMASK>(e, src.U, V, V, ok, nullptr, 0, src.zero_b != 0);
+    vapply_lowrank<R, N, Src::LOWRANK, Src::AMASK, Src::UMASK, src_smask<Src>()>(e, src.U, V, V, ok, nullptr, 0,
+                                                                                src.zero_b != 0);
   else
     vapply<R, N, false>(e, V, V, nullptr, ok);
 }

@@ -4,11 +4,11 @@
 
 namespace pmap_rt {
 
-template <typename R, int N, int NY, int KR, int NWC, uint32_t AM, uint32_t UM>
+template <typename R, int N, int NY, int KR, int NWC, uint32_t AM, uint32_t UM, uint32_t SM>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
                  const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
                  const double* Cm, const double* U) {
-  auto* rn = new RunnerT<R, N, NY, SrcLTI<R, N, NY, NWC, AM, UM>, KR>();
+  auto* rn = new RunnerT<R, N, NY, SrcLTI<R, N, NY, NWC, AM, UM, SM>, KR>();
   auto& s = rn->src;
   constexpr int NS = Dim<N>::NS;
   for (int i = 0; i < N; ++i) {

@@ -42,6 +42,10 @@ constexpr int kKTiny = 4;
 // zeros include these zeros uses the specialised kernels.
 constexpr uint32_t kWienerAMask = (1u << 0) | (1u << 2) | (1u << 5) | (1u << 7) | (1u << 10) | (1u << 15);
 constexpr uint32_t kWienerUMask = (1u << 4) | (1u << 7);
+// ... and the value function's S (R-SMASK): the two axes decouple, S has zeros at the packed
+// (i, j) with i, j on different axes (axis x = states {0, 2}, axis y = {1, 3}); used when
+// J and J0 have them too (the mask is closed under the node update for these A and U).
+constexpr uint32_t kWienerSMask = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 6) | (1u << 7) | (1u << 9);
 
 enum class Kind { LTI, TV, NL };
 
@@ -927,6 +931,10 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       LbTileTab<R, N>& e = ht[(size_t)j];
       for (int i = 0; i < N; ++i)
         for (int c = i; c < N; ++c) e.S[sidx(i, c, N)] = (R)(0.5 * (S[i * N + c] + S[c * N + i]));
+      if constexpr (src_smask<Src>() != ~0u) {  // R-SMASK: the chain keeps S's structural zeros exactly
+        for (int k = 0; k < NS; ++k)
+          if (!mask_nz(src_smask<Src>(), k) && e.S[k] != R(0)) return false;
+      }
       // Gt = A^T (I + S C)^-1, Hs = Gt S
       double M1[N * N], Mi[N * N], G[N * N], H[N * N];
       mm(S, CL, M1);
@@ -1267,7 +1275,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb_cov(PlanState& p) {
 // ---------------------------------------------------------- instantiation
 // Factories are declared here and explicitly instantiated, one (dtype, shape,
 // model kind) per translation unit, in inst.cu (see pmap_make.cuh).
-template <typename R, int N, int NY, int KR, int NWC, uint32_t AM, uint32_t UM>
+template <typename R, int N, int NY, int KR, int NWC, uint32_t AM, uint32_t UM, uint32_t SM = ~0u>
 Runner* make_lti(const double* A, const double* b, const double* C, const double* J, const double* K,
                  const double* h0, const double* J0, const double* h00, const double* Am, const double* bm,
                  const double* Cm, const double* U);

@@ -18,7 +18,7 @@ namespace pmap {
 // y-dependent eta is precomputed on the host at plan time.
 // NWC > 0: the diffusion has low rank, C = dt Q = U U^T with U (N x NWC), and the
 // per-node value-function update uses the Woodbury form (vapply_lowrank, R-LOWRANK).
-template <typename R, int N, int NY, int NWC = 0, uint32_t AM = ~0u, uint32_t UM = ~0u>
+template <typename R, int N, int NY, int NWC = 0, uint32_t AM = ~0u, uint32_t UM = ~0u, uint32_t SM = ~0u>
 struct SrcLTI {
   static constexpr int NS = Dim<N>::NS;
   static constexpr bool IS_LTI_SRC = true;
@@ -27,6 +27,10 @@ struct SrcLTI {
   // for (R-MASK); the plan picks it only when the model's zeros cover the mask's zeros
   static constexpr uint32_t AMASK = AM;
   static constexpr uint32_t UMASK = UM;
+  // structural zeros of S the look-back pass-2 node recursion skips (R-SMASK): closed under
+  // the low-rank update (static_assert in vapply_lowrank); J's and J0's zeros, and those of
+  // the plan's S chain, are checked at plan time
+  static constexpr uint32_t SMASK = SM;
   static constexpr int NXB = N;  // row width of the nominal trajectory (unused)
   static constexpr bool NEEDS_XBAR = false;
   static constexpr int NYROW = NY;         // doubles of y per node
@@ -49,7 +53,7 @@ struct SrcLTI {
 
   // the same model in another precision (mixed-precision pass 2, MAP_FLAG_MIXED)
   template <typename R2>
-  using rebind = SrcLTI<R2, N, NY, NWC, AM, UM>;
+  using rebind = SrcLTI<R2, N, NY, NWC, AM, UM, SM>;
   template <typename R2>
   __host__ rebind<R2> cast() const {
     rebind<R2> o;

@@ -191,3 +191,39 @@ def test_lb_mixed_precision(torch_cuda, T):
     e = rel(x[0].cpu().numpy(), xo)
     print(f"mixed precision T={T}: relative error {e:.3e}")
     assert e < 1e-5
+
+
+@pytest.mark.parametrize("T", [3 * TILE + 17, 200_003])
+def test_lb_s_mask(torch_cuda, T, monkeypatch):
+    """R-SMASK: for the Wiener-velocity model the two axes decouple, so S keeps exact zeros
+    between them and the pass-2 node recursion skips those entries.  Against the same plan
+    without the S mask (PMAP_NO_SMASK=1) the result agrees to rounding (the look-back's
+    association varies run to run, R-LBDET), and both match the oracle."""
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    _, y = wl.simulate_linear(spec, T, seed=21)
+    yd = to_dev(torch, y[None])
+    x_sm = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    monkeypatch.setenv("PMAP_NO_SMASK", "1")
+    x_full = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    assert rel(x_sm[0], x_full[0]) < 1e-13
+    assert rel(x_sm[0], xo) < TOL64
+    assert rel_comp(x_sm[0], xo) < 1e-8
+
+
+def test_lb_s_mask_not_eligible(torch_cuda):
+    """A prior that couples the axes (P0 with an x-y cross term) puts non-zeros into J0
+    outside the S mask: the plan must take the unmasked S path and still match the oracle."""
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    spec.P0 = spec.P0.copy()
+    spec.P0[0, 1] = spec.P0[1, 0] = 4e-3
+    T = 3 * TILE + 5
+    _, y = wl.simulate_linear(spec, T, seed=22)
+    plan = gpu_plan(spec, T)
+    x = plan.solve_linear(to_dev(torch, y[None]))
+    plan.sync()
+    assert plan.launches == LB_LAUNCHES
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    assert rel(x[0].cpu().numpy(), xo) < TOL64

@@ -11,5 +11,5 @@ for G in 8 4 2; do timeout 300 python tools/shard_probe.py $G >> gpurun_out/fina
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-seq"
 $CMD > gpurun_out/final_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv $CMD > gpurun_out/final_ncu1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_p1_down|k_p2_down|k_p1_reduce_lti|k_p1_tiles|k_p1_groups|k_p2_tiles|k_p2_groups" -s 9 -c 8 -o gpurun_out/final_prof $CMD > gpurun_out/final_ncu2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_lb_pass" -s 9 -c 3 -o gpurun_out/final_prof $CMD > gpurun_out/final_ncu2.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/final_plain.log
