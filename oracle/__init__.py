@@ -56,6 +56,8 @@ def _lib(long_double: bool = False):
         lib.ora_kf_rts_cov.argtypes = [ctypes.POINTER(OraModel), P, P, P]
         lib.ora_euler_rts.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P, ctypes.c_int]
         lib.ora_euler_block.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P, P, P, P, P, ctypes.c_int]
+        lib.ora_euler_refine.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P]
+        lib.ora_hjb_element.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int, P, P, P, P]
         lib.ora_batch.argtypes = [ctypes.POINTER(OraModel), ctypes.c_long, P, P, ctypes.c_int]
         lib.ora_ieks.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long,
                                  ctypes.c_double, ctypes.c_double, P, P, P, P, P, P, ctypes.c_int, P, P, P]
@@ -167,6 +169,39 @@ def euler_rts(model: LinearModel, y_fine, T: int, nsub: int, t0: float, tf: floa
     return x
 
 
+def euler_refine(model: LinearModel, y_fine, T: int, nsub: int, t0: float, tf: float, long_double: bool = False,
+                 lib=None):
+    """Euler blocks plus the intra-block refinement of P:485-507 (DESIGN.md
+    R-REFINE): x* at every fine point, the n - 1 inside each block from the value function
+    of the block's first k substeps, the forward-HJB element (first three
+    equations) of the remaining n - k and the transition P:456-459.  y_fine [nsub*T+1, ny];
+    returns x_fine [nsub*T+1, nx].  `lib`: another build of oracle.c (pin mutation checks)."""
+    y = _f64(y_fine).reshape(nsub * T + 1, model.ny)
+    x = np.empty((nsub * T + 1, model.nx))
+    s = model._struct(T, t0, tf)
+    L = lib or _lib(long_double)
+    rc = L.ora_euler_refine(ctypes.byref(s), nsub, _ptr(y), _ptr(x))
+    if rc:
+        raise FloatingPointError(f"oracle euler_refine failed rc={rc}")
+    return x
+
+
+def hjb_element(model: LinearModel, y_sub, m: int, length: float, lib=None):
+    """The forward-HJB element (A, b, C) of P:490-505 (first three equations) over one
+    interval of the given length: m explicit Euler steps in reversed time from the boundary
+    (I, 0, 0); y_sub [m, ny] in forward-time order (y_sub[k] at t_start + (k+1) length/m).
+    Step 2 of euler_refine's suffix, alone (pin P16)."""
+    nx = model.nx
+    y = _f64(y_sub).reshape(m, model.ny)
+    A, C = np.empty((nx, nx)), np.empty((nx, nx))
+    b = np.empty(nx)
+    s = model._struct(1, 0.0, length)
+    rc = (lib or _lib()).ora_hjb_element(ctypes.byref(s), m, _ptr(y), _ptr(A), _ptr(b), _ptr(C))
+    if rc:
+        raise FloatingPointError(f"oracle hjb_element failed rc={rc}")
+    return A, b, C
+
+
 def euler_block(model: LinearModel, y_sub, nsub: int, length: float, g6_printed: bool = False, lib=None):
     """One Euler block element alone (step 1 of euler_rts; P:416-427 from the boundary of
     P:427): nsub explicit Euler substeps of length length/nsub, substep k reading y_sub[k].
@@ -187,6 +222,8 @@ def load_variant(path: str):
     """ctypes handle of another build of oracle.c (pin mutation checks only)."""
     lib = ctypes.CDLL(path)
     lib.ora_euler_block.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int] + [ctypes.c_void_p] * 6 + [ctypes.c_int]
+    lib.ora_euler_refine.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int] + [ctypes.c_void_p] * 2
+    lib.ora_hjb_element.argtypes = [ctypes.POINTER(OraModel), ctypes.c_int] + [ctypes.c_void_p] * 4
     return lib
 
 

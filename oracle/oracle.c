@@ -734,6 +734,173 @@ int ora_euler_rts(const ora_model* md, int nsub, const double* y_fine, double* x
   return rc;
 }
 
+/* ---------------------------------------------------------------------------
+ * Intra-block refinement of the Euler-block method (
+ * DESIGN.md R-REFINE): x* at the n - 1 fine points inside every block, from
+ *   - the value function at the fine point t_k = t_{i-1} + k de: V_k = E_pre (x) V_{i-1},
+ *     E_pre = the element of the block's first k substeps (step 1 of ora_euler_rts with
+ *     k substeps: P:416-427 from the boundary of P:427);
+ *   - the element (A, b, C) from t_k to the block end t_i by the FORWARD HJB equation
+ *     of P:490-505 ("in practice, we only need the first three equations"), integrated
+ *     in tau (reversed time) by n - k explicit Euler steps from the boundary (I, 0, 0);
+ *   - the transition of R-TRANS with x* at the block end:
+ *     x*(t_k) = (I + C S_k)^-1 (A x*_i + b + C v_k).
+ * y_fine [n T + 1][ny]; x_fine [n T + 1][nx] (block boundaries: ora_euler_rts's x). */
+
+/* V' = E (x) V (P:333-336 with the combination rule P:395-407, right operand a value
+ * function):  S' = A^T S (I + C S)^-1 A + J,  v' = A^T (I + S C)^-1 (v - S b) + eta. */
+static int vf_combine(int nx, const REAL* A, const REAL* b, const REAL* C, const REAL* eta, const REAL* J,
+                      const REAL* S, const REAL* v, REAL* So, REAL* vo) {
+  REAL M[MAXN * MAXN], Mt[MAXN * MAXN], X[MAXN * MAXN], w[MAXN], Sb[MAXN], t[MAXN * MAXN];
+  mm_(nx, C, S, M);
+  for (int a = 0; a < nx * nx; ++a) M[a] += (a % (nx + 1) == 0) ? 1 : 0;             /* I + C S */
+  for (int a = 0; a < nx; ++a)
+    for (int c = 0; c < nx; ++c) Mt[a * nx + c] = M[c * nx + a];                    /* I + S C */
+  memcpy(X, A, sizeof(REAL) * nx * nx);
+  if (lu_solve(nx, nx, M, X)) return 1;                                             /* (I + C S)^-1 A */
+  mm_(nx, S, X, t);
+  for (int a = 0; a < nx; ++a)
+    for (int c = 0; c < nx; ++c) {
+      REAL s = J[a * nx + c];
+      for (int l = 0; l < nx; ++l) s += A[l * nx + a] * t[l * nx + c];
+      So[a * nx + c] = s;
+    }
+  symmetrize(nx, So);
+  mat_vec(nx, nx, S, b, Sb);
+  for (int a = 0; a < nx; ++a) w[a] = v[a] - Sb[a];
+  if (lu_solve(nx, 1, Mt, w)) return 1;
+  for (int a = 0; a < nx; ++a) {
+    REAL s = eta[a];
+    for (int l = 0; l < nx; ++l) s += A[l * nx + a] * w[l];
+    vo[a] = s;
+  }
+  return 0;
+}
+
+/* The forward-HJB element (A, b, C)(s, tau) of P:490-505 as a function of its end time
+ * tau, m explicit Euler steps of length de in tau from the boundary (I, 0, 0) at tau = s:
+ *   dA/dtau = -C H~^T R~^-1 H~ A + F~ A
+ *   db/dtau =  C H~^T R~^-1 (y~ - r~) + F~ b + c~ - C H~^T R~^-1 H~ b
+ *   dC/dtau = -C H~^T R~^-1 H~ C + Q~ + F~ C + C F~^T
+ * (F~ = -F, c~ = -c, Q~ = Q, H~ = H, R~ = R: P:78-102).  tau runs backwards in t from the
+ * block end t_i: step j reads y~ at its start, y at the fine time t_i - j de, which is
+ * y_blk[nsub - 1 - j] (the measurement placement of R-EULER: every fine point once). */
+static void hjb_suffix(int nx, int ny, int m, int nsub, REAL de, const node_model* nm, const REAL* Ft,
+                       const REAL* ct, const REAL* HRi, const REAL* HRH, const double* y_blk, REAL* A, REAL* b,
+                       REAL* C) {
+  for (int a = 0; a < nx * nx; ++a) {
+    A[a] = (a % (nx + 1) == 0) ? 1 : 0;
+    C[a] = 0;
+  }
+  for (int a = 0; a < nx; ++a) b[a] = 0;
+  for (int j = 0; j < m; ++j) {
+    const double* yk = y_blk + (long)(nsub - 1 - j) * ny;
+    REAL CM[MAXN * MAXN], t1[MAXN * MAXN], t2[MAXN * MAXN], dA[MAXN * MAXN], dC[MAXN * MAXN], db[MAXN];
+    REAL u[MAXN], e[MAXN], t3[MAXN];
+    mm_(nx, C, HRH, CM);                                     /* C H^T R^-1 H */
+    mm_(nx, CM, A, t1);
+    mm_(nx, Ft, A, t2);
+    for (int a = 0; a < nx * nx; ++a) dA[a] = -t1[a] + t2[a];
+    for (int q = 0; q < ny; ++q) e[q] = (REAL)yk[q] - nm->r[q];
+    mat_vec(nx, ny, HRi, e, u);                              /* H^T R^-1 (y - r) */
+    mat_vec(nx, nx, C, u, db);
+    mat_vec(nx, nx, Ft, b, t3);
+    for (int a = 0; a < nx; ++a) db[a] += t3[a] + ct[a];
+    mat_vec(nx, nx, CM, b, t3);
+    for (int a = 0; a < nx; ++a) db[a] -= t3[a];
+    mm_(nx, CM, C, t1);
+    mm_(nx, Ft, C, t2);
+    mat_mul_bt(nx, nx, nx, C, Ft, dC);                       /* C F~^T */
+    for (int a = 0; a < nx * nx; ++a) dC[a] += -t1[a] + nm->Q[a] + t2[a];
+    for (int a = 0; a < nx * nx; ++a) { A[a] += de * dA[a]; C[a] += de * dC[a]; }
+    for (int a = 0; a < nx; ++a) b[a] += de * db[a];
+  }
+  symmetrize(nx, C);
+}
+
+/* The forward-HJB element alone (pin P16): one block of length (tf - t0) / T, m Euler
+ * steps in tau; y_sub [m][ny] in the block's fine order (y_sub[k] at t_start + (k+1) de). */
+int ora_hjb_element(const ora_model* md, int m, const double* y_sub, double* A, double* b, double* C) {
+  int nx = md->nx;
+  if (nx > MAXN || md->ny > MAXN || md->T < 1 || m < 1) return 2;
+  node_model nm;
+  REAL Ft[MAXN * MAXN], ct[MAXN], HRi[MAXN * MAXN], HRH[MAXN * MAXN];
+  if (euler_setup(md, &nm, Ft, ct, HRi, HRH)) return 1;
+  REAL de = ((REAL)md->tf - (REAL)md->t0) / (REAL)md->T / m;
+  REAL A_[MAXN * MAXN], b_[MAXN], C_[MAXN * MAXN];
+  hjb_suffix(nx, md->ny, m, m, de, &nm, Ft, ct, HRi, HRH, y_sub, A_, b_, C_);
+  store(nx * nx, A_, A);
+  store(nx, b_, b);
+  store(nx * nx, C_, C);
+  return 0;
+}
+
+int ora_euler_refine(const ora_model* md, int nsub, const double* y_fine, double* x_fine) {
+  int nx = md->nx, ny = md->ny;
+  long T = md->T, N = T + 1;
+  if (nx > MAXN || ny > MAXN || md->nw > MAXN || T < 1 || nsub < 1 || md->g || md->sF || md->sc || md->sL ||
+      md->sW || md->sH || md->sr || md->sR)
+    return 2;
+  REAL dt = ((REAL)md->tf - (REAL)md->t0) / (REAL)T, de = dt / nsub;
+  node_model nm;
+  REAL Ft[MAXN * MAXN], ct[MAXN], HRi[MAXN * MAXN], HRH[MAXN * MAXN];
+  if (euler_setup(md, &nm, Ft, ct, HRi, HRH)) return 1;
+  double* xb = malloc(sizeof(double) * N * nx);
+  REAL* Vs = malloc(sizeof(REAL) * N * nx * nx);
+  REAL* Vv = malloc(sizeof(REAL) * N * nx);
+  int rc = (!xb || !Vs || !Vv) ? 3 : 0;
+  if (!rc) rc = ora_euler_rts(md, nsub, y_fine, xb, 0);      /* x* at the block boundaries */
+  /* value functions at the block boundaries (steps 2-3 of ora_euler_rts) */
+  if (!rc) {
+    REAL P0[MAXN * MAXN], P0i[MAXN * MAXN], m0[MAXN], e[MAXN];
+    load(nx * nx, md->P0, P0);
+    load(nx, md->m0, m0);
+    for (int a = 0; a < nx * nx; ++a) P0i[a] = (a % (nx + 1) == 0) ? 1 : 0;
+    if (lu_solve(nx, nx, P0, P0i)) rc = 1;
+    for (int q = 0; q < ny; ++q) e[q] = (REAL)y_fine[q] - nm.r[q];
+    for (int a = 0; a < nx && !rc; ++a) {
+      REAL s = 0;
+      for (int c = 0; c < nx; ++c) s += P0i[a * nx + c] * m0[c];
+      for (int q = 0; q < ny; ++q) s += de * HRi[a * ny + q] * e[q];
+      Vv[a] = s;
+      for (int c = 0; c < nx; ++c) Vs[a * nx + c] = P0i[a * nx + c] + de * HRH[a * nx + c];
+    }
+    symmetrize(nx, Vs);
+  }
+  for (long i = 1; i <= T && !rc; ++i) {
+    REAL A[MAXN * MAXN], b[MAXN], C[MAXN * MAXN], eta[MAXN], J[MAXN * MAXN];
+    euler_block(nx, ny, nsub, de, &nm, Ft, ct, HRi, HRH, y_fine + ((i - 1) * nsub + 1) * ny, 0, A, b, C, eta, J);
+    if (vf_combine(nx, A, b, C, eta, J, Vs + (i - 1) * nx * nx, Vv + (i - 1) * nx, Vs + i * nx * nx, Vv + i * nx))
+      rc = 1;
+  }
+  if (!rc) {
+    memcpy(x_fine, xb, sizeof(double) * nx);
+    for (long i = 1; i <= T; ++i) memcpy(x_fine + i * nsub * nx, xb + i * nx, sizeof(double) * nx);
+  }
+  for (long i = 1; i <= T && !rc; ++i) {
+    const double* y_blk = y_fine + ((i - 1) * nsub + 1) * ny;
+    REAL xi[MAXN];
+    load(nx, xb + i * nx, xi);
+    for (int k = 1; k < nsub && !rc; ++k) {
+      REAL A[MAXN * MAXN], b[MAXN], C[MAXN * MAXN], eta[MAXN], J[MAXN * MAXN], Sk[MAXN * MAXN], vk[MAXN];
+      euler_block(nx, ny, k, de, &nm, Ft, ct, HRi, HRH, y_blk, 0, A, b, C, eta, J);   /* first k substeps */
+      if (vf_combine(nx, A, b, C, eta, J, Vs + (i - 1) * nx * nx, Vv + (i - 1) * nx, Sk, vk)) { rc = 1; break; }
+      REAL As[MAXN * MAXN], bs[MAXN], Cs[MAXN * MAXN];
+      hjb_suffix(nx, ny, nsub - k, nsub, de, &nm, Ft, ct, HRi, HRH, y_blk, As, bs, Cs);
+      REAL M[MAXN * MAXN], r_[MAXN], Ax[MAXN], Cv[MAXN];
+      mm_(nx, Cs, Sk, M);
+      for (int a = 0; a < nx * nx; ++a) M[a] += (a % (nx + 1) == 0) ? 1 : 0;
+      mat_vec(nx, nx, As, xi, Ax);
+      mat_vec(nx, nx, Cs, vk, Cv);
+      for (int a = 0; a < nx; ++a) r_[a] = Ax[a] + bs[a] + Cv[a];
+      if (lu_solve(nx, 1, M, r_)) { rc = 1; break; }
+      store(nx, r_, x_fine + ((i - 1) * nsub + k) * nx);
+    }
+  }
+  free(xb); free(Vs); free(Vv);
+  return rc;
+}
+
 /* Batched linear MAP: `batch` independent trajectories sharing the model;
  * y: [batch][T+1][ny], x_map: [batch][T+1][nx].  mode 0 = RTS, 1 = two-filter.
  * OpenMP over trajectories (each recursion is sequential).  Returns the

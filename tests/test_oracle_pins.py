@@ -556,3 +556,161 @@ def test_P14_detects_mutations(mut, tmp_path):
         errs, ratios = _p14_ratios(P14_MODELS[name](), lib=lib)
         failed |= not (np.all((ratios > 1.9) & (ratios < 2.1)) and errs[-1].max() < 1e-3)
     assert failed, f"mutation {mut} not detected by P14"
+
+
+# ------------------------------------------------ P15-P17: intra-block refinement (f2)
+def _refine_spec():
+    spec = wl.wiener_velocity()
+    spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+    spec.r = np.array([0.5, -0.25])
+    spec.tf = 1.0
+    return spec
+
+
+def _smooth_y(t):
+    return np.stack([5 + np.sin(3 * t) + 0.3 * t, 5 + np.cos(2 * t)], -1)
+
+
+def _ora(spec):
+    return oracle.LinearModel(spec.F, spec.L, spec.W, spec.H, spec.R, spec.m0, spec.P0, c=spec.c, r=spec.r)
+
+
+def _p15_ratios(lib=None, T=8, ns=(8, 16, 32)):
+    """Error of the refined x* at the fine points inside the blocks against the MAP of the
+    one-element-per-fine-node discrete model on the same fine grid (R-ELEM, oracle.kf_rts,
+    itself pinned by P1-P3/P6); both converge to the continuous MAP at first order, so the
+    per-component error ratio per doubling of n tends to 2."""
+    spec = _refine_spec()
+    md = _ora(spec)
+    errs = []
+    for n in ns:
+        y = _smooth_y(np.linspace(spec.t0, spec.tf, n * T + 1))
+        xr = oracle.euler_refine(md, y, T, n, spec.t0, spec.tf, lib=lib)
+        xref = oracle.kf_rts(md, y, n * T, spec.t0, spec.tf)
+        inner = np.ones(n * T + 1, bool)
+        inner[::n] = False
+        errs.append(np.abs(xr - xref)[inner].max(axis=0))
+    errs = np.array(errs)
+    return errs, errs[:-1] / errs[1:]
+
+
+def test_P15_refinement_first_order():
+    """P15 -- x* at the sub-block points of the Euler-block
+    method (value function of the first k substeps, forward-HJB element of the remaining
+    n - k, transition P:456-459) converges to the continuous MAP at first order: against
+    the fine-grid discrete MAP the error ratio per doubling of n lies in [1.5, 2.5] for
+    every state component; the block boundaries are euler_rts's x exactly."""
+    errs, ratios = _p15_ratios()
+    assert np.all((ratios > 1.5) & (ratios < 2.5)), (errs, ratios)
+    spec = _refine_spec()
+    n, T = 5, 6
+    y = _smooth_y(np.linspace(spec.t0, spec.tf, n * T + 1))
+    xr = oracle.euler_refine(_ora(spec), y, T, n, spec.t0, spec.tf)
+    assert np.array_equal(xr[::n], oracle.euler_rts(_ora(spec), y, T, n, spec.t0, spec.tf))
+
+
+P16_MODELS = {"wiener": lambda: P14_MODELS["wiener"](), "dense": lambda: P14_MODELS["dense"]()}
+
+
+def _p16_ratios(model, lib=None, ns=(64, 128, 256, 512), length=0.2):
+    """Per-field error of the forward-HJB element (A, b, C) of P:490-505 over one interval
+    against the exact composition of n one-substep elements (as P14), and the ratios."""
+    F, c, L, W, H, R, r = model
+    Q = L @ W @ L.T
+    md = oracle.LinearModel(F, L, W, H, R, np.zeros(4), np.eye(4), c=c, r=r)
+    errs = []
+    for n in ns:
+        t = length * np.arange(1, n + 1) / n
+        ys = np.stack([np.sin(3 * t) + 0.5, np.cos(2 * t) - 0.2], 1)
+        hj = oracle.hjb_element(md, ys, n, length, lib=lib)
+        rf = _euler_block_reference(F, c, Q, H, R, r, ys, length)[:3]
+        errs.append([np.abs(a - b).max() / np.abs(b).max() for a, b in zip(hj, rf)])
+    errs = np.array(errs)
+    return errs, errs[:-1] / errs[1:]
+
+
+@pytest.mark.parametrize("name", sorted(P16_MODELS))
+def test_P16_forward_hjb_element(name):
+    """P16 -- the forward-HJB element (A, b, C) integrated in reversed time by
+    explicit Euler converges at first order (ratio in [1.9, 2.1] per doubling, every field)
+    to the element of the same interval as an exact composition of one-substep elements:
+    the same conditional value function reached from its other end (cf. P14)."""
+    errs, ratios = _p16_ratios(P16_MODELS[name]())
+    assert np.all((ratios > 1.9) & (ratios < 2.1)), (errs, ratios)
+    assert errs[-1].max() < 5e-3
+
+
+def _p17_err(lib=None):
+    """Largest relative difference between the refined fine midpoint (n = 2, one block) and
+    the textbook RTS step (see test_P17), over three random drift matrices."""
+    worst = 0.0
+    for seed in range(3):
+        spec = _refine_spec()
+        rng = np.random.default_rng(seed)
+        spec.F = spec.F + 0.3 * rng.standard_normal((4, 4))
+        spec.tf = 0.3
+        y = 5 + rng.standard_normal((3, 2))
+        md = _ora(spec)
+        xr = oracle.euler_refine(md, y, 1, 2, spec.t0, spec.tf, lib=lib)
+        _, fm, fP = oracle.kf_rts(md, y, 2, spec.t0, spec.tf, want_filter=True)
+        d = (spec.tf - spec.t0) / 2
+        Phi = np.linalg.inv(np.eye(4) - d * spec.F)
+        Q = spec.L @ spec.W @ spec.L.T
+        mp = Phi @ (fm[1] + d * spec.c)
+        Pp = Phi @ (fP[1] + d * Q) @ Phi.T
+        G = fP[1] @ Phi.T @ np.linalg.inv(Pp)
+        x1 = fm[1] + G @ (xr[2] - mp)
+        worst = max(worst, rel_inf(xr[1], x1))
+    return worst
+
+
+def test_P17_refinement_two_substeps_is_textbook_rts():
+    """P17 -- with n = 2 substeps and one block, the refinement at the fine midpoint reduces
+    to the textbook RTS step: the one-substep prefix is the exact discrete element of the
+    first fine step (so V_1 is the fine-grid Kalman filter at t_1) and the one-step forward-
+    HJB element is the exact (A, b, C) of the second; so x*(t_1) = m_1 + G (x*(t_2) - m_2^-),
+    G = P_1 Phi^T (P_2^-)^-1, Phi = (I - d F)^-1, m_2^- = Phi (m_1 + d c), P_2^- = Phi (P_1 + d Q) Phi^T,
+    with (m_1, P_1) the fine-grid filter (oracle.kf_rts, P1-pinned) and x*(t_2) the block end."""
+    assert _p17_err() < 1e-11
+
+
+REFINE_MUTATIONS = {
+    "CMA-sign": ("for (int a = 0; a < nx * nx; ++a) dA[a] = -t1[a] + t2[a];",
+                 "for (int a = 0; a < nx * nx; ++a) dA[a] = t1[a] + t2[a];"),
+    "FtA-sign": ("for (int a = 0; a < nx * nx; ++a) dA[a] = -t1[a] + t2[a];",
+                 "for (int a = 0; a < nx * nx; ++a) dA[a] = -t1[a] - t2[a];"),
+    "drop-ct": ("for (int a = 0; a < nx; ++a) db[a] += t3[a] + ct[a];", "for (int a = 0; a < nx; ++a) db[a] += t3[a];"),
+    "drop-CMb": ("    for (int a = 0; a < nx; ++a) db[a] -= t3[a];\n    mm_(nx, CM, C, t1);", "    mm_(nx, CM, C, t1);"),
+    "CFt^T->Ft^TC": ("mat_mul_bt(nx, nx, nx, C, Ft, dC);                       /* C F~^T */",
+                     "for (int a = 0; a < nx; ++a) for (int c = 0; c < nx; ++c) { REAL s_ = 0; "
+                     "for (int l = 0; l < nx; ++l) s_ += Ft[l * nx + a] * C[l * nx + c]; dC[a * nx + c] = s_; }"),
+    "y-order": ("const double* yk = y_blk + (long)(nsub - 1 - j) * ny;", "const double* yk = y_blk + (long)j * ny;"),
+    "prefix-k+1": ("euler_block(nx, ny, k, de, &nm, Ft, ct, HRi, HRH, y_blk, 0, A, b, C, eta, J);   /* first k substeps */",
+                   "euler_block(nx, ny, k + 1, de, &nm, Ft, ct, HRi, HRH, y_blk, 0, A, b, C, eta, J);"),
+}
+
+
+@pytest.mark.parametrize("mut", sorted(REFINE_MUTATIONS))
+def test_P15_P17_detect_mutations(mut, tmp_path):
+    """Every listed slip in the refinement (a sign, a dropped term, a transposed product,
+    the measurement order, an off-by-one prefix) fails P15, P16 or P17."""
+    import subprocess
+    src = open(os.path.join(os.path.dirname(oracle.__file__), "oracle.c")).read()
+    old, new = REFINE_MUTATIONS[mut]
+    assert src.count(old) == 1
+    path = tmp_path / "oracle_mut.c"
+    path.write_text(src.replace(old, new))
+    so = tmp_path / "liboracle_mut.so"
+    subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", str(so), str(path), "-lm"])
+    lib = oracle.load_variant(str(so))
+    failed = False
+    try:
+        _, r15 = _p15_ratios(lib=lib)
+        failed |= not np.all((r15 > 1.5) & (r15 < 2.5))
+        for name in sorted(P16_MODELS):
+            e16, r16 = _p16_ratios(P16_MODELS[name](), lib=lib)
+            failed |= not (np.all((r16 > 1.9) & (r16 < 2.1)) and e16[-1].max() < 5e-3)
+        failed |= _p17_err(lib) > 1e-11
+    except FloatingPointError:
+        failed = True
+    assert failed, f"mutation {mut} not detected by P15-P17"
