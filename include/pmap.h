@@ -158,6 +158,18 @@ map_status map_solve_linear(map_plan_t plan, const void* y, void* x_map, void* f
  * MAP_E_UNSUPPORTED (map_two_filter gives smoother covariances for every linear plan). */
 map_status map_solve_linear_cov(map_plan_t plan, const void* y, void* x_map, void* smooth_P);
 
+/* Euler-block plans (substeps = n > 1): x* at EVERY fine grid point, the
+ * block boundaries from the parallel RTS solve and the n - 1 points inside each block by
+ * the intra-block refinement of P:485-507 (DESIGN.md R-REFINE): the value function of the
+ * block's first k substeps combined with the filter at the block start, then
+ * the transition P:456-459 with the forward-HJB element (first three
+ * equations; n - k Euler steps in reversed time) from x* at the block end.
+ * y [batch][T+1][n*ny] (Euler rows, as map_solve_linear) -> x_fine [batch][n*T+1][nx]
+ * (fine point j at t0 + j (tf - t0) / (n T)).  Host or device buffers.  Other plans:
+ * MAP_E_UNSUPPORTED.  Workspace for the block solution and filter outputs is allocated
+ * on the first call and owned by the plan. */
+map_status map_solve_linear_fine(map_plan_t plan, const void* y, void* x_fine);
+
 /* Linear MAP by the parallel two-filter form (information-form
  * backward filter, DESIGN.md R-TF): the backward-information suffix scan runs
  * concurrently with pass 1 and the per-node combine is fused into its epilogue.

@@ -26,7 +26,8 @@ STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 
 EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter", "map_solve_nonlinear",
            "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
            "map_profile_enable", "map_profile_read", "map_shard_payload_bytes", "map_shard_phase",
-           "map_version", "map_solve_sequential", "map_debug_lb_timing", "map_solve_linear_cov"]
+           "map_version", "map_solve_sequential", "map_debug_lb_timing", "map_solve_linear_cov",
+           "map_solve_linear_fine"]
 
 
 class MapError(RuntimeError):
@@ -74,6 +75,8 @@ def load_library():
         lib.map_two_filter.argtypes = [P, P, P, P]
         lib.map_solve_linear_cov.argtypes = [P, P, P, P]
         lib.map_solve_linear_cov.restype = ctypes.c_int
+        lib.map_solve_linear_fine.argtypes = [P, P, P]
+        lib.map_solve_linear_fine.restype = ctypes.c_int
         lib.map_two_filter.restype = ctypes.c_int
         lib.map_solve_sequential.argtypes = [P, I32, P, I32, P, P]
         lib.map_solve_sequential.restype = ctypes.c_int
@@ -169,6 +172,10 @@ def map_plan_destroy(plan: int) -> None:
 
 def map_solve_linear(plan: int, y, x_map, filt_m=None, filt_P=None) -> None:
     _check(load_library().map_solve_linear(plan, _ptr(y), _ptr(x_map), _ptr(filt_m), _ptr(filt_P)), plan)
+
+
+def map_solve_linear_fine(plan: int, y, x_fine) -> None:
+    _check(load_library().map_solve_linear_fine(plan, _ptr(y), _ptr(x_fine)), plan)
 
 
 def map_solve_linear_cov(plan: int, y, x_map, smooth_P) -> None:
@@ -350,6 +357,17 @@ class Plan:
         self._check_io(y, x_map=x_map, smooth_P=smooth_P)
         map_solve_linear_cov(self.handle, y, x_map, smooth_P)
         return x_map, smooth_P
+
+    def solve_linear_fine(self, y, x_fine=None):
+        """Euler-block plans: x* at every fine point (map_solve_linear_fine, R-REFINE);
+        y as solve_linear (Euler rows), returns x_fine [batch][substeps*T+1][nx]."""
+        nf = self.substeps * self.T + 1
+        if x_fine is None:
+            x_fine = self._out(y, self.batch, nf, self.nx)
+        _check_buf("y", y, self.dtype, self.batch * (self.T + 1) * self.ny_row)
+        _check_buf("x_fine", x_fine, self.dtype, self.batch * nf * self.nx)
+        map_solve_linear_fine(self.handle, y, x_fine)
+        return x_fine
 
     def two_filter(self, y, x_map=None, smooth_P=None):
         """Parallel two-filter MAP; smooth_P (optional, [batch][T+1][nx(nx+1)/2]) receives

@@ -197,6 +197,116 @@ static void euler_block(int nx, int ny, int nsub, double dt, const double* F, co
   (void)I;
 }
 
+// Forward-HJB element of the last m substeps of a block (R-REFINE, the first
+// three equations): (A, b, C)(s, tau) integrated in reversed time tau by m explicit Euler
+// steps of length de from the boundary (I, 0, 0), every right-hand side at the current
+// state:  dA = -C M A + F~ A,  db = C H^T R^-1 (y - r) + F~ b + c~ - C M b,
+// dC = -C M C + Q~ + F~ C + C F~^T  (M = H^T R^-1 H; F~ = -F, c~ = -c, Q~ = Q).  Step j
+// reads the measurement of substep nsub - 1 - j (fine time t_i - j de).  b is affine in the
+// block's measurements: B is nx x (1 + nsub*ny), column 0 data-free, column 1 + k*ny + a
+// the coefficient of component a of substep k (the layout of euler_block).
+static void hjb_block(int nx, int ny, int nsub, int m, double de, const double* F, const double* c,
+                      const double* Q, const double* H, const double* r, const double* Ri, std::vector<double>& A,
+                      std::vector<double>& C, std::vector<double>& B) {
+  const int M = 1 + nsub * ny;
+  A.assign(nx * nx, 0.0);
+  for (int i = 0; i < nx; ++i) A[i * nx + i] = 1.0;
+  C.assign(nx * nx, 0.0);
+  B.assign(nx * M, 0.0);
+  std::vector<double> Ft(nx * nx), ct(nx), HRi(nx * ny, 0.0), HRH(nx * nx, 0.0), HRr(nx, 0.0);
+  for (int i = 0; i < nx * nx; ++i) Ft[i] = -F[i];
+  for (int i = 0; i < nx; ++i) ct[i] = c ? -c[i] : 0.0;
+  for (int i = 0; i < nx; ++i)
+    for (int a = 0; a < ny; ++a)
+      for (int q = 0; q < ny; ++q) HRi[i * ny + a] += H[q * nx + i] * Ri[q * ny + a];
+  for (int i = 0; i < nx; ++i) {
+    for (int j = 0; j < nx; ++j)
+      for (int a = 0; a < ny; ++a) HRH[i * nx + j] += HRi[i * ny + a] * H[a * nx + j];
+    for (int a = 0; a < ny; ++a) HRr[i] += HRi[i * ny + a] * (r ? r[a] : 0.0);
+  }
+  auto mm = [&](const double* X, int xc, const double* Y, int yc, std::vector<double>& Z) {  // Z = X Y
+    Z.assign(nx * yc, 0.0);
+    for (int i = 0; i < nx; ++i)
+      for (int k = 0; k < xc; ++k)
+        for (int j = 0; j < yc; ++j) Z[i * yc + j] += X[i * xc + k] * Y[k * yc + j];
+  };
+  std::vector<double> CM, t1, t2, dA(nx * nx), dB(nx * M), dC(nx * nx);
+  for (int j = 0; j < m; ++j) {
+    const int ks = nsub - 1 - j;
+    mm(C.data(), nx, HRH.data(), nx, CM);
+    mm(CM.data(), nx, A.data(), nx, t1);
+    mm(Ft.data(), nx, A.data(), nx, t2);
+    for (int i = 0; i < nx * nx; ++i) dA[i] = -t1[i] + t2[i];
+    mm(Ft.data(), nx, B.data(), M, t1);
+    mm(CM.data(), nx, B.data(), M, t2);
+    for (int i = 0; i < nx * M; ++i) dB[i] = t1[i] - t2[i];
+    for (int i = 0; i < nx; ++i) {
+      double s = ct[i];
+      for (int q = 0; q < nx; ++q) s -= C[i * nx + q] * HRr[q];
+      dB[i * M] += s;
+      for (int a = 0; a < ny; ++a) {
+        double u = 0;
+        for (int q = 0; q < nx; ++q) u += C[i * nx + q] * HRi[q * ny + a];
+        dB[i * M + 1 + ks * ny + a] += u;
+      }
+    }
+    mm(CM.data(), nx, C.data(), nx, t1);
+    mm(Ft.data(), nx, C.data(), nx, t2);
+    for (int i = 0; i < nx; ++i)
+      for (int q = 0; q < nx; ++q) {
+        double s = -t1[i * nx + q] + Q[i * nx + q] + t2[i * nx + q];
+        for (int l = 0; l < nx; ++l) s += C[i * nx + l] * Ft[q * nx + l];  // C F~^T
+        dC[i * nx + q] = s;
+      }
+    for (int i = 0; i < nx * nx; ++i) {
+      A[i] += de * dA[i];
+      C[i] += de * dC[i];
+    }
+    for (int i = 0; i < nx * M; ++i) B[i] += de * dB[i];
+  }
+  for (int i = 0; i < nx; ++i)
+    for (int q = i + 1; q < nx; ++q) C[i * nx + q] = C[q * nx + i] = 0.5 * (C[i * nx + q] + C[q * nx + i]);
+}
+
+// Refinement tables of every k = 1 .. nsub - 1 (layout RefineTab in pmap_refine.cuh).
+static std::vector<double> refine_tables(int nx, int ny, int nsub, double dt, const double* F, const double* c,
+                                         const double* Q, const double* H, const double* r, const double* Ri) {
+  const int NS = nx * (nx + 1) / 2, NR = nsub * ny, M = 1 + NR;
+  const double de = dt / nsub;
+  const int FR = 2 * nx * nx + 3 * NS + 3 * nx + 3 * nx * NR;
+  std::vector<double> out((size_t)(nsub - 1) * FR, 0.0);
+  std::vector<double> A, C, J, B, E, As, Cs, Bs, Cp(NS), Jp(NS), Csp(NS);
+  auto sym_pack = [&](const double* Mf, double* P) {  // upper triangle, row-major
+    for (int i = 0, k = 0; i < nx; ++i)
+      for (int j = i; j < nx; ++j) P[k++] = 0.5 * (Mf[i * nx + j] + Mf[j * nx + i]);
+  };
+  for (int k = 1; k < nsub; ++k) {
+    double* t = out.data() + (size_t)(k - 1) * FR;
+    euler_block(nx, ny, k, k * de, F, c, Q, H, r, Ri, A, C, J, B, E);  // the first k substeps
+    hjb_block(nx, ny, nsub, nsub - k, de, F, c, Q, H, r, Ri, As, Cs, Bs);
+    sym_pack(C.data(), Cp.data());
+    sym_pack(J.data(), Jp.data());
+    sym_pack(Cs.data(), Csp.data());
+    const int Mk = 1 + k * ny;  // euler_block's coefficient columns for k substeps
+    double* p = t;
+    for (int i = 0; i < nx * nx; ++i) *p++ = A[i];
+    for (int i = 0; i < NS; ++i) *p++ = Cp[i];
+    for (int i = 0; i < NS; ++i) *p++ = Jp[i];
+    for (int i = 0; i < nx; ++i) *p++ = B[i * Mk];
+    for (int i = 0; i < nx; ++i) *p++ = E[i * Mk];
+    for (int i = 0; i < nx; ++i)
+      for (int q = 0; q < NR; ++q) *p++ = q < k * ny ? B[i * Mk + 1 + q] : 0.0;
+    for (int i = 0; i < nx; ++i)
+      for (int q = 0; q < NR; ++q) *p++ = q < k * ny ? E[i * Mk + 1 + q] : 0.0;
+    for (int i = 0; i < nx * nx; ++i) *p++ = As[i];
+    for (int i = 0; i < NS; ++i) *p++ = Csp[i];
+    for (int i = 0; i < nx; ++i) *p++ = Bs[i * M];
+    for (int i = 0; i < nx; ++i)
+      for (int q = 0; q < NR; ++q) *p++ = Bs[i * M + 1 + q];
+  }
+  return out;
+}
+
 template <typename R>
 static Runner* dispatch_tv(int kr, int nx, int ny, const R* F, const R* c, const R* L, const R* Wm, const R* H,
                            const R* r, const R* Rm, const int64_t* str, int nw, double dt, const double* P0i,
@@ -472,6 +582,7 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
         for (int a = 0; a < ny; ++a) h00[i] -= K0[i * ny + a] * (lin->r ? lin->r[a] : 0.0);
       }
       p->ny_row = NR;
+      p->refine_host = refine_tables(nx, ny, nsub, dt, lin->F, lin->c, Q.data(), lin->H, lin->r, Ri.data());
       rn = f32 ? dispatch_euler<float>(kr, nx, ny, nsub, A.data(), Cp.data(), Jp.data(), b0.data(), h0.data(),
                                        Kb.data(), Ke.data(), J0.data(), h00.data(), K0.data())
                : dispatch_euler<double>(kr, nx, ny, nsub, A.data(), Cp.data(), Jp.data(), b0.data(), h0.data(),
@@ -769,6 +880,53 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
   return finish(*p, blocking, outs);
 }
 
+map_status map_solve_linear_fine(map_plan_t p, const void* y, void* x_fine) {
+  if (!p || !y || !x_fine) return MAP_E_ARG;
+  if (p->kind == Kind::NL || !p->euler) {
+    p->err = "map_solve_linear_fine needs a linear plan with Euler blocks (substeps > 1)";
+    return MAP_E_UNSUPPORTED;
+  }
+  if (p->d.world > 1) {
+    p->err = "map_solve_linear_fine: single-GPU plans only";
+    return MAP_E_UNSUPPORTED;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const int nx = p->d.nx, NS = nx * (nx + 1) / 2;
+  const int64_t T = g.Nn - 1, Nf = (int64_t)p->d.substeps * T + 1;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xfb = (size_t)g.batch * Nf * nx * es;
+  const size_t xbb = (size_t)g.batch * g.Nn * nx * es, Pbb = (size_t)g.batch * g.Nn * NS * es;
+  bool blocking = false;
+  const void* yd;
+  void* xd;
+  map_status st = stage_in(*p, y, yb, &yd, &blocking);
+  if (!st) st = stage_out_buf(*p, x_fine, xfb, &p->stage_x, &p->stage_x_bytes, &xd, &blocking);
+  if (st) return st;
+  if (p->fine_ws_bytes < 2 * xbb + Pbb) {  // block x, filter m, filter P
+    cudaFree(p->fine_ws);
+    p->fine_ws = nullptr;
+    p->fine_ws_bytes = 0;
+    if (cudaMalloc(&p->fine_ws, 2 * xbb + Pbb) != cudaSuccess) {
+      p->err = "map_solve_linear_fine: workspace allocation failed";
+      return MAP_E_CUDA;
+    }
+    p->fine_ws_bytes = 2 * xbb + Pbb;
+  }
+  char* w = static_cast<char*>(p->fine_ws);
+  void *xbd = w, *md = w + xbb, *Pd = w + 2 * xbb;
+  bool ok = true;
+  {
+    const void* key[6] = {yd, xd, nullptr, nullptr, nullptr, "fine"};
+    map_status gs = graph_run(*p, key, [&] { ok = p->runner->refine(*p, yd, xbd, md, Pd, xd); });
+    if (gs) return gs;
+  }
+  if (!ok) return MAP_E_UNSUPPORTED;
+  std::vector<std::pair<void*, std::pair<void*, size_t>>> outs;
+  outs.push_back({x_fine, {xd, xfb}});
+  return finish(*p, blocking, outs);
+}
 map_status map_solve_linear_cov(map_plan_t p, const void* y, void* x_map, void* smooth_P) {
   if (!p || !y || !x_map || !smooth_P) return MAP_E_ARG;
   if (p->kind == Kind::NL || p->euler) {

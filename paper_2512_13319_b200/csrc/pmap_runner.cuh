@@ -21,6 +21,7 @@
 #include "pmap_seq.cuh"
 #include "pmap_lti_scan.cuh"
 #include "pmap_lb.cuh"
+#include "pmap_refine.cuh"
 #include <cstdlib>
 #include <type_traits>
 
@@ -152,6 +153,11 @@ struct Runner {
   // out <- max |a - b| (atomicMax of the bit pattern); copy: also a <- b
   virtual void maxdiff(PlanState& p, void* a, const void* b, unsigned long long* out, bool copy) = 0;
   virtual int sizeof_real() const = 0;
+  // Euler-block plans: x* at every fine point from the block solution and the filter
+  // outputs at the block nodes (R-REFINE); false + p.err for other plans
+  virtual bool refine(PlanState& p, const void* y, const void* xb, const void* fm, const void* fP, void* xf) {
+    return false;
+  }
 };
 
 struct NcclApi {
@@ -222,6 +228,10 @@ struct PlanState {
   size_t lb_bytes = 0;       // look-back workspace
   unsigned long long* lb_tim = nullptr;  // PMAP_LB_TIMING=1: per-tile globaltimer stamps (diagnostics)
   size_t lb_tim_n = 0;
+  std::vector<double> refine_host;  // Euler blocks: intra-block refinement tables (R-REFINE), host copy
+  void* refine_tab = nullptr;       // ... on the device (R), uploaded on first map_solve_linear_fine
+  void* fine_ws = nullptr;          // block x, filter m, P of map_solve_linear_fine
+  size_t fine_ws_bytes = 0;
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
   cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -251,7 +261,8 @@ struct PlanState {
     for (auto& ge : lgraphs)
       if (ge.exec) cudaGraphExecDestroy(ge.exec);
     runner.reset();
-    for (void* q : {(void*)lb_tim, (void*)ws, (void*)dflag, xbuf[0], xbuf[1], stage_y, stage_x, stage_aux, dev_tv, scratch, m0_dev})
+    for (void* q : {(void*)lb_tim, (void*)ws, (void*)dflag, xbuf[0], xbuf[1], stage_y, stage_x, stage_aux, dev_tv, scratch, m0_dev,
+                    refine_tab, fine_ws})
       if (q) cudaFree(q);
     for (cudaStream_t s : {stream2, stream3, stream4})
       if (s) cudaStreamDestroy(s);
@@ -273,13 +284,14 @@ struct PlanState {
 // kernel classes reported by map_profile_read
 enum KernelId { K_P1_REDUCE = 0, K_P1_REDUCE_EDGE, K_P1_TILES, K_P1_GROUPS, K_P1_DOWN, K_P2_TILES, K_P2_GROUPS,
                 K_P2_DOWN, K_FILTER_OUT, K_TF_REDUCE, K_TF_REDUCE_EDGE, K_TF_TILES, K_TF_GROUPS, K_TF_DOWN, K_SHARD,
-                K_NL_MISC, K_SEQ, K_LB_P1, K_LB_P2, K_P1_REDUCE_LTI, K_LB_P1B, K_COUNT };
+                K_NL_MISC, K_SEQ, K_LB_P1, K_LB_P2, K_P1_REDUCE_LTI, K_LB_P1B, K_REFINE, K_COUNT };
 inline const char* kernel_name(int id) {
   static const char* names[K_COUNT] = {"k_p1_reduce", "k_p1_reduce_lti_edge", "k_p1_tiles", "k_p1_groups",
                                        "k_p1_down", "k_p2_tiles", "k_p2_groups", "k_p2_down", "k_filter_out",
                                        "k_tf_reduce", "k_tf_reduce_lti_edge", "k_tf_tiles", "k_tf_groups",
                                        "k_tf_down", "k_shard_*", "k_fill_m0/k_maxdiff", "k_seq_rts/k_seq_tf",
-                                       "k_lb_pass1a", "k_lb_pass2", "k_p1_reduce_lti", "k_lb_pass1b"};
+                                       "k_lb_pass1a", "k_lb_pass2", "k_p1_reduce_lti", "k_lb_pass1b",
+                                       "k_euler_refine"};
   return (id >= 0 && id < K_COUNT) ? names[id] : "?";
 }
 
@@ -320,6 +332,12 @@ template <class Src>
 struct LbSrcF<Src, std::void_t<typename Src::template rebind<float>>> {
   using type = typename Src::template rebind<float>;
 };
+
+// Euler-block sources (SrcEulerLTI) expose their substep count (R-REFINE)
+template <class Src, class = void>
+struct SrcIsEuler : std::false_type {};
+template <class Src>
+struct SrcIsEuler<Src, std::void_t<decltype(Src::NSUB_)>> : std::true_type {};
 
 template <typename R, int N, int NY, class Src, int K>
 struct RunnerT : Runner {
@@ -400,6 +418,35 @@ struct RunnerT : Runner {
         PM_LAUNCH(p, s, K_LB_P2,
                   (k_lb_pass2<R, N, NY, kNT, K, Src, 0><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr, nullptr,
                                                                          nullptr, p.dflag, p.lb_stress)));
+    }
+  }
+
+  bool refine(PlanState& p, const void* y, const void* xb, const void* fm, const void* fP, void* xf) override {
+    if constexpr (!SrcIsEuler<Src>::value) {
+      p.err = "map_solve_linear_fine needs a plan with Euler blocks (substeps > 1)";
+      return false;
+    } else {
+      constexpr int NSUB = Src::NSUB_, NYM = Src::NYM_;
+      const Geom& g = p.g;
+      const int64_t T = g.Nn - 1;
+      if (!p.refine_tab) {  // plan tables in R, uploaded once
+        std::vector<R> h(p.refine_host.size());
+        for (size_t k = 0; k < h.size(); ++k) h[k] = (R)p.refine_host[k];
+        if (cudaMalloc(&p.refine_tab, sizeof(R) * h.size()) != cudaSuccess ||
+            cudaMemcpy(p.refine_tab, h.data(), sizeof(R) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+          p.err = "refinement tables: device allocation failed";
+          return false;
+        }
+      }
+      rts(p, y, nullptr, const_cast<void*>(xb), const_cast<void*>(fm), const_cast<void*>(fP));
+      const int64_t n = g.batch * T;
+      if (n > 0)
+        PM_LAUNCH(p, p.stream, K_REFINE,
+                  (k_euler_refine<R, N, NYM, NSUB><<<(unsigned)((n + 127) / 128), 128, 0, p.stream>>>(
+                      static_cast<const R*>(p.refine_tab), T, g.batch, static_cast<const R*>(y),
+                      static_cast<const R*>(xb), static_cast<const R*>(fm), static_cast<const R*>(fP),
+                      static_cast<R*>(xf), p.dflag)));
+      return true;
     }
   }
 

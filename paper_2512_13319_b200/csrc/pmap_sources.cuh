@@ -549,6 +549,7 @@ template <typename R, int N, int NYM, int NSUB>
 struct SrcEulerLTI {
   static constexpr int NS = Dim<N>::NS;
   static constexpr int NYROW = NSUB * NYM;
+  static constexpr int NSUB_ = NSUB, NYM_ = NYM;  // refinement (R-REFINE)
   static constexpr bool IS_LTI_SRC = false;
   static constexpr int LOWRANK = 0;
   static constexpr bool NEEDS_XBAR = false;

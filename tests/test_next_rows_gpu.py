@@ -13,7 +13,7 @@ import pytest
 
 import oracle
 import workloads as wl
-from test_parity_gpu import TOL64, TOL32, gpu_plan, ora_model, random_lti, rel, to_dev, torch_cuda, tv_spec  # noqa: F401
+from test_parity_gpu import TOL64, TOL32, gpu_plan, ora_model, random_lti, rel, rel_comp, to_dev, torch_cuda, tv_spec  # noqa: F401
 
 pytestmark = pytest.mark.gpu
 
@@ -190,6 +190,58 @@ def test_euler_blocks(torch_cuda, case, T, B):
         xo = oracle.euler_rts(ora_model(spec), yf[b], T, n, spec.t0, spec.tf)
         assert rel(x[b], xo) < TOL64
         assert rel(xs[b], xo) < TOL64
+
+
+@pytest.mark.parametrize("case,T,B", [("wiener_c", 1, 1), ("wiener_c", 3000, 1), ("wiener", 100_000, 1),
+                                       ("wiener_c", 20_000, 3), ("ou", 4097, 2)])
+def test_euler_refinement(torch_cuda, case, T, B):
+    """f2 remainder: x* at every fine point (map_solve_linear_fine, R-REFINE) =
+    the oracle's step-by-step refinement (pins P15-P17), per component, host and device
+    buffers; block boundaries = the block solve."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    n = 10
+    if case.startswith("wiener"):
+        spec = wl.wiener_velocity()
+        if case == "wiener_c":
+            spec.c = np.array([0.3, -0.2, 0.1, 0.05])
+            spec.r = np.array([0.5, -0.25])
+        if T < 10:  # explicit Euler blocks need short blocks (delta H^T R^-1 H << 1): shorten the span
+            spec.tf = spec.t0 + 0.01 * T
+    else:
+        spec = wl.ornstein_uhlenbeck()
+    _, yf = wl.simulate_linear(spec, n * T, seed=T + 7, batch=B)
+    yf = yf.reshape(B, n * T + 1, spec.ny)
+    plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H, r=spec.r,
+                   R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, substeps=n)
+    rows = pm.binding.euler_rows(yf, n)
+    yd = to_dev(torch, rows)
+    xf = plan.solve_linear_fine(yd)
+    plan.sync()
+    xf = xf.cpu().numpy()
+    xh = plan.solve_linear_fine(torch.from_numpy(np.ascontiguousarray(rows)))  # host buffers
+    xb = plan.solve_linear(yd).cpu().numpy()
+    for b in range(B):
+        xo = oracle.euler_refine(ora_model(spec), yf[b], T, n, spec.t0, spec.tf)
+        assert xf[b].shape == (n * T + 1, spec.nx)
+        assert rel(xf[b], xo) < TOL64
+        assert rel_comp(xf[b], xo) < 1e-8
+        assert rel(xf[b][::n], xb[b]) < 1e-12
+        assert rel(xh[b].numpy(), xo) < TOL64
+
+
+def test_euler_refinement_unsupported(torch_cuda):
+    """map_solve_linear_fine on a plan without Euler blocks: MAP_E_UNSUPPORTED."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 100
+    _, y = wl.simulate_linear(spec, T, seed=1)
+    plan = gpu_plan(spec, T)
+    with pytest.raises(pm.MapError) as ei:
+        pm.map_solve_linear_fine(plan.handle, to_dev(torch, y[None]),
+                                 torch.empty((1, T + 1, 4), dtype=torch.float64, device="cuda"))
+    assert ei.value.status == 2
 
 
 def test_euler_blocks_errors(torch_cuda):
