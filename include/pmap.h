@@ -226,6 +226,13 @@ map_status map_solve_nonlinear(map_plan_t plan, const void* y, int32_t passes, d
  * Filter outputs (filt_m, filt_P) are written at phase 3 and must also be passed
  * (non-NULL) at phase 2: without them phase 2 of a low-rank-diffusion model keeps only
  * the pass-2 records (DESIGN.md R-P2REC) and phase 3 then fails with MAP_E_ARG.
+ * Sharded look-back (LTI model, batch == 1, every rank holding at least one full tile,
+ * DESIGN.md section 8): the same three phases with smaller payloads -- phase 1 the v-part
+ * of the value function leaving the chunk and the chunk's v-map (nx + nx^2 values),
+ * phase 2 x at the node before the chunk for x = 0 at its end, the chunk's x-map and
+ * x*_T (2 nx + nx^2); map_shard_payload_bytes reports the plan's sizes.  Phase 3 needs y
+ * again: pass it, or pass NULL and keep the phase-2 y buffer valid.  Each phase must run
+ * once per solve, in order (phase 2 updates phase 1's run values in place).
  * Unused pointers may be NULL.  Linear plans only. */
 int64_t map_shard_payload_bytes(map_plan_t plan, int32_t phase /* 1 or 2 */);
 map_status map_shard_phase(map_plan_t plan, int32_t phase, const void* y, const void* gathered, void* payload,

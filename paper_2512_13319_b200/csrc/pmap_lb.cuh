@@ -806,6 +806,40 @@ __global__ void __launch_bounds__(NT, 6)
   LB_STAMP(0, 3);
 }
 
+// The value function leaving the run that ends at the trajectory's (chunk's) last node,
+// from the value function entering it (S from the plan's run table, v = vp) and the run's
+// element (full or partial run; data parts kept by pass 1a in seedrb).
+template <typename R, int N, int NT, int K>
+PM_INLINE void lb_run_vend(const LtiTables<R, N, NT, K>* __restrict__ tab, const R* __restrict__ rt, const R (&vp)[N],
+                           int q, const R* __restrict__ seedrb, VF<R, N>& vend, bool& ok) {
+  constexpr int NS = Dim<N>::NS;
+  VF<R, N> cur;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) cur.S[k] = __ldg(rt + (LbRunTab<N>::SP + k) * NT);
+#pragma unroll
+  for (int i = 0; i < N; ++i) cur.v[i] = vp[i];
+  Elem<R, N> ra;
+  if (q == K) {
+    load(ra, tab->E1, 1);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) ra.A[i][jj] = __ldg(&tab->PA[q - 1][i][jj]);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      ra.C[k] = __ldg(&tab->PC[q - 1][k]);
+      ra.J[k] = __ldg(&tab->PJ[q - 1][k]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    ra.b[i] = seedrb[i];
+    ra.h[i] = seedrb[N + i];
+  }
+  vapply<R, N, false>(ra, cur, vend, nullptr, ok);
+}
+
 // ------------------------------------------------------------------ pass 1b
 // One warp per tile: the decoupled look-back for v entering the tile over the tile
 // aggregates g (pass 1a wrote every g and group g_G, so nothing is waited for; a
@@ -820,7 +854,11 @@ template <typename R, int N, int NY, int NT, int K, class Src>
 __global__ void __launch_bounds__(128)
     k_lb_pass1b(const __grid_constant__ Src src, const LbGeom g, const R* __restrict__ y,
                 const LtiTables<R, N, NT, K>* __restrict__ tab, const LbTileTab<R, N>* __restrict__ lt,
-                const R* __restrict__ lrt, const LbWs<R> w, unsigned long long* flag, int stress) {
+                const R* __restrict__ lrt, const LbWs<R> w, unsigned long long* flag, int stress,
+                const R* __restrict__ vin0, int probe, R* __restrict__ probe_out) {
+  // vin0 (nullable): v entering the chunk (a time shard's carry-in)
+  // instead of node 0's prior + y_0.  probe: one warp, the last tile only, no publication:
+  // the value function's v leaving the chunk -> probe_out (a shard's pass-1 payload).
   using E = Elem<R, N>;
   using V = VF<R, N>;
   using A = Aff<R, N>;
@@ -831,25 +869,31 @@ __global__ void __launch_bounds__(128)
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   const int64_t total = g.batch * g.tpt;
-  const int64_t nticket = lb_ticket_count(total, g.S1);
-  if ((int64_t)blockIdx.x * 4 + wid >= nticket) return;  // no ticket for the grid's spare warps
-  if (lane == 0) {
-    const unsigned t = atomicAdd(&w.ctr[0], 1u);
-    if (t == nticket - 1) atomicExch(&w.ctr[0], 0u);  // every ticket is taken: reset for the next solve
-    s_ticket[wid] = (int)t;
+  int64_t u;
+  if (probe) {
+    if (blockIdx.x != 0 || wid != 0) return;
+    u = g.tpt - 1;  // trajectory 0 (probes run on batch-1 plans), last tile
+  } else {
+    const int64_t nticket = lb_ticket_count(total, g.S1);
+    if ((int64_t)blockIdx.x * 4 + wid >= nticket) return;  // no ticket for the grid's spare warps
+    if (lane == 0) {
+      const unsigned t = atomicAdd(&w.ctr[0], 1u);
+      if (t == nticket - 1) atomicExch(&w.ctr[0], 0u);  // every ticket is taken: reset for the next solve
+      s_ticket[wid] = (int)t;
+    }
+    __syncwarp();
+    const int64_t t = s_ticket[wid];
+    if (t >= nticket) return;
+    u = lb_stride_map(t, total, g.S1);
+    if (u >= total) return;
   }
-  __syncwarp();
-  const int64_t t = s_ticket[wid];
-  if (t >= nticket) return;
-  const int64_t u = lb_stride_map(t, total, g.S1);
-  if (u >= total) return;
   const int64_t b = u / g.tpt, j = u % g.tpt;
   const int64_t tile = b * g.tpt + j;
   const int64_t G = j / kLbGroup;
   const bool last = (j == g.tpt - 1);
   const int64_t n0 = 1 + j * (int64_t)L;
   if (lane == 0) {
-    w.flag2[tile] = 0u;  // pass-2 prefix status of the previous solve
+    if (!probe) w.flag2[tile] = 0u;  // pass-2 prefix status of the previous solve
     if (w.tim) w.tim[tile * 8 + 4] = lb_now();
     // what the run values need after the look-back, into L2 now: GP, QB, c, the maps' offsets
     const R* rt0 = lrt + j * (int64_t)LbRunTab<N>::F * NT;
@@ -859,12 +903,16 @@ __global__ void __launch_bounds__(128)
     lb_prefetch_l2(w.ri + tile * (int64_t)A::SZ * NT + N * N * NT, (unsigned)(sizeof(R) * N * NT));
   }
   const R* yb = y + b * g.Nn * NY;
-  R eta0[N];  // v of node 0: P0^-1 m0 + K y_0 - K r (E_0's data)
+  R eta0[N];  // v of node 0: P0^-1 m0 + K y_0 - K r (E_0's data), or the chunk's carry-in
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     R s = src.h00[i];
+    if (vin0) {
+      s = vin0[b * N + i];
+    } else {
 #pragma unroll
-    for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], __ldg(yb + k), s);
+      for (int k = 0; k < NY; ++k) s = fma(src.K[i][k], __ldg(yb + k), s);
+    }
     eta0[i] = s;
   }
   R vin[N];
@@ -986,6 +1034,32 @@ __global__ void __launch_bounds__(128)
     for (int i = 0; i < N; ++i) vin[i] = sa[i];
   }
   if (lane == 0 && w.tim) w.tim[tile * 8 + 5] = lb_now();
+  if (probe) {  // v leaving the chunk: the run ending at its last node (read-only)
+    bool okp = true;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      const int q = (int)max((int64_t)0, min((int64_t)K, g.Nn - n0 - (int64_t)r * K));
+      if (q > 0 && n0 + (int64_t)r * K + q == g.Nn) {
+        const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+        const R* cv = w.rcv + tile * (int64_t)N * NT + r;
+        R vp[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R s = cv[i * NT];
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(__ldg(rt + (LbRunTab<N>::GP + i * N + k) * NT), vin[k], s);
+          vp[i] = s;
+        }
+        V vend;
+        lb_run_vend<R, N, NT, K>(tab, rt, vp, q, w.seedrb + b * 2 * N, vend, okp);
+#pragma unroll
+        for (int i = 0; i < N; ++i) probe_out[b * N + i] = vend.v[i];
+      }
+    }
+    if (!okp) atomicMin(flag, (unsigned long long)(g.Nn - 1));
+    return;
+  }
   if (lane == 0 && !last) {  // inclusive prefix: v leaving the tile
     lb_stress(stress, tile, 3);
 #pragma unroll
@@ -1028,31 +1102,8 @@ __global__ void __launch_bounds__(128)
     }
     const int q = (int)max((int64_t)0, min((int64_t)K, g.Nn - n0 - (int64_t)r * K));
     if (last && q > 0 && n0 + (int64_t)r * K + q == g.Nn) {  // the run ending at node T: x*_T = S_T^-1 v_T
-      V cur, vend;
-#pragma unroll
-      for (int k = 0; k < NS; ++k) cur.S[k] = __ldg(rt + (LbRunTab<N>::SP + k) * NT);
-#pragma unroll
-      for (int i = 0; i < N; ++i) cur.v[i] = vp[i];
-      E ra;
-      if (q == K) {
-        load(ra, tab->E1, 1);
-      } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int jj = 0; jj < N; ++jj) ra.A[i][jj] = __ldg(&tab->PA[q - 1][i][jj]);
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          ra.C[k] = __ldg(&tab->PC[q - 1][k]);
-          ra.J[k] = __ldg(&tab->PJ[q - 1][k]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        ra.b[i] = w.seedrb[b * 2 * N + i];
-        ra.h[i] = w.seedrb[b * 2 * N + N + i];
-      }
-      vapply<R, N, false>(ra, cur, vend, nullptr, ok);
+      V vend;
+      lb_run_vend<R, N, NT, K>(tab, rt, vp, q, w.seedrb + b * 2 * N, vend, ok);
       R xT[N];
       spd_solve<R, N>(vend.S, vend.v, xT, ok);
 #pragma unroll
@@ -1372,6 +1423,57 @@ __global__ void k_lb_cov_runs(const LtiTables<R, N, NT, K>* __restrict__ tab, co
   }
 }
 
+// ------------------------------------------------------------------ time shards
+// The two exchanges of the sharded look-back, one thread each (batch 1).
+// v entering rank r's chunk: v = (v leaving rank 0, absolute); v = Gc_s v + v0_s for s = 1..r-1,
+// gathered = [world][v0 (N) | Gc (N*N)].
+template <typename R, int N>
+__global__ void k_lb_shard_vin(const R* __restrict__ gathered, int rank, R* __restrict__ vin) {
+  constexpr int P1 = N + N * N;
+  R v[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = gathered[i];
+  for (int sr = 1; sr < rank; ++sr) {
+    const R* pl = gathered + (int64_t)sr * P1;
+    R nv[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R a = pl[i];
+#pragma unroll
+      for (int c = 0; c < N; ++c) a = fma(pl[N + i * N + c], v[c], a);
+      nv[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = nv[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) vin[i] = v[i];
+}
+// x at rank r's last node: x = x*_T (the last rank's); x = Pc_s x + beta_s for s = world-1 .. r+1,
+// gathered = [world][beta (N) | Pc (N*N) | x*_T (N)].
+template <typename R, int N>
+__global__ void k_lb_shard_xend(const R* __restrict__ gathered, int rank, int world, R* __restrict__ xend) {
+  constexpr int P2 = 2 * N + N * N;
+  R x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = gathered[(int64_t)(world - 1) * P2 + N + N * N + i];
+  for (int sr = world - 1; sr > rank; --sr) {
+    const R* pl = gathered + (int64_t)sr * P2;
+    R nx[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R a = pl[i];
+#pragma unroll
+      for (int c = 0; c < N; ++c) a = fma(pl[N + i * N + c], x[c], a);
+      nx[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = nx[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) xend[i] = x[i];
+}
+
 // ------------------------------------------------------------------ pass 2
 // OUT = 1: also write the filter outputs m_i = S_i^-1 v_i, P_i = S_i^-1 to
 // (fm, fP); OUT = 2: the smoother covariances P^s_i (R-SCOV) to fP, forward inside each run
@@ -1382,7 +1484,13 @@ template <typename R, int N, int NY, int NT, int K, class Src, int OUT, typename
 __global__ void __maxnreg__(PM_LB2_MAXREG)
     k_lb_pass2(const __grid_constant__ typename Src::template rebind<RC> src, const LbGeom g, const R* __restrict__ y,
                const R* __restrict__ lrt, const LbWs<R> w, R* __restrict__ x_out, R* __restrict__ fm,
-               R* __restrict__ fP, const R* __restrict__ lcov, unsigned long long* flag, int stress) {
+               R* __restrict__ fP, const R* __restrict__ lcov, unsigned long long* flag, int stress,
+               const R* __restrict__ seed_in, int store0, int probe, R* __restrict__ probe_out,
+               const R* __restrict__ phit) {
+  // seed_in (nullable): x* at the chunk's last node (a time shard's carry from the ranks
+  // after it) instead of x*_T from pass 1b; store0: write node 0 (rank 0 only).  probe: one
+  // CTA, tile 0 only, no publication, no node loop: x* at node 0 for x* = seed_in at the
+  // chunk's end -> probe_out (a shard's pass-2 payload; phit = the tiles' pass-2 matrices).
   constexpr bool FO = OUT == 1;
   constexpr bool MIXED = !std::is_same<R, RC>::value;
   static_assert(!MIXED || OUT == 0, "mixed precision: trajectory only");
@@ -1400,16 +1508,22 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
   const int r = threadIdx.x, lane = r & 31;
   const unsigned FULL = 0xffffffffu;
   const int64_t total = g.batch * g.tpt;
-  const int64_t nticket = lb_ticket_count(total, g.S2);
-  if (r == 0) {
-    const unsigned t = atomicAdd(&w.ctr[1], 1u);
-    if (t == nticket - 1) atomicExch(&w.ctr[1], 0u);
-    s_ticket = (int)t;
+  int64_t ur;
+  if (probe) {
+    if (blockIdx.x != 0 || r >= 32) return;
+    ur = 0;  // trajectory 0, tile 0
+  } else {
+    const int64_t nticket = lb_ticket_count(total, g.S2);
+    if (r == 0) {
+      const unsigned t = atomicAdd(&w.ctr[1], 1u);
+      if (t == nticket - 1) atomicExch(&w.ctr[1], 0u);
+      s_ticket = (int)t;
+    }
+    __syncthreads();
+    const int64_t u = lb_stride_map(s_ticket, total, g.S2);
+    if (u >= total) return;
+    ur = total - 1 - u;  // reverse order
   }
-  __syncthreads();
-  const int64_t u = lb_stride_map(s_ticket, total, g.S2);
-  if (u >= total) return;
-  const int64_t ur = total - 1 - u;  // reverse order
   const int64_t b = ur / g.tpt, j = ur % g.tpt;
   const int64_t tile = b * g.tpt + j;
   const int64_t G = j / kLbGroup;
@@ -1423,9 +1537,9 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
     lb_prefetch_l2(w.ri + tile * (int64_t)A::SZ * NT, (unsigned)(sizeof(R) * A::SZ * NT));
     lb_prefetch_l2(w.rcv + tile * (int64_t)N * NT, (unsigned)(sizeof(R) * N * NT));
   }
-  YS::issue(ys, yb + n0 * NY, nvalid, r, NT);  // lands while warp 0 looks back
+  if (!probe) YS::issue(ys, yb + n0 * NY, nvalid, r, NT);  // lands while warp 0 looks back
   if (r < 32) {
-    if (lane == 0) {  // pass-1 status of this solve (that kernel has finished): clear for the next one
+    if (lane == 0 && !probe) {  // pass-1 status of this solve (that kernel has finished): clear for the next one
       w.flag1[tile] = 0u;
       if (j % kLbGroup == 0) w.gflag1[b * g.gpt + G] = 0u;
     }
@@ -1441,7 +1555,7 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
     R seed[N], Phj[N][N], bej[N];  // x*_T; this tile's map (Phi_j = Qa[j-1][1], beta_j) for its prefix
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      seed[i] = w.seed[b * N + i];
+      seed[i] = seed_in ? seed_in[b * N + i] : w.seed[b * N + i];
       bej[i] = j > 0 ? w.agg2[tile * N + i] : R(0);
 #pragma unroll
       for (int c = 0; c < N; ++c) Phj[i][c] = j > 0 ? __ldg(w.Qa + (((j - 1) * (kLbGroup + 1) + 1) * N + i) * N + c) : R(0);
@@ -1569,6 +1683,18 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
       }
     }
     LB_STAMP(1, 1);
+    if (probe) {  // x* at node 0 = Phi_tile0 x_last(0) + beta_0
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          R a = w.agg2[tile * N + i];
+#pragma unroll
+          for (int c = 0; c < N; ++c) a = fma(__ldg(phit + (j * N + i) * N + c), xl[c], a);
+          probe_out[b * N + i] = a;
+        }
+      }
+      return;
+    }
     if (lane == 0) {
 #pragma unroll
       for (int i = 0; i < N; ++i) s_x[i] = xl[i];
@@ -1629,7 +1755,7 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
         lb_store_x<R, N>(dst, x);
       }
     };
-    if (s0 == 1) {  // node 0 (the carry-in of the first tile)
+    if (s0 == 1 && store0) {  // node 0 (the carry-in of the first tile; a later shard's belongs to the rank before)
       store_x(xo);
       if constexpr (OUT == 2) {
 #pragma unroll
@@ -1641,9 +1767,11 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
         R P[NS];
         spd_inverse<R, N>(cur.S, P, ok);
 #pragma unroll
-        for (int i = 0; i < N; ++i) fm[(b * g.Nn) * N + i] = m[i];
+        for (int i = 0; i < N; ++i)
+          if (fm) fm[(b * g.Nn) * N + i] = m[i];  // either filter output may be absent
 #pragma unroll
-        for (int k = 0; k < NS; ++k) fP[(b * g.Nn) * NS + k] = P[k];
+        for (int k = 0; k < NS; ++k)
+          if (fP) fP[(b * g.Nn) * NS + k] = P[k];
       }
     }
     const R* yr = ys + r * YS::ROW;
@@ -1672,9 +1800,11 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
         spd_inverse<R, N>(cur.S, P, ok);
         const int64_t idx = b * g.Nn + s0 + m;
 #pragma unroll
-        for (int i = 0; i < N; ++i) fm[idx * N + i] = mm[i];
+        for (int i = 0; i < N; ++i)
+          if (fm) fm[idx * N + i] = mm[i];
 #pragma unroll
-        for (int k = 0; k < NS; ++k) fP[idx * NS + k] = P[k];
+        for (int k = 0; k < NS; ++k)
+          if (fP) fP[idx * NS + k] = P[k];
       }
     }
     RC s = RC(0);

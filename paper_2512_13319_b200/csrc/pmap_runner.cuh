@@ -225,6 +225,7 @@ struct PlanState {
   bool no_lb = false;        // PMAP_NO_LB=1: LTI plans use the multi-kernel scan hierarchy instead of look-back
   int lb_stress = 0;         // PMAP_LB_STRESS=1: delay injection in the look-back kernels (tests)
   bool mixed = false;        // MAP_FLAG_MIXED: fp32 node recursion in pass 2 (look-back path, fp64 plans)
+  const void* lb_y = nullptr;  // sharded look-back: y of phase 2, reused by phase 3 when it passes none
   size_t lb_bytes = 0;       // look-back workspace
   unsigned long long* lb_tim = nullptr;  // PMAP_LB_TIMING=1: per-tile globaltimer stamps (diagnostics)
   size_t lb_tim_n = 0;
@@ -369,6 +370,11 @@ struct RunnerT : Runner {
   unsigned char* lbws = nullptr;     // workspace
   LbWs<R> lbw{};
   double lb_amp = 0.0;               // forward-recovery amplification bound over a run (R-FWD)
+  // time-sharded look-back: this rank's chunk on the look-back path,
+  // two small exchanges.  lbsh: [zeros N | v_in N | probe1 N | probe2 N | x_end N |
+  // Gc N*N (v-map of the chunk) | Pc N*N (x-map of the chunk) | Phi_tile0 N*N]
+  bool lb_shard = false;
+  R* lbsh = nullptr;
 
   ~RunnerT() override {
     cudaFree(tab);
@@ -380,6 +386,7 @@ struct RunnerT : Runner {
     cudaFree(lbrun);
     cudaFree(lbcov);
     cudaFree(lbws);
+    cudaFree(lbsh);
   }
 
   bool prepare(PlanState& p) override;
@@ -399,25 +406,116 @@ struct RunnerT : Runner {
       const unsigned n2 = (unsigned)lb_ticket_count(ntiles, lbg.S2);
       PM_LAUNCH(p, s, K_LB_P1B,
                 (k_lb_pass1b<R, N, NY, kNT, K, Src><<<n1b, 128, 0, s>>>(src, lbg, y, tab, lbtab, lbrun, lbw, p.dflag,
-                                                                      p.lb_stress)));
+                                                                      p.lb_stress, nullptr, 0, nullptr)));
       if (Ps)
         PM_LAUNCH(p, s, K_LB_P2,
                   (k_lb_pass2<R, N, NY, kNT, K, Src, 2><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr,
                                                                          static_cast<R*>(Ps), lbcov, p.dflag,
-                                                                         p.lb_stress)));
+                                                                         p.lb_stress, nullptr, 1, 0, nullptr,
+                                                                         nullptr)));
       else if (fm || fP)
         PM_LAUNCH(p, s, K_LB_P2,
                   (k_lb_pass2<R, N, NY, kNT, K, Src, 1><<<n2, kNT, 0, s>>>(
                       src, lbg, y, lbrun, lbw, x, static_cast<R*>(fm), static_cast<R*>(fP), nullptr, p.dflag,
-                      p.lb_stress)));
+                      p.lb_stress, nullptr, 1, 0, nullptr, nullptr)));
       else if (p.mixed && std::is_same<R, double>::value)  // MAP_FLAG_MIXED: fp32 node recursion
         PM_LAUNCH(p, s, K_LB_P2,
                   (k_lb_pass2<R, N, NY, kNT, K, Src, 0, float><<<n2, kNT, 0, s>>>(
-                      srcf, lbg, y, lbrun, lbw, x, nullptr, nullptr, nullptr, p.dflag, p.lb_stress)));
+                      srcf, lbg, y, lbrun, lbw, x, nullptr, nullptr, nullptr, p.dflag, p.lb_stress, nullptr, 1, 0,
+                      nullptr, nullptr)));
       else
         PM_LAUNCH(p, s, K_LB_P2,
                   (k_lb_pass2<R, N, NY, kNT, K, Src, 0><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr, nullptr,
-                                                                         nullptr, p.dflag, p.lb_stress)));
+                                                                         nullptr, p.dflag, p.lb_stress, nullptr, 1,
+                                                                         0, nullptr, nullptr)));
+    }
+  }
+
+  // ---- time-sharded look-back.  Rank r > 0 views its chunk with the
+  // node before it (owned by rank r - 1) as local node 0, the carry-in; buffers are offset
+  // by one node so the kernels keep their geometry.
+  //   phase 1: k_lb_pass1a, then k_lb_pass1b in probe mode (last tile, v_in = 0 on r > 0,
+  //            the true prior on rank 0) -> payload [v leaving the chunk | Gc]
+  //   phase 2: v_in = fold of the gathered ranks < r; k_lb_pass1b with it; k_lb_pass2 in
+  //            probe mode (tile 0, x at the chunk's end = 0) -> payload [x at local node 0
+  //            | Pc | x*_T (meaningful on the last rank)]
+  //   phase 3: x at the chunk's end = fold of the gathered ranks > r onto the last rank's
+  //            x*_T; k_lb_pass2 from it.
+  static constexpr size_t lbsh_elems() { return 5 * N + 3 * N * N; }
+  size_t lb_payload(int phase) const { return phase == 1 ? (size_t)(N + N * N) : (size_t)(2 * N + N * N); }
+  const R* lb_yview(PlanState& p, const void* y) const {
+    return static_cast<const R*>(y) - (p.d.rank > 0 ? NY : 0);
+  }
+  R* lb_xview(PlanState& p, void* x, int w) const { return x ? static_cast<R*>(x) - (p.d.rank > 0 ? w : 0) : nullptr; }
+  void lb_phase1(PlanState& p, const void* yv, void* payload) {
+    if constexpr (IS_LTI) {
+      const R* y = lb_yview(p, yv);
+      cudaStream_t s = p.stream;
+      const unsigned ntiles = (unsigned)(lbg.batch * lbg.tpt);
+      PM_LAUNCH(p, s, K_LB_P1,
+                (k_lb_pass1a<R, N, NY, kNT, K, Src><<<ntiles, kNT, 0, s>>>(fold, lbg, y, tab, lbtab, lbrun, lbw)));
+      PM_LAUNCH(p, s, K_LB_P1B,
+                (k_lb_pass1b<R, N, NY, kNT, K, Src><<<1, 128, 0, s>>>(src, lbg, y, tab, lbtab, lbrun, lbw, p.dflag, 0,
+                                                                    p.d.rank > 0 ? lbsh : nullptr, 1,
+                                                                    lbsh + 2 * N)));
+      if (payload) {
+        cudaMemcpyAsync(payload, lbsh + 2 * N, sizeof(R) * N, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(static_cast<R*>(payload) + N, lbsh + 5 * N, sizeof(R) * N * N, cudaMemcpyDeviceToDevice, s);
+      }
+    }
+  }
+  void lb_phase2(PlanState& p, const void* yv, const void* gathered, void* payload) {
+    if constexpr (IS_LTI) {
+      const R* y = lb_yview(p, yv);
+      p.lb_y = yv;
+      cudaStream_t s = p.stream;
+      const unsigned ntiles = (unsigned)(lbg.batch * lbg.tpt);
+      const unsigned n1b = (unsigned)((lb_ticket_count(ntiles, lbg.S1) + 3) / 4);
+      if (p.d.rank > 0)
+        PM_LAUNCH(p, s, K_SHARD,
+                  (k_lb_shard_vin<R, N><<<1, 1, 0, s>>>(static_cast<const R*>(gathered), p.d.rank, lbsh + N)));
+      PM_LAUNCH(p, s, K_LB_P1B,
+                (k_lb_pass1b<R, N, NY, kNT, K, Src><<<n1b, 128, 0, s>>>(src, lbg, y, tab, lbtab, lbrun, lbw, p.dflag,
+                                                                      p.lb_stress, p.d.rank > 0 ? lbsh + N : nullptr,
+                                                                      0, nullptr)));
+      PM_LAUNCH(p, s, K_LB_P2,
+                (k_lb_pass2<R, N, NY, kNT, K, Src, 0><<<1, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, nullptr, nullptr,
+                                                                      nullptr, nullptr, p.dflag, 0, lbsh, 0, 1,
+                                                                      lbsh + 3 * N, lbsh + 5 * N + 2 * N * N)));
+      if (payload) {
+        R* pl = static_cast<R*>(payload);
+        cudaMemcpyAsync(pl, lbsh + 3 * N, sizeof(R) * N, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(pl + N, lbsh + 5 * N + N * N, sizeof(R) * N * N, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(pl + N + N * N, lbw.seed, sizeof(R) * N, cudaMemcpyDeviceToDevice, s);
+      }
+    }
+  }
+  void lb_phase3(PlanState& p, const void* yv, const void* gathered, void* xv, void* fm, void* fP) {
+    if constexpr (IS_LTI) {
+      if (!yv) yv = p.lb_y;
+      if (!yv) {
+        p.err = "map_shard_phase: the look-back shard path needs y at phase 3 (or the phase-2 y still valid)";
+        return;
+      }
+      const R* y = lb_yview(p, yv);
+      R* x = lb_xview(p, xv, N);
+      cudaStream_t s = p.stream;
+      const unsigned ntiles = (unsigned)(lbg.batch * lbg.tpt);
+      const unsigned n2 = (unsigned)lb_ticket_count(ntiles, lbg.S2);
+      PM_LAUNCH(p, s, K_SHARD,
+                (k_lb_shard_xend<R, N><<<1, 1, 0, s>>>(static_cast<const R*>(gathered), p.d.rank, p.d.world,
+                                                       lbsh + 4 * N)));
+      const int store0 = p.d.rank == 0 ? 1 : 0;
+      if (fm || fP)
+        PM_LAUNCH(p, s, K_LB_P2,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, 1><<<n2, kNT, 0, s>>>(
+                      src, lbg, y, lbrun, lbw, x, lb_xview(p, fm, N), lb_xview(p, fP, Dim<N>::NS), nullptr, p.dflag,
+                      p.lb_stress, lbsh + 4 * N, store0, 0, nullptr, nullptr)));
+      else
+        PM_LAUNCH(p, s, K_LB_P2,
+                  (k_lb_pass2<R, N, NY, kNT, K, Src, 0><<<n2, kNT, 0, s>>>(src, lbg, y, lbrun, lbw, x, nullptr, nullptr,
+                                                                         nullptr, p.dflag, p.lb_stress, lbsh + 4 * N,
+                                                                         store0, 0, nullptr, nullptr)));
     }
   }
 
@@ -623,10 +721,15 @@ struct RunnerT : Runner {
   // map_solve_linear drives the exchange with ncclAllGather; map_shard_phase lets
   // the caller drive it (other communicators, single-GPU virtual shards in tests).
   size_t payload_elems(int phase) const override {
+    if (lb_shard) return lb_payload(phase);
     return phase == 1 ? (size_t)E::SZ : (size_t)(A::SZ + N);
   }
 
   void phase1(PlanState& p, const void* yv, const void* xbarv, void* payload) override {
+    if (lb_shard) {
+      lb_phase1(p, yv, payload);
+      return;
+    }
     const Geom& g = p.g;
     WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
@@ -642,6 +745,10 @@ struct RunnerT : Runner {
   }
 
   void phase2(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* payload) override {
+    if (lb_shard) {
+      lb_phase2(p, yv, gathered, payload);
+      return;
+    }
     const Geom& g = p.g;
     WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
@@ -681,6 +788,10 @@ struct RunnerT : Runner {
 
   void phase3(PlanState& p, const void* yv, const void* xbarv, const void* gathered, void* xv, void* fm,
               void* fP) override {
+    if (lb_shard) {
+      lb_phase3(p, yv, gathered, xv, fm, fP);
+      return;
+    }
     const Geom& g = p.g;
     WsLayout<R, N, K> L;
     L.plan(g, p.ws_tf);
@@ -920,7 +1031,12 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
   if constexpr (!IS_LTI) {
     return false;
   } else {
-    if (p.d.world != 1) return false;
+    // time-sharded plans (world > 1, or the 1-rank NCCL test path) take the sharded look-back
+    // for single trajectories when every rank holds at least one full tile; the decision
+    // uses global quantities only, so every rank makes the same one
+    const bool shard = p.d.world > 1 || p.force_shard;
+    lb_shard = false;
+    if (shard && (p.g.batch != 1 || p.no_lb || p.d.T + 1 < (int64_t)p.d.world * kNT * K)) return false;
     const bool ptime = getenv("PMAP_PLAN_TIMING") != nullptr;
     auto tnow = [] { return std::chrono::steady_clock::now(); };
     auto t0 = tnow();
@@ -935,7 +1051,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     constexpr int NS = Dim<N>::NS;
     const int64_t L = (int64_t)kNT * K;
     LbGeom g{};
-    g.Nn = p.g.Nn;
+    g.Nn = p.g.Nn + ((shard && p.d.rank > 0) ? 1 : 0);  // rank r > 0: local node 0 = the node before the chunk
     g.batch = p.g.batch;
     const int64_t M = g.Nn - 1;  // interior nodes
     if (M < 1) return false;
@@ -961,6 +1077,10 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     full(sj, JL);
     full(src.J0, S);
     full(src.C, Cn);
+    double An[N * N], Jn[N * N];  // one interior node's element (LTI)
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) An[i * N + j] = (double)src.A[i][j];
+    full(src.J, Jn);
     auto mm = [&](const double* X, const double* Y, double* Z) {
       double T[N * N];
       for (int i = 0; i < N; ++i)
@@ -971,6 +1091,68 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
         }
       memcpy(Z, T, sizeof T);
     };
+    // S <- J + A^T S (I + C S)^-1 A (an element of matrix parts (A, C, J) applied to S)
+    auto vstep = [&](const double* Ax, const double* Cx, const double* Jx, double* Sx) -> bool {
+      double M2[N * N], M2i[N * N], X[N * N], Y[N * N], Sn[N * N], At[N * N];
+      mm(Cx, Sx, M2);
+      for (int i = 0; i < N; ++i) M2[i * N + i] += 1.0;
+      if (!h_inv(N, M2, M2i)) return false;
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) At[i * N + c] = Ax[c * N + i];
+      mm(M2i, Ax, X);
+      mm(Sx, X, Y);
+      mm(At, Y, Sn);
+      for (int i = 0; i < N * N; ++i) Sn[i] += Jx[i];
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < N; ++c) Sx[i * N + c] = 0.5 * (Sn[i * N + c] + Sn[c * N + i]);
+      return h_is_finite(Sx, N * N);
+    };
+    // forward-recovery step map A^-1 (I + C S) at S: spectral norm by power iteration, ^K
+    auto amp_of = [&](const double* Sx) -> double {
+      double CS[N * N], Mf[N * N];
+      mm(Cn, Sx, CS);
+      for (int i = 0; i < N; ++i) CS[i * N + i] += 1.0;
+      mm(Am, CS, Mf);
+      double v[N], w2[N], nrm = 0;
+      for (int i = 0; i < N; ++i) v[i] = 1.0 / std::sqrt((double)N);
+      for (int it = 0; it < 60; ++it) {  // v <- M^T M v / |M^T M v|;  |M|_2^2 = |M^T M v| at convergence
+        double u[N];
+        for (int i = 0; i < N; ++i) {
+          u[i] = 0;
+          for (int k = 0; k < N; ++k) u[i] += Mf[i * N + k] * v[k];
+        }
+        double s2 = 0;
+        for (int i = 0; i < N; ++i) {
+          w2[i] = 0;
+          for (int k = 0; k < N; ++k) w2[i] += Mf[k * N + i] * u[k];
+          s2 += w2[i] * w2[i];
+        }
+        s2 = std::sqrt(s2);
+        if (!(s2 > 0)) break;
+        nrm = std::sqrt(s2);
+        for (int i = 0; i < N; ++i) v[i] = w2[i] / s2;
+      }
+      return std::pow(nrm, (double)K);
+    };
+    double amp_global = 0.0;
+    if (shard) {
+      // the decision: the amplification bound over the GLOBAL tile chain (same on every rank)
+      double Sg[N * N];
+      memcpy(Sg, S, sizeof Sg);
+      const int64_t gt_tiles = (p.d.T + L - 1) / L;
+      for (int64_t t = 0; t < gt_tiles; ++t) {
+        amp_global = std::max(amp_global, amp_of(Sg));
+        if (!vstep(AL, CL, JL, Sg)) return false;
+      }
+      // S after global node c0 - 1 (rank r > 0): whole global tiles, then node by node
+      if (p.d.rank > 0) {
+        const int64_t nint = p.g.node0 - 1;
+        for (int64_t t = 0; t < nint / L; ++t)
+          if (!vstep(AL, CL, JL, S)) return false;
+        for (int64_t t = 0; t < nint % L; ++t)
+          if (!vstep(An, Cn, Jn, S)) return false;
+      }
+    }
     std::vector<LbTileTab<R, N>> ht((size_t)g.tpt);
     std::vector<double> gt((size_t)g.tpt * N * N);
     double amp = 0.0;
@@ -1028,7 +1210,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
           nrm = std::sqrt(s2);
           for (int i = 0; i < N; ++i) v[i] = w2[i] / s2;
         }
-        amp = std::max(amp, std::pow(nrm, (double)K));
+        if (!shard) amp = std::max(amp, std::pow(nrm, (double)K));
       }
       // S_{j+1} = J_L + A_L^T S (I + C_L S)^-1 A_L
       double M2[N * N], M2i[N * N], X[N * N], Y[N * N], Sn[N * N];
@@ -1043,6 +1225,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
         for (int c = 0; c < N; ++c) S[i * N + c] = 0.5 * (Sn[i * N + c] + Sn[c * N + i]);
       if (!h_is_finite(S, N * N)) return false;
     }
+    if (shard) amp = amp_global;
     lb_amp = amp;
     tlog("S chain (host)");
     const char* ma = getenv("PMAP_LB_MAX_AMP");
@@ -1102,6 +1285,39 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       for (size_t i = 0; i < hphi.size(); ++i) phit[i] = (double)hphi[i];
     }
     lb_phit = phit;
+    if (shard) {  // the chunk's v-map Gc and x-map Pc, plan constants of the two exchanges
+      double Gc[N * N], Pc[N * N];
+      for (int i = 0; i < N * N; ++i) Gc[i] = Pc[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
+      for (int64_t j = 0; j + 1 < g.tpt; ++j) mm(&gt[(size_t)j * N * N], Gc, Gc);
+      {  // the last tile node by node: G_node = A^T (I + S C)^-1, then S <- the node's update
+        double Sx[N * N];
+        const LbTileTab<R, N>& e = ht[(size_t)g.tpt - 1];
+        for (int i = 0; i < N; ++i)
+          for (int c = 0; c < N; ++c) Sx[i * N + c] = (double)e.S[i <= c ? sidx(i, c, N) : sidx(c, i, N)];
+        const int64_t nlast = (g.Nn - 1) - (g.tpt - 1) * L;
+        for (int64_t t = 0; t < nlast; ++t) {
+          double M1[N * N], Mi[N * N], At[N * N], Gn[N * N];
+          mm(Sx, Cn, M1);
+          for (int i = 0; i < N; ++i) M1[i * N + i] += 1.0;
+          if (!h_inv(N, M1, Mi)) return false;
+          for (int i = 0; i < N; ++i)
+            for (int c = 0; c < N; ++c) At[i * N + c] = An[c * N + i];
+          mm(At, Mi, Gn);
+          mm(Gn, Gc, Gc);
+          if (!vstep(An, Cn, Jn, Sx)) return false;
+        }
+      }
+      for (int64_t j = 0; j < g.tpt; ++j) mm(Pc, &phit[(size_t)j * N * N], Pc);
+      std::vector<R> h(lbsh_elems(), R(0));
+      for (int i = 0; i < N * N; ++i) {
+        h[5 * N + i] = (R)Gc[i];
+        h[5 * N + N * N + i] = (R)Pc[i];
+        h[5 * N + 2 * N * N + i] = (R)phit[i];
+      }
+      if (cudaMalloc(&lbsh, sizeof(R) * h.size()) != cudaSuccess ||
+          cudaMemcpy(lbsh, h.data(), sizeof(R) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return false;
+    }
     const size_t nqa = (size_t)g.tpt * W1 * N * N, nqb = (size_t)(g.gpt * (g.gpt + 1) / 2) * N * N;
     std::vector<double> qb(nqb, 0.0), phig((size_t)g.gpt * N * N, 0.0);
     for (int64_t G = 1; G < g.gpt; ++G) {  // PhiG_G = Phi_{32G} ... Phi_{32G + n_G - 1} (the last group included)
@@ -1209,6 +1425,7 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
     srcf = src.template cast<float>();
     tlog("workspace");
     use_lb = true;
+    lb_shard = shard;
     return true;
   }
 }

@@ -104,6 +104,14 @@ def test_lb_filter_outputs(torch_cuda):
     assert rel(x[0].cpu().numpy(), xo) < TOL64
     assert rel(m[0].cpu().numpy(), fm) < TOL64
     assert rel(P[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
+    # either output alone (the other NULL)
+    m2 = torch.zeros_like(m)
+    P2 = torch.zeros_like(P)
+    plan.solve_linear(to_dev(torch, y[None]), filt_m=m2)
+    plan.solve_linear(to_dev(torch, y[None]), filt_P=P2)
+    plan.sync()
+    assert rel(m2[0].cpu().numpy(), fm) < TOL64
+    assert rel(P2[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
 
 
 @pytest.mark.parametrize("K", ["8", "32"])

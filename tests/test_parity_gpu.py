@@ -335,15 +335,26 @@ def test_lti_specialised_reduce_matches_general(torch_cuda, T, monkeypatch):
 
 
 @pytest.mark.parametrize("G,T,B,general", [(2, 10_000, 1, False), (3, 123_457, 2, False), (4, 7_000, 3, True),
-                                           (8, 300_000, 1, False), (2, 5, 1, False)])
+                                           (8, 300_000, 1, False), (2, 5, 1, False), (3, 6_143, 1, False),
+                                           (5, 1_000_003, 1, False), (2, 10_000, 1, "nolb"), (3, 5_000, 1, "k8"),
+                                           (4, 200_000, 1, "stress")])
 def test_virtual_time_shards(torch_cuda, G, T, B, general, monkeypatch):
     """The time-sharded protocol (map_shard_phase) with G virtual
     ranks on one GPU and the all-gathers done by device concatenation: matches the
-    single-GPU solve and the oracle."""
+    single-GPU solve and the oracle.  Single trajectories with at least one full tile per
+    rank take the sharded look-back (probe launches + two small folds; ragged chunk
+    boundaries, both run lengths, injected delays); batches, tiny T and PMAP_NO_LB the
+    scan hierarchy."""
     import paper_2512_13319_b200 as pm
     torch = torch_cuda
-    if general:
+    if general is True:
         monkeypatch.setenv("PMAP_GENERAL", "1")
+    elif general == "nolb":
+        monkeypatch.setenv("PMAP_NO_LB", "1")
+    elif general == "k8":
+        monkeypatch.setenv("PMAP_K", "8")
+    elif general == "stress":
+        monkeypatch.setenv("PMAP_LB_STRESS", "1")
     spec = wl.wiener_velocity()
     spec.c = np.array([0.3, -0.2, 0.1, 0.05])
     spec.r = np.array([0.5, -0.25])
@@ -364,6 +375,7 @@ def test_virtual_time_shards(torch_cuda, G, T, B, general, monkeypatch):
     for b in range(B):
         assert rel(x[b], x1[b]) < 1e-11
         assert rel(x[b], xo[b]) < TOL64
+        assert rel_comp(x[b], xo[b]) < 1e-8
     with pytest.raises(pm.MapError):       # no communicator: map_solve_linear refuses
         plans[0].solve_linear(ys[0])
 
@@ -392,12 +404,14 @@ def test_nccl_exchange_path_single_rank(torch_cuda, monkeypatch):
         yd = to_dev(torch, y[None])
         x_ref = gpu_plan(spec, T).solve_linear(yd).cpu().numpy()
         monkeypatch.setenv("PMAP_FORCE_SHARD", "1")
-        plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
-                       P0=spec.P0, nccl_comm=comm)
-        x = plan.solve_linear(yd)
-        plan.sync()
-        assert plan.launches >= 9  # phases + shard folds ran
-        assert rel(x.cpu().numpy(), x_ref) < 1e-12
+        for nolb in ("0", "1"):  # sharded look-back (6 launches), scan hierarchy (>= 9)
+            monkeypatch.setenv("PMAP_NO_LB", nolb)
+            plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R,
+                           m0=spec.m0, P0=spec.P0, nccl_comm=comm)
+            x = plan.solve_linear(yd)
+            plan.sync()
+            assert plan.launches >= (9 if nolb == "1" else 6)  # phases + shard folds ran
+            assert rel(x.cpu().numpy(), x_ref) < 1e-12
     finally:
         dist.destroy_process_group()
 
@@ -447,12 +461,16 @@ def test_both_run_lengths(torch_cuda, K, case, monkeypatch):
         assert rel(x[0].cpu().numpy(), xo) < TOL64
 
 
-def test_shard_filter_outputs(torch_cuda):
+@pytest.mark.parametrize("path", ["lb", "hier"])
+def test_shard_filter_outputs(torch_cuda, path, monkeypatch):
     """Virtual time shards with filter outputs: passed at phases 2 and 3 they match the
-    oracle's filter; passed at phase 3 only (phase 2 stored pass-2 records) they are
-    refused with MAP_E_ARG."""
+    oracle's filter; on the scan hierarchy, passed at phase 3 only (phase 2 stored pass-2
+    records) they are refused with MAP_E_ARG, on the sharded look-back (which recomputes
+    the filter in pass 2) they are accepted."""
     import paper_2512_13319_b200 as pm
     torch = torch_cuda
+    if path == "hier":
+        monkeypatch.setenv("PMAP_NO_LB", "1")
     spec = wl.wiener_velocity()
     T, G = 20_000, 3
     _, y = wl.simulate_linear(spec, T, seed=5)
@@ -472,9 +490,15 @@ def test_shard_filter_outputs(torch_cuda):
     assert rel(x[0].cpu().numpy(), xo) < TOL64
     assert rel(torch.cat(fms, dim=1)[0].cpu().numpy(), fm) < TOL64
     assert rel(torch.cat(fPs, dim=1)[0].cpu().numpy(), fP[:, iu[0], iu[1]]) < TOL64
+    g1 = torch.cat([plans[r].shard_phase(1, ys[r]) for r in range(G)])  # a fresh solve: phases 1, 2, 3
     g2 = torch.cat([plans[r].shard_phase(2, ys[r], g1) for r in range(G)])
-    with pytest.raises(pm.MapError):
+    if path == "hier":
+        with pytest.raises(pm.MapError):
+            plans[0].shard_phase(3, gathered=g2, filt_m=fms[0])
+    else:
         plans[0].shard_phase(3, gathered=g2, filt_m=fms[0])
+        plans[0].sync()
+        assert rel(fms[0][0].cpu().numpy(), fm[:plans[0].n_local]) < TOL64
 
 
 @pytest.mark.parametrize("lowrank", ["0", "1", "norec"])
