@@ -206,12 +206,17 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workloads
 def build_inputs(config: str, rank: int, world: int):
+    """This rank's inputs: batch workloads (C5) shard the trajectories (MAP_FLAG_BATCH_SHARD,
+    no exchange), single trajectories shard time."""
     import workloads as wl
-    from paper_2512_13319_b200.binding import shard_range
+    from paper_2512_13319_b200.binding import batch_range, shard_range
     spec, y, T, B = wl.make_workload(config, seed=0)
-    a0, a1 = shard_range(rank, world, T)
     if y.ndim == 2:
         y = y[None]
+    if B > 1 and world > 1:
+        b0, b1 = batch_range(rank, world, B)
+        return spec, np.ascontiguousarray(y[b0:b1]), T, B
+    a0, a1 = shard_range(rank, world, T)
     return spec, np.ascontiguousarray(y[:, a0:a1]), T, B
 
 
@@ -220,9 +225,10 @@ def make_plan(pm, spec, T, B, rank, world, comm, substeps=1, mixed=False):
     if isinstance(spec, wl.LinearSpec):
         return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, c=spec.c, L=spec.L, W=spec.W, H=spec.H,
                        r=spec.r, R=spec.R, m0=spec.m0, P0=spec.P0, batch=B, rank=rank, world=world,
-                       nccl_comm=comm, substeps=substeps, mixed=mixed)
+                       nccl_comm=comm, substeps=substeps, mixed=mixed, shard="batch" if B > 1 else "time")
     return pm.Plan(T=T, t0=spec.t0, tf=spec.tf, L=spec.L, W=spec.W, R=spec.R, m0=spec.m0, P0=spec.P0,
-                   nl_kind=spec.kind, params=spec.params, batch=B, rank=rank, world=world, nccl_comm=comm)
+                   nl_kind=spec.kind, params=spec.params, batch=B, rank=rank, world=world, nccl_comm=comm,
+                   shard="batch" if B > 1 else "time")
 
 
 def solve_fn(plan, config):
@@ -515,11 +521,12 @@ def main():
     dname, (dms, dl) = dom
     per_launch_ms = dms / dl
     rec = counts.get(dname)
-    tile_nodes = 64 * (32 if B * -(-plan.n_local // 2048) >= 4 * 148 else 8)
+    Bl = plan.batch  # this rank's trajectories (batch-sharded plans hold a slice of B)
+    tile_nodes = 64 * (32 if Bl * -(-plan.n_local // 2048) >= 4 * 148 else 8)
     if rec is not None:
         fl, by = rec[0], rec[1]
         # units one launch processes: every node, or the <= 2 boundary tiles per trajectory
-        nodes_per_launch = B * plan.n_local if len(rec) < 3 else B * min(plan.n_local, 2 * tile_nodes)
+        nodes_per_launch = Bl * plan.n_local if len(rec) < 3 else Bl * min(plan.n_local, 2 * tile_nodes)
     traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from a committed ncu capture
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -567,12 +574,13 @@ def main():
     lb = "k_lb_pass2" in prof
     sfl, sby = counts["solve_lb" if lb else "solve"]
     cfl, cby = counts["solve"]
-    solve_hbm = {"schedule": "look-back (3 kernels, R-FWD)" if lb else "scan hierarchy",
-                 "alg_bytes_per_node": sby, "achieved_gbs": sby * B * T / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
-                 "peak_source": hbm_src, "frac_of_hbm_roofline": sby * B * T / (ms * 1e-3) / 1e9 / hbm,
-                 "alg_tflops": sfl * B * T / (ms * 1e-3) / 1e12, "frac_of_fp64_peak": sfl * B * T / (ms * 1e-3) / 1e12 / fp64,
+    npg = B * T / world  # nodes per GPU per solve (per-GPU rooflines)
+    solve_hbm = {"schedule": "look-back (3 kernels, R-FWD)" if lb else "scan hierarchy", "per": "GPU",
+                 "alg_bytes_per_node": sby, "achieved_gbs": sby * npg / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                 "peak_source": hbm_src, "frac_of_hbm_roofline": sby * npg / (ms * 1e-3) / 1e9 / hbm,
+                 "alg_tflops": sfl * npg / (ms * 1e-3) / 1e12, "frac_of_fp64_peak": sfl * npg / (ms * 1e-3) / 1e12 / fp64,
                  "canonical_bytes_per_node": cby,
-                 "canonical_frac_of_hbm_roofline": cby * B * T / (ms * 1e-3) / 1e9 / hbm}
+                 "canonical_frac_of_hbm_roofline": cby * npg / (ms * 1e-3) / 1e9 / hbm}
 
     seq = None
     if world == 1 and not args.no_seq:
@@ -590,7 +598,8 @@ def main():
         "dtype": "f64 (pass-2 node recursion f32, MAP_FLAG_MIXED)" if args.mixed else "f64",
         "data": "synthetic (seeded Euler-Maruyama simulation of the paper's SDE, NumPy PCG64 seed 0)",
         "config": {"workload": workload_name(args.config, T, B), "T": T, "batch": B, "nx": plan.nx, "ny": plan.ny,
-                   "parallelism": f"time-shard x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"batch-shard x{world} (MAP_FLAG_BATCH_SHARD, no exchange)" if world > 1 and B > 1
+                                   else f"time-shard x{world}" if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2 (y %.0f MB, workspace %.0f MB per GPU)" % (
                        y_host.nbytes / 1e6, plan.workspace_bytes / 1e6)},
         "roofline": roofline,

@@ -83,6 +83,13 @@ typedef struct map_plan_s* map_plan_t;
  * does not accumulate across runs (each restarts from fp64 values): about 1e-6 relative
  * instead of 1e-15.  Ignored on other paths. */
 #define MAP_FLAG_MIXED 1
+/* map_plan_desc.flags.  MAP_FLAG_BATCH_SHARD (SURVEY section 8(b) shard_mode BATCH, 8(e)
+ * "replicas"): with world > 1, rank r owns the trajectories [floor(r batch / world),
+ * floor((r + 1) batch / world)) of the global batch and solves them as an independent
+ * single-GPU plan -- no exchange, no communicator; the y / x buffers of every call cover
+ * only the rank's trajectories (all of their T + 1 nodes).  MAP_E_ARG when a rank would
+ * own no trajectory.  Without the flag, world > 1 shards time (below). */
+#define MAP_FLAG_BATCH_SHARD 2
 
 typedef struct {
   int32_t nx, ny, nw;  /* state, measurement, diffusion dims */

@@ -11,10 +11,10 @@ behind the C ABI in ``include/pmap.h``.  This package is the thin Python binding
 from .binding import (MapError, Plan, load_library, map_last_error, map_plan, map_plan_destroy,
                       map_solve_linear, map_solve_linear_cov, map_solve_linear_fine, map_solve_nonlinear, map_sync, map_two_filter,
                       map_version, map_solve_sequential,
-                      map_shard_phase, map_shard_payload_bytes, shard_range,
+                      map_shard_phase, map_shard_payload_bytes, shard_range, batch_range,
                       LIB_PATH)
 
 __all__ = ["MapError", "Plan", "load_library", "map_plan", "map_plan_destroy", "map_solve_linear",
            "map_solve_linear_cov", "map_solve_linear_fine", "map_solve_sequential",
            "map_two_filter", "map_solve_nonlinear", "map_sync", "map_last_error", "map_version", "LIB_PATH",
-           "map_shard_phase", "map_shard_payload_bytes", "shard_range"]
+           "map_shard_phase", "map_shard_payload_bytes", "shard_range", "batch_range"]

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("PMAP_LIB") or os.path.join(os.path.dirname(os.path.ab
 
 MAP_F64, MAP_F32 = 0, 1
 MAP_FLAG_MIXED = 1  # mixed-precision pass 2 (include/pmap.h)
+MAP_FLAG_BATCH_SHARD = 2  # world > 1 shards the batch instead of time (include/pmap.h)
 MAP_NL_COORD_TURN, MAP_NL_VAN_DER_POL = 1, 2
 STATUS = {0: "MAP_OK", 1: "MAP_E_ARG", 2: "MAP_E_UNSUPPORTED", 3: "MAP_E_CUDA", 4: "MAP_E_NCCL",
           5: "MAP_E_NUMERIC", 6: "MAP_E_DIVERGED"}
@@ -150,6 +151,11 @@ def _check_buf(name: str, a, dtype: str, numel: int) -> None:
         raise ValueError(f"{name}: buffer must live in CUDA device memory or host memory")
 
 
+def batch_range(rank: int, world: int, batch: int) -> tuple[int, int]:
+    """Trajectories [a, b) owned by `rank` of a batch-sharded plan (MAP_FLAG_BATCH_SHARD)."""
+    return rank * batch // world, (rank + 1) * batch // world
+
+
 def shard_range(rank: int, world: int, T: int) -> tuple[int, int]:
     """Nodes [a, b) owned by `rank` of a time-sharded plan (include/pmap.h: a_r = floor(r (T+1) / world))."""
     N = T + 1
@@ -249,7 +255,7 @@ class Plan:
     def __init__(self, *, T: int, t0: float, tf: float, m0, P0, L, W, R, F=None, H=None, c=None, r=None,
                  batch: int = 1, dtype: str = "f64", nl_kind: int | None = None, params=None,
                  rank: int = 0, world: int = 1, nccl_comm: int | None = None, stream: int | None = None,
-                 substeps: int = 1, mixed: bool = False):
+                 substeps: int = 1, mixed: bool = False, shard: str = "time"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2512_13319_b200 needs a CUDA device (no CPU fallback)")
@@ -265,14 +271,23 @@ class Plan:
         d.T, d.batch, d.t0, d.tf = T, batch, t0, tf
         d.rank, d.world = rank, world
         d.substeps = substeps
-        d.flags = MAP_FLAG_MIXED if mixed else 0
+        if shard not in ("time", "batch"):
+            raise ValueError("shard: 'time' or 'batch'")
+        d.flags = (MAP_FLAG_MIXED if mixed else 0) | (MAP_FLAG_BATCH_SHARD if shard == "batch" else 0)
         self.substeps = substeps
         d.nccl_comm = nccl_comm
         self.stream = torch.cuda.current_stream().cuda_stream if stream is None else stream
         d.stream = self.stream
         self.rank, self.world = rank, world
-        self.node0, a1 = shard_range(rank, world, T)
-        self.n_local = a1 - self.node0
+        self.shard = shard
+        if shard == "batch" and world > 1:  # the rank's trajectories, every node
+            self.batch0, b1 = batch_range(rank, world, batch)
+            self.batch = b1 - self.batch0
+            self.node0, self.n_local = 0, T + 1  # an independent single-GPU plan over them
+        else:
+            self.batch0 = 0
+            self.node0, a1 = shard_range(rank, world, T)
+            self.n_local = a1 - self.node0
         self.ny_row = ny * max(1, substeps)
         lin = nl = None
 

@@ -480,10 +480,21 @@ map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, cons
                     map_plan_t* out) {
   if (!desc || !out || (!lin) == (!nl)) return MAP_E_ARG;
   *out = nullptr;
-  const map_plan_desc& d = *desc;
-  if (d.nx < 1 || d.ny < 1 || d.nw < 1 || d.nw > d.nx || d.T < 1 || d.batch < 1 || !(d.tf > d.t0) ||
-      (d.dtype != MAP_F64 && d.dtype != MAP_F32) || d.world < 1 || d.rank < 0 || d.rank >= d.world)
+  map_plan_desc dd = *desc;
+  if (dd.nx < 1 || dd.ny < 1 || dd.nw < 1 || dd.nw > dd.nx || dd.T < 1 || dd.batch < 1 || !(dd.tf > dd.t0) ||
+      (dd.dtype != MAP_F64 && dd.dtype != MAP_F32) || dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world)
     return MAP_E_ARG;
+  if ((dd.flags & MAP_FLAG_BATCH_SHARD) && dd.world > 1) {
+    // BATCH shard mode: rank r owns trajectories [r B / world, (r + 1) B / world) and solves
+    // them as an independent single-GPU plan (no exchange, no communicator)
+    const int64_t b0 = dd.batch * dd.rank / dd.world, b1 = dd.batch * (dd.rank + 1) / dd.world;
+    if (b1 <= b0) return MAP_E_ARG;  // more ranks than trajectories
+    dd.batch = b1 - b0;
+    dd.rank = 0;
+    dd.world = 1;
+    dd.nccl_comm = nullptr;
+  }
+  const map_plan_desc& d = dd;
   if (d.substeps < 0 || (d.substeps > 1 && (!lin || d.world != 1))) return MAP_E_ARG;
   std::unique_ptr<map_plan_s> p(new map_plan_s());
   p->d = d;

@@ -78,3 +78,13 @@ def test_nccl_symbol_lookup_strategy():
     RTLD_NOLOAD = 4
     h = ctypes.CDLL("libnccl.so.2", mode=RTLD_NOLOAD)
     assert hasattr(h, "ncclAllGather")
+
+
+def test_batch_range_partition():
+    """batch_range / shard_range partition [0, n) in rank order (MAP_FLAG_BATCH_SHARD, time shards)."""
+    from paper_2512_13319_b200.binding import batch_range, shard_range
+    for n, w in [(7, 3), (1024, 8), (4, 4), (10_001, 8)]:
+        for f, m in ((batch_range, n), (shard_range, n - 1)):
+            parts = [f(r, w, m) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[r][1] == parts[r + 1][0] for r in range(w - 1))

@@ -561,3 +561,31 @@ def test_fp32_c3_full_size(torch_cuda):
     e = rel(x[0].cpu().numpy(), xo)
     print(f"fp32 C3 relative error {e:.3e}")
     assert e < TOL32
+
+
+@pytest.mark.parametrize("W,B,method", [(3, 7, "rts"), (2, 4, "tf"), (4, 4, "rts")])
+def test_batch_shard_mode(torch_cuda, W, B, method):
+    """BATCH shard mode (MAP_FLAG_BATCH_SHARD): W virtual ranks each solve
+    their slice of the trajectories as an independent plan (no exchange); concatenated they
+    equal the oracle.  A rank without a trajectory is refused."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T = 3_000
+    _, y = wl.simulate_linear(spec, T, seed=B + W, batch=B)
+    y = y.reshape(B, T + 1, 2)
+    xs = []
+    for r in range(W):
+        b0, b1 = pm.batch_range(r, W, B)
+        plan = pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                       P0=spec.P0, batch=B, rank=r, world=W, shard="batch")
+        assert plan.batch == b1 - b0 and plan.n_local == T + 1
+        yd = to_dev(torch, y[b0:b1])
+        xs.append((plan.two_filter if method == "tf" else plan.solve_linear)(yd).cpu().numpy())
+    x = np.concatenate(xs)
+    xo = oracle.batch(ora_model(spec), y, T, spec.t0, spec.tf, mode=1 if method == "tf" else 0)
+    for b in range(B):
+        assert rel(x[b], xo[b]) < TOL64
+    with pytest.raises(pm.MapError):
+        pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                P0=spec.P0, batch=2, rank=0, world=3, shard="batch")  # rank 0 of 3 owns [0, 0)
