@@ -245,6 +245,17 @@ int64_t map_shard_payload_bytes(map_plan_t plan, int32_t phase /* 1 or 2 */);
 map_status map_shard_phase(map_plan_t plan, int32_t phase, const void* y, const void* gathered, void* payload,
                            void* x_map, void* filt_m, void* filt_P);
 
+/* Pipelined host-buffer solve (the map_solve_linear computation): enqueues the copy of y
+ * (HOST, pinned for the copies to overlap) into one of two plan-owned staging slots on a
+ * copy-in stream, the solve on the plan's stream and the copy of x back to x_host on a
+ * copy-out stream, and returns without waiting.  Consecutive calls overlap one solve's
+ * device-to-host copy with the next one's host-to-device copy (separate copy engines), so
+ * a stream of solves runs at the PCIe rate of the larger direction instead of the sum of
+ * both.  y_host must stay unchanged and x_host unread until map_sync returns (map_sync
+ * waits for every solve in flight and reports numeric failures).  Not combined with
+ * filter outputs; device buffers: use map_solve_linear (already asynchronous). */
+map_status map_solve_linear_pipelined(map_plan_t plan, const void* y_host, void* x_host);
+
 /* Wait for the plan's stream and surface device-side numeric flags. */
 map_status map_sync(map_plan_t plan);
 

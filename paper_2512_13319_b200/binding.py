@@ -28,7 +28,7 @@ EXPORTS = ["map_plan", "map_plan_destroy", "map_solve_linear", "map_two_filter",
            "map_sync", "map_last_error", "map_status_string", "map_workspace_bytes", "map_last_launch_count",
            "map_profile_enable", "map_profile_read", "map_shard_payload_bytes", "map_shard_phase",
            "map_version", "map_solve_sequential", "map_debug_lb_timing", "map_solve_linear_cov",
-           "map_solve_linear_fine"]
+           "map_solve_linear_fine", "map_solve_linear_pipelined"]
 
 
 class MapError(RuntimeError):
@@ -78,6 +78,8 @@ def load_library():
         lib.map_solve_linear_cov.restype = ctypes.c_int
         lib.map_solve_linear_fine.argtypes = [P, P, P]
         lib.map_solve_linear_fine.restype = ctypes.c_int
+        lib.map_solve_linear_pipelined.argtypes = [P, P, P]
+        lib.map_solve_linear_pipelined.restype = ctypes.c_int
         lib.map_two_filter.restype = ctypes.c_int
         lib.map_solve_sequential.argtypes = [P, I32, P, I32, P, P]
         lib.map_solve_sequential.restype = ctypes.c_int
@@ -178,6 +180,10 @@ def map_plan_destroy(plan: int) -> None:
 
 def map_solve_linear(plan: int, y, x_map, filt_m=None, filt_P=None) -> None:
     _check(load_library().map_solve_linear(plan, _ptr(y), _ptr(x_map), _ptr(filt_m), _ptr(filt_P)), plan)
+
+
+def map_solve_linear_pipelined(plan: int, y_host, x_host) -> None:
+    _check(load_library().map_solve_linear_pipelined(plan, _ptr(y_host), _ptr(x_host)), plan)
 
 
 def map_solve_linear_fine(plan: int, y, x_fine) -> None:
@@ -372,6 +378,12 @@ class Plan:
         self._check_io(y, x_map=x_map, smooth_P=smooth_P)
         map_solve_linear_cov(self.handle, y, x_map, smooth_P)
         return x_map, smooth_P
+
+    def solve_linear_pipelined(self, y_host, x_host):
+        """map_solve_linear_pipelined: host (pinned) buffers, returns at once; consecutive
+        calls overlap their copies; call sync() before reading x_host."""
+        self._check_io(y_host, x_map=x_host)
+        map_solve_linear_pipelined(self.handle, y_host, x_host)
 
     def solve_linear_fine(self, y, x_fine=None):
         """Euler-block plans: x* at every fine point (map_solve_linear_fine, R-REFINE);

@@ -1277,7 +1277,80 @@ map_status map_shard_phase(map_plan_t p, int32_t phase, const void* y, const voi
 
 map_status map_sync(map_plan_t p) {
   if (!p) return MAP_E_ARG;
+  for (cudaStream_t s : {p->pipe_in, p->pipe_out})  // pipelined host-buffer solves in flight
+    if (s) {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return cuda_fail(*p, e, "map_sync");
+    }
   return check_flag(*p);
+}
+
+map_status map_solve_linear_pipelined(map_plan_t p, const void* y_host, void* x_host) {
+  if (!p || !y_host || !x_host) return MAP_E_ARG;
+  if (p->kind == Kind::NL) {
+    p->err = "map_solve_linear_pipelined called on a nonlinear plan";
+    return MAP_E_ARG;
+  }
+  if (is_device_ptr(y_host) || is_device_ptr(x_host)) {
+    p->err = "map_solve_linear_pipelined takes host buffers (pinned, for the copies to overlap)";
+    return MAP_E_ARG;
+  }
+  if (p->d.world > 1 && !p->d.nccl_comm) {
+    p->err = "time-sharded plan without an NCCL communicator: drive the exchange with map_shard_phase";
+    return MAP_E_NCCL;
+  }
+  p->err.clear();
+  p->launches = 0;
+  const Geom& g = p->g;
+  const size_t es = p->elem_real;
+  const size_t yb = (size_t)g.batch * g.Nn * p->ny_row * es, xb = (size_t)g.batch * g.Nn * p->d.nx * es;
+  if (!p->pipe_in) {
+    PM_CK(*p, cudaStreamCreateWithFlags(&p->pipe_in, cudaStreamNonBlocking));
+    PM_CK(*p, cudaStreamCreateWithFlags(&p->pipe_out, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t* e : {&p->pipe_ev_in[k], &p->pipe_ev_comp[k], &p->pipe_ev_out[k]})
+        PM_CK(*p, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  if (p->pipe_y_bytes < yb || p->pipe_x_bytes < xb) {  // (re)size the staging slots
+    for (cudaStream_t s : {p->pipe_in, p->pipe_out, p->stream}) cudaStreamSynchronize(s);
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(p->pipe_y[k]);
+      cudaFree(p->pipe_x[k]);
+      p->pipe_y[k] = p->pipe_x[k] = nullptr;
+    }
+    p->pipe_y_bytes = p->pipe_x_bytes = 0;
+    for (int k = 0; k < 2; ++k) {
+      PM_CK(*p, cudaMalloc(&p->pipe_y[k], yb));
+      PM_CK(*p, cudaMalloc(&p->pipe_x[k], xb));
+    }
+    p->pipe_y_bytes = yb;
+    p->pipe_x_bytes = xb;
+    p->pipe_k = 0;
+  }
+  const int sl = (int)(p->pipe_k & 1);
+  const bool reuse = p->pipe_k >= 2;  // the slot served solve k - 2
+  // copy in: after solve k - 2 has read the y slot
+  if (reuse) PM_CK(*p, cudaStreamWaitEvent(p->pipe_in, p->pipe_ev_comp[sl], 0));
+  PM_CK(*p, cudaMemcpyAsync(p->pipe_y[sl], y_host, yb, cudaMemcpyHostToDevice, p->pipe_in));
+  PM_CK(*p, cudaEventRecord(p->pipe_ev_in[sl], p->pipe_in));
+  // compute: after the copy in, and after the copy out of solve k - 2 has drained the x slot
+  PM_CK(*p, cudaStreamWaitEvent(p->stream, p->pipe_ev_in[sl], 0));
+  if (reuse) PM_CK(*p, cudaStreamWaitEvent(p->stream, p->pipe_ev_out[sl], 0));
+  {
+    const void* key[6] = {p->pipe_y[sl], p->pipe_x[sl], nullptr, nullptr, nullptr, "rts"};
+    map_status gs = graph_run(*p, key, [&] { p->runner->rts(*p, p->pipe_y[sl], nullptr, p->pipe_x[sl], nullptr, nullptr); });
+    if (gs) return gs;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(*p, e, "kernel launch");
+  if (!p->err.empty()) return p->err.rfind("ncclAllGather", 0) == 0 ? MAP_E_NCCL : MAP_E_ARG;
+  PM_CK(*p, cudaEventRecord(p->pipe_ev_comp[sl], p->stream));
+  // copy out: after the solve
+  PM_CK(*p, cudaStreamWaitEvent(p->pipe_out, p->pipe_ev_comp[sl], 0));
+  PM_CK(*p, cudaMemcpyAsync(x_host, p->pipe_x[sl], xb, cudaMemcpyDeviceToHost, p->pipe_out));
+  PM_CK(*p, cudaEventRecord(p->pipe_ev_out[sl], p->pipe_out));
+  ++p->pipe_k;
+  return MAP_OK;
 }
 
 const char* map_last_error(map_plan_t p) { return p ? p->err.c_str() : "null plan"; }

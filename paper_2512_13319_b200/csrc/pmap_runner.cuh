@@ -233,6 +233,15 @@ struct PlanState {
   void* refine_tab = nullptr;       // ... on the device (R), uploaded on first map_solve_linear_fine
   void* fine_ws = nullptr;          // block x, filter m, P of map_solve_linear_fine
   size_t fine_ws_bytes = 0;
+  // map_solve_linear_pipelined: host-buffer solves in flight on three streams (copy in,
+  // compute = stream, copy out), two staging slots each for y and x
+  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  cudaEvent_t pipe_ev_in[2] = {nullptr, nullptr}, pipe_ev_comp[2] = {nullptr, nullptr},
+              pipe_ev_out[2] = {nullptr, nullptr};
+  void* pipe_y[2] = {nullptr, nullptr};
+  void* pipe_x[2] = {nullptr, nullptr};
+  size_t pipe_y_bytes = 0, pipe_x_bytes = 0;
+  int64_t pipe_k = 0;
   cudaStream_t stream2 = nullptr;  // second stream of the two-filter fork
   cudaStream_t stream3 = nullptr, stream4 = nullptr;  // boundary-tile forks of stream / stream2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -265,7 +274,13 @@ struct PlanState {
     for (void* q : {(void*)lb_tim, (void*)ws, (void*)dflag, xbuf[0], xbuf[1], stage_y, stage_x, stage_aux, dev_tv, scratch, m0_dev,
                     refine_tab, fine_ws})
       if (q) cudaFree(q);
-    for (cudaStream_t s : {stream2, stream3, stream4})
+    for (cudaStream_t s : {pipe_in, pipe_out})
+      if (s) cudaStreamSynchronize(s);
+    for (void* q : {pipe_y[0], pipe_y[1], pipe_x[0], pipe_x[1]})
+      if (q) cudaFree(q);
+    for (cudaEvent_t e : {pipe_ev_in[0], pipe_ev_in[1], pipe_ev_comp[0], pipe_ev_comp[1], pipe_ev_out[0], pipe_ev_out[1]})
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {stream2, stream3, stream4, pipe_in, pipe_out})
       if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : {ev_edge0, ev_edge1, ev_edge2, ev_edge3, ev_fork, ev_join})
       if (e) cudaEventDestroy(e);

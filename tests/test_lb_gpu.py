@@ -235,3 +235,27 @@ def test_lb_s_mask_not_eligible(torch_cuda):
     assert plan.launches == LB_LAUNCHES
     xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
     assert rel(x[0].cpu().numpy(), xo) < TOL64
+
+
+@pytest.mark.parametrize("T", [TILE + 5, 300_001])
+def test_pipelined_host_solves(torch_cuda, T):
+    """map_solve_linear_pipelined: five host-buffer solves in flight (distinct inputs and
+    outputs, staging slots reused every second call), then one map_sync: each equals the
+    oracle; a device buffer is refused."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = _wiener_offsets()
+    plan = gpu_plan(spec, T)
+    ys, xs = [], []
+    for k in range(5):
+        _, y = wl.simulate_linear(spec, T, seed=100 + k)
+        ys.append(torch.from_numpy(np.ascontiguousarray(y[None])).pin_memory())
+        xs.append(torch.zeros((1, T + 1, 4), dtype=torch.float64).pin_memory())
+    for k in range(5):
+        plan.solve_linear_pipelined(ys[k], xs[k])
+    plan.sync()
+    for k in range(5):
+        xo = oracle.kf_rts(ora_model(spec), ys[k][0].numpy(), T, spec.t0, spec.tf)
+        assert rel(xs[k][0].numpy(), xo) < TOL64
+    with pytest.raises(pm.MapError):
+        plan.solve_linear_pipelined(to_dev(torch, ys[0].numpy()), xs[0])
