@@ -7,6 +7,7 @@
 // NCCL all-gathers of chunk carries.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <climits>
@@ -453,6 +454,13 @@ static map_status ensure_stage(PlanState& p, void** buf, size_t* have, size_t ne
 
 struct map_plan_s : PlanState {};
 
+// NVTX range around every ABI entry point (host-side timeline of plans, solves and shard
+// phases in Nsight tools; header-only NVTX3, a no-op when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" {
 
 const char* map_version(void) { return "pmap 0.1 (sm_100a)"; }
@@ -478,6 +486,7 @@ static int hi_prio() {
 
 map_status map_plan(const map_plan_desc* desc, const map_linear_model* lin, const map_nl_model* nl,
                     map_plan_t* out) {
+  NvtxRange nvtx_("pmap:map_plan");
   if (!desc || !out || (!lin) == (!nl)) return MAP_E_ARG;
   *out = nullptr;
   map_plan_desc dd = *desc;
@@ -845,6 +854,7 @@ static map_status finish(PlanState& p, bool blocking, const std::vector<std::pai
 }
 
 map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt_m, void* filt_P) {
+  NvtxRange nvtx_("pmap:map_solve_linear");
   if (!p || !y || !x_map) return MAP_E_ARG;
   if (p->kind == Kind::NL) {
     p->err = "map_solve_linear called on a nonlinear plan";
@@ -892,6 +902,7 @@ map_status map_solve_linear(map_plan_t p, const void* y, void* x_map, void* filt
 }
 
 map_status map_solve_linear_fine(map_plan_t p, const void* y, void* x_fine) {
+  NvtxRange nvtx_("pmap:map_solve_linear_fine");
   if (!p || !y || !x_fine) return MAP_E_ARG;
   if (p->kind == Kind::NL || !p->euler) {
     p->err = "map_solve_linear_fine needs a linear plan with Euler blocks (substeps > 1)";
@@ -939,6 +950,7 @@ map_status map_solve_linear_fine(map_plan_t p, const void* y, void* x_fine) {
   return finish(*p, blocking, outs);
 }
 map_status map_solve_linear_cov(map_plan_t p, const void* y, void* x_map, void* smooth_P) {
+  NvtxRange nvtx_("pmap:map_solve_linear_cov");
   if (!p || !y || !x_map || !smooth_P) return MAP_E_ARG;
   if (p->kind == Kind::NL || p->euler) {
     p->err = "map_solve_linear_cov needs a linear plan without Euler blocks";
@@ -971,6 +983,7 @@ map_status map_solve_linear_cov(map_plan_t p, const void* y, void* x_map, void* 
 }
 
 map_status map_two_filter(map_plan_t p, const void* y, void* x_map, void* smooth_P) {
+  NvtxRange nvtx_("pmap:map_two_filter");
   if (!p || !y || !x_map) return MAP_E_ARG;
   if (p->euler) {
     p->err = "two-filter is not available with Euler blocks (the block element mixes dynamics and measurements)";
@@ -1006,6 +1019,7 @@ map_status map_two_filter(map_plan_t p, const void* y, void* x_map, void* smooth
 
 map_status map_solve_sequential(map_plan_t p, int32_t method, const void* y, int32_t passes, void* x_map,
                                 void* smooth_P) {
+  NvtxRange nvtx_("pmap:map_solve_sequential");
   if (!p || !y || !x_map || (method != 0 && method != 1)) return MAP_E_ARG;
   if (p->d.world != 1) {
     p->err = "map_solve_sequential needs a single-GPU plan (world == 1)";
@@ -1047,6 +1061,7 @@ map_status map_solve_sequential(map_plan_t p, int32_t method, const void* y, int
 
 map_status map_solve_nonlinear(map_plan_t p, const void* y, int32_t passes, double tol, const void* x_init,
                                void* x_map, int32_t* passes_run) {
+  NvtxRange nvtx_("pmap:map_solve_nonlinear");
   if (!p || !y || !x_map || passes < 1 || tol < 0) return MAP_E_ARG;
   if (p->kind != Kind::NL) {
     p->err = "map_solve_nonlinear called on a linear plan";
@@ -1247,6 +1262,7 @@ int64_t map_shard_payload_bytes(map_plan_t p, int32_t phase) {
 
 map_status map_shard_phase(map_plan_t p, int32_t phase, const void* y, const void* gathered, void* payload,
                            void* x_map, void* filt_m, void* filt_P) {
+  NvtxRange nvtx_("pmap:map_shard_phase");
   if (!p || phase < 1 || phase > 3) return MAP_E_ARG;
   if (p->kind == Kind::NL || p->d.world < 2) {
     p->err = "map_shard_phase needs a linear time-sharded plan (world > 1)";
@@ -1286,6 +1302,7 @@ map_status map_sync(map_plan_t p) {
 }
 
 map_status map_solve_linear_pipelined(map_plan_t p, const void* y_host, void* x_host) {
+  NvtxRange nvtx_("pmap:map_solve_linear_pipelined");
   if (!p || !y_host || !x_host) return MAP_E_ARG;
   if (p->kind == Kind::NL) {
     p->err = "map_solve_linear_pipelined called on a nonlinear plan";
