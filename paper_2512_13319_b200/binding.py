@@ -431,7 +431,7 @@ class Plan:
         if phase in (1, 2):
             self._check_io(y, filt_m=filt_m, filt_P=filt_P)
         else:
-            self._check_io(None, x_map=x_map, filt_m=filt_m, filt_P=filt_P)
+            self._check_io(y, x_map=x_map, filt_m=filt_m, filt_P=filt_P)
         if gathered is not None:
             per = {2: map_shard_payload_bytes(self.handle, 1), 3: map_shard_payload_bytes(self.handle, 2)}[phase]
             _check_buf("gathered", gathered, self.dtype, self.world * per // (8 if self.dtype == "f64" else 4))
@@ -442,7 +442,7 @@ class Plan:
             return payload
         if x_map is None:
             x_map = torch.empty((self.batch, self.n_local, self.nx), dtype=self.torch_dtype, device="cuda")
-        map_shard_phase(self.handle, 3, None, gathered, None, x_map, filt_m, filt_P)
+        map_shard_phase(self.handle, 3, y, gathered, None, x_map, filt_m, filt_P)  # y: optional at phase 3
         return x_map
 
     def profile(self, enable: bool = True) -> None:

@@ -1268,7 +1268,7 @@ map_status map_shard_phase(map_plan_t p, int32_t phase, const void* y, const voi
     p->err = "map_shard_phase needs a linear time-sharded plan (world > 1)";
     return MAP_E_ARG;
   }
-  const bool dev_ok = (phase == 3 || is_device_ptr(y)) && (phase == 1 || is_device_ptr(gathered)) &&
+  const bool dev_ok = (phase == 3 ? (!y || is_device_ptr(y)) : is_device_ptr(y)) && (phase == 1 || is_device_ptr(gathered)) &&
                       (phase == 3 || is_device_ptr(payload)) && (phase != 3 || is_device_ptr(x_map)) &&
                       (!filt_m || is_device_ptr(filt_m)) && (!filt_P || is_device_ptr(filt_P));
   if (!dev_ok) {

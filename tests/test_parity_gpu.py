@@ -589,3 +589,22 @@ def test_batch_shard_mode(torch_cuda, W, B, method):
     with pytest.raises(pm.MapError):
         pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
                 P0=spec.P0, batch=2, rank=0, world=3, shard="batch")  # rank 0 of 3 owns [0, 0)
+
+
+def test_virtual_time_shards_fp32(torch_cuda):
+    """The sharded look-back in fp32 (3 virtual ranks): within the fp32 tolerance of the oracle."""
+    import paper_2512_13319_b200 as pm
+    torch = torch_cuda
+    spec = wl.wiener_velocity()
+    T, G = 200_000, 3
+    _, y = wl.simulate_linear(spec, T, seed=31)
+    plans = [pm.Plan(T=T, t0=spec.t0, tf=spec.tf, F=spec.F, L=spec.L, W=spec.W, H=spec.H, R=spec.R, m0=spec.m0,
+                     P0=spec.P0, rank=r, world=G, dtype="f32") for r in range(G)]
+    ys = [to_dev(torch, y[None, slice(*pm.shard_range(r, G, T))], dtype=torch.float32) for r in range(G)]
+    g1 = torch.cat([plans[r].shard_phase(1, ys[r]) for r in range(G)])
+    g2 = torch.cat([plans[r].shard_phase(2, ys[r], g1) for r in range(G)])
+    x = torch.cat([plans[r].shard_phase(3, ys[r], g2) for r in range(G)], dim=1)
+    for p in plans:
+        p.sync()
+    xo = oracle.kf_rts(ora_model(spec), y, T, spec.t0, spec.tf)
+    assert rel(x[0].cpu().numpy(), xo) < TOL32
