@@ -1434,6 +1434,10 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       g.S1 = plain ? (int64_t)1 << 40 : std::max<int64_t>(1, (int64_t)b1 * 4 * nsm);
       g.S2 = plain ? (int64_t)1 << 40 : std::max<int64_t>(1, (int64_t)b2 * nsm);
       if (plain) g.S1 = g.S2 = std::max<int64_t>(1, g.batch * g.tpt);
+      const char* sg1 = getenv("PMAP_LB_STAGGER1_NS");  // first-wave stagger steps (lb_stagger); "0" = off
+      const char* sg2 = getenv("PMAP_LB_STAGGER2_NS");
+      g.stagger1 = sg1 ? atoi(sg1) : 1500;
+      g.stagger2 = sg2 ? atoi(sg2) : 3500;
     }
     lbg = g;
     p.lb_bytes += off;
