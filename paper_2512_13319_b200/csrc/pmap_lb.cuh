@@ -65,6 +65,7 @@ struct LbGeom {
   int64_t batch;
   int64_t S1, S2;  // ticket strides of pass 1b (warps) and pass 2 (CTAs): the resident counts
   int stagger1, stagger2;  // first-wave start stagger of passes 1a / 2 (ns per step; 0 = off), lb_stagger
+  int stmod1, stmod2;      // ... and its number of distinct start offsets
 };
 
 // Strided ticket order of the look-back kernels: ticket t -> tile (t mod S) C + t div S,
@@ -416,12 +417,13 @@ PM_INLINE R lb_ldcg(const R* p) {
 // First-wave stagger: with several waves of tiles, the CTAs of the first wave would run their
 // phases in lock step (all staging y, then all looking back, then all storing x), so DRAM
 // sees bursts of reads and of writes instead of a mix.  Delaying the start of the first
-// wave's CTAs by (slot mod 6) steps spreads the phases (C3: pass 1a 0.1327 -> 0.1297 ms
-// with 1.5 us steps, pass 2 0.1356 -> 0.1295 ms with 3.5 us steps); later waves inherit the
-// spread.  Off for problems of < 2 waves, whose CTAs would only wait.
-PM_INLINE void lb_stagger(int64_t slot, int64_t resident, int64_t total, int step_ns) {
-  if (step_ns > 0 && total >= 2 * resident && slot < resident) {
-    const unsigned ns = (unsigned)(slot % 6) * (unsigned)step_ns;
+// wave's CTAs by (slot mod m) steps spreads the phases (C3, A/B on one box: pass 1a
+// 0.1327 -> 0.1272 ms with m = 8, 1.1 us steps; pass 2 0.1361 -> 0.1291 ms with m = 6, 3 us
+// steps); later waves inherit the spread.  Off for problems of < 2 waves, whose CTAs would
+// only wait.
+PM_INLINE void lb_stagger(int64_t slot, int64_t resident, int64_t total, int step_ns, int mod) {
+  if (step_ns > 0 && mod > 1 && total >= 2 * resident && slot < resident) {
+    const unsigned ns = (unsigned)(slot % mod) * (unsigned)step_ns;
     for (unsigned t = 0; t < ns; t += 250u) __nanosleep(250u);
   }
 }
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(NT, 6)
   const int64_t b = tile / g.tpt, j = tile % g.tpt;
   const int64_t G = j / kLbGroup;
   const bool last = (j == g.tpt - 1);
-  lb_stagger((int64_t)blockIdx.x, g.S2, (int64_t)gridDim.x, g.stagger1);
+  lb_stagger((int64_t)blockIdx.x, g.S2, (int64_t)gridDim.x, g.stagger1, g.stmod1);
   LB_STAMP(0, 0);
   const int64_t n0 = 1 + j * (int64_t)L;
   const int nvalid = (int)min((int64_t)L, g.Nn - n0);
@@ -1535,7 +1537,7 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
       s_ticket = (int)t;
     }
     __syncthreads();
-    lb_stagger(s_ticket, g.S2, total, g.stagger2);
+    lb_stagger(s_ticket, g.S2, total, g.stagger2, g.stmod2);
     const int64_t u = lb_stride_map(s_ticket, total, g.S2);
     if (u >= total) return;
     ur = total - 1 - u;  // reverse order

@@ -1436,8 +1436,10 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       if (plain) g.S1 = g.S2 = std::max<int64_t>(1, g.batch * g.tpt);
       const char* sg1 = getenv("PMAP_LB_STAGGER1_NS");  // first-wave stagger steps (lb_stagger); "0" = off
       const char* sg2 = getenv("PMAP_LB_STAGGER2_NS");
-      g.stagger1 = sg1 ? atoi(sg1) : 1500;
-      g.stagger2 = sg2 ? atoi(sg2) : 3500;
+      g.stagger1 = sg1 ? atoi(sg1) : 1100;
+      g.stagger2 = sg2 ? atoi(sg2) : 3000;
+      g.stmod1 = 8;
+      g.stmod2 = 6;
     }
     lbg = g;
     p.lb_bytes += off;
