@@ -98,11 +98,14 @@ struct LbTileTab {
 //   QB  = sum_{k >= r} Phi_r..Phi_{k-1} WR_k C_Rk GP_k   the v_in-coefficient of the run's
 //                                    suffix offset (beta_k = WR_k (rb_k + C_Rk v_{s-1,k}))
 //   SP  = S_{s-1}                   S entering the run (pass 2 restarts the node recursion there)
+//   PS  = Phi_r Phi_{r+1} ... Phi_{NT-1}  the matrix of the run's in-tile suffix map (x at the
+//                                    tile's last node -> x*_{s-1}); data-free, so pass 1a
+//                                    writes only the map's offset and pass 2 reads PS here
 // Empty runs of a ragged last tile are identity maps (PHI = I, WR = QB... = 0).
 template <int N>
 struct LbRunTab {
   static constexpr int GP = 0, WR = N * N, PHI = 2 * N * N, QB = 3 * N * N, SP = 4 * N * N,
-                       F = 4 * N * N + Dim<N>::NS;
+                       PS = 4 * N * N + Dim<N>::NS, F = 5 * N * N + Dim<N>::NS;
 };
 
 // One thread per (tile, run): GP, WR, PHI, SP from the tile's S and the LTI span tables.
@@ -242,7 +245,10 @@ __global__ void k_lb_setup_tiles(const LtiTables<R, N, NT, K>* __restrict__ tab,
 #pragma unroll
       for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int c = 0; c < N; ++c) rt[(LbRunTab<N>::QB + i * N + c) * NT] = R(0);
+        for (int c = 0; c < N; ++c) {
+          rt[(LbRunTab<N>::QB + i * N + c) * NT] = R(0);
+          rt[(LbRunTab<N>::PS + i * N + c) * NT] = P[i][c];  // an empty run: the suffix product so far
+        }
       continue;
     }
     R CR[Dim<N>::NS];
@@ -297,6 +303,7 @@ __global__ void k_lb_setup_tiles(const LtiTables<R, N, NT, K>* __restrict__ tab,
         Q[i][c] = Nq[i][c];
         P[i][c] = Np[i][c];
         rt[(LbRunTab<N>::QB + i * N + c) * NT] = Q[i][c];
+        rt[(LbRunTab<N>::PS + i * N + c) * NT] = P[i][c];
       }
   }
 #pragma unroll
@@ -792,7 +799,8 @@ __global__ void __launch_bounds__(NT, 6)
   }
 #pragma unroll
   for (int i = 0; i < N; ++i) w.rcv[(tile * N + i) * NT + r] = cvec[i];
-  store(agg, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
+#pragma unroll
+  for (int i = 0; i < N; ++i) w.ri[(tile * (int64_t)A::SZ + N * N + i) * NT + r] = agg.q[i];  // the matrix is PS
   if (last && q > 0 && n0 + (int64_t)r * K + q == g.Nn) {  // the run ending at node T: keep its data parts
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -1551,8 +1559,9 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
   const R* yb = y + b * g.Nn * NY;
   LB_STAMP(1, 0);
   if (r == 0) {  // what the runs read after the look-back, into L2 now: S, the maps, v
-    lb_prefetch_l2(lrt + j * (int64_t)LbRunTab<N>::F * NT + LbRunTab<N>::SP * NT, (unsigned)(sizeof(R) * NS * NT));
-    lb_prefetch_l2(w.ri + tile * (int64_t)A::SZ * NT, (unsigned)(sizeof(R) * A::SZ * NT));
+    lb_prefetch_l2(lrt + j * (int64_t)LbRunTab<N>::F * NT + LbRunTab<N>::SP * NT,
+                   (unsigned)(sizeof(R) * (NS + N * N) * NT));  // SP and PS
+    lb_prefetch_l2(w.ri + (tile * (int64_t)A::SZ + N * N) * NT, (unsigned)(sizeof(R) * N * NT));
     lb_prefetch_l2(w.rcv + tile * (int64_t)N * NT, (unsigned)(sizeof(R) * N * NT));
   }
   if (!probe) YS::issue(ys, yb + n0 * NY, nvalid, r, NT);  // lands while warp 0 looks back
@@ -1739,8 +1748,17 @@ __global__ void __maxnreg__(PM_LB2_MAXREG)
     // the plan's run table, v from pass 1); then the forward sweep over the run's nodes
     RC x[N];
     {
-      A inc;
-      load(inc, w.ri + tile * (int64_t)A::SZ * NT + r, NT);
+      A inc;  // the run's in-tile suffix map: matrix from the plan (PS), offset from pass 1
+      {
+        const R* rt = lrt + j * (int64_t)LbRunTab<N>::F * NT + r;
+        const R* qv = w.ri + (tile * (int64_t)A::SZ + N * N) * NT + r;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) inc.P[i][c] = __ldg(rt + (LbRunTab<N>::PS + i * N + c) * NT);
+          inc.q[i] = qv[i * NT];
+        }
+      }
       R xr[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) xr[i] = s_x[i];
