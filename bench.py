@@ -123,7 +123,9 @@ def alg_counts(nx: int, ny: int, K: int = 32, lti: bool = True, nw: int = 0, zer
         xstep = nU * (N + 1) + nU + nA + (0 if zero_b else N)
     else:
         xstep = 3 * N * N + N
-    lb1 = (2 * (2 * N * ny + 4 * N * N / K), d * (ny + 3 * N * N / K + N / K + asz / K))
+    # pass 1a writes v_{s-1} (N) and only the offset (N) of each run's suffix map: its matrix
+    # is a plan table (LbRunTab::PS) that pass 2 reads instead (counted there as asz / K)
+    lb1 = (2 * (2 * N * ny + 4 * N * N / K), d * (ny + 3 * N * N / K + N / K + N / K))
     # pass 1b: per run v_{s-1} = GP v_in + c and the map offset q += QB v_in (reads GP, QB, c, q;
     # writes c, q): 2 N^2 FMA and 2 N^2 + 4 N values per run
     lb1b = (2 * (2 * N * N / K), d * ((2 * N * N + 4 * N) / K))

@@ -1,68 +1,73 @@
-"""Summarise an ncu report (--page raw) and a launch list (gpu__time_duration csv) into markdown."""
+"""Write profiles/r02_ncu_summary.md from a `ncu --set full` report and an ncu launch list.
+
+Usage: python tools/ncu_summary.py <report.ncu-rep> <launches.csv> <out.md>
+"""
+import collections
 import csv
 import io
 import subprocess
 import sys
-from collections import defaultdict
 
-METRICS = [
-    ("gpu__time_duration.sum", "time"),
-    ("dram__bytes_read.sum", "DRAM read"),
-    ("dram__bytes_write.sum", "DRAM write"),
-    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
-    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
-    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
-    ("launch__registers_per_thread", "regs"),
-    ("sass__inst_executed_local_loads", "local loads"),
-    ("smsp__inst_executed.sum", "warp instrs"),
-    ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem thru %"),
-]
+rep, launches, out_path = sys.argv[1:4]
+KEEP = ['Duration', 'DRAM Throughput', 'Memory Throughput', 'Compute (SM) Throughput', 'Registers Per Thread',
+        'Theoretical Occupancy', 'Achieved Occupancy', 'Executed Ipc Active', 'Issue Slots Busy', 'L1/TEX Hit Rate',
+        'L2 Hit Rate', 'Warp Cycles Per Issued Instruction', 'Static Shared Memory Per Block', 'Block Limit Registers',
+        'Block Limit Shared Mem']
 
 
-def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    return rows[0], rows[1], rows[2:]
+def short(name):
+    return name.split('<')[0].replace('void ', '').replace('pmap::', '').split('(')[0]
 
 
-def main(rep, launches=None):
-    print(f"## ncu --set full: `{rep}`\n")
-    hdr, units, rows = raw(rep)
-    cols = ["kernel"] + [m[1] for m in METRICS]
-    print("| " + " | ".join(cols) + " |")
-    print("|" + "---|" * len(cols))
-    for r in rows:
-        name = r[hdr.index("Kernel Name")].split("(")[0][:60]
-        vals = []
-        for m, _ in METRICS:
-            if m in hdr:
-                i = hdr.index(m)
-                vals.append(f"{r[i]} {units[i]}".strip())
-            else:
-                vals.append("-")
-        print("| " + " | ".join([name] + vals) + " |")
-    if launches:
-        print(f"\n## launch list (ncu --metrics gpu__time_duration.sum, cold-cache, serialised): `{launches}`\n")
-        txt = open(launches).read()
-        txt = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
-        rows = list(csv.DictReader(io.StringIO(txt)))
-        tot = defaultdict(float)
-        cnt = defaultdict(int)
-        for r in rows:
-            if r.get("Metric Name") != "gpu__time_duration.sum":
-                continue
-            k = r["Kernel Name"].split("(")[0].split("<")[0]
-            v = float(r["Metric Value"].replace(",", ""))
-            unit = r.get("Metric Unit", "")
-            v = v / 1000.0 if unit in ("nsecond", "ns") else (v * 1000.0 if unit in ("msecond", "ms") else v)
-            tot[k] += v
-            cnt[k] += 1
-        s = sum(tot.values())
-        print("| kernel | launches | total us | share |")
-        print("|---|---|---|---|")
-        for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-            print(f"| {k} | {cnt[k]} | {v:.1f} | {v / s:.1%} |")
-
-
-if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
+txt = subprocess.run(['ncu', '-i', rep, '--page', 'details', '--csv'], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(txt)))
+h = rows[0]
+per = collections.OrderedDict()
+for r in rows[1:]:
+    d = dict(zip(h, r))
+    if d['Metric Name'] in KEEP:
+        per.setdefault(short(d['Kernel Name']), {})[d['Metric Name']] = d['Metric Value'] + ' ' + d['Metric Unit']
+raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+rr = list(csv.reader(io.StringIO(raw)))
+H = rr[0]
+stalls, dram = {}, {}
+for r in rr[2:]:
+    k = short(r[H.index('Kernel Name')])
+    st = [(H[i], r[i]) for i in range(len(H))
+          if H[i].startswith('smsp__pcsamp_warps_issue_stalled') and not H[i].endswith('not_issued')]
+    vals = sorted([(float(v.replace(',', '')), n) for n, v in st if v.replace(',', '').replace('.', '').isdigit()],
+                  reverse=True)
+    tot = sum(v for v, _ in vals)
+    stalls[k] = ', '.join(f"{n.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * v / tot:.0f}%"
+                          for v, n in vals[:6])
+lines = [l for l in open(launches) if l.startswith('"')]
+lr = list(csv.reader(io.StringIO(''.join(lines))))
+lh = lr[0]
+tot, cnt = collections.Counter(), collections.Counter()
+for r in lr[1:]:
+    if r[lh.index('Metric Name')] != 'gpu__time_duration.sum':
+        continue
+    k = short(r[lh.index('Kernel Name')])
+    tot[k] += float(r[lh.index('Metric Value')].replace(',', ''))
+    cnt[k] += 1
+out = ['# ncu summary, round 2 (C3: Wiener velocity, T = 1e7, fp64, 1 B200)', '',
+       'Command: `python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-seq` (tools/gpu_final.sh), '
+       'final round-2 code.',
+       'Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` (r02_launches.csv; cold-cache, '
+       'serialised).',
+       'Full capture: `ncu --set full --clock-control none --import-source on -k regex:k_lb_pass -s 9 -c 3`.', '',
+       '## Launch list (solve kernels)', '', '| kernel | launches | mean µs | share of the solve kernels |',
+       '|---|---|---|---|']
+solve = {k: v for k, v in tot.items() if k.startswith('k_lb_pass')}
+S = sum(solve.values())
+for k, v in sorted(solve.items(), key=lambda x: -x[1]):
+    m = v / cnt[k]
+    out.append(f'| {k} | {cnt[k]} | {m / 1000 if m > 1000 else m:.1f} | {100 * v / S:.1f} % |')
+out += ['', '## Full capture']
+for k, d in per.items():
+    out.append(f'### {k}')
+    out += [f'- {m}: {d[m]}' for m in KEEP if m in d]
+    out.append(f'- top stall reasons (pc sampling): {stalls.get(k, "")}')
+    out.append('')
+open(out_path, 'w').write('\n'.join(out) + '\n')
+print('\n'.join(out))
