@@ -66,6 +66,7 @@ struct LbGeom {
   int64_t S1, S2;  // ticket strides of pass 1b (warps) and pass 2 (CTAs): the resident counts
   int stagger1, stagger2;  // first-wave start stagger of passes 1a / 2 (ns per step; 0 = off), lb_stagger
   int stmod1, stmod2;      // ... and its number of distinct start offsets
+  int stagger1b;           // ... of pass 1b (per warp, 8 offsets)
 };
 
 // Strided ticket order of the look-back kernels: ticket t -> tile (t mod S) C + t div S,
@@ -426,7 +427,8 @@ PM_INLINE R lb_ldcg(const R* p) {
 // sees bursts of reads and of writes instead of a mix.  Delaying the start of the first
 // wave's CTAs by (slot mod m) steps spreads the phases (C3, A/B on one box: pass 1a
 // 0.1327 -> 0.1272 ms with m = 8, 1.1 us steps; pass 2 0.1361 -> 0.1291 ms with m = 6, 3 us
-// steps); later waves inherit the spread.  Off for problems of < 2 waves, whose CTAs would
+// steps; pass 1b, per warp, 0.0471 -> 0.0455 ms with m = 8, 0.8 us steps); later waves
+// inherit the spread.  Off for problems of < 2 waves, whose CTAs would
 // only wait.
 PM_INLINE void lb_stagger(int64_t slot, int64_t resident, int64_t total, int step_ns, int mod) {
   if (step_ns > 0 && mod > 1 && total >= 2 * resident && slot < resident) {
@@ -911,6 +913,7 @@ __global__ void __launch_bounds__(128)
     if (t >= nticket) return;
     u = lb_stride_map(t, total, g.S1);
     if (u >= total) return;
+    lb_stagger(t, g.S1, total, g.stagger1b, 8);
   }
   const int64_t b = u / g.tpt, j = u % g.tpt;
   const int64_t tile = b * g.tpt + j;

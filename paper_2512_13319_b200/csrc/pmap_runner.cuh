@@ -1440,6 +1440,8 @@ bool RunnerT<R, N, NY, Src, K>::prepare_lb(PlanState& p) {
       g.stagger2 = sg2 ? atoi(sg2) : 3000;
       g.stmod1 = 8;
       g.stmod2 = 6;
+      const char* sg1b = getenv("PMAP_LB_STAGGER1B_NS");
+      g.stagger1b = sg1b ? atoi(sg1b) : 800;
     }
     lbg = g;
     p.lb_bytes += off;
